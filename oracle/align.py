@@ -1,0 +1,129 @@
+"""Oracle: unpad-append-repad and KV realignment (Alg. 2 Phase 3, PAPER.md:348-356;
+§3.1 invariants PAPER.md:444-447; Fig. 4).
+
+Test infrastructure only (see oracle/__init__.py).
+
+Conventions:
+  * a batch row holds n_i content tokens right-aligned at width L (left pads p_i = L - n_i);
+    the last content token is "pending": it has no KV entry yet;
+  * after the verify forward the KV width is L + k and row i's valid KV is [p_i, L + a_i);
+  * after repad row i's kept_i = n_i + a_i entries live at [p'_i, p'_i + kept_i) = [p'_i, L' - 1).
+Readings: R7 (pos = 0 on pads), R8 (pad KV is don't-care unless ZERO_PADS), R9 (dummy rows).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+# ----------------------------------------------------------------------------- tokens
+def build_batch(seqs, cap: int, pad_id: int = 0):
+    """Batch left padding (Alg. 2 line 1): content right-aligned at
+    L = max length; returns tokens [B, cap], pad [B], L."""
+    lens = np.array([len(s) for s in seqs], np.int32)
+    L = int(lens.max())
+    tok = np.full((len(seqs), cap), pad_id, np.int64)
+    for i, s in enumerate(seqs):
+        tok[i, L - len(s):L] = s
+    return tok, (L - lens).astype(np.int32), L
+
+
+def unpad(tokens, pad, L):
+    """S[i] <- Unpad(S[i]): the content columns [p_i, L)."""
+    return [list(map(int, tokens[i, pad[i]:L])) for i in range(len(pad))]
+
+
+def append_accepted(rows, E_rows):
+    """S[i] <- S[i] (+) A[i] (+) B[i] -- E already holds A ++ [B], EOS-cut."""
+    return [r + list(e) for r, e in zip(rows, E_rows)]
+
+
+def mask_pos_row(pad_new: int, width: int):
+    """Padding-agnostic positions and masks: mask = 1 exactly on content
+    columns c >= p'; pos = c - p' there, 0 on pads (R7)."""
+    c = np.arange(width)
+    mask = (c >= pad_new).astype(np.int64)
+    pos = np.where(c >= pad_new, c - pad_new, 0).astype(np.int64)
+    return mask, pos
+
+
+def repad_tokens(tokens, cap, k, pad_old, L_old, vres, pad_id=0):
+    """Tokens' / mask / pos after Phase 3.
+
+    vres is batch_verify()'s result (plan included).  Returns (tokens' [B, cap],
+    mask [B, L'+k], pos [B, L'+k]); only columns [0, L') of tokens' are defined."""
+    B = len(pad_old)
+    L_new = vres["L_new"]
+    out = np.full((B, cap), pad_id, np.int64)
+    mask = np.zeros((B, L_new + k), np.int64)
+    pos = np.zeros((B, L_new + k), np.int64)
+    if L_new == 0:
+        return out, mask, pos
+    rows = unpad(tokens, pad_old, L_old)
+    rows = append_accepted(rows, vres["E"])
+    for i in range(B):
+        if vres["finished"][i]:
+            content = [pad_id]                         # R9 dummy row
+        else:
+            content = rows[i]
+        assert len(content) == vres["n_new"][i]
+        p = int(vres["pad_new"][i])
+        out[i, p:L_new] = content
+        mask[i], pos[i] = mask_pos_row(p, L_new + k)
+    return out, mask, pos
+
+
+# ----------------------------------------------------------------------------- KV
+def realign_kv(kv, pad_old, pad_new, kept):
+    """KVCache <- Realign(KVCache, offset) as a fresh rectangle
+    (SPEC.md:176 style): KV'[.., i, h, p'_i + c, :] = KV[.., i, h, p_i + c, :] for
+    c < kept_i.  kv: [planes, B, H, cap, D] (any dtype; bytes are copied).
+    Returns (KV', defined [B, cap] bool): the positions whose value is specified."""
+    out = np.zeros_like(kv)
+    B, cap = kv.shape[1], kv.shape[3]
+    defined = np.zeros((B, cap), bool)
+    for i in range(B):
+        c = int(kept[i])
+        if c <= 0:
+            continue
+        po, pn = int(pad_old[i]), int(pad_new[i])
+        out[:, i, :, pn:pn + c, :] = kv[:, i, :, po:po + c, :]
+        defined[i, pn:pn + c] = True
+    return out, defined
+
+
+def zero_pad_region(pad_old, pad_new, kept):
+    """ZERO_PADS flag: the old content columns that become pads, [p_i, p'_i) when
+    p'_i > p_i (rows with kept_i > 0).  Returns a list of (row, lo, hi)."""
+    res = []
+    for i in range(len(pad_old)):
+        if kept[i] > 0 and pad_new[i] > pad_old[i]:
+            res.append((i, int(pad_old[i]), int(pad_new[i])))
+    return res
+
+
+def copy_rows(src, dst, count, src_col=None, dst_col=None, src_row=None, dst_row=None):
+    """Generic row-mapped KV move (a3/a5): for every batch row i with count_i > 0 and
+    mapped rows >= 0: dst[dst_row_i][:, :, dst_col_i + c] = src[src_row_i][:, :, src_col_i + c]
+    for c < count_i.  src/dst are logical [rows][planes][H][cap][D] views.
+    dst is modified in place; the definition is out-of-place (src is read first)."""
+    src = np.array(src, copy=True)
+    for i in range(len(count)):
+        c = int(count[i])
+        sr = i if src_row is None else int(src_row[i])
+        dr = i if dst_row is None else int(dst_row[i])
+        if c <= 0 or sr < 0 or dr < 0:
+            continue
+        sc = 0 if src_col is None else int(src_col[i])
+        dc = 0 if dst_col is None else int(dst_col[i])
+        dst[dr, :, :, dc:dc + c, :] = src[sr, :, :, sc:sc + c, :]
+    return dst
+
+
+def moved_bytes(pad_old, pad_new, kept, bpt):
+    """Algorithmic bytes of an in-place realign: 2 * kept_i * bpt over
+    rows whose padding changed (rows with Delta_i = 0 move nothing)."""
+    tot = 0
+    for i in range(len(kept)):
+        if kept[i] > 0 and pad_new[i] != pad_old[i]:
+            tot += 2 * int(kept[i]) * bpt
+    return tot

@@ -1,0 +1,118 @@
+"""Pins for oracle/pool.py (Alg. 3 GetBatch / RefillWindow; §3.2
+PAPER.md:532-537): SPEC worked examples, a library cross-check against Python's
+sorted(), brute-force partition properties, and toy-LM EXSpec equivalence."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle.loops import exspec_decode
+from oracle.pool import admission_order, form_batches, refill_window
+from oracle.toy_lm import ToyLM
+
+
+def test_form_batch_spec_examples():
+    # window lengths [5,5,3,5], B=2 -> same-length batch of two length-5 members
+    p = form_batches([5, 5, 3, 5], [1] * 4, [0, 1, 2, 3], W=4, B=2, min_group=2)
+    assert p["batches"][0] == [0, 1] and p["kind"][0] == 1
+    # [5,4,3], B=2 -> no group of size >= 2 -> fallback over [5,4]
+    p = form_batches([5, 4, 3], [1] * 3, [0, 1, 2], W=3, B=2, min_group=2)
+    assert p["batches"][0] == [0, 1] and p["kind"][0] == 0
+    # uniform lengths -> every batch same-length
+    p = form_batches([7] * 9, [1] * 9, list(range(9)), W=9, B=4, min_group=2)
+    assert all(p["kind"])
+
+
+def test_admission_and_window():
+    order = admission_order([5, 2, 9, 2], sort_by_length=True)
+    assert list(order) == [1, 3, 0, 2]          # ascending prompt length, ties by id
+    assert list(admission_order([5, 2, 9], False)) == [0, 1, 2]
+    assert refill_window([1, 0, 1, 1], order, 2) == [3, 0]
+
+
+def _reference_plan(lens, window, B, mg):
+    """Independent formulation: sort the window by the library sort on the key
+    (-group count, length, window position); walk it cutting batches."""
+    cnt = {l: sum(1 for s in window if lens[s] == l) for l in {lens[s] for s in window}}
+    pos = {s: t for t, s in enumerate(window)}
+    srt = sorted(window, key=lambda s: (-cnt[lens[s]], lens[s], pos[s]))
+    same, left = [], []
+    for l, grp in itertools.groupby(srt, key=lambda s: lens[s]):
+        grp = list(grp)
+        full = [grp[i:i + B] for i in range(0, len(grp), B)]
+        while full and len(full[-1]) < (1 if B == 1 else mg):
+            left += full.pop()
+        same += full
+    left = sorted(left, key=lambda s: pos[s])
+    return same + [left[i:i + B] for i in range(0, len(left), B)]
+
+
+def test_plan_matches_sorted_library_crosscheck():
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        N = int(rng.integers(1, 40))
+        lens = rng.integers(1, 6, N).tolist()
+        active = (rng.random(N) < 0.8).astype(int).tolist()
+        order = rng.permutation(N).tolist()
+        W = int(rng.integers(1, N + 1))
+        B = int(rng.integers(1, 9))
+        mg = int(rng.integers(2, max(3, B + 1))) if B > 1 else 2
+        mg = min(mg, B) if B > 1 else mg
+        p = form_batches(lens, active, order, W, B, mg)
+        assert p["batches"] == _reference_plan(lens, p["window"], B, mg)
+
+
+def test_brute_force_partition_properties():
+    """Every window of W <= 6 with lengths in {1,2,3} (SURVEY §4 tier 2)."""
+    for W in range(1, 7):
+        for lens in itertools.product([1, 2, 3], repeat=W):
+            for B, mg in [(1, 2), (2, 2), (3, 2), (4, 4), (8, 2)]:
+                p = form_batches(list(lens), [1] * W, list(range(W)), W, B, mg)
+                members = [s for b in p["batches"] for s in b]
+                assert sorted(members) == list(range(W))                # partition
+                for b, kind, bl in zip(p["batches"], p["kind"], p["blen"]):
+                    assert 1 <= len(b) <= B
+                    assert b == sorted(b)                               # window order
+                    assert kind == (len({lens[s] for s in b}) == 1)
+                    assert bl == max(lens[s] for s in b)
+                c = p["counters"]
+                assert c[0] == len(p["batches"]) and c[1] == sum(p["kind"])
+
+
+def test_grouping_rate_collapses_with_batch_size():
+    """grouping rates collapse as batch size grows (random lengths)."""
+    rng = np.random.default_rng(5)
+    rates = {}
+    for B in (2, 8):
+        tot_same = tot = 0
+        for _ in range(50):
+            lens = rng.integers(60, 90, 64).tolist()
+            p = form_batches(lens, [1] * 64, list(range(64)), 32, B, B)
+            tot_same += p["counters"][1]
+            tot += p["counters"][0]
+        rates[B] = tot_same / tot
+    assert rates[8] < rates[2]
+
+
+@pytest.mark.parametrize("W,B,mg,seq,noise", [(4, 2, 2, False, 0.3), (6, 3, 2, True, 0.2),
+                                            (5, 5, 5, False, 0.0), (1, 1, 2, False, 0.3)])
+def test_exspec_equals_autoregressive_greedy(W, B, mg, seq, noise):
+    """Scheduling is semantically invisible."""
+    T = ToyLM(seed=7)
+    rng = np.random.default_rng(W * 10 + B)
+    prompts = [list(map(int, rng.integers(2, 32, size=int(l)))) for l in rng.integers(1, 12, 6)]
+    ref = [T.greedy_generate(p, 14, 1, 64) for p in prompts]
+    out, st = exspec_decode(T, T, prompts, 4, 14, 1, 64, W=W, B=B, min_group=mg,
+                            sequential=seq, noise=noise)
+    assert out == ref
+    assert st["verify_calls"] == st["batches"]
+
+
+def test_exspec_uniform_lengths_all_same_length():
+    """All-Mean analog: uniform prompt lengths and clone
+    drafts (uniform acceptance) -> grouping rate 1.0 and no realigned members."""
+    T = ToyLM(seed=7)
+    rng = np.random.default_rng(1)
+    prompts = [list(map(int, rng.integers(2, 32, size=6))) for _ in range(4)]
+    out, st = exspec_decode(T, T, prompts, 3, 8, -1, 64, W=4, B=2, min_group=2)
+    assert st["same_length"] == st["batches"] and st["realigned_members"] == 0
