@@ -1,0 +1,226 @@
+/*
+ * specdec.h -- C ABI of libspecdec.so: the per-round hot path of batch speculative
+ * decoding (EqSpec / EXSpec, arXiv 2510.22876) on NVIDIA B200 (sm_100a).
+ *
+ * Conventions (all entry points)
+ *  - Every compute call is ASYNCHRONOUS on the caller's CUDA stream (`stream`, a
+ *    cudaStream_t; NULL = legacy default stream).  It never allocates, never
+ *    synchronises the host and never copies device->host.  It is stateless and
+ *    thread-safe for disjoint buffers.
+ *  - Pointers named `d_*` are DEVICE pointers owned by the caller; they must stay
+ *    valid until the stream reaches the call.  Scalars are passed by value.
+ *  - Token ids, positions and masks are int64 (HuggingFace layout); lengths, pads,
+ *    counts are int32; flags are uint8.
+ *  - Return value: SPECDEC_OK (0) or a negative SPECDEC_ERR_* detected on the host
+ *    from the arguments alone (nothing is launched on error).  Errors that depend
+ *    on device data are OR-ed into the optional device word `d_status` (bits
+ *    SPECDEC_ST_*) without any synchronisation; the affected row/item is skipped.
+ *
+ * Notation (Alg. 1-3): a batch row i holds n_i content tokens
+ * right-aligned at width L (left pads p_i = L - n_i); its last content token is
+ * "pending" (no KV yet).  The verify forward appends k+1 KV entries,
+ * so row i's valid KV after it is [p_i, L + a_i) and kept_i = n_i + a_i.
+ */
+#ifndef SPECDEC_H_
+#define SPECDEC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *specdec_stream_t; /* == cudaStream_t */
+
+/* host-detected errors */
+#define SPECDEC_OK 0
+#define SPECDEC_ERR_ARG (-1)      /* null / misaligned pointer, k < 1, bad flag, unsupported stride */
+#define SPECDEC_ERR_SHAPE (-2)    /* inconsistent sizes (e.g. V < 1, row_stride < V, W < 1) */
+#define SPECDEC_ERR_DTYPE (-3)    /* unknown dtype code */
+#define SPECDEC_ERR_CAPACITY (-4) /* statically impossible capacity (e.g. cap < k + 2) */
+#define SPECDEC_ERR_CUDA (-5)     /* a CUDA launch/runtime error; see specdec_last_cuda_error() */
+
+/* element dtypes */
+#define SPECDEC_F32 0
+#define SPECDEC_F16 1
+#define SPECDEC_BF16 2
+
+/* device status bits (OR-ed into *d_status) */
+#define SPECDEC_ST_NAN 1u      /* a NaN logit was seen (the argmax is still defined: first NaN) */
+#define SPECDEC_ST_CAPACITY 2u /* a width / buffer bound would be exceeded; the row was skipped */
+#define SPECDEC_ST_KEPT 4u     /* a KV row range lies outside [0, cap); the item was skipped */
+
+/* specdec_realign_kv flags */
+#define SPECDEC_ZERO_PADS 1u /* also zero the old content columns that became pads */
+
+/* ------------------------------------------------------------------------------ misc */
+int specdec_version(void);                /* ABI version (major*100 + minor) */
+const char *specdec_last_cuda_error(void); /* message for the last SPECDEC_ERR_CUDA (thread-local) */
+
+/* Bytes of the device workspace specdec_verify needs for (B, k).  The workspace must be
+ * zero-filled ONCE when allocated; every completed specdec_verify leaves it zeroed again
+ * (self-cleaning), so it can be reused by consecutive calls on one stream. */
+size_t specdec_verify_workspace_size(int64_t B, int64_t k);
+
+/* ------------------------------------------------------------------------------ a1
+ * specdec_verify -- Alg. 1 BatchVerify fused with the BatchRepad plan
+ * (Alg. 2 line "S, offset <- BatchRepad(S)").
+ *
+ *   pred[i][j] = argmax_v logits[i][j][v]      j = 0..k
+ *       ties -> lowest v; NaN ranks above +inf and the first NaN wins; +0 == -0.
+ *   a_i = first j < k with pred[i][j] != draft[i][j], else k   (R1)
+ *   b_i = pred[i][a_i]                                         (R2)
+ *   E_i = draft[i][0:a_i] ++ [b_i], cut after the first eos_id (eos_id >= 0) and to
+ *         budget[i] tokens (if d_budget); either cut sets finished_i; emit_i = |E_i|.
+ *   Plan (R6, R9): rows still active: n'_i = n_i + a_i + 1,
+ *         kept_i = n_i + a_i; finished rows: n'_i = 1, kept_i = 0;
+ *         L' = max n' over still-active rows (0 if none); p'_i = L' - n'_i.
+ *   Rows with d_active[i] == 0 yield a=0, b=pad_id, emit=0, finished=1.
+ *
+ * d_logits  [B][k+1][row_stride] of `dtype` (the k+1-row tail of the verify forward;
+ *           row j predicts draft slot j, row k the token after d_k).  16-B aligned,
+ *           row_stride*sizeof(dtype) % 16 == 0, row_stride >= V.
+ * d_draft   [B][k] int64; d_n [B] int32 (content lengths).
+ * d_active  [B] uint8, IN/OUT: rows to verify; on completion d_active[i] = !finished_i,
+ *           so a fixed-pointer round loop (or CUDA graph) carries it to the next round.
+ * d_budget  [B] int32 remaining new-token budget, or NULL (unbounded); IN/OUT: on
+ *           completion d_budget[i] = max(budget_i, 0) - emit_i.
+ * Outputs: d_accept [B] int32, d_bonus [B] int64, d_emit [B] int32, d_finished [B] uint8,
+ *          d_pred [B][k+1] int64 or NULL, d_plan_L [1] int32, d_n_new, d_pad_new,
+ *          d_kept [B] int32.
+ * d_ws: workspace of specdec_verify_workspace_size(B, k) bytes (see above).
+ * d_status: optional (NULL ok); SPECDEC_ST_NAN.
+ */
+int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_t k, int64_t V,
+                   int64_t row_stride, const int64_t *d_draft, const int32_t *d_n,
+                   uint8_t *d_active, int64_t eos_id, int64_t pad_id,
+                   int32_t *d_budget, int32_t *d_accept, int64_t *d_bonus,
+                   int32_t *d_emit, uint8_t *d_finished, int64_t *d_pred, int32_t *d_plan_L,
+                   int32_t *d_n_new, int32_t *d_pad_new, int32_t *d_kept, uint32_t *d_status,
+                   void *d_ws, size_t ws_bytes, specdec_stream_t stream);
+
+/* ------------------------------------------------------------------------------ a2
+ * specdec_rebuild_pos_mask -- Alg. 2 Phase 3 unpad-append-repad and
+ * the padding-agnostic positions / masks of §3.1, from specdec_verify's
+ * outputs, entirely on device (the new width L' is read from d_plan_L).
+ *
+ *   still-active row i: content' = tokens[i][p_i .. L) ++ draft[i][0:a_i] ++ [b_i]
+ *                       written at [p'_i, L'), pad_id on [0, p'_i);
+ *   finished row (R9):  content' = [pad_id] at L'-1 (a dummy length-1 row);
+ *   for c in [0, L'+k): mask[i][c] = (c >= p'_i); pos[i][c] = c >= p'_i ? c - p'_i : 0 (R7).
+ *   If d_out_buf: E_i (the first emit_i tokens of draft[i][0:a_i] ++ [b_i]) is appended
+ *   at d_out_buf[i][d_gen[i] ..] and d_gen[i] += emit_i.
+ *   If L' == 0 (every row finished) only the out_buf / gen update happens.
+ *
+ * d_tokens_in / d_tokens_out [B][cap_tok] int64 -- may be the SAME buffer (in place).
+ * d_n_old, d_pad_old [B] int32: the state before this round (L = pad_old + n_old).
+ * d_accept, d_bonus, d_emit, d_finished, d_plan_L, d_pad_new: specdec_verify outputs.
+ * d_draft [B][k] int64.  d_mask, d_pos [B][mp_stride] int64 (columns [0, L'+k) written).
+ * d_out_buf [B][max_new] int64 and d_gen [B] int32, or both NULL.
+ * d_status: SPECDEC_ST_CAPACITY if L' > cap_tok, L'+k > mp_stride or gen+emit > max_new.
+ */
+int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_tokens_out, int64_t B,
+                             int64_t cap_tok, int64_t k, int64_t pad_id,
+                             const int32_t *d_n_old, const int32_t *d_pad_old,
+                             const int64_t *d_draft, const int32_t *d_accept,
+                             const int64_t *d_bonus, const int32_t *d_emit,
+                             const uint8_t *d_finished, const int32_t *d_plan_L,
+                             const int32_t *d_pad_new, int64_t *d_mask, int64_t *d_pos,
+                             int64_t mp_stride, int64_t *d_out_buf, int32_t *d_gen,
+                             int64_t max_new, uint32_t *d_status, specdec_stream_t stream);
+
+/* ------------------------------------------------------------------------------ a3 / a5
+ * specdec_realign_kv -- KVCache <- Realign(KVCache, offset) (§3.1
+ * PAPER.md:447), and the EXSpec pool gather / write-back scatter (Alg. 3 PAPER.md:492,
+ * 505), as one row-mapped KV move:
+ *
+ *   for every batch row r in [0, n_rows) with cnt_r = count[r] + count_add > 0,
+ *   srow = src_row_map ? src_row_map[r] : r  (skipped if < 0), drow likewise,
+ *   scol = (src_col ? src_col[r] : 0) + src_col_add, dcol likewise,
+ *   and every plane (layer x {K,V}) and KV head h:
+ *       dst[plane, drow, h, dcol + c, :] = src[plane, srow, h, scol + c, :]   c < cnt_r
+ *
+ * EqSpec in place: kv_dst == kv_src, src_col = pad_old, dst_col = pad_new, count = kept.
+ * Rows whose source and destination coincide move nothing.  Each (plane, row, head)
+ * slab is streamed by one CTA in the hazard-free direction through a TMA bulk-copy
+ * (cp.async.bulk) shared-memory ring, so in-place shifts of either sign are exact.
+ * In-place calls (kv_dst == kv_src) must not pass row maps.  Distinct src/dst buffers
+ * must not overlap.
+ *
+ * dtype: SPECDEC_F16 / SPECDEC_BF16 / SPECDEC_F32 (only its size matters: bytes are copied).
+ * Layout: element (plane, row, head, pos, d) at base + plane*s_plane + row*s_row +
+ *   head*s_head + pos*D + d (strides in ELEMENTS; a KV row of D elements is contiguous
+ *   and D*elem % 16 == 0; base 16-B aligned; strides*elem multiples of 16).
+ * cap_src / cap_dst: position capacity of each buffer (scol+cnt <= cap_src and
+ *   dcol+cnt <= cap_dst, else SPECDEC_ST_KEPT and the row is skipped).
+ * flags: SPECDEC_ZERO_PADS (in place only): zero [scol, dcol) when dcol > scol.
+ * d_moved_bytes: optional uint64 accumulator of bytes read + written by this call.
+ */
+int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtype, int64_t n_planes,
+                       int64_t n_rows, int64_t H, int64_t D, int64_t src_s_plane,
+                       int64_t src_s_row, int64_t src_s_head, int64_t cap_src,
+                       int64_t dst_s_plane, int64_t dst_s_row, int64_t dst_s_head,
+                       int64_t cap_dst, const int32_t *d_src_col, int32_t src_col_add,
+                       const int32_t *d_dst_col, int32_t dst_col_add, const int32_t *d_count,
+                       int32_t count_add, const int32_t *d_src_row_map,
+                       const int32_t *d_dst_row_map, uint32_t flags,
+                       unsigned long long *d_moved_bytes, uint32_t *d_status,
+                       specdec_stream_t stream);
+
+/* ------------------------------------------------------------------------------ a4
+ * specdec_pool_group -- EXSpec GetBatch over a sliding window (Alg. 3 PAPER.md:488-494,
+ * 508; §3.2; readings R11-R14):
+ *
+ *   window  = the first W sequence ids s of d_order[0..N) with d_active[s] (RefillWindow);
+ *   lengths = d_len[s] (total tokens incl. the pending one; the grouping key, R13);
+ *   distinct lengths are visited by (-count, length); each length's members, in window
+ *   order, yield same-length batches of min(B, remaining) while remaining >= min_group
+ *   (>= 1 when B == 1); leftovers, in window order, form fallback batches of B.
+ *   bkind[b] = 1 iff all member lengths of batch b are equal.
+ *
+ * Outputs (nb_max = W batches at most):
+ *   d_window [W], d_window_size [1]; d_batch_of, d_slot_of [N] (-1 if not in the window);
+ *   d_members [W][B] sequence ids (-1 = empty slot); per slot: d_mlen [W][B] = len,
+ *   d_mpad [W][B] = blen - len, d_mactive [W][B] (1 = real member) -- i.e. each batch's
+ *   (n, p, active) arrays for specdec_verify / specdec_realign_kv;
+ *   d_bsize, d_bkind, d_blen [W]; d_n_batches [1];
+ *   d_counters [8] int64, ACCUMULATED (+=): {batches, same-length batches, members in
+ *   same-length batches, members in fallback batches, fallback member tokens, window
+ *   size, distinct lengths, 0}.
+ * Limits: 1 <= W <= 2048, 1 <= B <= W, 1 <= min_group; d_len values >= 1.
+ */
+int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order,
+                       int32_t N, int32_t W, int32_t B, int32_t min_group, int32_t *d_window,
+                       int32_t *d_window_size, int32_t *d_batch_of, int32_t *d_slot_of,
+                       int32_t *d_members, int32_t *d_mlen, int32_t *d_mpad,
+                       uint8_t *d_mactive, int32_t *d_bsize, uint8_t *d_bkind,
+                       int32_t *d_blen, int32_t *d_n_batches, int64_t *d_counters,
+                       specdec_stream_t stream);
+
+/* ------------------------------------------------------------------------------ a5
+ * specdec_pool_writeback -- Alg. 3 Phase 4: the pool-mode half of
+ * the repad step.  For every batch slot r with d_members[r] = s >= 0:
+ *   E_r = the first e_r tokens of draft[r][0:a_r] ++ [bonus_r], where
+ *         e_r = min(emit_r, max_new - gen_s)  (the per-sequence budget);
+ *   pool_tokens[s][len_s .. len_s+e_r) = E_r;  out_buf[s][gen_s .. gen_s+e_r) = E_r;
+ *   len_s += e_r; gen_s += e_r;
+ *   if finished_r or gen_s == max_new: active_s = 0 (isComplete -> Pool.deactivate).
+ * The KV write-back is a specdec_realign_kv scatter (fallback batches only: same-length
+ * batches were served zero-copy from the pool).
+ * d_pool_tokens [N][cap_tok] int64, d_out_buf [N][max_new] int64 (either may be NULL);
+ * max_new >= 1.  Pass d_budget = NULL to specdec_verify in pool mode.
+ * d_status: SPECDEC_ST_CAPACITY on overflow (row skipped).
+ */
+int specdec_pool_writeback(const int32_t *d_members, int64_t B, int64_t k,
+                           const int64_t *d_draft, const int32_t *d_accept,
+                           const int64_t *d_bonus,
+                           const int32_t *d_emit, const uint8_t *d_finished,
+                           int32_t *d_pool_len, int32_t *d_pool_gen, uint8_t *d_pool_active,
+                           int64_t *d_pool_tokens, int64_t cap_tok, int64_t *d_out_buf,
+                           int64_t max_new, uint32_t *d_status, specdec_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECDEC_H_ */

@@ -75,8 +75,8 @@ def emitted_tokens(draft_row, a: int, bonus: int, eos_id: int, budget: int | Non
     if eos_id >= 0 and eos_id in E:
         E = E[: E.index(eos_id) + 1]
         finished = True
-    if budget is not None and len(E) >= budget:
-        E = E[:budget]
+    if budget is not None and len(E) >= max(int(budget), 0):
+        E = E[:max(int(budget), 0)]
         finished = True
     return E, finished
 

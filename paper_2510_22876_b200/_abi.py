@@ -1,0 +1,159 @@
+"""Thin ctypes binding of libspecdec.so (include/specdec.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels behind
+the C ABI.  Functions keep the C names, take torch CUDA tensors (or None for nullable
+pointers) and launch on the current torch stream unless `stream` is given.  A missing
+library raises immediately -- there is no fallback of any kind.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspecdec.so")
+_lib = None
+
+OK, ERR_ARG, ERR_SHAPE, ERR_DTYPE, ERR_CAPACITY, ERR_CUDA = 0, -1, -2, -3, -4, -5
+ST_NAN, ST_CAPACITY, ST_KEPT = 1, 2, 4
+ZERO_PADS = 1
+DTYPE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+_U32 = ctypes.c_uint32
+_INT = ctypes.c_int
+
+_SIGS = {
+    "specdec_version": ([], _INT),
+    "specdec_last_cuda_error": ([], ctypes.c_char_p),
+    "specdec_verify_workspace_size": ([_I64, _I64], ctypes.c_size_t),
+    "specdec_verify": ([_P, _INT, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
+                        _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _INT),
+    "specdec_rebuild_pos_mask": ([_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P,
+                                  _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P], _INT),
+    "specdec_realign_kv": ([_P, _P, _INT, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
+                            _I64, _I64, _I64, _P, _I32, _P, _I32, _P, _I32, _P, _P, _U32, _P,
+                            _P, _P], _INT),
+    "specdec_pool_group": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
+                            _P, _P, _P, _P, _P, _P], _INT),
+    "specdec_pool_writeback": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
+                                _I64, _P, _P], _INT),
+}
+EXPORTS = tuple(_SIGS)
+
+
+class SpecdecError(RuntimeError):
+    pass
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load(path: str | None = None):
+    """Load libspecdec.so (once).  Raises if it is missing: the product has no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = path or _LIB_PATH
+    if not os.path.exists(p):
+        raise SpecdecError(f"{p} not built: run `python -m paper_2510_22876_b200.build` "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(p)
+    for name, (args, res) in _SIGS.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise SpecdecError("device pointer expected (CUDA tensor)")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(rc: int, name: str):
+    if rc != OK:
+        msg = {ERR_ARG: "ERR_ARG", ERR_SHAPE: "ERR_SHAPE", ERR_DTYPE: "ERR_DTYPE",
+               ERR_CAPACITY: "ERR_CAPACITY", ERR_CUDA: "ERR_CUDA"}.get(rc, str(rc))
+        if rc == ERR_CUDA:
+            msg += ": " + load().specdec_last_cuda_error().decode()
+        raise SpecdecError(f"{name} -> {msg}")
+
+
+def version() -> int:
+    return load().specdec_version()
+
+
+def specdec_verify_workspace_size(B: int, k: int) -> int:
+    return load().specdec_verify_workspace_size(B, k)
+
+
+def specdec_verify(logits, draft, n, active, accept, bonus, emit, finished, plan_L, n_new,
+                   pad_new, kept, ws, *, V=None, eos_id=-1, pad_id=0, budget=None, pred=None,
+                   status=None, stream=None):
+    """logits [B, k+1, row_stride] (fp32/fp16/bf16); see include/specdec.h."""
+    B, K1, rs = logits.shape
+    _check(load().specdec_verify(
+        _ptr(logits), DTYPE[logits.dtype], B, K1 - 1, rs if V is None else V, logits.stride(1),
+        _ptr(draft), _ptr(n), _ptr(active), eos_id, pad_id, _ptr(budget), _ptr(accept),
+        _ptr(bonus), _ptr(emit), _ptr(finished), _ptr(pred), _ptr(plan_L), _ptr(n_new),
+        _ptr(pad_new), _ptr(kept), _ptr(status), _ptr(ws), ws.numel() * ws.element_size(),
+        _stream(stream)), "specdec_verify")
+
+
+def specdec_rebuild_pos_mask(tokens_in, tokens_out, k, n_old, pad_old, draft, accept, bonus,
+                             emit, finished, plan_L, pad_new, mask, pos, *, pad_id=0,
+                             out_buf=None, gen=None, status=None, stream=None):
+    B, cap_tok = tokens_in.shape
+    _check(load().specdec_rebuild_pos_mask(
+        _ptr(tokens_in), _ptr(tokens_out), B, cap_tok, k, pad_id, _ptr(n_old), _ptr(pad_old),
+        _ptr(draft), _ptr(accept), _ptr(bonus), _ptr(emit), _ptr(finished), _ptr(plan_L),
+        _ptr(pad_new), _ptr(mask), _ptr(pos), mask.stride(0), _ptr(out_buf), _ptr(gen),
+        0 if out_buf is None else out_buf.shape[1], _ptr(status), _stream(stream)),
+        "specdec_rebuild_pos_mask")
+
+
+def specdec_realign_kv(kv_src, kv_dst, count, *, n_planes, n_rows, H, D, src_strides,
+                       dst_strides, cap_src, cap_dst, src_col=None, src_col_add=0,
+                       dst_col=None, dst_col_add=0, count_add=0, src_row_map=None,
+                       dst_row_map=None, flags=0, moved_bytes=None, status=None, stream=None):
+    """src/dst_strides = (s_plane, s_row, s_head) in elements; positions are D apart."""
+    _check(load().specdec_realign_kv(
+        _ptr(kv_src), _ptr(kv_dst), DTYPE[kv_src.dtype], n_planes, n_rows, H, D,
+        src_strides[0], src_strides[1], src_strides[2], cap_src, dst_strides[0],
+        dst_strides[1], dst_strides[2], cap_dst, _ptr(src_col), src_col_add, _ptr(dst_col),
+        dst_col_add, _ptr(count), count_add, _ptr(src_row_map), _ptr(dst_row_map), flags,
+        _ptr(moved_bytes), _ptr(status), _stream(stream)), "specdec_realign_kv")
+
+
+def specdec_pool_group(length, active, order, W, B, min_group, window, window_size, batch_of,
+                       slot_of, members, mlen, mpad, mactive, bsize, bkind, blen, n_batches,
+                       counters, *, stream=None):
+    _check(load().specdec_pool_group(
+        _ptr(length), _ptr(active), _ptr(order), length.numel(), W, B, min_group, _ptr(window),
+        _ptr(window_size), _ptr(batch_of), _ptr(slot_of), _ptr(members), _ptr(mlen), _ptr(mpad),
+        _ptr(mactive), _ptr(bsize), _ptr(bkind), _ptr(blen), _ptr(n_batches), _ptr(counters),
+        _stream(stream)), "specdec_pool_group")
+
+
+def specdec_pool_writeback(members, k, draft, accept, bonus, emit, finished, pool_len,
+                           pool_gen, pool_active, *, max_new, pool_tokens=None, out_buf=None,
+                           status=None, stream=None):
+    _check(load().specdec_pool_writeback(
+        _ptr(members), members.numel(), k, _ptr(draft), _ptr(accept), _ptr(bonus), _ptr(emit),
+        _ptr(finished), _ptr(pool_len), _ptr(pool_gen), _ptr(pool_active), _ptr(pool_tokens),
+        0 if pool_tokens is None else pool_tokens.shape[1], _ptr(out_buf), max_new,
+        _ptr(status), _stream(stream)), "specdec_pool_writeback")

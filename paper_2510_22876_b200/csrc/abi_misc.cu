@@ -1,0 +1,36 @@
+// abi_misc.cu -- version, error reporting and device-property cache for libspecdec.so.
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "host_util.h"
+
+namespace specdec {
+
+static thread_local std::string g_last_error;
+
+int record_cuda_error(cudaError_t e) {
+    g_last_error = cudaGetErrorString(e);
+    return SPECDEC_ERR_CUDA;
+}
+
+int device_sm_count() {
+    static std::mutex mu;
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache[dev] == 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
+}  // namespace specdec
+
+extern "C" int specdec_version(void) { return 100; }
+
+extern "C" const char *specdec_last_cuda_error(void) { return specdec::g_last_error.c_str(); }

@@ -1,0 +1,31 @@
+// host_util.h -- host-side helpers for the C ABI entry points.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "specdec.h"
+
+namespace specdec {
+
+int record_cuda_error(cudaError_t e);  // stores the message, returns SPECDEC_ERR_CUDA
+int device_sm_count();                 // SMs of the current device (cached per device)
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int dtype_size(int dtype) {
+    switch (dtype) {
+        case SPECDEC_F32: return 4;
+        case SPECDEC_F16: return 2;
+        case SPECDEC_BF16: return 2;
+        default: return 0;
+    }
+}
+
+inline int check_launch() {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPECDEC_OK : record_cuda_error(e);
+}
+
+}  // namespace specdec

@@ -1,0 +1,284 @@
+// realign.cu -- K2: KVCache <- Realign(KVCache, offset) (Alg. 2; §3.1
+// PAPER.md:447) and the EXSpec pool gather / write-back scatter (Alg. 3, PAPER.md:492,
+// 505) as one row-mapped KV move.
+//
+// Work item = one (plane, moving row, KV head) slab: `cnt` contiguous KV rows of D
+// elements (head_dim contiguous).  One single-warp CTA streams a slab through a ring of
+// shared-memory stages with TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP): a bulk
+// load lands a chunk and completes an mbarrier transaction, the same elected lane then
+// bulk-stores it to the destination.  In place, the slab is walked in the hazard-free
+// direction: right shifts (dst > src) from the top chunk down, left shifts from the
+// bottom up.  Chunk j's store can only overwrite bytes at or beyond its own source in
+// the walking direction -- bytes that were already loaded (chunks < j completed their
+// loads before j was stored) -- and never the source of a later chunk, so loads may run
+// STAGES-1 chunks ahead of the stores.  Slabs are disjoint, so CTAs never interact.
+// The chunk stream is continuous across a CTA's items, so small slabs (pool write-back)
+// stay pipelined too.  Rows whose source and destination coincide (Delta = 0) are
+// skipped: in place, they cost zero bytes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "host_util.h"
+
+namespace specdec {
+
+constexpr int kRealignMaxRows = 1024;
+constexpr int kZeroBytes = 2048;
+
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+struct RealignParams {
+    const char *src;
+    char *dst;
+    int64_t n_planes, n_rows, H;
+    int64_t rb;  // bytes per KV row (D * elem)
+    int64_t ss_plane, ss_row, ss_head, cap_src;  // src strides in bytes
+    int64_t ds_plane, ds_row, ds_head, cap_dst;  // dst strides in bytes
+    const int32_t *src_col, *dst_col, *count, *src_map, *dst_map;
+    int32_t src_col_add, dst_col_add, count_add;
+    uint32_t flags;
+    int inplace;
+    unsigned long long *moved;
+    uint32_t *status;
+};
+
+struct RowGeom {
+    int64_t src_off, dst_off, bytes;  // row-level offsets (plane 0, head 0), slab bytes
+};
+
+__device__ __forceinline__ bool row_geom(const RealignParams &p, int r, RowGeom &g, bool &bad) {
+    bad = false;
+    const int32_t cnt = p.count[r] + p.count_add;
+    if (cnt <= 0) return false;
+    const int32_t sr = p.src_map ? p.src_map[r] : r;
+    const int32_t dr = p.dst_map ? p.dst_map[r] : r;
+    if (sr < 0 || dr < 0) return false;
+    const int32_t sc = (p.src_col ? p.src_col[r] : 0) + p.src_col_add;
+    const int32_t dc = (p.dst_col ? p.dst_col[r] : 0) + p.dst_col_add;
+    if (sc < 0 || dc < 0 || sc + cnt > p.cap_src || dc + cnt > p.cap_dst) {
+        bad = true;
+        return false;
+    }
+    g.src_off = sr * p.ss_row + sc * p.rb;
+    g.dst_off = dr * p.ds_row + dc * p.rb;
+    g.bytes = static_cast<int64_t>(cnt) * p.rb;
+    if (p.inplace && g.src_off == g.dst_off) return false;  // Delta = 0: nothing moves
+    return true;
+}
+
+template <int STAGES, int CHUNK>
+struct RealignSmem {
+    alignas(128) unsigned char ring[STAGES][CHUNK];
+    alignas(128) unsigned char zeros[kZeroBytes];
+    uint64_t bar[STAGES];
+    char *st_dst[STAGES];
+    uint32_t st_bytes[STAGES];
+    char *st_zero[STAGES];      // zero-fill target after this chunk (item end), or null
+    int64_t st_zero_bytes[STAGES];
+    int32_t rows[kRealignMaxRows];
+    int32_t n_mv;
+};
+
+// Load-side iterator over this CTA's (item, chunk) stream.
+struct ChunkIter {
+    int64_t t, n_items, stride;
+    int64_t q, nchunks;
+    const char *s;
+    char *d;
+    int64_t bytes;
+    bool down;     // walk high -> low
+    char *zptr;    // zero-fill region at item end
+    int64_t zbytes;
+};
+
+template <int STAGES, int CHUNK>
+__device__ __forceinline__ void iter_item(const RealignParams &p, const RealignSmem<STAGES, CHUNK> &sm,
+                                          ChunkIter &it) {
+    // item -> (plane, moving row, head); head innermost
+    const int64_t head = it.t % p.H;
+    const int64_t mi = (it.t / p.H) % sm.n_mv;
+    const int64_t plane = it.t / (p.H * sm.n_mv);
+    RowGeom g;
+    bool bad;
+    row_geom(p, sm.rows[mi], g, bad);
+    it.s = p.src + plane * p.ss_plane + head * p.ss_head + g.src_off;
+    it.d = p.dst + plane * p.ds_plane + head * p.ds_head + g.dst_off;
+    it.bytes = g.bytes;
+    it.down = it.d > it.s;
+    it.nchunks = (g.bytes + CHUNK - 1) / CHUNK;
+    it.q = 0;
+    it.zptr = nullptr;
+    it.zbytes = 0;
+    if ((p.flags & SPECDEC_ZERO_PADS) && p.inplace && it.down) {
+        it.zptr = const_cast<char *>(it.s);
+        it.zbytes = it.d - it.s;
+    }
+}
+
+template <int STAGES, int CHUNK>
+__global__ void __launch_bounds__(32) realign_kernel(RealignParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    auto &sm = *reinterpret_cast<RealignSmem<STAGES, CHUNK> *>(smem_raw);
+    const int lane = threadIdx.x;
+
+    // ---- moving rows (warp ballot compaction, row order preserved)
+    bool any_bad = false;
+    int n_mv = 0;
+    for (int64_t base = 0; base < p.n_rows; base += 32) {
+        const int r = static_cast<int>(base) + lane;
+        RowGeom g;
+        bool bad = false, mv = false;
+        if (r < p.n_rows) mv = row_geom(p, r, g, bad);
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, mv);
+        if (mv) sm.rows[n_mv + __popc(bal & ((1u << lane) - 1u))] = r;
+        n_mv += __popc(bal);
+        any_bad |= bad;
+    }
+    any_bad = __any_sync(0xFFFFFFFFu, any_bad);
+    for (int z = lane * 16; z < kZeroBytes; z += 32 * 16)
+        *reinterpret_cast<uint4 *>(sm.zeros + z) = make_uint4(0, 0, 0, 0);
+    if (lane == 0) {
+        sm.n_mv = n_mv;
+        if (any_bad && blockIdx.x == 0 && p.status) atomicOr(p.status, SPECDEC_ST_KEPT);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&sm.bar[s], 1);
+        fence_mbar_init();
+    }
+    fence_proxy_async_smem();  // zero buffer (generic writes) visible to the bulk engine
+    __syncwarp();
+    if (lane != 0 || n_mv == 0) return;
+
+    const uint64_t pol = policy_evict_first();
+    ChunkIter it;
+    it.n_items = p.n_planes * static_cast<int64_t>(n_mv) * p.H;
+    it.stride = gridDim.x;
+    it.t = blockIdx.x;
+    if (it.t >= it.n_items) return;
+    iter_item<STAGES, CHUNK>(p, sm, it);
+    unsigned long long moved = 0;
+
+    auto issue = [&](int stage) {
+        int64_t off, nb;
+        if (!it.down) {
+            off = it.q * CHUNK;
+            nb = imin64(CHUNK, it.bytes - off);
+        } else {
+            const int64_t end = it.bytes - it.q * CHUNK;
+            off = imax64(0, end - CHUNK);
+            nb = end - off;
+        }
+        sm.st_dst[stage] = it.d + off;
+        sm.st_bytes[stage] = static_cast<uint32_t>(nb);
+        const bool last = (it.q + 1 == it.nchunks);
+        sm.st_zero[stage] = last ? it.zptr : nullptr;
+        sm.st_zero_bytes[stage] = last ? it.zbytes : 0;
+        if (last) moved += 2ull * static_cast<unsigned long long>(it.bytes);
+        mbar_arrive_expect_tx(&sm.bar[stage], static_cast<uint32_t>(nb));
+        bulk_load(sm.ring[stage], it.s + off, static_cast<uint32_t>(nb), &sm.bar[stage], pol);
+        // advance
+        if (++it.q == it.nchunks) {
+            it.t += it.stride;
+            if (it.t < it.n_items) iter_item<STAGES, CHUNK>(p, sm, it);
+        }
+    };
+    auto more = [&]() { return it.t < it.n_items; };
+
+    int64_t issued = 0;
+    while (issued < STAGES && more()) {
+        issue(static_cast<int>(issued % STAGES));
+        ++issued;
+    }
+    for (int64_t c = 0; c < issued; ++c) {
+        const int stage = static_cast<int>(c % STAGES);
+        mbar_wait(&sm.bar[stage], static_cast<uint32_t>((c / STAGES) & 1));
+        bulk_store(sm.st_dst[stage], sm.ring[stage], sm.st_bytes[stage], pol);
+        if (sm.st_zero[stage]) {
+            // ZERO_PADS: old content columns that became pads (this slab's last chunk is
+            // loaded, so its source bytes may now be overwritten)
+            char *z = sm.st_zero[stage];
+            for (int64_t zb = sm.st_zero_bytes[stage]; zb > 0;) {
+                const uint32_t nb = static_cast<uint32_t>(imin64(zb, kZeroBytes));
+                bulk_store(z, sm.zeros, nb, pol);
+                z += nb;
+                zb -= nb;
+            }
+        }
+        bulk_commit();
+        if (issued < c + STAGES && more()) {
+            // the stage to refill held chunk issued-STAGES <= c-1: its store group is not
+            // the newest one, so waiting until <= 1 group is still reading frees it
+            bulk_wait_read<1>();
+            issue(static_cast<int>(issued % STAGES));
+            ++issued;
+        }
+    }
+    bulk_wait_all<0>();
+    if (p.moved && moved) atomicAdd(p.moved, moved);
+}
+
+template <int STAGES, int CHUNK>
+int launch_realign(const RealignParams &p, int64_t max_items, cudaStream_t s) {
+    using Sm = RealignSmem<STAGES, CHUNK>;
+    const int smem = static_cast<int>(sizeof(Sm));
+    static bool attr_done = false;  // per-process; same for every device of one arch
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(realign_kernel<STAGES, CHUNK>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return record_cuda_error(e);
+        attr_done = true;
+    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, realign_kernel<STAGES, CHUNK>, 32, smem);
+    if (e != cudaSuccess) return record_cuda_error(e);
+    per_sm = std::max(1, per_sm);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_items, static_cast<int64_t>(device_sm_count()) * per_sm));
+    realign_kernel<STAGES, CHUNK><<<static_cast<unsigned>(grid), 32, smem, s>>>(p);
+    return check_launch();
+}
+
+}  // namespace specdec
+
+using namespace specdec;
+
+extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtype, int64_t n_planes,
+                                  int64_t n_rows, int64_t H, int64_t D, int64_t src_s_plane,
+                                  int64_t src_s_row, int64_t src_s_head, int64_t cap_src,
+                                  int64_t dst_s_plane, int64_t dst_s_row, int64_t dst_s_head,
+                                  int64_t cap_dst, const int32_t *d_src_col, int32_t src_col_add,
+                                  const int32_t *d_dst_col, int32_t dst_col_add,
+                                  const int32_t *d_count, int32_t count_add,
+                                  const int32_t *d_src_row_map, const int32_t *d_dst_row_map,
+                                  uint32_t flags, unsigned long long *d_moved_bytes,
+                                  uint32_t *d_status, specdec_stream_t stream) {
+    const int es = dtype_size(dtype);
+    if (es == 0) return SPECDEC_ERR_DTYPE;
+    if (!d_kv_src || !d_kv_dst || !d_count) return SPECDEC_ERR_ARG;
+    if (n_planes < 1 || n_rows < 1 || H < 1 || D < 1 || cap_src < 1 || cap_dst < 1) return SPECDEC_ERR_SHAPE;
+    if (n_rows > kRealignMaxRows) return SPECDEC_ERR_SHAPE;
+    if (flags & ~SPECDEC_ZERO_PADS) return SPECDEC_ERR_ARG;
+    const int64_t rb = D * es;
+    if (rb % 16 != 0 || !aligned16(d_kv_src) || !aligned16(d_kv_dst)) return SPECDEC_ERR_ARG;
+    const int64_t st[6] = {src_s_plane, src_s_row, src_s_head, dst_s_plane, dst_s_row, dst_s_head};
+    for (int64_t x : st)
+        if (x < 0 || (x * es) % 16 != 0) return SPECDEC_ERR_ARG;
+    const bool inplace = d_kv_src == d_kv_dst;
+    if (inplace && (d_src_row_map || d_dst_row_map)) return SPECDEC_ERR_ARG;
+    if (inplace && (src_s_plane != dst_s_plane || src_s_row != dst_s_row || src_s_head != dst_s_head))
+        return SPECDEC_ERR_ARG;
+    if ((flags & SPECDEC_ZERO_PADS) && !inplace) return SPECDEC_ERR_ARG;
+    RealignParams p;
+    p.src = static_cast<const char *>(d_kv_src);
+    p.dst = static_cast<char *>(d_kv_dst);
+    p.n_planes = n_planes; p.n_rows = n_rows; p.H = H; p.rb = rb;
+    p.ss_plane = src_s_plane * es; p.ss_row = src_s_row * es; p.ss_head = src_s_head * es; p.cap_src = cap_src;
+    p.ds_plane = dst_s_plane * es; p.ds_row = dst_s_row * es; p.ds_head = dst_s_head * es; p.cap_dst = cap_dst;
+    p.src_col = d_src_col; p.dst_col = d_dst_col; p.count = d_count;
+    p.src_map = d_src_row_map; p.dst_map = d_dst_row_map;
+    p.src_col_add = src_col_add; p.dst_col_add = dst_col_add; p.count_add = count_add;
+    p.flags = flags; p.inplace = inplace ? 1 : 0;
+    p.moved = d_moved_bytes; p.status = d_status;
+    const int64_t max_items = n_planes * n_rows * H;
+    return launch_realign<4, 16384>(p, max_items, reinterpret_cast<cudaStream_t>(stream));
+}

@@ -1,0 +1,120 @@
+"""EqSpec batch state and one verification round on device (Alg. 2).
+
+A round is three C-ABI calls on one stream with no host synchronisation:
+
+    specdec_verify            K1  Alg. 1 BatchVerify + the BatchRepad plan (L', p', kept)
+    specdec_rebuild_pos_mask  K3  unpad-append-repad of the tokens, positions, masks
+    specdec_realign_kv        K2  Realign(KVCache, offset), in place
+
+The per-row state (n, p) is double-buffered: round r reads slot r&1 and K1 writes the
+plan into slot 1-(r&1), which K3/K2 consume and round r+1 reads.  `active` and the
+remaining `budget` are updated in place by K1.  Everything is capacity-sized, so the
+data-dependent width L' never leaves the device.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _abi
+
+TORCH_DT = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}
+
+
+class EqSpecBatch:
+    def __init__(self, B, k, cap, layers, H, D, kv_dtype="bf16", device="cuda", max_new=0,
+                 eos_id=-1, pad_id=0, with_pred=False):
+        dev = torch.device(device)
+        i32, i64, u8 = torch.int32, torch.int64, torch.uint8
+        self.B, self.k, self.cap, self.layers, self.H, self.D = B, k, cap, layers, H, D
+        self.n_planes = 2 * layers
+        self.eos_id, self.pad_id, self.max_new = eos_id, pad_id, max_new
+        self.device = dev
+        self.tokens = torch.full((B, cap), pad_id, dtype=i64, device=dev)
+        self.mask = torch.zeros((B, cap + k), dtype=i64, device=dev)
+        self.pos = torch.zeros((B, cap + k), dtype=i64, device=dev)
+        self.n = torch.zeros((2, B), dtype=i32, device=dev)
+        self.pad = torch.zeros((2, B), dtype=i32, device=dev)
+        self.active = torch.ones(B, dtype=u8, device=dev)
+        self.budget = torch.full((B,), max_new, dtype=i32, device=dev) if max_new else None
+        self.gen = torch.zeros(B, dtype=i32, device=dev)
+        self.out_buf = torch.zeros((B, max_new), dtype=i64, device=dev) if max_new else None
+        self.accept = torch.zeros(B, dtype=i32, device=dev)
+        self.bonus = torch.zeros(B, dtype=i64, device=dev)
+        self.emit = torch.zeros(B, dtype=i32, device=dev)
+        self.finished = torch.zeros(B, dtype=u8, device=dev)
+        self.kept = torch.zeros(B, dtype=i32, device=dev)
+        self.plan_L = torch.zeros(1, dtype=i32, device=dev)
+        self.pred = torch.zeros((B, k + 1), dtype=i64, device=dev) if with_pred else None
+        self.status = torch.zeros(1, dtype=i32, device=dev)
+        self.moved = torch.zeros(1, dtype=i64, device=dev)
+        ws = _abi.specdec_verify_workspace_size(B, k)
+        self.ws = torch.zeros((ws + 7) // 8, dtype=i64, device=dev)
+        self.kv = torch.zeros((self.n_planes, B, H, cap, D), dtype=TORCH_DT[kv_dtype], device=dev)
+        self.cur = 0
+
+    # ----------------------------------------------------------------- state I/O
+    def load(self, tokens, lengths, kv=None):
+        """tokens [B, cap] left-padded at width L = max(lengths); kv [planes, B, H, cap, D]."""
+        lengths = torch.as_tensor(np.asarray(lengths), dtype=torch.int32)
+        L = int(lengths.max())
+        self.tokens.copy_(torch.as_tensor(tokens))
+        self.cur = 0
+        self.n[0].copy_(lengths)
+        self.pad[0].copy_(L - lengths)
+        self.active.fill_(1)
+        if self.budget is not None:
+            self.budget.fill_(self.max_new)
+        self.gen.zero_()
+        if kv is not None:
+            self.kv.copy_(kv)
+
+    @property
+    def n_cur(self):
+        return self.n[self.cur]
+
+    @property
+    def pad_cur(self):
+        return self.pad[self.cur]
+
+    @property
+    def kv_strides(self):
+        s = self.kv.stride()
+        return (s[0], s[1], s[2])
+
+    # ----------------------------------------------------------------- one round
+    def verify(self, logits, draft, stream=None):
+        c, nx = self.cur, 1 - self.cur
+        _abi.specdec_verify(logits, draft, self.n[c], self.active, self.accept, self.bonus,
+                            self.emit, self.finished, self.plan_L, self.n[nx], self.pad[nx],
+                            self.kept, self.ws, V=logits.shape[2] if self._V is None else self._V,
+                            eos_id=self.eos_id, pad_id=self.pad_id, budget=self.budget,
+                            pred=self.pred, status=self.status, stream=stream)
+
+    _V = None
+
+    def repad(self, draft, stream=None):
+        c, nx = self.cur, 1 - self.cur
+        _abi.specdec_rebuild_pos_mask(self.tokens, self.tokens, self.k, self.n[c], self.pad[c],
+                                      draft, self.accept, self.bonus, self.emit, self.finished,
+                                      self.plan_L, self.pad[nx], self.mask, self.pos,
+                                      pad_id=self.pad_id, out_buf=self.out_buf,
+                                      gen=self.gen if self.out_buf is not None else None,
+                                      status=self.status, stream=stream)
+
+    def realign(self, zero_pads=False, stream=None):
+        c, nx = self.cur, 1 - self.cur
+        _abi.specdec_realign_kv(self.kv, self.kv, self.kept, n_planes=self.n_planes,
+                                n_rows=self.B, H=self.H, D=self.D, src_strides=self.kv_strides,
+                                dst_strides=self.kv_strides, cap_src=self.cap, cap_dst=self.cap,
+                                src_col=self.pad[c], dst_col=self.pad[nx],
+                                flags=_abi.ZERO_PADS if zero_pads else 0,
+                                moved_bytes=self.moved, status=self.status, stream=stream)
+
+    def step(self, logits, draft, V=None, zero_pads=False, stream=None):
+        """One EqSpec round: K1 -> K3 -> K2 on `stream`; flips the (n, p) slot."""
+        self._V = V
+        self.verify(logits, draft, stream)
+        self.repad(draft, stream)
+        self.realign(zero_pads, stream)
+        self.cur = 1 - self.cur

@@ -1,0 +1,84 @@
+"""The C-ABI library loads and exports every symbol include/specdec.h declares, and its
+host-side argument validation rejects bad calls before any launch (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2510_22876_b200 import _abi
+from paper_2510_22876_b200 import build as B
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    B.build()
+    return _abi.load()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "specdec.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(specdec_\w+)\s*\(", src)))
+
+
+def test_header_symbols_exported(lib):
+    names = declared_symbols()
+    assert {"specdec_verify", "specdec_realign_kv", "specdec_rebuild_pos_mask",
+            "specdec_pool_group"} <= set(names)
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_abi.EXPORTS)
+
+
+def test_version_and_workspace(lib):
+    assert _abi.version() == 100
+    assert _abi.specdec_verify_workspace_size(8, 5) == 8 * 6 * 8 + 16
+    assert _abi.specdec_verify_workspace_size(0, 5) == 0
+
+
+def test_host_validation_without_gpu(lib):
+    L = lib
+    nz = ctypes.c_void_p(16)   # never dereferenced: validation fails first
+    # k < 1 -> ERR_ARG
+    rc = L.specdec_verify(nz, 2, 8, 0, 100, 100, *([nz] * 3), -1, 0, None, *([nz] * 4), None,
+                          *([nz] * 4), None, nz, 1 << 20, None)
+    assert rc == _abi.ERR_ARG
+    # unknown dtype
+    rc = L.specdec_verify(nz, 9, 8, 5, 100, 100, *([nz] * 3), -1, 0, None, *([nz] * 4), None,
+                          *([nz] * 4), None, nz, 1 << 20, None)
+    assert rc == _abi.ERR_DTYPE
+    # row_stride < V
+    rc = L.specdec_verify(nz, 2, 8, 5, 100, 50, *([nz] * 3), -1, 0, None, *([nz] * 4), None,
+                          *([nz] * 4), None, nz, 1 << 20, None)
+    assert rc == _abi.ERR_SHAPE
+    # misaligned row stride (bf16, 100 elements = 200 B, not a multiple of 16)
+    rc = L.specdec_verify(nz, 2, 8, 5, 100, 100, *([nz] * 3), -1, 0, None, *([nz] * 4), None,
+                          *([nz] * 4), None, nz, 1 << 20, None)
+    assert rc == _abi.ERR_ARG
+    # realign: D*elem not a multiple of 16
+    rc = L.specdec_realign_kv(nz, nz, 2, 2, 2, 2, 4, 64, 64, 64, 8, 64, 64, 64, 8, None, 0,
+                              None, 0, nz, 0, None, None, 0, None, None, None)
+    assert rc == _abi.ERR_ARG
+    # in place with row maps -> ERR_ARG
+    rc = L.specdec_realign_kv(nz, nz, 2, 2, 2, 2, 8, 64, 64, 64, 8, 64, 64, 64, 8, None, 0,
+                              None, 0, nz, 0, nz, None, 0, None, None, None)
+    assert rc == _abi.ERR_ARG
+    # pool_group: B > W
+    rc = L.specdec_pool_group(nz, nz, nz, 10, 4, 8, 2, *([nz] * 14))
+    assert rc == _abi.ERR_SHAPE
+    # rebuild: capacity statically impossible
+    rc = L.specdec_rebuild_pos_mask(nz, nz, 2, 4, 5, 0, *([nz] * 11), 64, None, None, 0, None, None)
+    assert rc == _abi.ERR_CAPACITY
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    saved = _abi._lib
+    try:
+        _abi._lib = None
+        with pytest.raises(_abi.SpecdecError):
+            _abi.load(str(tmp_path / "nope.so"))
+    finally:
+        _abi._lib = saved

@@ -1,0 +1,253 @@
+"""EqSpec round parity: K1 -> K3 -> K2 through the C ABI vs the oracle on the same bytes,
+over many rounds (tokens, masks, positions, output buffers, every valid KV entry, moved
+bytes), plus K2 alone under adversarial shift patterns and in gather/scatter mode."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import align as OA
+from oracle import verify as OV
+from paper_2510_22876_b200 import _abi
+from paper_2510_22876_b200.eqspec import EqSpecBatch
+from synth import workloads as W
+from tests.gpu_helpers import bits_to_torch, padded_logits, torch_to_bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos_id=-1,
+                zero_pads=False, full_check=True):
+    k, V = shape.k, shape.V
+    cap = W.derive_cap(shape.with_(B=B), rounds)
+    lengths = W.gen_lengths(shape, seed, B)
+    tokens = W.left_padded_tokens(lengths, cap, seed, V)
+    kvshape = (shape.n_planes, B, shape.H, cap, shape.D)
+    kv_bits = W.gen_kv_bits_np(seed, int(np.prod(kvshape))).reshape(kvshape)
+    bt = EqSpecBatch(B, k, cap, shape.layers, shape.H, shape.D, shape.kv_dtype, cuda,
+                     max_new=max_new, eos_id=eos_id, pad_id=W.PAD_ID)
+    bt.load(tokens, lengths, bits_to_torch(kv_bits, shape.kv_dtype, cuda))
+    # oracle state
+    tok_o, kv_o = tokens.copy(), kv_bits.copy()
+    n_o = lengths.astype(np.int32)
+    L = int(n_o.max())
+    pad_o = (L - n_o).astype(np.int32)
+    act_o = np.ones(B, np.uint8)
+    gen_o = np.zeros(B, np.int64)
+    out_o = [[] for _ in range(B)]
+    moved_expect = 0
+    for r in range(rounds):
+        if not act_o.any():
+            break
+        # synthetic verify forward: k+1 new KV entries at [L-1, L+k) on both sides
+        fwd = W.gen_kv_bits_np(seed + 1000 + r, shape.n_planes * B * shape.H * (k + 1) * shape.D)
+        fwd = fwd.reshape(shape.n_planes, B, shape.H, k + 1, shape.D)
+        kv_o[:, :, :, L - 1:L + k, :] = fwd
+        bt.kv[:, :, :, L - 1:L + k, :] = bits_to_torch(fwd, shape.kv_dtype, cuda)
+        rt = W.gen_round_truth(seed, r, B, k, V, pattern)
+        bits = W.gen_logits_np(seed, r, B, k, V, shape.logit_dtype)
+        lg = padded_logits(bits, shape.logit_dtype, cuda, extra=16)
+        draft = torch.from_numpy(rt.draft).to(cuda)
+        bt.step(lg, draft, V=V, zero_pads=zero_pads)
+        # oracle
+        budget = None if not max_new else (max_new - gen_o)
+        v = OV.batch_verify(bits, shape.logit_dtype, rt.draft, n_o, pad_o, act_o, eos_id, budget, W.PAD_ID)
+        tok_n, mask_n, pos_n = OA.repad_tokens(tok_o, cap, k, pad_o, L, v, W.PAD_ID)
+        kv_n, defined = OA.realign_kv(kv_o, pad_o, v["pad_new"], v["kept"])
+        moved_expect += OA.moved_bytes(pad_o, v["pad_new"], v["kept"], shape.bpt)
+        zero_regions = OA.zero_pad_region(pad_o, v["pad_new"], v["kept"])
+        for i in range(B):
+            out_o[i] += v["E"][i]
+        gen_o += v["emit"]
+        torch.cuda.synchronize()
+        # ---- compare
+        for key, g in (("accept", bt.accept), ("bonus", bt.bonus), ("emit", bt.emit),
+                       ("finished", bt.finished), ("kept", bt.kept)):
+            assert np.array_equal(g.cpu().numpy(), v[key]), (r, key)
+        Ln = v["L_new"]
+        assert int(bt.plan_L.item()) == Ln
+        assert np.array_equal(bt.pad_cur.cpu().numpy(), v["pad_new"]), r
+        assert np.array_equal(bt.n_cur.cpu().numpy(), v["n_new"]), r
+        assert int(bt.status.item()) == 0
+        if Ln > 0:
+            assert np.array_equal(bt.tokens[:, :Ln].cpu().numpy(), tok_n[:, :Ln]), r
+            assert np.array_equal(bt.mask[:, :Ln + k].cpu().numpy(), mask_n), r
+            assert np.array_equal(bt.pos[:, :Ln + k].cpu().numpy(), pos_n), r
+        if full_check:
+            kv_g = torch_to_bits(bt.kv)
+            for i in range(B):
+                cols = np.flatnonzero(defined[i])
+                if len(cols):
+                    assert np.array_equal(kv_g[:, i, :, cols], kv_n[:, i, :, cols]), (r, i)
+            if zero_pads:
+                for i, lo, hi in zero_regions:
+                    assert not kv_g[:, i, :, lo:hi].any(), (r, i)
+            kv_o = kv_n
+        if max_new:
+            gen_g = bt.gen.cpu().numpy()
+            assert np.array_equal(gen_g, gen_o)
+            ob = bt.out_buf.cpu().numpy()
+            for i in range(B):
+                assert list(ob[i, :gen_g[i]]) == out_o[i]
+        # advance oracle state
+        tok_o, n_o, pad_o, L = tok_n, v["n_new"], v["pad_new"], Ln
+        act_o = (v["finished"] == 0).astype(np.uint8)
+    assert int(bt.moved.item()) == moved_expect
+    return r + 1
+
+
+SMALL = W.Shape("small", 3001, 2, 2, 64, "bf16", "bf16", 8, 5, 160, 40, 160)
+SMALL16 = W.Shape("small16", 2003, 3, 1, 128, "fp16", "fp16", 6, 4, 300, 100, 300)
+
+
+@pytest.mark.parametrize("pattern", ["alpha", "alternating", "one_zero", "all_k", "all_0"])
+def test_rounds_small(cuda, pattern):
+    _run_rounds(cuda, SMALL, 8, 10, pattern)
+
+
+def test_rounds_toy_with_budget_and_finish(cuda):
+    n = _run_rounds(cuda, W.SHAPES["toy"], 2, 40, "alpha", max_new=20)
+    assert n < 40  # every row finished before the round cap
+
+
+@pytest.mark.parametrize("B", [1, 3, 8])
+def test_rounds_budget_staggered_finish(cuda, B):
+    # rows finish at different rounds -> the longest row can leave and L' shrinks
+    _run_rounds(cuda, SMALL16, B, 14, "alpha", seed=B, max_new=33)
+
+
+def test_rounds_zero_pads(cuda):
+    _run_rounds(cuda, SMALL, 8, 6, "alternating", zero_pads=True, seed=5)
+
+
+# ----------------------------------------------------------------------------- K2 alone
+def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, dtype="bf16", zero=False):
+    B = len(kept)
+    cap = cap or int(max(np.max(pad_old), np.max(pad_new)) + np.max(kept) + 4)
+    shp = (planes, B, H, cap, D)
+    bits = W.gen_kv_bits_np(7, int(np.prod(shp))).reshape(shp)
+    kv = bits_to_torch(bits, dtype, cuda)
+    t32 = lambda x: torch.as_tensor(np.asarray(x, np.int32), device=cuda)
+    moved = torch.zeros(1, dtype=torch.int64, device=cuda)
+    st = torch.zeros(1, dtype=torch.int32, device=cuda)
+    s = kv.stride()
+    _abi.specdec_realign_kv(kv, kv, t32(kept), n_planes=planes, n_rows=B, H=H, D=D,
+                            src_strides=s[:3], dst_strides=s[:3], cap_src=cap, cap_dst=cap,
+                            src_col=t32(pad_old), dst_col=t32(pad_new),
+                            flags=_abi.ZERO_PADS if zero else 0, moved_bytes=moved, status=st)
+    torch.cuda.synchronize()
+    g = torch_to_bits(kv)
+    o, defined = OA.realign_kv(bits, pad_old, pad_new, kept)
+    for i in range(B):
+        cols = np.flatnonzero(defined[i])
+        assert np.array_equal(g[:, i, :, cols], o[:, i, :, cols]), i
+        if pad_old[i] == pad_new[i]:
+            assert np.array_equal(g[:, i], bits[:, i])            # untouched
+    if zero:
+        for i, lo, hi in OA.zero_pad_region(pad_old, pad_new, kept):
+            assert not g[:, i, :, lo:hi].any()
+    elem = 2 if dtype != "fp32" else 4
+    assert int(moved.item()) == OA.moved_bytes(pad_old, pad_new, kept, planes * H * D * elem)
+    assert int(st.item()) == 0
+
+
+@pytest.mark.parametrize("D,dtype", [(128, "bf16"), (8, "bf16"), (64, "fp16"), (4, "fp32")])
+def test_realign_adversarial_shifts(cuda, D, dtype):
+    k = 5
+    big = 700  # 700 rows x 256 B = 175 KB -> many 16 KB chunks
+    cases = [
+        ([0] * 4, [k] * 4, [big, 300, 65, 1]),                 # all +k
+        ([k] * 4, [0] * 4, [big, 300, 65, 1]),                 # all -k
+        ([0, k, 0, k], [k, 0, k, 0], [big, big, 64, 63]),      # alternating
+        ([900, 3, 0, 7], [0, 3, 500, 6], [big, 40, big, 129]),  # large shifts, one Delta=0
+        ([1, 2, 3, 4], [2, 3, 4, 5], [1, 2, 3, 4]),            # tiny slabs
+    ]
+    for po, pn, kp in cases:
+        _realign_case(cuda, po, pn, kp, D=D, dtype=dtype)
+
+
+def test_realign_zero_pads_and_skips(cuda):
+    _realign_case(cuda, [0, 4, 2, 0], [3, 4, 0, 9], [50, 0, 70, 1000], zero=True)
+
+
+def test_realign_gather_scatter(cuda):
+    """Pool mode (a5): gather from a sequence-major pool into a plane-major staging
+    rectangle at right-aligned columns, then scatter a tail back (distinct buffers)."""
+    N, planes, H, cap, D = 6, 4, 2, 90, 64
+    B, cap_b = 3, 100
+    pool_bits = W.gen_kv_bits_np(11, N * planes * H * cap * D).reshape(N, planes, H, cap, D)
+    pool = bits_to_torch(pool_bits, "bf16", cuda)
+    stage = torch.zeros((planes, B, H, cap_b, D), dtype=torch.bfloat16, device=cuda)
+    members = np.array([4, 0, 2], np.int32)
+    lens = np.array([50, 81, 20], np.int32)
+    Lb = int(lens.max())
+    mpad = (Lb - lens).astype(np.int32)
+    t32 = lambda x: torch.as_tensor(np.asarray(x, np.int32), device=cuda)
+    ps, ss = pool.stride(), stage.stride()
+    # gather: pool[s, :, :, 0:len-1] -> stage[:, i, :, mpad_i : mpad_i + len - 1]
+    _abi.specdec_realign_kv(pool, stage, t32(lens), count_add=-1, n_planes=planes, n_rows=B, H=H, D=D,
+                            src_strides=(ps[1], ps[0], ps[2]), dst_strides=ss[:3], cap_src=cap,
+                            cap_dst=cap_b, dst_col=t32(mpad), src_row_map=t32(members))
+    torch.cuda.synchronize()
+    st = torch_to_bits(stage)
+    logical_pool = pool_bits.transpose(0, 1, 2, 3, 4)     # [rows][planes][H][cap][D]
+    exp = np.zeros((B, planes, H, cap_b, D), np.uint16)
+    OA.copy_rows(logical_pool, exp, count=lens - 1, src_row=members, dst_col=mpad)
+    for i in range(B):
+        c0, c1 = mpad[i], mpad[i] + lens[i] - 1
+        assert np.array_equal(st[:, i, :, c0:c1], exp[i][:, :, c0:c1])
+    # scatter: stage[:, i, :, Lb-1 : Lb+a_i] -> pool[s, :, :, len-1 : len+a_i]
+    acc = np.array([5, 0, 2], np.int32)
+    tail = W.gen_kv_bits_np(12, planes * B * H * 6 * D).reshape(planes, B, H, 6, D)
+    stage[:, :, :, Lb - 1:Lb + 5, :] = bits_to_torch(tail, "bf16", cuda)
+    _abi.specdec_realign_kv(stage, pool, t32(acc), count_add=1, n_planes=planes, n_rows=B, H=H, D=D,
+                            src_strides=ss[:3], dst_strides=(ps[1], ps[0], ps[2]), cap_src=cap_b,
+                            cap_dst=cap, src_col_add=Lb - 1, dst_col=t32(lens), dst_col_add=-1,
+                            dst_row_map=t32(members))
+    torch.cuda.synchronize()
+    pg = torch_to_bits(pool)
+    for i, s in enumerate(members):
+        lo = lens[i] - 1
+        assert np.array_equal(pg[s][:, :, lo:lo + acc[i] + 1], tail[:, i, :, :acc[i] + 1])
+        assert np.array_equal(pg[s][:, :, :lo], pool_bits[s][:, :, :lo])
+    untouched = [s for s in range(N) if s not in members]
+    assert np.array_equal(pg[untouched], pool_bits[untouched])
+
+
+# ----------------------------------------------------------------------------- full size
+@pytest.mark.parametrize("name", ["qwen3", "glm4", "vicuna"])
+def test_full_size_sampled(cuda, name):
+    """BASELINE.json full sizes in the bench's launch configuration: every integer output
+    of the round exactly; KV checked on a sample of (plane, row, head) slabs."""
+    shape = W.SHAPES[name]
+    B, k = shape.B, shape.k
+    rounds = 3
+    cap = W.derive_cap(shape, rounds)
+    lengths = W.gen_lengths(shape, 0, B)
+    tokens = W.left_padded_tokens(lengths, cap, 0, shape.V)
+    bt = EqSpecBatch(B, k, cap, shape.layers, shape.H, shape.D, shape.kv_dtype, cuda)
+    bt.load(tokens, lengths)
+    bt.kv.copy_(W.gen_kv_torch(0, bt.kv.shape, bt.kv.dtype, cuda))
+    rng = np.random.default_rng(0)
+    samples = [(int(rng.integers(shape.n_planes)), int(rng.integers(B)), int(rng.integers(shape.H)))
+               for _ in range(24)]
+    n_o = lengths.astype(np.int32)
+    pad_o = (n_o.max() - n_o).astype(np.int32)
+    act = np.ones(B, np.uint8)
+    for r in range(rounds):
+        before = {s: torch_to_bits(bt.kv[s[0], s[1], s[2]]) for s in samples}
+        rt = W.gen_round_truth(0, r, B, k, shape.V, "alpha")
+        lg = W.gen_logits_torch(0, r, B, k, shape.V, shape.logit_dtype, cuda)
+        bits = torch_to_bits(lg)
+        bt.step(lg, torch.from_numpy(rt.draft).to(cuda))
+        v = OV.batch_verify(bits, shape.logit_dtype, rt.draft, n_o, pad_o, act)
+        torch.cuda.synchronize()
+        assert np.array_equal(bt.accept.cpu().numpy(), v["accept"])
+        assert np.array_equal(bt.accept.cpu().numpy(), rt.accept)
+        assert np.array_equal(bt.bonus.cpu().numpy(), v["bonus"])
+        assert np.array_equal(bt.pad_cur.cpu().numpy(), v["pad_new"])
+        for (pl, i, h), old in before.items():
+            new = torch_to_bits(bt.kv[pl, i, h])
+            po, pn, kp = pad_o[i], v["pad_new"][i], v["kept"][i]
+            assert np.array_equal(new[pn:pn + kp], old[po:po + kp]), (r, pl, i, h)
+        n_o, pad_o = v["n_new"], v["pad_new"]
+    assert int(bt.status.item()) == 0
