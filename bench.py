@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""bench.py -- per-round hot path of batch speculative decoding on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen3|vicuna|glm4|toy]
+                    [--impl ours|reference]
+
+A step is one EqSpec verification round over one batch:
+specdec_verify (K1) -> specdec_rebuild_pos_mask (K3) -> specdec_realign_kv (K2, in
+place), on one stream, no host synchronisation.  Default workload: the Qwen3-8B-shaped
+KV (36 layers x 8 KV heads x 128, bf16), B=8, k=5, vocab 151936, contexts
+n_i ~ U[1536, 2048] (BASELINE.json north_star target config), alpha_i ~ U[0.5, 0.9].
+
+Inputs are synthetic (synth/): planted logits ring (16 buffers, > L2) + matching drafts,
+hashed KV over the full capacity.  `value` = rounds/s with inputs resident in HBM;
+`e2e` = the same rounds through the C ABI with each step's logits + drafts copied from
+pinned host memory and the step's (accept, bonus, emit) read back.  `--impl reference`
+times the CPU oracle (oracle/) on the same workload.  N > 1 runs independent replicas
+(one process per GPU; the EqSpec round does not shard -- DESIGN.md "Multi-GPU").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import workloads as W  # noqa: E402
+
+METRIC = "verify+realign rounds/s (B=8,k=5); KV-realign HBM GB/s vs ~8 TB/s peak"
+RING = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="qwen3", choices=["qwen3", "vicuna", "glm4", "toy"])
+    ap.add_argument("--B", type=int, default=0, help="override batch size")
+    ap.add_argument("--pattern", default="alpha", choices=list(W.ACCEPT_PATTERNS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy_ burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config_key):
+    """dram bytes per launch of K2 from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(config_key, {}).get("realign_dram_bytes_per_launch")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons while the timed region runs."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 -- clocks are reported as unavailable
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload
+def shape_for(args):
+    sh = W.SHAPES[args.config]
+    if args.B:
+        sh = sh.with_(B=args.B)
+    return sh
+
+
+def workload_name(sh, args):
+    return (f"{sh.name} EqSpec round: B={sh.B} k={sh.k} V={sh.V} KV {sh.layers}x{sh.H}x{sh.D} "
+            f"{sh.kv_dtype}, n~U[{sh.len_lo},{sh.len_hi}], accept={args.pattern}")
+
+
+class RoundBench:
+    """Device state + logits/draft ring for the timed EqSpec rounds."""
+
+    def __init__(self, sh, args, device, total_rounds):
+        import torch
+
+        from paper_2510_22876_b200.eqspec import EqSpecBatch
+        self.torch = torch
+        self.sh, self.dev = sh, device
+        B, k = sh.B, sh.k
+        self.cap = W.derive_cap(sh, total_rounds) if sh.name != "toy" else max(sh.cap, W.derive_cap(sh, total_rounds))
+        self.lengths = W.gen_lengths(sh, args.seed, B)
+        self.tokens = W.left_padded_tokens(self.lengths, self.cap, args.seed, sh.V)
+        self.bt = EqSpecBatch(B, k, self.cap, sh.layers, sh.H, sh.D, sh.kv_dtype, device)
+        self.bt.load(self.tokens, self.lengths)
+        self.bt.kv.copy_(W.gen_kv_torch(args.seed, self.bt.kv.shape, self.bt.kv.dtype, device))
+        self.logits = [W.gen_logits_torch(args.seed, r, B, k, sh.V, sh.logit_dtype, device)
+                       for r in range(RING)]
+        self.truth = [W.gen_round_truth(args.seed, r, B, k, sh.V, args.pattern) for r in range(RING)]
+        self.drafts = [torch.from_numpy(t.draft).to(device) for t in self.truth]
+        self.stream = torch.cuda.current_stream(device)
+
+    def reset(self):
+        self.bt.load(self.tokens, self.lengths)   # KV content is arbitrary; (n, p) restart
+
+    def step(self, r, ev=None):
+        bt, lg, d = self.bt, self.logits[r % RING], self.drafts[r % RING]
+        if ev is not None:
+            ev[0].record(self.stream)
+        bt.verify(lg, d)
+        if ev is not None:
+            ev[1].record(self.stream)
+        bt.repad(d)
+        if ev is not None:
+            ev[2].record(self.stream)
+        bt.realign()
+        if ev is not None:
+            ev[3].record(self.stream)
+        bt.cur = 1 - bt.cur
+
+    def mean_width(self):
+        return None
+
+
+def run_ours(args, rank, world, device):
+    import torch
+    import torch.distributed as dist
+
+    sh = shape_for(args)
+    total = args.warmup + args.steps + 2
+    rb = RoundBench(sh, args, device, total)
+    torch.cuda.synchronize()
+    for r in range(args.warmup):
+        rb.step(r)
+    torch.cuda.synchronize()
+    rb.reset()
+    for r in range(args.warmup):  # warm again from the reset state (same workload as timed)
+        rb.step(r)
+    rb.reset()
+    moved0 = int(rb.bt.moved.item())
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    widths = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(device.index if device.index is not None else 0)
+    with clocks:
+        t0.record(rb.stream)
+        for r in range(args.steps):
+            rb.step(r, evs[r])
+        t1.record(rb.stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    moved = int(rb.bt.moved.item()) - moved0
+    k1 = sum(e[0].elapsed_time(e[1]) for e in evs)
+    k3 = sum(e[1].elapsed_time(e[2]) for e in evs)
+    k2 = sum(e[2].elapsed_time(e[3]) for e in evs)
+    status = int(rb.bt.status.item())
+    mean_L = float(rb.bt.pad_cur.add(rb.bt.n_cur).max().item())
+    # ---- e2e: host buffers through the C ABI
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(rb, args, world)
+    # max over ranks
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    logits_bytes = sh.B * (sh.k + 1) * sh.V * (4 if sh.logit_dtype == "fp32" else 2)
+    return dict(sh=sh, ms=ms_max, moved=moved, k1_ms=k1, k3_ms=k3, k2_ms=k2, status=status,
+                clocks=clocks.summary(), e2e=e2e, end_width=mean_L, logits_bytes=logits_bytes)
+
+
+def run_e2e(rb, args, world):
+    """Each step: H2D of that step's logits + drafts from pinned host memory, the round,
+    D2H of (accept, bonus, emit).  Copies and kernels share the stream (serial)."""
+    import torch
+    import torch.distributed as dist
+    sh, dev = rb.sh, rb.dev
+    host_lg = [lg.cpu().pin_memory() for lg in rb.logits]
+    host_dr = [d.cpu().pin_memory() for d in rb.drafts]
+    dev_lg = torch.empty_like(rb.logits[0])
+    dev_dr = torch.empty_like(rb.drafts[0])
+    out_a = torch.empty((args.steps, sh.B), dtype=torch.int32).pin_memory()
+    out_b = torch.empty((args.steps, sh.B), dtype=torch.int64).pin_memory()
+    out_e = torch.empty((args.steps, sh.B), dtype=torch.int32).pin_memory()
+    bt = rb.bt
+
+    def one(r, i):
+        dev_lg.copy_(host_lg[r % RING], non_blocking=True)
+        dev_dr.copy_(host_dr[r % RING], non_blocking=True)
+        bt.step(dev_lg, dev_dr)
+        out_a[i].copy_(bt.accept, non_blocking=True)
+        out_b[i].copy_(bt.bonus, non_blocking=True)
+        out_e[i].copy_(bt.emit, non_blocking=True)
+
+    rb.reset()
+    for r in range(min(args.warmup, args.steps)):
+        one(r, r)
+    torch.cuda.synchronize()
+    rb.reset()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for r in range(args.steps):
+        one(r, r)
+    e1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # results are the method's: accept of the first step matches the planted answer
+    assert np.array_equal(out_a[0].numpy(), rb.truth[0].accept), "e2e accept mismatch"
+    h2d = rb.logits[0].numel() * rb.logits[0].element_size() + rb.drafts[0].numel() * 8
+    d2h = sh.B * (4 + 8 + 4)
+    return {"value": world * args.steps / (ms / 1e3), "unit": "rounds/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.steps, "wall_s": wall}
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_round_sample(sh, args, plane_sample=2, rounds=2, seed=0):
+    """Time the CPU oracle (never tuned) on the same workload: full verify over the
+    logits tail, full repad, realign over `plane_sample` of the 2*layers KV planes
+    (extrapolated linearly -- the realign is per-plane independent).  Returns rounds/s."""
+    from oracle import align as OA
+    from oracle import verify as OV
+    B, k = sh.B, sh.k
+    cap = W.derive_cap(sh, rounds + 2)
+    lengths = W.gen_lengths(sh, seed, B)
+    tokens = W.left_padded_tokens(lengths, cap, seed, sh.V)
+    P = min(plane_sample, sh.n_planes)
+    shp = (P, B, sh.H, cap, sh.D)
+    kv = W.gen_kv_bits_np(seed, int(np.prod(shp))).reshape(shp)
+    n = lengths.astype(np.int32)
+    L = int(n.max())
+    pad = (L - n).astype(np.int32)
+    act = np.ones(B, np.uint8)
+    tv = tr = tk = 0.0
+    for r in range(rounds):
+        bits = W.gen_logits_np(seed, r, B, k, sh.V, sh.logit_dtype)
+        rt = W.gen_round_truth(seed, r, B, k, sh.V, args.pattern)
+        a = time.perf_counter()
+        v = OV.batch_verify(bits, sh.logit_dtype, rt.draft, n, pad, act)
+        b = time.perf_counter()
+        tokens, _, _ = OA.repad_tokens(tokens, cap, k, pad, L, v)
+        c = time.perf_counter()
+        kv, _ = OA.realign_kv(kv, pad, v["pad_new"], v["kept"])
+        d = time.perf_counter()
+        tv, tr, tk = tv + b - a, tr + c - b, tk + d - c
+        n, pad, L = v["n_new"], v["pad_new"], v["L_new"]
+    per_round = (tv + tr + tk * sh.n_planes / P) / rounds
+    return 1.0 / per_round, dict(verify_s=tv / rounds, repad_s=tr / rounds,
+                                 realign_sample_s=tk / rounds, planes=P)
+
+
+def cpu_info():
+    model = platform.processor()
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, rank 0 only."""
+    if rank != 0:
+        return None
+    sh = shape_for(args)
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle_round_sample(sh, args, rounds=1)
+    n = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    rps, parts = oracle_round_sample(sh, args, rounds=n)
+    wall = time.perf_counter() - t0
+    sample = (f"{n} oracle rounds of the {sh.name} workload; verify + repad in full, realign on "
+              f"{parts['planes']} of {sh.n_planes} KV planes extrapolated x{sh.n_planes / parts['planes']:.0f}; "
+              f"numpy single-threaded on {cpu_info()}")
+    return {"impl": "reference", "metric": METRIC, "value": rps, "unit": "rounds/s",
+            "n_gpus": world, "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 / rps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": sh.kv_dtype,
+            "data": "synthetic", "config": {"workload": workload_name(sh, args)},
+            "cpu_baseline": {"value": rps, "unit": "rounds/s", "cores": 1, "kind": "oracle",
+                             "sample": sample, "parts_s": parts, "wall_s": wall},
+            "e2e": {"value": rps, "unit": "rounds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out))
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    res = run_ours(args, rank, world, device)
+    sh = res["sh"]
+    if rank == 0:
+        peak, peak_src = peaks()
+        value = world * args.steps / (res["ms"] / 1e3)
+        k2_launch_ms = res["k2_ms"] / args.steps
+        bytes_per_launch = res["moved"] / args.steps
+        achieved = bytes_per_launch / (k2_launch_ms / 1e3) / 1e9
+        traffic = ncu_traffic(f"{sh.name}_B{sh.B}")
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rps, parts = oracle_round_sample(sh, args, rounds=2)
+            cpu = {"value": rps, "unit": "rounds/s", "cores": 1, "kind": "oracle",
+                   "sample": (f"2 oracle rounds, verify+repad in full, realign on {parts['planes']} of "
+                              f"{sh.n_planes} planes extrapolated; numpy 1 thread; {cpu_info()}"),
+                   "parts_s": parts}
+        out = {
+            "metric": METRIC, "value": value, "unit": "rounds/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": sh.kv_dtype, "data": "synthetic",
+            "config": {"workload": workload_name(sh, args), "B": sh.B, "k": sh.k, "V": sh.V,
+                       "kv": f"{sh.layers}x{sh.H}x{sh.D} {sh.kv_dtype}", "cap": W.derive_cap(sh, args.warmup + args.steps + 2),
+                       "width_end": res["end_width"],
+                       "l2": f"inputs > L2: {RING}-buffer logits ring ({RING * res['logits_bytes'] / 1e6:.0f} MB) "
+                             f"and the KV cache (GB-scale); no flush needed",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "hbm", "kernel": "specdec_realign_kv (K2)", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "bytes_per_launch": bytes_per_launch, "launch_ms": k2_launch_ms},
+            "kernels_ms_per_step": {"verify_K1": res["k1_ms"] / args.steps,
+                                    "repad_K3": res["k3_ms"] / args.steps,
+                                    "realign_K2": k2_launch_ms},
+            "verify_logits_GBps": res["logits_bytes"] / (res["k1_ms"] / args.steps / 1e3) / 1e9,
+            "clocks": res["clocks"],
+            "e2e": res["e2e"],
+            "gpu_launches": 3 * args.steps,
+            "status": res["status"],
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -28,9 +28,10 @@ def padded_logits(bits: np.ndarray, dtype: str, device, extra: int = 0) -> torch
     which must never be read)."""
     B, K1, V = bits.shape
     t = bits_to_torch(bits, dtype, device)
-    if not extra:
+    ve = 4 if dtype == "fp32" else 8
+    if not extra and V % ve == 0:
         return t
-    rs = V + extra
+    rs = (V + extra + ve - 1) // ve * ve       # 16-byte aligned rows (specdec.h)
     out = torch.full((B, K1, rs), float("inf"), dtype=TDT[dtype], device=device)
     out[:, :, :V] = t
     return out
