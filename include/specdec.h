@@ -113,7 +113,9 @@ int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_t k, int64_
  *   at d_out_buf[i][d_gen[i] ..] and d_gen[i] += emit_i.
  *   If L' == 0 (every row finished) only the out_buf / gen update happens.
  *
- * d_tokens_in / d_tokens_out [B][cap_tok] int64 -- may be the SAME buffer (in place).
+ * d_tokens_in / d_tokens_out [B][cap_tok] int64 -- may be the SAME buffer (in place: one CTA
+ *   per row walks it in the hazard-free direction) or two buffers (ping-pong: every output
+ *   column is an independent gather, spread over many CTAs -- the fast path).
  * d_n_old, d_pad_old [B] int32: the state before this round (L = pad_old + n_old).
  * d_accept, d_bonus, d_emit, d_finished, d_plan_L, d_pad_new: specdec_verify outputs.
  * d_draft [B][k] int64.  d_mask, d_pos [B][mp_stride] int64 (columns [0, L'+k) written).

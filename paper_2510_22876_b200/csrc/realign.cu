@@ -222,17 +222,18 @@ template <int STAGES, int CHUNK>
 int launch_realign(const RealignParams &p, int64_t max_items, cudaStream_t s) {
     using Sm = RealignSmem<STAGES, CHUNK>;
     const int smem = static_cast<int>(sizeof(Sm));
-    static bool attr_done = false;  // per-process; same for every device of one arch
-    if (!attr_done) {
+    // attribute + occupancy once per process (one arch per process; also keeps these
+    // non-stream calls out of CUDA-graph capture after the first launch)
+    static int per_sm = 0;
+    if (per_sm == 0) {
         cudaError_t e = cudaFuncSetAttribute(realign_kernel<STAGES, CHUNK>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return record_cuda_error(e);
-        attr_done = true;
+        int occ = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, realign_kernel<STAGES, CHUNK>, 32, smem);
+        if (e != cudaSuccess) return record_cuda_error(e);
+        per_sm = std::max(1, occ);
     }
-    int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, realign_kernel<STAGES, CHUNK>, 32, smem);
-    if (e != cudaSuccess) return record_cuda_error(e);
-    per_sm = std::max(1, per_sm);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_items, static_cast<int64_t>(device_sm_count()) * per_sm));
     realign_kernel<STAGES, CHUNK><<<static_cast<unsigned>(grid), 32, smem, s>>>(p);
     return check_launch();

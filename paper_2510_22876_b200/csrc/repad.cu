@@ -9,6 +9,8 @@
 // columns at a time, reading the block into registers before any thread writes it.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "host_util.h"
 
@@ -106,6 +108,63 @@ __global__ void __launch_bounds__(kRepadThreads) repad_kernel(RepadParams p) {
     }
 }
 
+// Out-of-place variant (tokens_out != tokens_in): every output column is an independent
+// gather, so a row is spread over many CTAs with no ordering at all.
+//   c <  p'            : pad
+//   p' <= c < p' + n   : old token at column c - p' + p      (unpad + repad)
+//   p' + n <= c < L'   : E[c - p' - n]                        (append A ++ [B])
+constexpr int kRepadCols = 4;  // columns per thread
+__global__ void __launch_bounds__(kRepadThreads) repad_gather_kernel(RepadParams p) {
+    const int64_t i = blockIdx.y;
+    const int tid = threadIdx.x;
+    const int32_t Lnew = *p.plan_L;
+    const int32_t a = p.accept[i];
+    const int32_t em = p.emit[i];
+    const int64_t *d = p.draft + i * p.k;
+    const int64_t b = p.bonus[i];
+    if (blockIdx.x == 0 && p.out_buf && em > 0) {
+        const int32_t g = p.gen[i];
+        if (g + em > p.max_new) {
+            if (tid == 0 && p.status) atomicOr(p.status, SPECDEC_ST_CAPACITY);
+        } else {
+            if (tid < em) p.out_buf[i * p.max_new + g + tid] = emitted_token(d, a, b, tid);
+            __syncthreads();
+            if (tid == 0) p.gen[i] = g + em;
+        }
+    }
+    if (Lnew <= 0) return;
+    if (Lnew > p.cap_tok || Lnew + p.k > p.mp_stride) {
+        if (blockIdx.x == 0 && tid == 0 && p.status) atomicOr(p.status, SPECDEC_ST_CAPACITY);
+        return;
+    }
+    const int32_t pn = p.pad_new[i];
+    const bool fin = p.finished[i] != 0;
+    const int32_t po = p.pad_old[i];
+    const int32_t n = fin ? 0 : p.n_old[i];
+    const int64_t *src = p.tok_in + i * p.cap_tok;
+    int64_t *dst = p.tok_out + i * p.cap_tok;
+    int64_t *mrow = p.mask + i * p.mp_stride;
+    int64_t *prow = p.pos + i * p.mp_stride;
+    const int32_t W = Lnew + static_cast<int32_t>(p.k);
+    const int c0 = blockIdx.x * (kRepadThreads * kRepadCols) + tid;
+#pragma unroll
+    for (int u = 0; u < kRepadCols; ++u) {
+        const int c = c0 + u * kRepadThreads;
+        if (c >= W) break;
+        const bool content = c >= pn;
+        mrow[c] = content ? 1 : 0;
+        prow[c] = content ? c - pn : 0;
+        if (c < Lnew) {
+            int64_t t = p.pad_id;           // pads, and the dummy row of a finished row (R9)
+            if (!fin && content) {
+                const int32_t j = c - pn;
+                t = j < n ? src[po + j] : emitted_token(d, a, b, j - n);
+            }
+            dst[c] = t;
+        }
+    }
+}
+
 // ----------------------------------------------------------------------------- pool write-back
 // One CTA per batch slot r; E_r = first emit_r tokens of draft[r][0:a_r] ++ [bonus_r].
 __global__ void pool_writeback_kernel(const int32_t *members, int64_t k, const int64_t *draft,
@@ -173,8 +232,17 @@ extern "C" int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_t
     p.bonus = d_bonus; p.emit = d_emit; p.finished = d_finished; p.plan_L = d_plan_L;
     p.pad_new = d_pad_new; p.mask = d_mask; p.pos = d_pos; p.mp_stride = mp_stride;
     p.out_buf = d_out_buf; p.gen = d_gen; p.max_new = max_new; p.status = d_status;
-    repad_kernel<<<static_cast<unsigned>(B), kRepadThreads, 0,
-                   reinterpret_cast<cudaStream_t>(stream)>>>(p);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (d_tokens_in == d_tokens_out) {
+        // in place: one CTA walks each row in the hazard-free direction
+        repad_kernel<<<static_cast<unsigned>(B), kRepadThreads, 0, s>>>(p);
+    } else {
+        if (B > 65535) return SPECDEC_ERR_SHAPE;
+        const int64_t cols = std::max(cap_tok, mp_stride);
+        const int64_t per = static_cast<int64_t>(kRepadThreads) * kRepadCols;
+        dim3 grid(static_cast<unsigned>((cols + per - 1) / per), static_cast<unsigned>(B));
+        repad_gather_kernel<<<grid, kRepadThreads, 0, s>>>(p);
+    }
     return check_launch();
 }
 

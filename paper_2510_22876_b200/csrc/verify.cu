@@ -12,6 +12,9 @@
 
 #include <algorithm>
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "host_util.h"
 
@@ -159,65 +162,151 @@ __device__ void verify_epilogue(const VerifyParams &p) {
     }
 }
 
-template <int DT>
-__global__ void __launch_bounds__(kVerifyThreads) verify_kernel(VerifyParams p) {
-    using L = Lane<DT>;
+// Arrival on the grid-wide counter; the last CTA runs the epilogue.
+__device__ __forceinline__ void arrive_and_maybe_finish(const VerifyParams &p, int *s_last) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int total = gridDim.x * gridDim.y;
+        const unsigned int prev = atomicAdd(p.ws_counter, 1u);
+        *s_last = (prev == total - 1);
+    }
+    __syncthreads();
+    if (!*s_last) return;
+    __threadfence();
+    verify_epilogue(p);
+}
+
+__device__ __forceinline__ void cta_merge(const VerifyParams &p, int64_t row, unsigned long long best,
+                                          unsigned long long *s_red) {
+    const int tid = threadIdx.x;
+    best = warp_max_u64(best);
+    if ((tid & 31) == 0) s_red[tid >> 5] = best;
+    __syncthreads();
+    if (tid < kWarp) {
+        unsigned long long v = tid < kVerifyThreads / kWarp ? s_red[tid] : 0ull;
+        v = warp_max_u64(v);
+        if (tid == 0) {
+            atomicMax(p.ws_keys + row, v);
+            if ((v >> 32) == 0xFFFFFFFFull && p.status) atomicOr(p.status, SPECDEC_ST_NAN);
+        }
+    }
+}
+
+// fp32 logits (toy config): per-element keys, strict '>' in ascending index order.
+__global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams p) {
+    using L = Lane<SPECDEC_F32>;
     constexpr int VE = L::VE;
-    constexpr int ES = 16 / VE;
     __shared__ unsigned long long s_red[kVerifyThreads / kWarp];
     __shared__ int s_last;
     const int tid = threadIdx.x;
     const int64_t row = blockIdx.y;
     const int64_t i = row / (p.k + 1);
     if (p.active[i]) {
-        const char *rowp = static_cast<const char *>(p.logits) + row * p.row_stride * ES;
+        const char *rowp = static_cast<const char *>(p.logits) + row * p.row_stride * 4;
         const int64_t v0 = static_cast<int64_t>(blockIdx.x) * p.chunk;
         const int64_t v1 = min(p.V, v0 + p.chunk);
-        const int64_t vec_end = v1 / VE;  // full vectors only
+        const int64_t vec_end = v1 / VE;
         uint32_t bk = 0, bi = 0;
-        constexpr int U = 4;
-        for (int64_t vb = v0 / VE + tid; vb < vec_end; vb += U * kVerifyThreads) {
-            uint4 w[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t vv = vb + u * kVerifyThreads;
-                if (vv < vec_end) w[u] = ld_stream_v4(rowp + vv * 16);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int64_t vv = vb + u * kVerifyThreads;
-                if (vv < vec_end) L::scan(w[u], static_cast<uint32_t>(vv * VE), bk, bi);
-            }
-        }
-        // ragged tail (V % VE) -- only the chunk that ends at V has one
+        for (int64_t vb = v0 / VE + tid; vb < vec_end; vb += kVerifyThreads)
+            L::scan(ld_stream_v4(rowp + vb * 16), static_cast<uint32_t>(vb * VE), bk, bi);
         for (int64_t v = max(vec_end * VE, v0) + tid; v < v1; v += kVerifyThreads) {
             const uint32_t kk = L::key_at(rowp, v);
             if (kk > bk || (kk == bk && static_cast<uint32_t>(v) < bi)) { bk = kk; bi = static_cast<uint32_t>(v); }
         }
-        unsigned long long best = bk ? pack_key(bk, bi) : 0ull;
-        best = warp_max_u64(best);
-        if ((tid & 31) == 0) s_red[tid >> 5] = best;
-        __syncthreads();
-        if (tid < kWarp) {
-            unsigned long long v = tid < kVerifyThreads / kWarp ? s_red[tid] : 0ull;
-            v = warp_max_u64(v);
-            if (tid == 0) {
-                atomicMax(p.ws_keys + row, v);
-                if ((v >> 32) == 0xFFFFFFFFull && p.status) atomicOr(p.status, SPECDEC_ST_NAN);
-            }
+        cta_merge(p, row, bk ? pack_key(bk, bi) : 0ull, s_red);
+    }
+    arrive_and_maybe_finish(p, &s_last);
+}
+
+// 16-bit logits (fp16 / bf16): two passes over registers.
+//  pass 1: packed max with NaN propagation (HMNMX2, one instruction per 2 logits), reduced
+//          over the CTA -> M;
+//  pass 2: only threads whose own max equals M look for their first element whose key
+//          equals key(M) (keys make +0 == -0 and NaN == NaN); CTA min-index -> winner.
+// The CTA's (key(M), ~first index) joins the grid-wide atomicMax like every other path.
+template <bool BF16>
+struct H16 {
+    __device__ static uint32_t max2(uint32_t a, uint32_t b) {
+        if constexpr (BF16) {
+            __nv_bfloat162 r = __hmax2_nan(*reinterpret_cast<__nv_bfloat162 *>(&a), *reinterpret_cast<__nv_bfloat162 *>(&b));
+            return *reinterpret_cast<uint32_t *>(&r);
+        } else {
+            __half2 r = __hmax2_nan(*reinterpret_cast<__half2 *>(&a), *reinterpret_cast<__half2 *>(&b));
+            return *reinterpret_cast<uint32_t *>(&r);
         }
     }
-    // arrival: the last CTA of the grid runs the epilogue
-    if (tid == 0) {
-        __threadfence();
-        const unsigned int total = gridDim.x * gridDim.y;
-        const unsigned int prev = atomicAdd(p.ws_counter, 1u);
-        s_last = (prev == total - 1);
+    static constexpr uint32_t kExp = BF16 ? 0x7F80u : 0x7C00u;
+    static constexpr uint32_t kNegInf2 = BF16 ? 0xFF80FF80u : 0xFC00FC00u;
+};
+
+constexpr int kMaxVPT = 8;  // 16-byte vectors per thread
+
+template <bool BF16>
+__global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p) {
+    using T = H16<BF16>;
+    __shared__ unsigned long long s_red[kVerifyThreads / kWarp];
+    __shared__ uint32_t s_m[kVerifyThreads / kWarp];
+    __shared__ int s_last;
+    const int tid = threadIdx.x;
+    const int64_t row = blockIdx.y;
+    const int64_t i = row / (p.k + 1);
+    if (p.active[i]) {
+        const char *rowp = static_cast<const char *>(p.logits) + row * p.row_stride * 2;
+        const int64_t v0 = static_cast<int64_t>(blockIdx.x) * p.chunk;
+        const int64_t v1 = min(p.V, v0 + p.chunk);
+        const int64_t vec0 = v0 / 8, vec_end = v1 / 8;
+        uint4 w[kMaxVPT];
+#pragma unroll
+        for (int u = 0; u < kMaxVPT; ++u) {
+            const int64_t vv = vec0 + u * kVerifyThreads + tid;
+            w[u] = vv < vec_end ? ld_stream_v4(rowp + vv * 16)
+                                : make_uint4(T::kNegInf2, T::kNegInf2, T::kNegInf2, T::kNegInf2);
+        }
+        uint32_t m2 = T::kNegInf2;
+#pragma unroll
+        for (int u = 0; u < kMaxVPT; ++u)
+            m2 = T::max2(T::max2(m2, T::max2(w[u].x, w[u].y)), T::max2(w[u].z, w[u].w));
+        // ragged tail (V % 8): scalar elements folded into the pair max
+        const int64_t tail0 = max(vec_end * 8, v0);
+        for (int64_t v = tail0 + tid; v < v1; v += kVerifyThreads) {
+            const uint32_t x = reinterpret_cast<const uint16_t *>(rowp)[v];
+            m2 = T::max2(m2, x | (x << 16));
+        }
+        uint32_t m = T::max2(m2, (m2 >> 16) | (m2 << 16)) & 0xFFFFu;
+        const uint32_t my_m = m;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, m, o);
+            m = T::max2(m | (m << 16), y | (y << 16)) & 0xFFFFu;
+        }
+        if ((tid & 31) == 0) s_m[tid >> 5] = m;
+        __syncthreads();
+        m = s_m[0];
+#pragma unroll
+        for (int q = 1; q < kVerifyThreads / kWarp; ++q) m = T::max2(m | (m << 16), s_m[q] | (s_m[q] << 16)) & 0xFFFFu;
+        const uint32_t kM = key16(m, T::kExp);
+        uint32_t first = 0xFFFFFFFFu;
+        if (key16(my_m, T::kExp) == kM) {
+#pragma unroll
+            for (int u = 0; u < kMaxVPT; ++u) {
+                const int64_t vv = vec0 + u * kVerifyThreads + tid;
+                if (vv >= vec_end || first != 0xFFFFFFFFu) break;
+                const uint32_t e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (first == 0xFFFFFFFFu && key16(e[q] & 0xFFFFu, T::kExp) == kM) first = static_cast<uint32_t>(vv * 8 + 2 * q);
+                    if (first == 0xFFFFFFFFu && key16(e[q] >> 16, T::kExp) == kM) first = static_cast<uint32_t>(vv * 8 + 2 * q + 1);
+                }
+            }
+            if (first == 0xFFFFFFFFu) {
+                for (int64_t v = tail0 + tid; v < v1; v += kVerifyThreads)
+                    if (key16(reinterpret_cast<const uint16_t *>(rowp)[v], T::kExp) == kM) { first = static_cast<uint32_t>(v); break; }
+            }
+        }
+        // every thread holding M contributes (key(M), ~first); max -> lowest index
+        cta_merge(p, row, first != 0xFFFFFFFFu ? pack_key(kM, first) : 0ull, s_red);
     }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    verify_epilogue(p);
+    arrive_and_maybe_finish(p, &s_last);
 }
 
 }  // namespace specdec
@@ -259,22 +348,23 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
     p.ws_keys = static_cast<unsigned long long *>(d_ws);
     p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
 
-    // chunk: aim for >= 6 CTAs per SM over the whole tail, 1..8 vectors per thread
+    // chunk: 16-bit paths hold up to kMaxVPT vectors per thread in registers; aim for
+    // >= 4 CTAs per SM over the whole tail.  fp32 (toy) uses one vector per step.
     const int VE = 16 / es;
     const int64_t rows = B * (k + 1);
     const int64_t quantum = static_cast<int64_t>(kVerifyThreads) * VE;
-    const int64_t target_ctas = 6ll * device_sm_count();
+    const int64_t target_ctas = 4ll * device_sm_count();
     int64_t chunk = (V * rows + target_ctas - 1) / target_ctas;
     chunk = (chunk + quantum - 1) / quantum * quantum;
-    chunk = std::max<int64_t>(quantum, std::min<int64_t>(chunk, quantum * 8));
+    chunk = std::max<int64_t>(quantum, std::min<int64_t>(chunk, quantum * (es == 2 ? kMaxVPT : 8)));
     p.chunk = chunk;
     const int64_t n_chunks = (V + chunk - 1) / chunk;
     dim3 grid(static_cast<unsigned>(n_chunks), static_cast<unsigned>(rows));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     switch (dtype) {
-        case SPECDEC_F32: verify_kernel<SPECDEC_F32><<<grid, kVerifyThreads, 0, s>>>(p); break;
-        case SPECDEC_F16: verify_kernel<SPECDEC_F16><<<grid, kVerifyThreads, 0, s>>>(p); break;
-        default: verify_kernel<SPECDEC_BF16><<<grid, kVerifyThreads, 0, s>>>(p); break;
+        case SPECDEC_F32: verify_kernel_f32<<<grid, kVerifyThreads, 0, s>>>(p); break;
+        case SPECDEC_F16: verify_kernel16<false><<<grid, kVerifyThreads, 0, s>>>(p); break;
+        default: verify_kernel16<true><<<grid, kVerifyThreads, 0, s>>>(p); break;
     }
     return check_launch();
 }

@@ -6,10 +6,12 @@ A round is three C-ABI calls on one stream with no host synchronisation:
     specdec_rebuild_pos_mask  K3  unpad-append-repad of the tokens, positions, masks
     specdec_realign_kv        K2  Realign(KVCache, offset), in place
 
-The per-row state (n, p) is double-buffered: round r reads slot r&1 and K1 writes the
-plan into slot 1-(r&1), which K3/K2 consume and round r+1 reads.  `active` and the
-remaining `budget` are updated in place by K1.  Everything is capacity-sized, so the
-data-dependent width L' never leaves the device.
+The small per-row state (n, p, tokens) is double-buffered: round r reads slot r&1 and
+writes slot 1-(r&1), which round r+1 reads (the token rebuild is then a pure gather,
+spread over many CTAs).  The KV cache -- the only large state -- is realigned in place.
+`active` and the remaining `budget` are updated in place by K1.  Everything is
+capacity-sized, so the data-dependent width L' never leaves the device,
+and a round can be captured once per (parity, input buffer) as a CUDA graph.
 """
 from __future__ import annotations
 
@@ -30,7 +32,7 @@ class EqSpecBatch:
         self.n_planes = 2 * layers
         self.eos_id, self.pad_id, self.max_new = eos_id, pad_id, max_new
         self.device = dev
-        self.tokens = torch.full((B, cap), pad_id, dtype=i64, device=dev)
+        self.tok = torch.full((2, B, cap), pad_id, dtype=i64, device=dev)
         self.mask = torch.zeros((B, cap + k), dtype=i64, device=dev)
         self.pos = torch.zeros((B, cap + k), dtype=i64, device=dev)
         self.n = torch.zeros((2, B), dtype=i32, device=dev)
@@ -52,14 +54,17 @@ class EqSpecBatch:
         self.ws = torch.zeros((ws + 7) // 8, dtype=i64, device=dev)
         self.kv = torch.zeros((self.n_planes, B, H, cap, D), dtype=TORCH_DT[kv_dtype], device=dev)
         self.cur = 0
+        self.V = None
+        self.zero_pads = False
+        self._graphs = {}
 
     # ----------------------------------------------------------------- state I/O
     def load(self, tokens, lengths, kv=None):
         """tokens [B, cap] left-padded at width L = max(lengths); kv [planes, B, H, cap, D]."""
         lengths = torch.as_tensor(np.asarray(lengths), dtype=torch.int32)
         L = int(lengths.max())
-        self.tokens.copy_(torch.as_tensor(tokens))
         self.cur = 0
+        self.tok[0].copy_(torch.as_tensor(tokens))
         self.n[0].copy_(lengths)
         self.pad[0].copy_(L - lengths)
         self.active.fill_(1)
@@ -68,6 +73,10 @@ class EqSpecBatch:
         self.gen.zero_()
         if kv is not None:
             self.kv.copy_(kv)
+
+    @property
+    def tokens(self):
+        return self.tok[self.cur]
 
     @property
     def n_cur(self):
@@ -82,39 +91,66 @@ class EqSpecBatch:
         s = self.kv.stride()
         return (s[0], s[1], s[2])
 
-    # ----------------------------------------------------------------- one round
+    # ----------------------------------------------------------------- the three calls
     def verify(self, logits, draft, stream=None):
         c, nx = self.cur, 1 - self.cur
         _abi.specdec_verify(logits, draft, self.n[c], self.active, self.accept, self.bonus,
                             self.emit, self.finished, self.plan_L, self.n[nx], self.pad[nx],
-                            self.kept, self.ws, V=logits.shape[2] if self._V is None else self._V,
+                            self.kept, self.ws, V=self.V or logits.shape[2],
                             eos_id=self.eos_id, pad_id=self.pad_id, budget=self.budget,
                             pred=self.pred, status=self.status, stream=stream)
 
-    _V = None
-
     def repad(self, draft, stream=None):
         c, nx = self.cur, 1 - self.cur
-        _abi.specdec_rebuild_pos_mask(self.tokens, self.tokens, self.k, self.n[c], self.pad[c],
+        _abi.specdec_rebuild_pos_mask(self.tok[c], self.tok[nx], self.k, self.n[c], self.pad[c],
                                       draft, self.accept, self.bonus, self.emit, self.finished,
                                       self.plan_L, self.pad[nx], self.mask, self.pos,
                                       pad_id=self.pad_id, out_buf=self.out_buf,
                                       gen=self.gen if self.out_buf is not None else None,
                                       status=self.status, stream=stream)
 
-    def realign(self, zero_pads=False, stream=None):
+    def realign(self, stream=None):
         c, nx = self.cur, 1 - self.cur
         _abi.specdec_realign_kv(self.kv, self.kv, self.kept, n_planes=self.n_planes,
                                 n_rows=self.B, H=self.H, D=self.D, src_strides=self.kv_strides,
                                 dst_strides=self.kv_strides, cap_src=self.cap, cap_dst=self.cap,
                                 src_col=self.pad[c], dst_col=self.pad[nx],
-                                flags=_abi.ZERO_PADS if zero_pads else 0,
+                                flags=_abi.ZERO_PADS if self.zero_pads else 0,
                                 moved_bytes=self.moved, status=self.status, stream=stream)
 
-    def step(self, logits, draft, V=None, zero_pads=False, stream=None):
-        """One EqSpec round: K1 -> K3 -> K2 on `stream`; flips the (n, p) slot."""
-        self._V = V
+    def launch_round(self, logits, draft, stream=None):
+        """Enqueue K1 -> K3 -> K2 for the current parity (does not flip it)."""
         self.verify(logits, draft, stream)
         self.repad(draft, stream)
-        self.realign(zero_pads, stream)
+        self.realign(stream)
+
+    def step(self, logits, draft, V=None, zero_pads=False, stream=None):
+        """One EqSpec round on `stream`; flips the state parity."""
+        self.V, self.zero_pads = V, zero_pads
+        self.launch_round(logits, draft, stream)
+        self.cur = 1 - self.cur
+
+    # ----------------------------------------------------------------- CUDA graphs
+    def capture(self, inputs, V=None):
+        """Capture one graph per (parity, (logits, draft) pair): the round's three kernels
+        replay with a single launch.  `inputs` is a list of (logits, draft) tensors whose
+        storage must stay alive and fixed."""
+        self.V = V
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        saved = self.cur
+        with torch.cuda.stream(s):
+            for parity in (0, 1):
+                for j, (lg, d) in enumerate(inputs):
+                    g = torch.cuda.CUDAGraph()
+                    self.cur = parity
+                    with torch.cuda.graph(g, stream=s):
+                        self.launch_round(lg, d, stream=s)
+                    self._graphs[(parity, j)] = g
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self.cur = saved
+
+    def replay(self, j):
+        """One EqSpec round from input pair j via its captured graph; flips the parity."""
+        self._graphs[(self.cur, j)].replay()
         self.cur = 1 - self.cur
