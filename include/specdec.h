@@ -35,7 +35,7 @@ typedef struct CUstream_st *specdec_stream_t; /* == cudaStream_t */
 
 /* host-detected errors */
 #define SPECDEC_OK 0
-#define SPECDEC_ERR_ARG (-1)      /* null / misaligned pointer, k < 1, bad flag, unsupported stride */
+#define SPECDEC_ERR_ARG (-1)      /* null / misaligned pointer, k outside [1, 31], bad flag, unsupported stride */
 #define SPECDEC_ERR_SHAPE (-2)    /* inconsistent sizes (e.g. V < 1, row_stride < V, W < 1) */
 #define SPECDEC_ERR_DTYPE (-3)    /* unknown dtype code */
 #define SPECDEC_ERR_CAPACITY (-4) /* statically impossible capacity (e.g. cap < k + 2) */

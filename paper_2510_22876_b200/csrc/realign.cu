@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "host_util.h"
@@ -281,5 +282,20 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     p.flags = flags; p.inplace = inplace ? 1 : 0;
     p.moved = d_moved_bytes; p.status = d_status;
     const int64_t max_items = n_planes * n_rows * H;
-    return launch_realign<4, 16384>(p, max_items, reinterpret_cast<cudaStream_t>(stream));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    // pipeline shape (stages x chunk bytes); SPECDEC_REALIGN_CFG selects a variant for
+    // tuning sweeps (bench/profiles); the default is the measured best.
+    static int cfg = -1;
+    if (cfg < 0) {
+        const char *e = getenv("SPECDEC_REALIGN_CFG");
+        cfg = e ? atoi(e) : 0;
+    }
+    switch (cfg) {
+        case 1: return launch_realign<8, 8192>(p, max_items, s);
+        case 2: return launch_realign<3, 32768>(p, max_items, s);
+        case 3: return launch_realign<6, 16384>(p, max_items, s);
+        case 4: return launch_realign<12, 8192>(p, max_items, s);
+        case 5: return launch_realign<4, 8192>(p, max_items, s);
+        default: return launch_realign<4, 16384>(p, max_items, s);
+    }
 }

@@ -2,18 +2,20 @@
 // (§3.1).
 //
 // One pass over the logits tail [B][k+1][V]: every CTA scans one vocab chunk of one
-// (row, slot) with 128-bit streaming loads, reduces to a packed (key, ~index) 64-bit
-// maximum and merges it with one atomicMax (order-independent => bit-exact argmax with
-// lowest-index ties, first-NaN rule).  The last CTA to arrive (acq/rel counter) runs the
-// epilogue: first-mismatch scan (PAPER.md:304-306 with R1), bonus (R2), EOS/budget
-// trim (R10) and the repad plan (L', p', kept) -- no host round trip, no second launch.
-// The workspace is left zeroed for the next call.
+// (row, slot) with 128-bit streaming loads and reduces it to a packed (key, ~index)
+// 64-bit maximum, merged into the row's workspace word with one atomicMax.  The packing
+// makes "largest value, then lowest index" a plain unsigned max -- associative and
+// commutative -- so the split and the atomic order never change the winner: the argmax
+// is bit-exact with lowest-index ties, +0 == -0, and the first-NaN rule (R4, R5).
+// The last CTA to arrive (grid-wide counter) runs the epilogue, one warp per batch row:
+// first-mismatch scan by warp ballot (PAPER.md:304-306 with R1), bonus (R2), EOS /
+// budget trim (R10) and the repad plan (L', p', kept) -- no host round trip and no
+// second launch.  The workspace is left zeroed for the next call.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
-
-#include <cuda_bf16.h>
-#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "host_util.h"
@@ -21,6 +23,7 @@
 namespace specdec {
 
 constexpr int kVerifyThreads = 256;
+constexpr int kMaxK = 31;  // k + 1 <= 32: one lane per slot in the epilogue
 
 struct VerifyParams {
     const void *logits;
@@ -41,46 +44,6 @@ struct VerifyParams {
     unsigned int *ws_counter;      // [1]
 };
 
-// Elements per 16-byte vector and key function per dtype.
-template <int DT>
-struct Lane;
-template <>
-struct Lane<SPECDEC_F32> {
-    static constexpr int VE = 4;
-    __device__ static void scan(const uint4 &w, uint32_t base, uint32_t &bk, uint32_t &bi) {
-        const uint32_t e[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t kk = key32(e[q]);
-            if (kk > bk) { bk = kk; bi = base + q; }
-        }
-    }
-    __device__ static uint32_t key_at(const void *row, int64_t v) {
-        return key32(reinterpret_cast<const uint32_t *>(row)[v]);
-    }
-};
-template <uint32_t EXP1>
-struct Lane16 {
-    static constexpr int VE = 8;
-    __device__ static void scan(const uint4 &w, uint32_t base, uint32_t &bk, uint32_t &bi) {
-        const uint32_t e[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t lo = key16(e[q] & 0xFFFFu, EXP1);
-            if (lo > bk) { bk = lo; bi = base + 2 * q; }
-            const uint32_t hi = key16(e[q] >> 16, EXP1);
-            if (hi > bk) { bk = hi; bi = base + 2 * q + 1; }
-        }
-    }
-    __device__ static uint32_t key_at(const void *row, int64_t v) {
-        return key16(reinterpret_cast<const uint16_t *>(row)[v], EXP1);
-    }
-};
-template <>
-struct Lane<SPECDEC_F16> : Lane16<0x7C00u> {};
-template <>
-struct Lane<SPECDEC_BF16> : Lane16<0x7F80u> {};
-
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -90,73 +53,67 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     return v;
 }
 
+// ----------------------------------------------------------------------------- epilogue
 __device__ void verify_epilogue(const VerifyParams &p) {
     __shared__ int s_red[kVerifyThreads / kWarp];
-    const int tid = threadIdx.x;
-    const int64_t K1 = p.k + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int k = static_cast<int>(p.k);
+    const int K1 = k + 1;
     int local_max = 0;
-    for (int64_t i = tid; i < p.B; i += blockDim.x) {
-        int32_t a = 0, m = 0, nn = 1, kp = 0;
+    for (int64_t i = warp; i < p.B; i += nwarps) {
+        const bool act = p.active[i] != 0;
+        int a = 0, m = 0, nn = 1, kp = 0;
         int64_t b = p.pad_id;
-        uint8_t fin = 1;
-        if (p.active[i]) {
-            const int64_t *d = p.draft + i * p.k;
-            int64_t pr_a = -1;
-            a = static_cast<int32_t>(p.k);
+        bool fin = true;
+        int64_t pr = -1, d = -1;
+        if (lane < K1) pr = act ? static_cast<int64_t>(unpack_idx(__ldcg(p.ws_keys + i * K1 + lane))) : -1;
+        if (lane < k) d = p.draft[i * k + lane];
+        if (p.pred && lane < K1) p.pred[i * K1 + lane] = pr;
+        if (act) {
             // first mismatch; R1: all k match -> a = k
-            for (int64_t j = 0; j <= p.k; ++j) {
-                const int64_t pr = unpack_idx(__ldcg(p.ws_keys + i * K1 + j));
-                if (p.pred) p.pred[i * K1 + j] = pr;
-                if (j < p.k && a == p.k && pr != d[j]) a = static_cast<int32_t>(j);
-            }
-            pr_a = unpack_idx(__ldcg(p.ws_keys + i * K1 + a));
-            b = pr_a;  // bonus = pred at the first mismatch (R2)
-            // E = D[:a] ++ [b]; cut after the first EOS, then to the budget (R10)
+            const unsigned mism = __ballot_sync(0xFFFFFFFFu, lane < k && pr != d);
+            a = mism ? __ffs(mism) - 1 : k;
+            b = __shfl_sync(0xFFFFFFFFu, pr, a);  // bonus = pred at the first mismatch (R2)
+            // E = D[:a] ++ [b]: lane t < a holds D[t], lane a holds b; cut after the first EOS
+            const int64_t tok = lane < a ? d : b;
             m = a + 1;
-            fin = 0;
+            fin = false;
             if (p.eos_id >= 0) {
-                for (int32_t t = 0; t <= a; ++t) {
-                    const int64_t tok = t < a ? d[t] : b;
-                    if (tok == p.eos_id) { m = t + 1; fin = 1; break; }
-                }
+                const unsigned e = __ballot_sync(0xFFFFFFFFu, lane <= a && tok == p.eos_id);
+                if (e) { m = __ffs(e); fin = true; }
             }
-            if (p.budget) {
-                const int32_t bud = max(p.budget[i], 0);
-                if (m >= bud) { m = bud; fin = 1; }
-                p.budget[i] = bud - m;  // in/out: remaining budget after this round
+            if (p.budget) {  // then to the remaining budget (R10)
+                const int bud = max(p.budget[i], 0);
+                if (m >= bud) { m = bud; fin = true; }
+                if (lane == 0) p.budget[i] = bud - m;  // in/out
             }
             if (!fin) {
-                nn = p.n[i] + a + 1;
-                kp = p.n[i] + a;
+                nn = p.n[i] + a + 1;  // accepted + bonus
+                kp = p.n[i] + a;      // the bonus has no KV yet
                 local_max = max(local_max, nn);
             }
-        } else if (p.pred) {
-            for (int64_t j = 0; j <= p.k; ++j) p.pred[i * K1 + j] = -1;
         }
-        for (int64_t j = 0; j <= p.k; ++j) p.ws_keys[i * K1 + j] = 0ull;  // self-clean
-        p.accept[i] = a;
-        p.bonus[i] = b;
-        p.emit[i] = m;
-        p.finished[i] = fin;
-        p.active[i] = fin ? 0 : 1;  // in/out: rows still active after this round
-        p.n_new[i] = nn;
-        p.kept[i] = kp;
+        if (lane < K1) p.ws_keys[i * K1 + lane] = 0ull;  // self-clean
+        if (lane == 0) {
+            p.accept[i] = a;
+            p.bonus[i] = b;
+            p.emit[i] = m;
+            p.finished[i] = fin ? 1 : 0;
+            p.active[i] = fin ? 0 : 1;  // in/out: rows still active after this round
+            p.n_new[i] = nn;
+            p.kept[i] = kp;
+        }
     }
     // L' = max n' over still-active rows (R6 minimal padding)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local_max = max(local_max, __shfl_xor_sync(0xFFFFFFFFu, local_max, o));
-    if ((tid & 31) == 0) s_red[tid >> 5] = local_max;
+    if (lane == 0) s_red[warp] = local_max;
     __syncthreads();
-    if (tid < kWarp) {
-        int v = tid < blockDim.x / kWarp ? s_red[tid] : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
-        if (tid == 0) s_red[0] = v;
-    }
-    __syncthreads();
-    const int Lnew = s_red[0];
-    for (int64_t i = tid; i < p.B; i += blockDim.x) p.pad_new[i] = Lnew > 0 ? Lnew - p.n_new[i] : 0;
-    if (tid == 0) {
+    int Lnew = 0;
+    for (int w = 0; w < nwarps; ++w) Lnew = max(Lnew, s_red[w]);
+    for (int64_t i = threadIdx.x; i < p.B; i += blockDim.x) p.pad_new[i] = Lnew > 0 ? Lnew - p.n_new[i] : 0;
+    if (threadIdx.x == 0) {
         *p.plan_L = Lnew;
         *p.ws_counter = 0u;  // self-clean
     }
@@ -192,10 +149,9 @@ __device__ __forceinline__ void cta_merge(const VerifyParams &p, int64_t row, un
     }
 }
 
-// fp32 logits (toy config): per-element keys, strict '>' in ascending index order.
+// ----------------------------------------------------------------------------- fp32 (toy)
+// Per-element keys, strict '>' over ascending indices within a thread.
 __global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams p) {
-    using L = Lane<SPECDEC_F32>;
-    constexpr int VE = L::VE;
     __shared__ unsigned long long s_red[kVerifyThreads / kWarp];
     __shared__ int s_last;
     const int tid = threadIdx.x;
@@ -205,12 +161,19 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams
         const char *rowp = static_cast<const char *>(p.logits) + row * p.row_stride * 4;
         const int64_t v0 = static_cast<int64_t>(blockIdx.x) * p.chunk;
         const int64_t v1 = min(p.V, v0 + p.chunk);
-        const int64_t vec_end = v1 / VE;
+        const int64_t vec_end = v1 / 4;
         uint32_t bk = 0, bi = 0;
-        for (int64_t vb = v0 / VE + tid; vb < vec_end; vb += kVerifyThreads)
-            L::scan(ld_stream_v4(rowp + vb * 16), static_cast<uint32_t>(vb * VE), bk, bi);
-        for (int64_t v = max(vec_end * VE, v0) + tid; v < v1; v += kVerifyThreads) {
-            const uint32_t kk = L::key_at(rowp, v);
+        for (int64_t vb = v0 / 4 + tid; vb < vec_end; vb += kVerifyThreads) {
+            const uint4 w = ld_stream_v4(rowp + vb * 16);
+            const uint32_t e[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t kk = key32(e[q]);
+                if (kk > bk) { bk = kk; bi = static_cast<uint32_t>(vb * 4 + q); }
+            }
+        }
+        for (int64_t v = max(vec_end * 4, v0) + tid; v < v1; v += kVerifyThreads) {
+            const uint32_t kk = key32(reinterpret_cast<const uint32_t *>(rowp)[v]);
             if (kk > bk || (kk == bk && static_cast<uint32_t>(v) < bi)) { bk = kk; bi = static_cast<uint32_t>(v); }
         }
         cta_merge(p, row, bk ? pack_key(bk, bi) : 0ull, s_red);
@@ -218,17 +181,18 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams
     arrive_and_maybe_finish(p, &s_last);
 }
 
-// 16-bit logits (fp16 / bf16): two passes over registers.
-//  pass 1: packed max with NaN propagation (HMNMX2, one instruction per 2 logits), reduced
-//          over the CTA -> M;
-//  pass 2: only threads whose own max equals M look for their first element whose key
-//          equals key(M) (keys make +0 == -0 and NaN == NaN); CTA min-index -> winner.
-// The CTA's (key(M), ~first index) joins the grid-wide atomicMax like every other path.
+// ----------------------------------------------------------------------------- fp16 / bf16
+// Pass 1 streams the chunk keeping only a packed pair maximum with NaN propagation
+// (HMNMX2: one instruction per two logits), reduced over the CTA -> M.  Pass 2 runs only
+// in threads whose own maximum has key(M) (usually one): they re-read their elements
+// (L2-resident, 14.6 MB << 126 MB) and report the first one whose key equals key(M) --
+// keys make +0 == -0 and NaN == NaN, exactly the argmax equality of R4/R5.
 template <bool BF16>
 struct H16 {
     __device__ static uint32_t max2(uint32_t a, uint32_t b) {
         if constexpr (BF16) {
-            __nv_bfloat162 r = __hmax2_nan(*reinterpret_cast<__nv_bfloat162 *>(&a), *reinterpret_cast<__nv_bfloat162 *>(&b));
+            __nv_bfloat162 r = __hmax2_nan(*reinterpret_cast<__nv_bfloat162 *>(&a),
+                                           *reinterpret_cast<__nv_bfloat162 *>(&b));
             return *reinterpret_cast<uint32_t *>(&r);
         } else {
             __half2 r = __hmax2_nan(*reinterpret_cast<__half2 *>(&a), *reinterpret_cast<__half2 *>(&b));
@@ -239,7 +203,7 @@ struct H16 {
     static constexpr uint32_t kNegInf2 = BF16 ? 0xFF80FF80u : 0xFC00FC00u;
 };
 
-constexpr int kMaxVPT = 8;  // 16-byte vectors per thread
+constexpr int kVPT = 8;  // 16-byte vectors per thread, all in flight, kept in registers
 
 template <bool BF16>
 __global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p) {
@@ -255,25 +219,26 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p
         const int64_t v0 = static_cast<int64_t>(blockIdx.x) * p.chunk;
         const int64_t v1 = min(p.V, v0 + p.chunk);
         const int64_t vec0 = v0 / 8, vec_end = v1 / 8;
-        uint4 w[kMaxVPT];
+        // this thread's vectors: vec0 + tid + u*256, u < mine (<= kVPT by the host's chunk)
+        const int nvec = static_cast<int>(vec_end - vec0);
+        const int mine = nvec > tid ? (nvec - tid + kVerifyThreads - 1) / kVerifyThreads : 0;
+        const uint4 *vp = reinterpret_cast<const uint4 *>(rowp) + vec0 + tid;
+        uint4 w[kVPT];
 #pragma unroll
-        for (int u = 0; u < kMaxVPT; ++u) {
-            const int64_t vv = vec0 + u * kVerifyThreads + tid;
-            w[u] = vv < vec_end ? ld_stream_v4(rowp + vv * 16)
-                                : make_uint4(T::kNegInf2, T::kNegInf2, T::kNegInf2, T::kNegInf2);
-        }
+        for (int u = 0; u < kVPT; ++u)
+            w[u] = u < mine ? ld_stream_v4(vp + u * kVerifyThreads)
+                            : make_uint4(T::kNegInf2, T::kNegInf2, T::kNegInf2, T::kNegInf2);
         uint32_t m2 = T::kNegInf2;
 #pragma unroll
-        for (int u = 0; u < kMaxVPT; ++u)
+        for (int u = 0; u < kVPT; ++u)
             m2 = T::max2(T::max2(m2, T::max2(w[u].x, w[u].y)), T::max2(w[u].z, w[u].w));
-        // ragged tail (V % 8): scalar elements folded into the pair max
-        const int64_t tail0 = max(vec_end * 8, v0);
+        const int64_t tail0 = max(vec_end * 8, v0);  // ragged tail (V % 8), scalar
         for (int64_t v = tail0 + tid; v < v1; v += kVerifyThreads) {
             const uint32_t x = reinterpret_cast<const uint16_t *>(rowp)[v];
             m2 = T::max2(m2, x | (x << 16));
         }
-        uint32_t m = T::max2(m2, (m2 >> 16) | (m2 << 16)) & 0xFFFFu;
-        const uint32_t my_m = m;
+        const uint32_t my_m = T::max2(m2, (m2 >> 16) | (m2 << 16)) & 0xFFFFu;
+        uint32_t m = my_m;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, m, o);
@@ -287,23 +252,27 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p
         const uint32_t kM = key16(m, T::kExp);
         uint32_t first = 0xFFFFFFFFu;
         if (key16(my_m, T::kExp) == kM) {
+            // pass 2 over the registers, ascending index; an ordinary M (not NaN, not +-0)
+            // matches by exact bits, the special cases by key
+            const bool plain = (m & 0x7FFFu) != 0 && (m & 0x7FFFu) <= T::kExp;
 #pragma unroll
-            for (int u = 0; u < kMaxVPT; ++u) {
-                const int64_t vv = vec0 + u * kVerifyThreads + tid;
-                if (vv >= vec_end || first != 0xFFFFFFFFu) break;
+            for (int u = 0; u < kVPT; ++u) {
+                if (u >= mine || first != 0xFFFFFFFFu) break;
                 const uint32_t e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+                const uint32_t base = static_cast<uint32_t>((vec0 + tid + u * kVerifyThreads) * 8);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if (first == 0xFFFFFFFFu && key16(e[q] & 0xFFFFu, T::kExp) == kM) first = static_cast<uint32_t>(vv * 8 + 2 * q);
-                    if (first == 0xFFFFFFFFu && key16(e[q] >> 16, T::kExp) == kM) first = static_cast<uint32_t>(vv * 8 + 2 * q + 1);
+                    const uint32_t lo = e[q] & 0xFFFFu, hi = e[q] >> 16;
+                    const bool mlo = plain ? lo == m : key16(lo, T::kExp) == kM;
+                    const bool mhi = plain ? hi == m : key16(hi, T::kExp) == kM;
+                    if (first == 0xFFFFFFFFu && mlo) first = base + 2 * q;
+                    if (first == 0xFFFFFFFFu && mhi) first = base + 2 * q + 1;
                 }
             }
-            if (first == 0xFFFFFFFFu) {
-                for (int64_t v = tail0 + tid; v < v1; v += kVerifyThreads)
-                    if (key16(reinterpret_cast<const uint16_t *>(rowp)[v], T::kExp) == kM) { first = static_cast<uint32_t>(v); break; }
-            }
+            for (int64_t v = tail0 + tid; v < v1 && first == 0xFFFFFFFFu; v += kVerifyThreads)
+                if (key16(reinterpret_cast<const uint16_t *>(rowp)[v], T::kExp) == kM) first = static_cast<uint32_t>(v);
         }
-        // every thread holding M contributes (key(M), ~first); max -> lowest index
+        // every thread holding M contributes (key(M), ~first); the max picks the lowest index
         cta_merge(p, row, first != 0xFFFFFFFFu ? pack_key(kM, first) : 0ull, s_red);
     }
     arrive_and_maybe_finish(p, &s_last);
@@ -328,8 +297,9 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
                               specdec_stream_t stream) {
     const int es = dtype_size(dtype);
     if (es == 0) return SPECDEC_ERR_DTYPE;
-    if (B < 1 || k < 1 || V < 1 || row_stride < V || V > 0x7FFFFFFFll) return k < 1 ? SPECDEC_ERR_ARG : SPECDEC_ERR_SHAPE;
-    if (B > 65535 / (k + 1) + 0) return SPECDEC_ERR_SHAPE;  // gridDim.y limit
+    if (k < 1 || k > kMaxK) return SPECDEC_ERR_ARG;
+    if (B < 1 || V < 1 || row_stride < V || V > 0x7FFFFFFFll) return SPECDEC_ERR_SHAPE;
+    if (B * (k + 1) > 65535) return SPECDEC_ERR_SHAPE;  // gridDim.y
     if (!d_logits || !d_draft || !d_n || !d_active || !d_accept || !d_bonus || !d_emit ||
         !d_finished || !d_plan_L || !d_n_new || !d_pad_new || !d_kept || !d_ws)
         return SPECDEC_ERR_ARG;
@@ -348,15 +318,16 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
     p.ws_keys = static_cast<unsigned long long *>(d_ws);
     p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
 
-    // chunk: 16-bit paths hold up to kMaxVPT vectors per thread in registers; aim for
-    // >= 4 CTAs per SM over the whole tail.  fp32 (toy) uses one vector per step.
+    // one wave: about 4 CTAs per SM over the whole logits tail, chunks in multiples of
+    // one 16-byte vector per thread, so there is no tail wave and every SM streams.
     const int VE = 16 / es;
     const int64_t rows = B * (k + 1);
     const int64_t quantum = static_cast<int64_t>(kVerifyThreads) * VE;
     const int64_t target_ctas = 4ll * device_sm_count();
-    int64_t chunk = (V * rows + target_ctas - 1) / target_ctas;
-    chunk = (chunk + quantum - 1) / quantum * quantum;
-    chunk = std::max<int64_t>(quantum, std::min<int64_t>(chunk, quantum * (es == 2 ? kMaxVPT : 8)));
+    const int64_t per_row = std::max<int64_t>(1, target_ctas / rows);  // CTAs per (row, slot)
+    int64_t chunk = (V + per_row - 1) / per_row;
+    chunk = std::max<int64_t>(quantum, (chunk + quantum - 1) / quantum * quantum);
+    if (es == 2) chunk = std::min<int64_t>(chunk, quantum * kVPT);  // register-resident
     p.chunk = chunk;
     const int64_t n_chunks = (V + chunk - 1) / chunk;
     dim3 grid(static_cast<unsigned>(n_chunks), static_cast<unsigned>(rows));

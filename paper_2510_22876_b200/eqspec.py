@@ -119,10 +119,20 @@ class EqSpecBatch:
                                 moved_bytes=self.moved, status=self.status, stream=stream)
 
     def launch_round(self, logits, draft, stream=None):
-        """Enqueue K1 -> K3 -> K2 for the current parity (does not flip it)."""
-        self.verify(logits, draft, stream)
-        self.repad(draft, stream)
-        self.realign(stream)
+        """Enqueue K1 -> {K3 || K2} for the current parity (does not flip it).  K3 (tokens,
+        masks, positions) and K2 (KV) both depend only on K1's plan and touch disjoint
+        memory, so K3 runs on a side stream under K2; the main stream joins it at the end."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(self.device)
+            self._ev_plan, self._ev_rep = torch.cuda.Event(), torch.cuda.Event()
+        self.verify(logits, draft, s)
+        self._ev_plan.record(s)
+        self._side.wait_event(self._ev_plan)
+        self.repad(draft, self._side)
+        self._ev_rep.record(self._side)
+        self.realign(s)
+        s.wait_event(self._ev_rep)
 
     def step(self, logits, draft, V=None, zero_pads=False, stream=None):
         """One EqSpec round on `stream`; flips the state parity."""
