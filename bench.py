@@ -43,7 +43,13 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="qwen3", choices=["qwen3", "vicuna", "glm4", "toy"])
+    ap.add_argument("--config", default="qwen3", choices=["qwen3", "vicuna", "glm4", "toy", "pool"])
+    ap.add_argument("--pool-n", type=int, default=1024, help="pool: total sequences (all ranks)")
+    ap.add_argument("--pool-lengths", default="random", choices=["random", "uniform"])
+    ap.add_argument("--pool-W", type=int, default=0, help="pool: window (0 = whole shard, <= 2048)")
+    ap.add_argument("--min-group", type=int, default=2)
+    ap.add_argument("--max-new", type=int, default=256)
+    ap.add_argument("--shard", default="band", choices=["band", "strided"])
     ap.add_argument("--B", type=int, default=0, help="override batch size")
     ap.add_argument("--pattern", default="alpha", choices=list(W.ACCEPT_PATTERNS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -368,6 +374,135 @@ def cpu_info():
     return model
 
 
+def run_pool(args, rank, world, device):
+    """EXSpec pool (BASELINE.json configs[4]): N Qwen3-shaped sequences, band-sharded over
+    the ranks; each rank drains its shard (K4 plan, per batch gather / verify / write-back
+    / scatter); one NCCL all-gather of outputs + counters at the end.  value = sequences/s
+    over the whole job (max over ranks); strong scaling (N fixed)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_22876_b200.dist import gather_results, shard_bands, shard_strided
+    from paper_2510_22876_b200.exspec import SequencePool
+
+    sh = W.SHAPES["qwen3"]
+    k, V, B = sh.k, sh.V, sh.B
+    N = args.pool_n
+    rng_h = W.hash_np(args.seed, W.S_POOL, np.arange(N))
+    if args.pool_lengths == "uniform":
+        lens = np.full(N, 256, np.int32)                      # All-Mean analog (PAPER.md:700)
+    else:
+        lens = (64 + (rng_h % np.uint64(512 - 64 + 1)).astype(np.int64)).astype(np.int32)
+    order = np.array(sorted(range(N), key=lambda s: (int(lens[s]), s)), np.int32)  # sort on
+    shards = (shard_bands if args.shard == "band" else shard_strided)(order, world)
+    mine = shards[rank]
+    n_loc = len(mine)
+    cap = ((int(lens.max()) + args.max_new + k + 1) + 15) // 16 * 16
+    Wn = min(args.pool_W or n_loc, 2048, n_loc)
+    sp = SequencePool(n_loc, cap, sh.layers, sh.H, sh.D, k, W=Wn, B=min(B, Wn),
+                      min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False)
+    local_lens = lens[mine]
+    local_order = np.arange(n_loc)            # `mine` is already in admission order
+    ring_lg = [W.gen_logits_torch(args.seed, r, sp.B, k, V, sh.logit_dtype, device) for r in range(RING)]
+    ring_dr = [torch.from_numpy(W.gen_round_truth(args.seed, r, sp.B, k, V, args.pattern).draft).to(device)
+               for r in range(RING)]
+    ctr = {"i": 0}
+
+    def inputs(b):
+        j = ctr["i"] % RING
+        ctr["i"] += 1
+        return ring_lg[j], ring_dr[j]
+
+    def drain(events=None):
+        sp.load(local_lens, order=local_order)
+        sp.moved.zero_()
+        epochs = batches = 0
+        while True:
+            nb, kinds, blens, sizes = sp.plan()
+            if nb == 0:
+                break
+            epochs += 1
+            for b in range(nb):
+                lg, d = inputs(b)
+                if events is not None and not kinds[b]:
+                    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                    e[0].record()
+                    sp.gather(b)
+                    e[1].record()
+                    sp.verify(b, lg, d, V)
+                    sp.writeback(b, d)
+                    e[2].record()
+                    sp.scatter(b, blens[b])
+                    e[3].record()
+                    events.append(e)
+                else:
+                    sp.run_batch(b, kinds[b], blens[b], lg, d, V=V)
+                batches += 1
+        return epochs, batches
+
+    drain()                                   # warm-up drain (attributes, allocator)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(device.index if device.index is not None else 0)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with clocks:
+        t0.record()
+        epochs, batches = drain()
+        # the only collective: finished outputs + counters, once, at the end
+        counters = sp.counters.clone()
+        t1.record()
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    moved = int(sp.moved.item())
+    cnt = counters.cpu().numpy()
+    status = int(sp.status.item())
+    out_loc = sp.out_buf.cpu().numpy()
+    gen_loc = sp.gen.cpu().numpy()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        g0 = time.perf_counter()
+        _, gen_all, cnt_all = gather_results(mine, out_loc, gen_loc, cnt, N, args.max_new, device=device)
+        gather_ms = (time.perf_counter() - g0) * 1e3
+    else:
+        gen_all, cnt_all, gather_ms = gen_loc, cnt, 0.0
+    assert int((gen_all == args.max_new).sum()) == N, "every sequence reaches max_new (EOS off)"
+    # second drain with events around the fallback batches' KV moves (roofline of K2)
+    evs = []
+    if rank == 0:
+        drain(evs)
+        torch.cuda.synchronize()
+    k2_ms = sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in evs)
+    moved2 = int(sp.moved.item()) if rank == 0 else 0
+    peak, peak_src = peaks()
+    achieved = moved2 / (k2_ms / 1e3) / 1e9 if k2_ms else 0.0
+    rate_same = cnt_all[1] / max(1, cnt_all[0])
+    return {
+        "metric": "EXSpec pool sequences/s (Qwen3-8B shape, N=%d, B=%d, k=%d)" % (N, sp.B, k),
+        "value": N / (ms / 1e3), "unit": "sequences/s", "n_gpus": world, "steps": epochs,
+        "warmup": 1, "ms_per_step": ms / max(1, epochs), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": sh.kv_dtype, "data": "synthetic",
+        "config": {"workload": f"EXSpec pool drain: {N} seqs, prompt {args.pool_lengths} "
+                               f"{'U[64,512]' if args.pool_lengths == 'random' else '256'}, max_new "
+                               f"{args.max_new}, W={Wn}/rank, B={sp.B}, min_group={args.min_group}, "
+                               f"sort on, {args.shard} shards, EOS off",
+                   "cap": cap, "pool_kv_GB_per_rank": sp.kv.numel() * 2 / 1e9,
+                   "parallelism": f"pool sharded x{world}", "step": "one epoch (K4 plan + its batches)"},
+        "pool": {"epochs": epochs, "batch_verifications": int(cnt_all[0]),
+                 "grouping_rate": rate_same, "same_length_batches": int(cnt_all[1]),
+                 "fallback_members": int(cnt_all[3]), "kv_bytes_moved_rank0": moved,
+                 "gather_ms": gather_ms},
+        "roofline": {"bound": "hbm", "kernel": "specdec_realign_kv gather+scatter (fallback batches)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src},
+        "clocks": clocks.summary(), "status": status,
+        "gpu_launches": None, "e2e": None, "cpu_baseline": None,
+    }
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle as it stands, rank 0 only."""
     if rank != 0:
@@ -408,6 +543,14 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
+    if args.config == "pool":
+        out = run_pool(args, rank, world, device)
+        if rank == 0:
+            print(json.dumps(out))
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     res = run_ours(args, rank, world, device)
     sh = res["sh"]
     if rank == 0:

@@ -1,0 +1,182 @@
+"""EXSpec SequencePool on device (Alg. 3; §3.2).
+
+Sequences live individually in a pool -- tokens, generated output and a left-aligned KV
+slab each ([N][planes][H][cap][D], sequence-major) -- in their ragged state.  An epoch:
+
+    specdec_pool_group       K4  RefillWindow + same-length GetBatch plan for the window
+    (one small D2H of the plan header: n_batches, kind, width -- the only host sync)
+    for every batch of the plan:
+        fallback batches only:   specdec_realign_kv gather  (pool -> right-aligned staging)
+        [the model's verify forward runs here; synthetic workloads pass a hook]
+        specdec_verify           K1  Alg. 1 on the batch rows (no budget: the pool applies it)
+        specdec_pool_writeback   Phase 4: Pool[i] (+)= A[i] (+) B[i], deactivate if complete
+        fallback batches only:   specdec_realign_kv scatter (the a+1 new KV rows back)
+
+Same-length batches move no KV at all (lazy realignment): the consumer
+reads the pool slots directly (zero-copy).  Sharding over GPUs is in dist.py.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _abi
+from .eqspec import TORCH_DT
+
+
+class SequencePool:
+    def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
+                 max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True):
+        dev = torch.device(device)
+        i32, i64, u8 = torch.int32, torch.int64, torch.uint8
+        if B > W:
+            raise ValueError("B must be <= W")
+        self.N, self.cap, self.layers, self.H, self.D, self.k = N, cap, layers, H, D, k
+        self.n_planes = 2 * layers
+        self.W, self.B, self.min_group = W, B, min_group
+        self.max_new, self.eos_id, self.pad_id = max_new, eos_id, pad_id
+        self.device = dev
+        self.cap_tok = cap_tok or cap
+        # pool state
+        self.len = torch.zeros(N, dtype=i32, device=dev)
+        self.gen = torch.zeros(N, dtype=i32, device=dev)
+        self.active = torch.zeros(N, dtype=u8, device=dev)
+        self.order = torch.arange(N, dtype=i32, device=dev)
+        self.tokens = torch.full((N, self.cap_tok), pad_id, dtype=i64, device=dev)
+        self.out_buf = torch.zeros((N, max_new), dtype=i64, device=dev)
+        alloc = torch.zeros if kv_init else torch.empty
+        self.kv = alloc((N, self.n_planes, H, cap, D), dtype=TORCH_DT[kv_dtype], device=dev)
+        self.staging = alloc((self.n_planes, B, H, cap, D), dtype=TORCH_DT[kv_dtype], device=dev)
+        # plan (K4 outputs)
+        self.window = torch.zeros(W, dtype=i32, device=dev)
+        self.window_size = torch.zeros(1, dtype=i32, device=dev)
+        self.batch_of = torch.zeros(N, dtype=i32, device=dev)
+        self.slot_of = torch.zeros(N, dtype=i32, device=dev)
+        self.members = torch.zeros((W, B), dtype=i32, device=dev)
+        self.mlen = torch.zeros((W, B), dtype=i32, device=dev)
+        self.mpad = torch.zeros((W, B), dtype=i32, device=dev)
+        self.mactive = torch.zeros((W, B), dtype=u8, device=dev)
+        self.bsize = torch.zeros(W, dtype=i32, device=dev)
+        self.bkind = torch.zeros(W, dtype=u8, device=dev)
+        self.blen = torch.zeros(W, dtype=i32, device=dev)
+        self.n_batches = torch.zeros(1, dtype=i32, device=dev)
+        self.counters = torch.zeros(8, dtype=i64, device=dev)
+        # per-batch verify scratch
+        self.accept = torch.zeros(B, dtype=i32, device=dev)
+        self.bonus = torch.zeros(B, dtype=i64, device=dev)
+        self.emit = torch.zeros(B, dtype=i32, device=dev)
+        self.finished = torch.zeros(B, dtype=u8, device=dev)
+        self.n_new = torch.zeros(B, dtype=i32, device=dev)
+        self.pad_new = torch.zeros(B, dtype=i32, device=dev)
+        self.kept = torch.zeros(B, dtype=i32, device=dev)
+        self.plan_L = torch.zeros(1, dtype=i32, device=dev)
+        ws = _abi.specdec_verify_workspace_size(B, k)
+        self.ws = torch.zeros((ws + 7) // 8, dtype=i64, device=dev)
+        self.status = torch.zeros(1, dtype=i32, device=dev)
+        self.moved = torch.zeros(1, dtype=i64, device=dev)
+        self.verify_calls = 0
+        self._pinned = torch.zeros(1 + 3 * W, dtype=i32).pin_memory()
+
+    # ----------------------------------------------------------------- state
+    def load(self, prompts_lens, tokens=None, order=None, kv=None):
+        """Admit N sequences: lengths (prompt incl. the pending last token), optional
+        tokens [N, cap_tok], admission order (default by id) and KV."""
+        self.len.copy_(torch.as_tensor(np.asarray(prompts_lens), dtype=torch.int32))
+        self.gen.zero_()
+        self.active.fill_(1)
+        if order is not None:
+            self.order.copy_(torch.as_tensor(np.asarray(order), dtype=torch.int32))
+        if tokens is not None:
+            self.tokens.copy_(torch.as_tensor(tokens))
+        if kv is not None:
+            self.kv.copy_(kv)
+        self.counters.zero_()
+        self.verify_calls = 0
+
+    @property
+    def kv_strides(self):
+        s = self.kv.stride()          # [N][planes][H][cap][D]
+        return (s[1], s[0], s[2])     # (plane, row, head)
+
+    @property
+    def staging_strides(self):
+        s = self.staging.stride()     # [planes][B][H][cap][D]
+        return (s[0], s[1], s[2])
+
+    # ----------------------------------------------------------------- plan
+    def plan(self, stream=None):
+        """K4 over the window; returns the host copy of the plan header
+        (n_batches, kinds, widths, sizes) -- the epoch's single device->host sync."""
+        _abi.specdec_pool_group(self.len, self.active, self.order, self.W, self.B, self.min_group,
+                                self.window, self.window_size, self.batch_of, self.slot_of,
+                                self.members, self.mlen, self.mpad, self.mactive, self.bsize,
+                                self.bkind, self.blen, self.n_batches, self.counters, stream=stream)
+        W = self.W
+        hdr = self._pinned
+        hdr[0:1].copy_(self.n_batches, non_blocking=True)
+        hdr[1:1 + W].copy_(self.bkind.to(torch.int32), non_blocking=True)
+        hdr[1 + W:1 + 2 * W].copy_(self.blen, non_blocking=True)
+        hdr[1 + 2 * W:1 + 3 * W].copy_(self.bsize, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
+        nb = int(hdr[0])
+        h = hdr.numpy()
+        return nb, h[1:1 + nb].copy(), h[1 + W:1 + W + nb].copy(), h[1 + 2 * W:1 + 2 * W + nb].copy()
+
+    # ----------------------------------------------------------------- one batch
+    def gather(self, b, stream=None):
+        """Fallback batch b: pool slots [0, len-1) -> staging rows right-aligned at the
+        batch width (unpad-repad realignment)."""
+        _abi.specdec_realign_kv(self.kv, self.staging, self.mlen[b], count_add=-1,
+                                n_planes=self.n_planes, n_rows=self.B, H=self.H, D=self.D,
+                                src_strides=self.kv_strides, dst_strides=self.staging_strides,
+                                cap_src=self.cap, cap_dst=self.cap, dst_col=self.mpad[b],
+                                src_row_map=self.members[b], moved_bytes=self.moved,
+                                status=self.status, stream=stream)
+
+    def scatter(self, b, blen, stream=None):
+        """Write-back Pool.KV[i] <- KV[i]: the a+1 new rows
+        staging [L_b-1, L_b+a) -> pool [len-1, len+a)."""
+        _abi.specdec_realign_kv(self.staging, self.kv, self.accept, count_add=1,
+                                n_planes=self.n_planes, n_rows=self.B, H=self.H, D=self.D,
+                                src_strides=self.staging_strides, dst_strides=self.kv_strides,
+                                cap_src=self.cap, cap_dst=self.cap, src_col_add=int(blen) - 1,
+                                dst_col=self.mlen[b], dst_col_add=-1,
+                                dst_row_map=self.members[b], moved_bytes=self.moved,
+                                status=self.status, stream=stream)
+
+    def verify(self, b, logits, draft, V=None, stream=None):
+        _abi.specdec_verify(logits, draft, self.mlen[b], self.mactive[b], self.accept, self.bonus,
+                            self.emit, self.finished, self.plan_L, self.n_new, self.pad_new,
+                            self.kept, self.ws, V=V or logits.shape[2], eos_id=self.eos_id,
+                            pad_id=self.pad_id, budget=None, status=self.status, stream=stream)
+        self.verify_calls += 1
+
+    def writeback(self, b, draft, stream=None):
+        _abi.specdec_pool_writeback(self.members[b], self.k, draft, self.accept, self.bonus,
+                                    self.emit, self.finished, self.len, self.gen, self.active,
+                                    max_new=self.max_new, pool_tokens=self.tokens,
+                                    out_buf=self.out_buf, status=self.status, stream=stream)
+
+    def run_batch(self, b, kind, blen, logits, draft, forward=None, V=None, stream=None):
+        fallback = not kind
+        if fallback:
+            self.gather(b, stream)
+        if forward is not None:
+            forward(self, b, bool(kind), int(blen))
+        self.verify(b, logits, draft, V, stream)
+        self.writeback(b, draft, stream)
+        if fallback:
+            self.scatter(b, blen, stream)
+
+    def epoch(self, inputs, forward=None, V=None, stream=None):
+        """Plan the window and run every batch of the plan.  `inputs(i)` returns the
+        (logits [B, k+1, V], draft [B, k]) of the epoch's i-th batch.  Returns the plan
+        header (n_batches, kinds, widths, sizes)."""
+        nb, kinds, blens, sizes = self.plan(stream)
+        for b in range(nb):
+            lg, d = inputs(b)
+            self.run_batch(b, kinds[b], blens[b], lg, d, forward, V, stream)
+        return nb, kinds, blens, sizes
+
+    def has_active(self) -> bool:
+        return bool(self.active.any().item())
