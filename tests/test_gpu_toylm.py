@@ -1,0 +1,147 @@
+"""End-to-end equivalence on the CUDA path (BASELINE.json north_star):
+the toy LM (oracle side, CPU, fp64, bf16 KV) supplies logits and KV; every step of the hot
+path -- verify, repad/positions/masks, KV realign, pool plan, gather/scatter, write-back --
+runs in libspecdec.so.  Batched speculative output must equal per-sequence greedy output
+token for token, which only holds if positions, masks and every realigned KV row are
+right (SPEC.md:169 alignment soundness)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.align import build_batch, mask_pos_row
+from oracle.toy_lm import ToyLM
+from paper_2510_22876_b200.eqspec import EqSpecBatch
+from paper_2510_22876_b200.exspec import SequencePool
+
+pytestmark = pytest.mark.gpu
+
+V, LAYERS, H, D = 32, 2, 2, 8
+
+
+def _bits(t):
+    return t.detach().cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+def _to_dev(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).to(dev).view(torch.bfloat16)
+
+
+def _prompts(n, seed):
+    rng = np.random.default_rng(seed)
+    return [list(map(int, rng.integers(2, V, size=int(l)))) for l in rng.integers(1, 15, n)]
+
+
+@pytest.mark.parametrize("B,noise,eos,k", [(2, 0.3, 1, 4), (4, 0.0, -1, 4), (5, 0.45, 1, 3), (1, 0.2, 1, 5)])
+def test_eqspec_on_gpu_equals_greedy(cuda, B, noise, eos, k):
+    T = ToyLM(V, LAYERS, H, D, seed=7)
+    prompts = _prompts(B, seed=B * 10 + k)
+    max_new, cap = 18, 64
+    ref = [T.greedy_generate(p, max_new, eos, cap) for p in prompts]
+    tokens, pad, L = build_batch(prompts, cap)
+    bt = EqSpecBatch(B, k, cap, LAYERS, H, D, "bf16", cuda, max_new=max_new, eos_id=eos)
+    bt.load(tokens, [len(p) for p in prompts])
+    first = True
+    for _ in range(64):
+        if not bt.active.any().item():
+            break
+        act = bt.active.cpu().numpy()
+        tok = bt.tokens.cpu().numpy()
+        pad_c = bt.pad_cur.cpu().numpy()
+        L = int((bt.pad_cur + bt.n_cur).max().item())
+        if first:
+            mask = np.stack([mask_pos_row(int(p), L + k)[0] for p in pad_c])
+            pos = np.stack([mask_pos_row(int(p), L + k)[1] for p in pad_c])
+        else:                                    # K3's outputs drive the forward
+            mask = bt.mask[:, :L + k].cpu().numpy()
+            pos = bt.pos[:, :L + k].cpu().numpy()
+        draft = np.zeros((B, k), np.int64)
+        for i in range(B):
+            if act[i]:
+                draft[i] = T.propose(list(tok[i, pad_c[i]:L]), k, noise)
+        cache = _bits(bt.kv).copy()
+        logits = np.zeros((B, k + 1, V), np.float32)
+        for i in range(B):
+            if not act[i]:
+                continue
+            for c in range(0 if first else L - 1, L + k):
+                if mask[i, c]:
+                    t = int(tok[i, c]) if c < L else int(draft[i, c - L])
+                    lg = T.token_forward(t, int(pos[i, c]), c, cache[:, i], mask[i])
+                    if c >= L - 1:
+                        logits[i, c - L + 1] = lg.astype(np.float32)
+        bt.kv.copy_(_to_dev(cache, cuda))
+        bt.step(torch.from_numpy(logits).to(cuda), torch.from_numpy(draft).to(cuda), V=V)
+        first = False
+    gen = bt.gen.cpu().numpy()
+    out = bt.out_buf.cpu().numpy()
+    assert [list(out[i, :gen[i]]) for i in range(B)] == ref
+    assert int(bt.status.item()) == 0
+
+
+@pytest.mark.parametrize("N,Wn,B,mg", [(10, 6, 3, 2), (8, 8, 4, 4), (7, 7, 1, 2)])
+def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg):
+    T = ToyLM(V, LAYERS, H, D, seed=7)
+    k, max_new = 3, 12
+    prompts = _prompts(N, seed=N + B)
+    ref = [T.greedy_generate(p, max_new, 1, 64) for p in prompts]
+    lens = np.array([len(p) for p in prompts], np.int32)
+    cap = int(lens.max()) + max_new + k + 4
+    order = np.array(sorted(range(N), key=lambda s: (lens[s], s)), np.int32)
+    tokens = np.zeros((N, cap), np.int64)
+    kv = np.zeros((N, 2 * LAYERS, H, cap, D), np.uint16)
+    ones = np.ones(cap, np.int64)
+    for s, p in enumerate(prompts):
+        tokens[s, :len(p)] = p
+        for c, t in enumerate(p[:-1]):                    # prefill all but the pending token
+            T.token_forward(t, c, c, kv[s], ones)
+    sp = SequencePool(N, cap, LAYERS, H, D, k, W=Wn, B=B, min_group=mg, max_new=max_new, eos_id=1,
+                      device=cuda)
+    sp.load(lens, tokens, order, _to_dev(kv, cuda))
+    kinds_seen = set()
+    for _ in range(80):
+        nb, kinds, blens, sizes = sp.plan()
+        if nb == 0:
+            break
+        for b in range(nb):
+            mem = sp.members[b].cpu().numpy()
+            Lb = int(blens[b])
+            fallback = not kinds[b]
+            kinds_seen.add(int(kinds[b]))
+            if fallback:
+                sp.gather(b)
+            ptok = sp.tokens.cpu().numpy()
+            plen = sp.len.cpu().numpy()
+            src = _bits(sp.staging).copy() if fallback else None
+            pool_kv = _bits(sp.kv).copy() if not fallback else None
+            logits = np.zeros((B, k + 1, V), np.float32)
+            draft = np.zeros((B, k), np.int64)
+            for j, s in enumerate(mem):
+                if s < 0:
+                    continue
+                n = int(plen[s])
+                p = Lb - n
+                content = list(ptok[s, :n])
+                draft[j] = T.propose(content, k, 0.3)
+                mask, pos = mask_pos_row(p, Lb + k)
+                if fallback:
+                    row = src[:, j]                        # right-aligned staging row
+                else:
+                    row = pool_kv[s]                       # zero-copy: the pool slot itself
+                for c in range(Lb - 1, Lb + k):
+                    t = content[-1] if c == Lb - 1 else int(draft[j, c - Lb])
+                    lg = T.token_forward(t, int(pos[c]), c, row, mask)
+                    logits[j, c - Lb + 1] = lg.astype(np.float32)
+            if fallback:
+                sp.staging.copy_(_to_dev(src, cuda))
+            else:
+                sp.kv.copy_(_to_dev(pool_kv, cuda))
+            sp.verify(b, torch.from_numpy(logits).to(cuda), torch.from_numpy(draft).to(cuda), V=V)
+            sp.writeback(b, torch.from_numpy(draft).to(cuda))
+            if fallback:
+                sp.scatter(b, Lb)
+    gen = sp.gen.cpu().numpy()
+    out = sp.out_buf.cpu().numpy()
+    assert [list(out[s, :gen[s]]) for s in range(N)] == ref
+    assert not sp.has_active() and int(sp.status.item()) == 0
+    if B > 1:
+        assert kinds_seen == {0, 1}           # both lazy (same-length) and fallback batches ran
