@@ -26,6 +26,7 @@
 namespace specdec {
 
 constexpr int kRealignMaxRows = 1024;
+static int g_ctas_per_sm = 0;  // tuning override (SPECDEC_REALIGN_CTAS), 0 = occupancy
 constexpr int kZeroBytes = 2048;
 
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -42,6 +43,7 @@ struct RealignParams {
     int32_t src_col_add, dst_col_add, count_add;
     uint32_t flags;
     int inplace;
+    int policy_mode;  // 0: L2 evict_first on the streamed bytes, 1: evict_normal
     unsigned long long *moved;
     uint32_t *status;
 };
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(32) realign_kernel(RealignParams p) {
     __syncwarp();
     if (lane != 0 || n_mv == 0) return;
 
-    const uint64_t pol = policy_evict_first();
+    const uint64_t pol = p.policy_mode == 0 ? policy_evict_first() : policy_evict_normal();
     ChunkIter it;
     it.n_items = p.n_planes * static_cast<int64_t>(n_mv) * p.H;
     it.stride = gridDim.x;
@@ -235,8 +237,101 @@ int launch_realign(const RealignParams &p, int64_t max_items, cudaStream_t s) {
         if (e != cudaSuccess) return record_cuda_error(e);
         per_sm = std::max(1, occ);
     }
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_items, static_cast<int64_t>(device_sm_count()) * per_sm));
+    // CTAs per SM: with many slabs per SM, one streaming CTA per SM is fastest (fewer
+    // concurrent DRAM streams, finer tail: measured in profiles/r01/realign_sweep.txt);
+    // with few slabs, fill the SM to occupancy so every slab gets its own CTA.
+    const int64_t sms = device_sm_count();
+    int ctas = max_items >= 16 * sms ? 1 : per_sm;
+    if (g_ctas_per_sm > 0) ctas = std::min(per_sm, g_ctas_per_sm);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_items, sms * ctas));
     realign_kernel<STAGES, CHUNK><<<static_cast<unsigned>(grid), 32, smem, s>>>(p);
+    return check_launch();
+}
+
+// ----------------------------------------------------------------------------- LDG/STG variant
+// Register-staged alternative (SPECDEC_REALIGN_CFG=9): one 256-thread CTA per slab at a
+// time, 16 KB chunks of 128-bit coalesced loads, a CTA barrier (all loads of the chunk
+// performed) before the chunk's stores, chunks walked in the hazard-free direction.
+constexpr int kLdgThreads = 256;
+constexpr int kLdgU = 4;
+
+__global__ void __launch_bounds__(kLdgThreads) realign_ldg_kernel(RealignParams p) {
+    __shared__ int32_t rows[kRealignMaxRows];
+    __shared__ int s_n;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid < 32) {
+        bool any_bad = false;
+        int n_mv = 0;
+        for (int64_t base = 0; base < p.n_rows; base += 32) {
+            const int r = static_cast<int>(base) + lane;
+            RowGeom g;
+            bool bad = false, mv = false;
+            if (r < p.n_rows) mv = row_geom(p, r, g, bad);
+            const unsigned bal = __ballot_sync(0xFFFFFFFFu, mv);
+            if (mv) rows[n_mv + __popc(bal & ((1u << lane) - 1u))] = r;
+            n_mv += __popc(bal);
+            any_bad |= bad;
+        }
+        any_bad = __any_sync(0xFFFFFFFFu, any_bad);
+        if (lane == 0) {
+            s_n = n_mv;
+            if (any_bad && blockIdx.x == 0 && p.status) atomicOr(p.status, SPECDEC_ST_KEPT);
+        }
+    }
+    __syncthreads();
+    const int n_mv = s_n;
+    const int64_t n_items = p.n_planes * static_cast<int64_t>(n_mv) * p.H;
+    unsigned long long moved = 0;
+    for (int64_t t = blockIdx.x; t < n_items; t += gridDim.x) {
+        const int64_t head = t % p.H, mi = (t / p.H) % n_mv, plane = t / (p.H * n_mv);
+        RowGeom g;
+        bool bad;
+        row_geom(p, rows[mi], g, bad);
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.src + plane * p.ss_plane + head * p.ss_head + g.src_off);
+        uint4 *dst = reinterpret_cast<uint4 *>(p.dst + plane * p.ds_plane + head * p.ds_head + g.dst_off);
+        const bool down = reinterpret_cast<const char *>(dst) > reinterpret_cast<const char *>(src);
+        const int64_t nvec = g.bytes / 16;
+        constexpr int CV = kLdgThreads * kLdgU;
+        const int64_t nch = (nvec + CV - 1) / CV;
+        for (int64_t q = 0; q < nch; ++q) {
+            const int64_t hi = down ? nvec - q * CV : imin64(nvec, (q + 1) * CV);
+            const int64_t lo = down ? imax64(0, hi - CV) : q * CV;
+            uint4 buf[kLdgU];
+#pragma unroll
+            for (int u = 0; u < kLdgU; ++u) {
+                const int64_t v = lo + u * kLdgThreads + tid;
+                if (v < hi) buf[u] = ld_stream_v4(src + v);
+            }
+            __syncthreads();  // every load of this chunk is performed before any store
+#pragma unroll
+            for (int u = 0; u < kLdgU; ++u) {
+                const int64_t v = lo + u * kLdgThreads + tid;
+                if (v < hi) dst[v] = buf[u];
+            }
+        }
+        if ((p.flags & SPECDEC_ZERO_PADS) && p.inplace && down) {
+            __syncthreads();
+            const int64_t zv = (reinterpret_cast<const char *>(dst) - reinterpret_cast<const char *>(src)) / 16;
+            uint4 *z = const_cast<uint4 *>(src);
+            for (int64_t v = tid; v < zv; v += kLdgThreads) z[v] = make_uint4(0, 0, 0, 0);
+        }
+        __syncthreads();
+        moved += 2ull * static_cast<unsigned long long>(g.bytes);
+    }
+    if (tid == 0 && p.moved && moved) atomicAdd(p.moved, moved);
+}
+
+int launch_realign_ldg(const RealignParams &p, int64_t max_items, cudaStream_t s) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        int occ = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, realign_ldg_kernel, kLdgThreads, 0);
+        if (e != cudaSuccess) return record_cuda_error(e);
+        per_sm = std::max(1, occ);
+    }
+    const int ctas = g_ctas_per_sm > 0 ? std::min(per_sm, g_ctas_per_sm) : per_sm;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_items, static_cast<int64_t>(device_sm_count()) * ctas));
+    realign_ldg_kernel<<<static_cast<unsigned>(grid), kLdgThreads, 0, s>>>(p);
     return check_launch();
 }
 
@@ -283,19 +378,32 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     p.moved = d_moved_bytes; p.status = d_status;
     const int64_t max_items = n_planes * n_rows * H;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    // pipeline shape (stages x chunk bytes); SPECDEC_REALIGN_CFG selects a variant for
-    // tuning sweeps (bench/profiles); the default is the measured best.
-    static int cfg = -1;
+    // pipeline shape (stages x chunk bytes), L2 policy and CTAs/SM: tuning overrides for
+    // sweeps (tools/kbench.py, profiles/); the default is the measured best.
+    static int cfg = -1, pol = 0;
     if (cfg < 0) {
         const char *e = getenv("SPECDEC_REALIGN_CFG");
         cfg = e ? atoi(e) : 0;
+        const char *q = getenv("SPECDEC_REALIGN_POLICY");
+        pol = q ? atoi(q) : 0;
+        const char *c = getenv("SPECDEC_REALIGN_CTAS");
+        g_ctas_per_sm = c ? atoi(c) : 0;
     }
+    p.policy_mode = pol;
     switch (cfg) {
         case 1: return launch_realign<8, 8192>(p, max_items, s);
-        case 2: return launch_realign<3, 32768>(p, max_items, s);
+        case 2: return launch_realign<4, 16384>(p, max_items, s);
         case 3: return launch_realign<6, 16384>(p, max_items, s);
         case 4: return launch_realign<12, 8192>(p, max_items, s);
         case 5: return launch_realign<4, 8192>(p, max_items, s);
-        default: return launch_realign<4, 16384>(p, max_items, s);
+        case 6: return launch_realign<2, 16384>(p, max_items, s);
+        case 7: return launch_realign<3, 8192>(p, max_items, s);
+        case 9: return launch_realign_ldg(p, max_items, s);
+        case 10: return launch_realign<8, 16384>(p, max_items, s);
+        case 11: return launch_realign<12, 16384>(p, max_items, s);
+        case 12: return launch_realign<6, 32768>(p, max_items, s);
+        case 13: return launch_realign<4, 32768>(p, max_items, s);
+        case 14: return launch_realign<16, 8192>(p, max_items, s);
+        default: return launch_realign<3, 32768>(p, max_items, s);  // measured best
     }
 }
