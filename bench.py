@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--round-mode", default="graph-serial",
+                    choices=["graph-fork", "graph-serial", "direct-fork", "direct-serial"],
+                    help="value region: CUDA-graph replay or direct launches; K3 forked under K2 or serial")
     return ap.parse_args()
 
 
@@ -204,7 +207,18 @@ def run_ours(args, rank, world, device):
     for r in range(args.warmup):          # direct launches: sets kernel attributes
         rb.step(r)
     torch.cuda.synchronize()
-    bt.capture(list(zip(rb.logits, rb.drafts)), V=sh.V)
+    bt.fork = args.round_mode.endswith("fork")
+    use_graph = args.round_mode.startswith("graph")
+    bt.V = sh.V
+    if use_graph:
+        bt.capture(list(zip(rb.logits, rb.drafts)), V=sh.V)
+
+    def one_round(r):
+        if use_graph:
+            bt.replay(r % RING)
+        else:
+            bt.launch_round(rb.logits[r % RING], rb.drafts[r % RING])
+            bt.cur = 1 - bt.cur
 
     def sync():
         if world > 1:
@@ -214,7 +228,7 @@ def run_ours(args, rank, world, device):
     # ---- A: value (graphs)
     rb.reset()
     for r in range(args.warmup):
-        bt.replay(r % RING)
+        one_round(r)
     rb.reset()
     moved0 = int(bt.moved.item())
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -223,7 +237,7 @@ def run_ours(args, rank, world, device):
     with clocks:
         t0.record(rb.stream)
         for r in range(args.steps):
-            bt.replay(r % RING)
+            one_round(r)
         t1.record(rb.stream)
         torch.cuda.synchronize()
     sync()
@@ -589,7 +603,7 @@ def main():
             "clocks": res["clocks"],
             "e2e": res["e2e"],
             "gpu_launches": 3 * args.steps,
-            "launch_mode": "CUDA graph per (parity, ring slot): 3 kernels per replay",
+            "launch_mode": args.round_mode + " (graph: one CUDA graph per (parity, ring slot), 3 kernels per replay)",
             "bytes_moved_check": {"value_region": res["moved_A"], "kernel_region": res["moved"]},
             "status": res["status"],
             "cpu_baseline": cpu,

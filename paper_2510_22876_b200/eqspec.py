@@ -56,6 +56,9 @@ class EqSpecBatch:
         self.cur = 0
         self.V = None
         self.zero_pads = False
+        # K3 on a side stream under K2: a small win for direct launches, a loss inside a
+        # CUDA graph (measured: profiles/r01/round_modes.txt), so off by default
+        self.fork = False
         self._graphs = {}
 
     # ----------------------------------------------------------------- state I/O
@@ -123,6 +126,11 @@ class EqSpecBatch:
         masks, positions) and K2 (KV) both depend only on K1's plan and touch disjoint
         memory, so K3 runs on a side stream under K2; the main stream joins it at the end."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if not self.fork:
+            self.verify(logits, draft, s)
+            self.repad(draft, s)
+            self.realign(s)
+            return
         if not hasattr(self, "_side"):
             self._side = torch.cuda.Stream(self.device)
             self._ev_plan, self._ev_rep = torch.cuda.Event(), torch.cuda.Event()
