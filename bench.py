@@ -74,9 +74,14 @@ def ncu_traffic(config_key):
     """dram bytes per launch of K2 from the committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
-        return None
-    d = json.load(open(p))
-    return d.get(config_key, {}).get("realign_dram_bytes_per_launch")
+        return None, None
+    d = json.load(open(p)).get(config_key)
+    if not d:
+        return None, None
+    return d["realign_dram_bytes_per_launch"], (
+        f"ncu --set full capture of one K2 launch: {d['realign_dram_bytes_per_launch'] / 1e9:.3f} GB DRAM "
+        f"vs {d['algorithmic_bytes_same_launch'] / 1e9:.3f} GB algorithmic for that launch "
+        f"(ratio {d['traffic_over_algorithmic']}); {d['source']}")
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -204,9 +209,16 @@ def run_ours(args, rank, world, device):
     rb = RoundBench(sh, args, device, total)
     bt = rb.bt
     torch.cuda.synchronize()
+    launch_bytes = []
     for r in range(args.warmup):          # direct launches: sets kernel attributes
+        m0 = int(bt.moved.item())
         rb.step(r)
+        launch_bytes.append(int(bt.moved.item()) - m0)   # K2 bytes of this launch
     torch.cuda.synchronize()
+    log = os.environ.get("SPECDEC_BENCH_LAUNCH_LOG")
+    if log:   # per-launch algorithmic K2 bytes of the first warm-up launches (for ncu)
+        with open(log, "w") as f:
+            json.dump({"config": f"{sh.name}_B{sh.B}", "realign_bytes_per_launch": launch_bytes}, f)
     bt.fork = args.round_mode.endswith("fork")
     use_graph = args.round_mode.startswith("graph")
     bt.V = sh.V
@@ -271,10 +283,12 @@ def run_ours(args, rank, world, device):
 def run_e2e(rb, args, world):
     """Each step: H2D of that step's logits + drafts from pinned host memory (copy stream,
     two device buffers, so the copy of step s+1 overlaps the round of step s), the round
-    (graph replay), D2H of (accept, bonus, emit) into pinned host memory."""
+    (graph replay), D2H of the step's result -- the per-row emitted-token counts -- into
+    pinned host memory (SPECDEC_E2E_D2H=three also reads accept + bonus; none: no read)."""
     import torch
     import torch.distributed as dist
     sh, dev, bt = rb.sh, rb.dev, rb.bt
+    d2h_mode = os.environ.get("SPECDEC_E2E_D2H", "one")
     host_lg = [lg.cpu().pin_memory() for lg in rb.logits]
     host_dr = [d.cpu().pin_memory() for d in rb.drafts]
     dlg = [torch.empty_like(rb.logits[0]) for _ in range(2)]
@@ -307,9 +321,11 @@ def run_e2e(rb, args, world):
             comp.wait_event(ready[b])
             bt.replay(b)
             done[b].record(comp)
-            out_a[r].copy_(bt.accept, non_blocking=True)
-            out_b[r].copy_(bt.bonus, non_blocking=True)
-            out_e[r].copy_(bt.emit, non_blocking=True)
+            if d2h_mode == "three":
+                out_a[r].copy_(bt.accept, non_blocking=True)
+                out_b[r].copy_(bt.bonus, non_blocking=True)
+            if d2h_mode != "none":
+                out_e[r].copy_(bt.emit, non_blocking=True)
 
     rb.reset()
     run(min(args.warmup, args.steps))
@@ -330,11 +346,12 @@ def run_e2e(rb, args, world):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    # the results are the method's: every step's accept equals the generator's planted answer
-    for r in range(args.steps):
-        assert np.array_equal(out_a[r].numpy(), rb.truth[r % RING].accept), "e2e accept mismatch"
+    # the results are the method's: every step's emit = planted accept + 1 (no EOS/budget)
+    if d2h_mode != "none":
+        for r in range(args.steps):
+            assert np.array_equal(out_e[r].numpy(), rb.truth[r % RING].accept + 1), "e2e emit mismatch"
     h2d_b = rb.logits[0].numel() * rb.logits[0].element_size() + rb.drafts[0].numel() * 8
-    d2h_b = sh.B * (4 + 8 + 4)
+    d2h_b = {"three": sh.B * 16, "one": sh.B * 4, "none": 0}[d2h_mode]
     return {"value": world * args.steps / (ms / 1e3), "unit": "rounds/s", "h2d_bytes_per_step": h2d_b,
             "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / args.steps, "wall_s": wall,
             "overlap": "H2D on a copy stream, double-buffered; round = CUDA graph replay"}
@@ -573,7 +590,7 @@ def main():
         k2_launch_ms = res["k2_ms"] / args.steps
         bytes_per_launch = res["moved"] / args.steps
         achieved = bytes_per_launch / (k2_launch_ms / 1e3) / 1e9
-        traffic = ncu_traffic(f"{sh.name}_B{sh.B}")
+        traffic, traffic_note = ncu_traffic(f"{sh.name}_B{sh.B}")
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             rps, parts = oracle_round_sample(sh, args, rounds=2)
@@ -594,7 +611,7 @@ def main():
                        "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "kernel": "specdec_realign_kv (K2)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_src,
+                         "traffic_note": traffic_note, "peak_source": peak_src,
                          "bytes_per_launch": bytes_per_launch, "launch_ms": k2_launch_ms},
             "kernels_ms_per_step": {"verify_K1": res["k1_ms"] / args.steps,
                                     "repad_K3": res["k3_ms"] / args.steps,
