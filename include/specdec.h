@@ -89,6 +89,10 @@ size_t specdec_verify_workspace_size(int64_t B, int64_t k);
  * Outputs: d_accept [B] int32, d_bonus [B] int64, d_emit [B] int32, d_finished [B] uint8,
  *          d_pred [B][k+1] int64 or NULL, d_plan_L [1] int32, d_n_new, d_pad_new,
  *          d_kept [B] int32.
+ * d_kept_draft [B] int32 or NULL: the draft model's kept KV count when
+ *          it caches its own k forwards (pending token, d_1..d_{k-1}; d_k has no draft KV):
+ *          n_i + min(a_i, k-1) for still-active rows, 0 for finished rows.  Realign the
+ *          draft cache with the same p -> p' as the target and this count.
  * d_ws: workspace of specdec_verify_workspace_size(B, k) bytes (see above).
  * d_status: optional (NULL ok); SPECDEC_ST_NAN.
  */
@@ -97,8 +101,9 @@ int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_t k, int64_
                    uint8_t *d_active, int64_t eos_id, int64_t pad_id,
                    int32_t *d_budget, int32_t *d_accept, int64_t *d_bonus,
                    int32_t *d_emit, uint8_t *d_finished, int64_t *d_pred, int32_t *d_plan_L,
-                   int32_t *d_n_new, int32_t *d_pad_new, int32_t *d_kept, uint32_t *d_status,
-                   void *d_ws, size_t ws_bytes, specdec_stream_t stream);
+                   int32_t *d_n_new, int32_t *d_pad_new, int32_t *d_kept,
+                   int32_t *d_kept_draft, uint32_t *d_status, void *d_ws, size_t ws_bytes,
+                   specdec_stream_t stream);
 
 /* ------------------------------------------------------------------------------ a2
  * specdec_rebuild_pos_mask -- Alg. 2 Phase 3 unpad-append-repad and

@@ -12,7 +12,7 @@ import numpy as np
 
 from .align import build_batch, mask_pos_row, realign_kv, repad_tokens, unpad
 from .pool import admission_order, form_batches
-from .toy_lm import ToyLM
+from .toy_lm import ToyLM, greedy_fp32
 from .verify import batch_verify
 
 
@@ -37,9 +37,37 @@ def verify_forward(model: ToyLM, tokens, draft, pad, L, k, cache, active, mask, 
     return logits
 
 
+def draft_cached(model: ToyLM, tokens_row, pad: int, L: int, dkept: int, cache_row, k: int,
+                 noise: float = 0.0, seed: int = 0):
+    """Draft generation with the drafter's own KV cache (f1; Alg. 2 Phase 1, PAPER.md:337-339;
+    SPEC.md:217).  Content = tokens_row[pad:L]; the draft cache holds valid KV on
+    [pad, pad + dkept).  Forwards the tokens that lack draft KV (1 normally, 2 after a
+    full acceptance), then d_1..d_{k-1}; d_k is generated but never forwarded.  The
+    proposals (and their noise) equal ToyLM.propose's recompute-mode ones."""
+    cap = cache_row.shape[2]
+    mask = (np.arange(cap) >= pad).astype(np.int64)
+    content = [int(t) for t in tokens_row[pad:L]]
+    rng = np.random.default_rng([seed, len(content), int(np.sum(content)) % (1 << 31)])
+    logits = None
+    for c in range(pad + dkept, L):
+        logits = model.token_forward(int(tokens_row[c]), c - pad, c, cache_row, mask)
+    props, c = [], L
+    for j in range(k):
+        t = greedy_fp32(logits)
+        if noise > 0 and rng.random() < noise:
+            t = (t + 1 + int(rng.integers(model.V - 1))) % model.V
+        props.append(t)
+        if j < k - 1:
+            logits = model.token_forward(t, c - pad, c, cache_row, mask)
+            c += 1
+    return props
+
+
 def eqspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, cap,
-                  noise=0.0, pad_id=0, trace=None):
-    """Alg. 2.  Returns (outputs per prompt, rounds)."""
+                  noise=0.0, pad_id=0, trace=None, draft_cache=False, draft_log=None):
+    """Alg. 2.  Returns (outputs per prompt, rounds).  With draft_cache=True the drafter
+    keeps its own KV cache, realigned every round with kept_draft (f1); draft_log, if a
+    list, receives (cached proposals, recompute proposals) per round."""
     B = len(prompts)
     tokens, pad, L = build_batch(prompts, cap, pad_id)
     n = np.array([len(p) for p in prompts], np.int32)
@@ -49,6 +77,8 @@ def eqspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, ca
     cache = np.zeros((target.n_planes, B, target.H, cap, target.D), np.uint16)
     mask = np.stack([mask_pos_row(int(p), L + k)[0] for p in pad])
     pos = np.stack([mask_pos_row(int(p), L + k)[1] for p in pad])
+    dcache = np.zeros((drafter.n_planes, B, drafter.H, cap, drafter.D), np.uint16)
+    dkept = np.zeros(B, np.int32)
     first, rounds = True, 0
     while active.any():
         assert L + k <= cap, "capacity"
@@ -56,7 +86,13 @@ def eqspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, ca
         draft = np.full((B, k), pad_id, np.int64)
         for i in range(B):
             if active[i]:
-                draft[i] = drafter.propose(content[i], k, noise)
+                if draft_cache:
+                    draft[i] = draft_cached(drafter, tokens[i], int(pad[i]), L, int(dkept[i]),
+                                            dcache[:, i], k, noise)
+                else:
+                    draft[i] = drafter.propose(content[i], k, noise)
+                if draft_log is not None:
+                    draft_log.append((list(draft[i]), drafter.propose(content[i], k, noise)))
         logits = verify_forward(target, tokens, draft, pad, L, k, cache, active, mask, pos, first)
         budget = (max_new - gen).astype(np.int64)
         v = batch_verify(logits, "fp32", draft, n, pad, active, eos_id, budget, pad_id)
@@ -68,6 +104,9 @@ def eqspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, ca
                               kept=v["kept"].copy(), pad_new=v["pad_new"].copy()))
         tokens, mask, pos = repad_tokens(tokens, cap, k, pad, L, v, pad_id)
         cache, _ = realign_kv(cache, pad, v["pad_new"], v["kept"])
+        if draft_cache:
+            dcache, _ = realign_kv(dcache, pad, v["pad_new"], v["kept_draft"])
+            dkept = v["kept_draft"]
         pad, n, L = v["pad_new"], v["n_new"], v["L_new"]
         active = (v["finished"] == 0).astype(np.uint8)
         first = False

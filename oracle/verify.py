@@ -104,12 +104,12 @@ def batch_verify(logit_bits, dtype, draft, n, pad, active, eos_id=-1, budget=Non
         E, fin = emitted_tokens(draft[i], a, b, eos_id, None if budget is None else int(budget[i]))
         accept[i], bonus[i], emit[i], finished[i] = a, b, len(E), int(fin)
         E_rows.append(E)
-    plan = repad_plan(n, accept, finished)
+    plan = repad_plan(n, accept, finished, k)
     return dict(pred=pred, accept=accept, bonus=bonus, emit=emit, finished=finished,
                 E=E_rows, nan=nan_seen, **plan)
 
 
-def repad_plan(n, accept, finished):
+def repad_plan(n, accept, finished, k=None):
     """BatchRepad plan (§3.1; R6 minimal padding, R9 dummies).
 
     Still-active rows: n' = n + a + 1 (accepted + bonus), kept = n + a (the bonus has
@@ -124,5 +124,13 @@ def repad_plan(n, accept, finished):
     kept[alive] = n[alive] + np.asarray(accept, np.int64)[alive]
     L_new = int(n_new[alive].max()) if alive.any() else 0
     pad_new = np.where(L_new > 0, L_new - n_new, 0)
-    return dict(L_new=L_new, n_new=n_new.astype(np.int32), pad_new=pad_new.astype(np.int32),
-                kept=kept.astype(np.int32))
+    out = dict(L_new=L_new, n_new=n_new.astype(np.int32), pad_new=pad_new.astype(np.int32),
+               kept=kept.astype(np.int32))
+    if k is not None:
+        # f1: a draft model that cached its own forwards holds KV for the
+        # pending token and d_1..d_{k-1} (d_k is generated, never forwarded),
+        # so it keeps the old content plus min(a, k-1) accepted drafts.
+        kd = np.zeros(B, np.int64)
+        kd[alive] = n[alive] + np.minimum(np.asarray(accept, np.int64)[alive], k - 1)
+        out["kept_draft"] = kd.astype(np.int32)
+    return out

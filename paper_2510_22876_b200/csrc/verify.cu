@@ -38,7 +38,7 @@ struct VerifyParams {
     int32_t *emit;
     uint8_t *finished;
     int64_t *pred;
-    int32_t *plan_L, *n_new, *pad_new, *kept;
+    int32_t *plan_L, *n_new, *pad_new, *kept, *kept_draft;
     uint32_t *status;
     unsigned long long *ws_keys;  // [B*(k+1)]
     unsigned int *ws_counter;      // [1]
@@ -103,6 +103,9 @@ __device__ void verify_epilogue(const VerifyParams &p) {
             p.active[i] = fin ? 0 : 1;  // in/out: rows still active after this round
             p.n_new[i] = nn;
             p.kept[i] = kp;
+            // f1: a draft model that cached its own k forwards (pending token, d_1..d_{k-1})
+            // keeps n + min(a, k-1) entries: d_k never had a draft KV entry
+            if (p.kept_draft) p.kept_draft[i] = kp ? p.n[i] + min(a, k - 1) : 0;
         }
     }
     // L' = max n' over still-active rows (R6 minimal padding)
@@ -293,8 +296,8 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
                               int32_t *d_budget, int32_t *d_accept, int64_t *d_bonus,
                               int32_t *d_emit, uint8_t *d_finished, int64_t *d_pred,
                               int32_t *d_plan_L, int32_t *d_n_new, int32_t *d_pad_new,
-                              int32_t *d_kept, uint32_t *d_status, void *d_ws, size_t ws_bytes,
-                              specdec_stream_t stream) {
+                              int32_t *d_kept, int32_t *d_kept_draft, uint32_t *d_status,
+                              void *d_ws, size_t ws_bytes, specdec_stream_t stream) {
     const int es = dtype_size(dtype);
     if (es == 0) return SPECDEC_ERR_DTYPE;
     if (k < 1 || k > kMaxK) return SPECDEC_ERR_ARG;
@@ -314,6 +317,7 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
     p.eos_id = eos_id; p.pad_id = pad_id; p.budget = d_budget;
     p.accept = d_accept; p.bonus = d_bonus; p.emit = d_emit; p.finished = d_finished;
     p.pred = d_pred; p.plan_L = d_plan_L; p.n_new = d_n_new; p.pad_new = d_pad_new; p.kept = d_kept;
+    p.kept_draft = d_kept_draft;
     p.status = d_status;
     p.ws_keys = static_cast<unsigned long long *>(d_ws);
     p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);

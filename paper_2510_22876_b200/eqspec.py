@@ -25,7 +25,9 @@ TORCH_DT = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16
 
 class EqSpecBatch:
     def __init__(self, B, k, cap, layers, H, D, kv_dtype="bf16", device="cuda", max_new=0,
-                 eos_id=-1, pad_id=0, with_pred=False):
+                 eos_id=-1, pad_id=0, with_pred=False, draft=None):
+        """draft = (layers, H, D) of a draft model that keeps its own KV cache (f1): it is
+        realigned every round with the target's p -> p' and kept_draft = n + min(a, k-1)."""
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         self.B, self.k, self.cap, self.layers, self.H, self.D = B, k, cap, layers, H, D
@@ -53,6 +55,13 @@ class EqSpecBatch:
         ws = _abi.specdec_verify_workspace_size(B, k)
         self.ws = torch.zeros((ws + 7) // 8, dtype=i64, device=dev)
         self.kv = torch.zeros((self.n_planes, B, H, cap, D), dtype=TORCH_DT[kv_dtype], device=dev)
+        self.dkv = None
+        self.kept_draft = None
+        if draft is not None:
+            dl, dh, dd = draft
+            self.d_dims = (2 * dl, dh, dd)
+            self.dkv = torch.zeros((2 * dl, B, dh, cap, dd), dtype=TORCH_DT[kv_dtype], device=dev)
+            self.kept_draft = torch.zeros(B, dtype=i32, device=dev)
         self.cur = 0
         self.V = None
         self.zero_pads = False
@@ -74,6 +83,8 @@ class EqSpecBatch:
         if self.budget is not None:
             self.budget.fill_(self.max_new)
         self.gen.zero_()
+        if self.kept_draft is not None:
+            self.kept_draft.zero_()     # no draft KV yet: the drafter prefills in round 1
         if kv is not None:
             self.kv.copy_(kv)
 
@@ -101,7 +112,8 @@ class EqSpecBatch:
                             self.emit, self.finished, self.plan_L, self.n[nx], self.pad[nx],
                             self.kept, self.ws, V=self.V or logits.shape[2],
                             eos_id=self.eos_id, pad_id=self.pad_id, budget=self.budget,
-                            pred=self.pred, status=self.status, stream=stream)
+                            pred=self.pred, kept_draft=self.kept_draft, status=self.status,
+                            stream=stream)
 
     def repad(self, draft, stream=None):
         c, nx = self.cur, 1 - self.cur
@@ -120,6 +132,15 @@ class EqSpecBatch:
                                 src_col=self.pad[c], dst_col=self.pad[nx],
                                 flags=_abi.ZERO_PADS if self.zero_pads else 0,
                                 moved_bytes=self.moved, status=self.status, stream=stream)
+        if self.dkv is not None:     # f1: the draft model's own cache, same shift, kept_draft
+            dp, dh, dd = self.d_dims
+            s = self.dkv.stride()
+            _abi.specdec_realign_kv(self.dkv, self.dkv, self.kept_draft, n_planes=dp,
+                                    n_rows=self.B, H=dh, D=dd, src_strides=s[:3],
+                                    dst_strides=s[:3], cap_src=self.cap, cap_dst=self.cap,
+                                    src_col=self.pad[c], dst_col=self.pad[nx],
+                                    flags=_abi.ZERO_PADS if self.zero_pads else 0,
+                                    moved_bytes=self.moved, status=self.status, stream=stream)
 
     def launch_round(self, logits, draft, stream=None):
         """Enqueue K1 -> {K3 || K2} for the current parity (does not flip it).  K3 (tokens,

@@ -9,6 +9,7 @@ import pytest
 import torch
 
 from oracle.align import build_batch, mask_pos_row
+from oracle.loops import draft_cached
 from oracle.toy_lm import ToyLM
 from paper_2510_22876_b200.eqspec import EqSpecBatch
 from paper_2510_22876_b200.exspec import SequencePool
@@ -31,16 +32,30 @@ def _prompts(n, seed):
     return [list(map(int, rng.integers(2, V, size=int(l)))) for l in rng.integers(1, 15, n)]
 
 
-@pytest.mark.parametrize("B,noise,eos,k", [(2, 0.3, 1, 4), (4, 0.0, -1, 4), (5, 0.45, 1, 3), (1, 0.2, 1, 5)])
-def test_eqspec_on_gpu_equals_greedy(cuda, B, noise, eos, k):
-    T = ToyLM(V, LAYERS, H, D, seed=7)
-    prompts = _prompts(B, seed=B * 10 + k)
-    max_new, cap = 18, 64
-    ref = [T.greedy_generate(p, max_new, eos, cap) for p in prompts]
+def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, drafter=None,
+                draft_log=None):
+    """EqSpec with the toy LM on the host and K1/K3/K2 in libspecdec.so.  `fault` injects
+    one of the paper's §2 failure classes at a module seam.  With a
+    `drafter`, the draft model keeps its own KV cache on the GPU, realigned by K2 with
+    K1's kept_draft (f1); its proposals are logged next to recompute-mode proposals."""
+    B = len(prompts)
     tokens, pad, L = build_batch(prompts, cap)
-    bt = EqSpecBatch(B, k, cap, LAYERS, H, D, "bf16", cuda, max_new=max_new, eos_id=eos)
+    bt = EqSpecBatch(B, k, cap, LAYERS, H, D, "bf16", cuda, max_new=max_new, eos_id=eos,
+                     draft=None if drafter is None else (LAYERS, H, D))
     bt.load(tokens, [len(p) for p in prompts])
+    if fault == "skip_kv_realign":             # DSD error (iii): KV not realigned
+        bt.realign = lambda stream=None: None
+    if fault == "bonus_from_draft":            # DSD error (i): bonus from the draft
+        orig = bt.verify
+
+        def verify(logits, draft, stream=None):
+            orig(logits, draft, stream)
+            a = bt.accept.long().clamp(max=draft.shape[1] - 1)
+            bt.bonus.copy_(torch.gather(draft, 1, a[:, None])[:, 0])
+        bt.verify = verify
+    stale = None
     first = True
+    rounds = 0
     for _ in range(64):
         if not bt.active.any().item():
             break
@@ -54,10 +69,26 @@ def test_eqspec_on_gpu_equals_greedy(cuda, B, noise, eos, k):
         else:                                    # K3's outputs drive the forward
             mask = bt.mask[:, :L + k].cpu().numpy()
             pos = bt.pos[:, :L + k].cpu().numpy()
+        if fault == "stale_position_ids":        # BSP: positions not recomputed
+            if stale is not None:
+                w = min(pos.shape[1], stale.shape[1])
+                pos = pos.copy()
+                pos[:, :w] = stale[:, :w]
+            stale = pos.copy()
         draft = np.zeros((B, k), np.int64)
-        for i in range(B):
-            if act[i]:
-                draft[i] = T.propose(list(tok[i, pad_c[i]:L]), k, noise)
+        if drafter is None:
+            for i in range(B):
+                if act[i]:
+                    draft[i] = T.propose(list(tok[i, pad_c[i]:L]), k, noise)
+        else:
+            dcache = _bits(bt.dkv).copy()
+            dkept = bt.kept_draft.cpu().numpy()
+            for i in range(B):
+                if act[i]:
+                    draft[i] = draft_cached(drafter, tok[i], int(pad_c[i]), L, int(dkept[i]),
+                                            dcache[:, i], k, noise)
+                    draft_log.append((list(draft[i]), drafter.propose(list(tok[i, pad_c[i]:L]), k, noise)))
+            bt.dkv.copy_(_to_dev(dcache, cuda))
         cache = _bits(bt.kv).copy()
         logits = np.zeros((B, k + 1, V), np.float32)
         for i in range(B):
@@ -72,10 +103,46 @@ def test_eqspec_on_gpu_equals_greedy(cuda, B, noise, eos, k):
         bt.kv.copy_(_to_dev(cache, cuda))
         bt.step(torch.from_numpy(logits).to(cuda), torch.from_numpy(draft).to(cuda), V=V)
         first = False
+        rounds += 1
     gen = bt.gen.cpu().numpy()
     out = bt.out_buf.cpu().numpy()
-    assert [list(out[i, :gen[i]]) for i in range(B)] == ref
-    assert int(bt.status.item()) == 0
+    return [list(out[i, :gen[i]]) for i in range(B)], rounds, int(bt.status.item())
+
+
+@pytest.mark.parametrize("B,noise,eos,k", [(2, 0.3, 1, 4), (4, 0.0, -1, 4), (5, 0.45, 1, 3), (1, 0.2, 1, 5)])
+def test_eqspec_on_gpu_equals_greedy(cuda, B, noise, eos, k):
+    T = ToyLM(V, LAYERS, H, D, seed=7)
+    prompts = _prompts(B, seed=B * 10 + k)
+    ref = [T.greedy_generate(p, 18, eos, 64) for p in prompts]
+    out, rounds, status = _eqspec_gpu(cuda, T, prompts, k, 18, eos, noise)
+    assert out == ref and status == 0
+
+
+@pytest.mark.parametrize("B,noise", [(3, 0.3), (4, 0.0), (2, 0.5)])
+def test_draft_kv_realign_on_gpu(cuda, B, noise):
+    """f1: the drafter's own KV cache, realigned on the GPU with kept_draft = n + min(a, k-1),
+    reproduces recompute-mode proposals every round; output == greedy."""
+    T = ToyLM(V, LAYERS, H, D, seed=7)
+    Dm = ToyLM(V, LAYERS, H, D, seed=8)
+    prompts = _prompts(B, seed=200 + B)
+    ref = [T.greedy_generate(p, 18, 1, 64) for p in prompts]
+    log = []
+    out, rounds, status = _eqspec_gpu(cuda, T, prompts, 4, 18, 1, noise, drafter=Dm, draft_log=log)
+    assert out == ref and status == 0
+    assert len(log) >= rounds and all(c == r for c, r in log)
+
+
+@pytest.mark.parametrize("fault", ["skip_kv_realign", "bonus_from_draft", "stale_position_ids"])
+def test_fault_modes_break_equivalence(cuda, fault):
+    """f4: each §2 failure class, injected at its
+    seam of the GPU path, must be caught by the equivalence check (exact match < 1)."""
+    T = ToyLM(V, LAYERS, H, D, seed=7)
+    prompts = _prompts(4, seed=44)
+    ref = [T.greedy_generate(p, 16, -1, 64) for p in prompts]
+    out, _, _ = _eqspec_gpu(cuda, T, prompts, 4, 16, -1, 0.35)
+    assert out == ref                              # control
+    bad, _, _ = _eqspec_gpu(cuda, T, prompts, 4, 16, -1, 0.35, fault=fault)
+    assert bad != ref
 
 
 @pytest.mark.parametrize("N,Wn,B,mg", [(10, 6, 3, 2), (8, 8, 4, 4), (7, 7, 1, 2)])

@@ -212,3 +212,45 @@ def test_alignment_soundness_from_scratch():
     # the run exercised real shifts in both directions
     shifts = [int(s) for t in trace for s in (t["pad_new"] - t["pad"])]
     assert any(s > 0 for s in shifts) and any(s < 0 for s in shifts)
+
+
+# --------------------------------------------------------------------------- f1: draft KV realign
+def test_kept_draft_rule():
+    """n + min(a, k-1): d_k is generated by the draft but never forwarded."""
+    plan = V.repad_plan([10, 10, 10], [0, 3, 4], [0, 0, 1], k=4)
+    assert list(plan["kept_draft"]) == [10, 13, 0]
+    assert list(plan["kept"]) == [10, 13, 0]
+    plan = V.repad_plan([7], [4], [0], k=4)
+    assert plan["kept_draft"][0] == 7 + 3 and plan["kept"][0] == 11
+
+
+@pytest.mark.parametrize("noise,B", [(0.0, 3), (0.3, 4), (0.5, 2)])
+def test_draft_cache_realign_reproduces_recompute_drafts(noise, B):
+    """With its own KV cache realigned by kept_draft every round, the drafter proposes
+    exactly what a from-scratch (recompute) drafter proposes -- token for token, every
+    round -- and the batched output still equals greedy decoding."""
+    T = ToyLM(seed=7)
+    Dm = ToyLM(seed=8)
+    prompts = _prompts(B, seed=100 + B)
+    ref = [T.greedy_generate(p, 18, 1, 64) for p in prompts]
+    log = []
+    out, _ = eqspec_decode(T, Dm, prompts, 4, 18, 1, 64, noise=noise, draft_cache=True, draft_log=log)
+    assert out == ref
+    assert len(log) > 5 and all(c == r for c, r in log)
+    # a wrong kept rule (keeping d_k's slot as if it had draft KV) is caught
+    import oracle.verify as OVm
+    orig = OVm.repad_plan
+
+    def wrong(n, accept, finished, k=None):
+        p = orig(n, accept, finished, k)
+        if k is not None:
+            p["kept_draft"] = p["kept"].copy()
+        return p
+    import oracle.verify
+    oracle.verify.repad_plan = wrong
+    try:
+        log2 = []
+        eqspec_decode(T, T, prompts, 4, 18, 1, 64, noise=0.0, draft_cache=True, draft_log=log2)
+    finally:
+        oracle.verify.repad_plan = orig
+    assert any(c != r for c, r in log2)
