@@ -50,12 +50,16 @@ def parse():
     ap.add_argument("--min-group", type=int, default=2)
     ap.add_argument("--max-new", type=int, default=256)
     ap.add_argument("--shard", default="band", choices=["band", "strided"])
+    ap.add_argument("--pool-mode", default="epoch", choices=["epoch", "alg3"],
+                    help="epoch: run every batch of the window plan; alg3: batch 0 then re-plan")
     ap.add_argument("--B", type=int, default=0, help="override batch size")
     ap.add_argument("--pattern", default="alpha", choices=list(W.ACCEPT_PATTERNS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--draft-kv", action="store_true",
+                    help="f1: the draft model keeps its own KV cache, realigned every round too")
     ap.add_argument("--round-mode", default="graph-serial",
                     choices=["graph-fork", "graph-serial", "direct-fork", "direct-serial"],
                     help="value region: CUDA-graph replay or direct launches; K3 forked under K2 or serial")
@@ -143,9 +147,15 @@ def shape_for(args):
     return sh
 
 
+# draft models of the BASELINE pairs (layers, KV heads, head_dim): Vicuna-68M (2 x 12 x 64),
+# Qwen3-0.6B (28 x 8 x 128) for the Qwen3 and GLM-4 pairs; toy drafter = toy shape.
+DRAFT_DIMS = {"vicuna": (2, 12, 64), "qwen3": (28, 8, 128), "glm4": (28, 8, 128), "toy": (2, 2, 8)}
+
+
 def workload_name(sh, args):
+    d = f", draft KV {DRAFT_DIMS[sh.name]} realigned too" if getattr(args, "draft_kv", False) else ""
     return (f"{sh.name} EqSpec round: B={sh.B} k={sh.k} V={sh.V} KV {sh.layers}x{sh.H}x{sh.D} "
-            f"{sh.kv_dtype}, n~U[{sh.len_lo},{sh.len_hi}], accept={args.pattern}")
+            f"{sh.kv_dtype}, n~U[{sh.len_lo},{sh.len_hi}], accept={args.pattern}{d}")
 
 
 class RoundBench:
@@ -161,7 +171,10 @@ class RoundBench:
         self.cap = W.derive_cap(sh, total_rounds) if sh.name != "toy" else max(sh.cap, W.derive_cap(sh, total_rounds))
         self.lengths = W.gen_lengths(sh, args.seed, B)
         self.tokens = W.left_padded_tokens(self.lengths, self.cap, args.seed, sh.V)
-        self.bt = EqSpecBatch(B, k, self.cap, sh.layers, sh.H, sh.D, sh.kv_dtype, device)
+        draft = DRAFT_DIMS[sh.name] if args.draft_kv else None
+        self.bt = EqSpecBatch(B, k, self.cap, sh.layers, sh.H, sh.D, sh.kv_dtype, device, draft=draft)
+        if draft is not None:
+            self.bt.dkv.copy_(W.gen_kv_torch(args.seed + 1, self.bt.dkv.shape, self.bt.dkv.dtype, device))
         self.bt.load(self.tokens, self.lengths)
         self.bt.kv.copy_(W.gen_kv_torch(args.seed, self.bt.kv.shape, self.bt.kv.dtype, device))
         self.logits = [W.gen_logits_torch(args.seed, r, B, k, sh.V, sh.logit_dtype, device)
@@ -444,16 +457,26 @@ def run_pool(args, rank, world, device):
         ctr["i"] += 1
         return ring_lg[j], ring_dr[j]
 
+    ran = np.zeros(8, np.int64)
+
     def drain(events=None):
         sp.load(local_lens, order=local_order)
         sp.moved.zero_()
         epochs = batches = 0
+        ran[:] = 0
         while True:
             nb, kinds, blens, sizes = sp.plan()
             if nb == 0:
                 break
             epochs += 1
+            if args.pool_mode == "alg3":   # Alg. 3 as printed: batch 0, then re-plan
+                nb = 1
             for b in range(nb):
+                # counters of the batches that RAN: batches, same-length, their members,
+                # fallback members (K4's own counters count planned batches)
+                ran[0] += 1
+                ran[1 if kinds[b] else 3] += 1 if kinds[b] else int(sizes[b])
+                ran[2] += int(sizes[b]) if kinds[b] else 0
                 lg, d = inputs(b)
                 if events is not None and not kinds[b]:
                     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -487,7 +510,8 @@ def run_pool(args, rank, world, device):
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     moved = int(sp.moved.item())
-    cnt = counters.cpu().numpy()
+    cnt = ran.copy()          # executed batches (see drain); K4's counters: planned ones
+    cnt[5] = int(counters[0].item())
     status = int(sp.status.item())
     out_loc = sp.out_buf.cpu().numpy()
     gen_loc = sp.gen.cpu().numpy()
@@ -519,13 +543,14 @@ def run_pool(args, rank, world, device):
         "config": {"workload": f"EXSpec pool drain: {N} seqs, prompt {args.pool_lengths} "
                                f"{'U[64,512]' if args.pool_lengths == 'random' else '256'}, max_new "
                                f"{args.max_new}, W={Wn}/rank, B={sp.B}, min_group={args.min_group}, "
-                               f"sort on, {args.shard} shards, EOS off",
+                               f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}",
                    "cap": cap, "pool_kv_GB_per_rank": sp.kv.numel() * 2 / 1e9,
                    "parallelism": f"pool sharded x{world}", "step": "one epoch (K4 plan + its batches)"},
         "pool": {"epochs": epochs, "batch_verifications": int(cnt_all[0]),
                  "grouping_rate": rate_same, "same_length_batches": int(cnt_all[1]),
-                 "fallback_members": int(cnt_all[3]), "kv_bytes_moved_rank0": moved,
-                 "gather_ms": gather_ms},
+                 "fallback_members": int(cnt_all[3]), "planned_batches_K4": int(cnt_all[5]),
+                 "mean_batch": (int(cnt_all[2]) + int(cnt_all[3])) / max(1, int(cnt_all[0])),
+                 "kv_bytes_moved_rank0": moved, "gather_ms": gather_ms},
         "roofline": {"bound": "hbm", "kernel": "specdec_realign_kv gather+scatter (fallback batches)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_src},

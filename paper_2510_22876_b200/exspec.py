@@ -178,5 +178,17 @@ class SequencePool:
             self.run_batch(b, kinds[b], blens[b], lg, d, forward, V, stream)
         return nb, kinds, blens, sizes
 
+    def alg3_step(self, inputs, forward=None, V=None, stream=None):
+        """One iteration of Alg. 3 as printed: GetBatch -> draft ->
+        verify -> write-back -> RefillWindow, i.e. only batch 0 of the window plan runs
+        before the window is re-planned.  Returns False when the
+        pool has no active sequence."""
+        nb, kinds, blens, sizes = self.plan(stream)
+        if nb == 0:
+            return False
+        lg, d = inputs(0)
+        self.run_batch(0, kinds[0], blens[0], lg, d, forward, V, stream)
+        return True
+
     def has_active(self) -> bool:
         return bool(self.active.any().item())
