@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--anchor", action="store_true",
+                    help="f3: anchored-origin realign (K1 moves the KV origin to minimise moved rows)")
     ap.add_argument("--draft-kv", action="store_true",
                     help="f1: the draft model keeps its own KV cache, realigned every round too")
     ap.add_argument("--round-mode", default="graph-serial",
@@ -154,6 +156,7 @@ DRAFT_DIMS = {"vicuna": (2, 12, 64), "qwen3": (28, 8, 128), "glm4": (28, 8, 128)
 
 def workload_name(sh, args):
     d = f", draft KV {DRAFT_DIMS[sh.name]} realigned too" if getattr(args, "draft_kv", False) else ""
+    d += ", anchored origin (f3)" if getattr(args, "anchor", False) else ""
     return (f"{sh.name} EqSpec round: B={sh.B} k={sh.k} V={sh.V} KV {sh.layers}x{sh.H}x{sh.D} "
             f"{sh.kv_dtype}, n~U[{sh.len_lo},{sh.len_hi}], accept={args.pattern}{d}")
 
@@ -172,7 +175,10 @@ class RoundBench:
         self.lengths = W.gen_lengths(sh, args.seed, B)
         self.tokens = W.left_padded_tokens(self.lengths, self.cap, args.seed, sh.V)
         draft = DRAFT_DIMS[sh.name] if args.draft_kv else None
-        self.bt = EqSpecBatch(B, k, self.cap, sh.layers, sh.H, sh.D, sh.kv_dtype, device, draft=draft)
+        # f3: slack for the moving origin: at most k+1 columns of drift per round
+        slack = (k + 1) * total_rounds if args.anchor else 0
+        self.bt = EqSpecBatch(B, k, self.cap, sh.layers, sh.H, sh.D, sh.kv_dtype, device, draft=draft,
+                              anchor_slack=slack)
         if draft is not None:
             self.bt.dkv.copy_(W.gen_kv_torch(args.seed + 1, self.bt.dkv.shape, self.bt.dkv.dtype, device))
         self.bt.load(self.tokens, self.lengths)

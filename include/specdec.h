@@ -93,6 +93,14 @@ size_t specdec_verify_workspace_size(int64_t B, int64_t k);
  *          it caches its own k forwards (pending token, d_1..d_{k-1}; d_k has no draft KV):
  *          n_i + min(a_i, k-1) for still-active rows, 0 for finished rows.  Realign the
  *          draft cache with the same p -> p' as the target and this count.
+ * d_anchor [1] int32 or NULL (anchored origin), IN/OUT: the physical
+ *          column of the KV buffer where logical column 0 lives (base).  The logical
+ *          plan (tokens, masks, positions, p') is unchanged; the new origin base' = base + d
+ *          is chosen among d = 0 and d = (a+1) - (L'-L), a = 0..k, to minimise the KV rows
+ *          that move (ties: d = 0, then larger d), subject to 0 <= base' and
+ *          base' + L' + k <= anchor_cap (the physical capacity).  Then
+ *          d_phys_old[i] = base + (L - n_i) and d_phys_new[i] = base' + p'_i [B] int32 are
+ *          the src/dst columns for specdec_realign_kv (L = max n_i, R6).
  * d_ws: workspace of specdec_verify_workspace_size(B, k) bytes (see above).
  * d_status: optional (NULL ok); SPECDEC_ST_NAN.
  */
@@ -102,8 +110,9 @@ int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_t k, int64_
                    int32_t *d_budget, int32_t *d_accept, int64_t *d_bonus,
                    int32_t *d_emit, uint8_t *d_finished, int64_t *d_pred, int32_t *d_plan_L,
                    int32_t *d_n_new, int32_t *d_pad_new, int32_t *d_kept,
-                   int32_t *d_kept_draft, uint32_t *d_status, void *d_ws, size_t ws_bytes,
-                   specdec_stream_t stream);
+                   int32_t *d_kept_draft, int32_t *d_anchor, int64_t anchor_cap,
+                   int32_t *d_phys_old, int32_t *d_phys_new, uint32_t *d_status, void *d_ws,
+                   size_t ws_bytes, specdec_stream_t stream);
 
 /* ------------------------------------------------------------------------------ a2
  * specdec_rebuild_pos_mask -- Alg. 2 Phase 3 unpad-append-repad and

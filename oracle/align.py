@@ -119,6 +119,34 @@ def copy_rows(src, dst, count, src_col=None, dst_col=None, src_row=None, dst_row
     return dst
 
 
+def anchor_plan(pad_old, pad_new, kept, finished, accept, L_old, L_new, base, cap_phys, k):
+    """f3 ("anchored-origin realign"; PAPER.md:746 names KV locality as future
+    work).  The logical rectangle -- tokens, masks, positions, and the KV of logical
+    column c -- is exactly Alg. 2's; only its PHYSICAL origin `base` in the KV buffer may
+    move: logical column c lives at physical base + c.  Per round the new origin
+    base' = base + d is chosen among d = 0 and the shifts that leave one accept class in
+    place, d = (a + 1) - (L' - L), minimising the KV rows that must move (ties: d = 0,
+    then larger d), subject to 0 <= base' and base' + L' + k <= cap_phys.
+    Returns (base', physical old columns, physical new columns)."""
+    pad_old = np.asarray(pad_old, np.int64)
+    pad_new = np.asarray(pad_new, np.int64)
+    kept = np.asarray(kept, np.int64)
+    alive = np.asarray(finished) == 0
+    best_d, best_cost = 0, None
+    if L_new > 0:
+        cands = sorted({0} | {(a + 1) - (L_new - L_old) for a in range(k + 1)},
+                       key=lambda d: (d != 0, -d))
+        for d in cands:
+            if base + d < 0 or base + d + L_new + k > cap_phys:
+                continue
+            cost = int(sum(kept[i] for i in range(len(kept))
+                           if alive[i] and kept[i] > 0 and d + pad_new[i] != pad_old[i]))
+            if best_cost is None or cost < best_cost:
+                best_d, best_cost = d, cost
+    base_new = base + best_d
+    return base_new, (base + pad_old).astype(np.int32), (base_new + pad_new).astype(np.int32)
+
+
 def moved_bytes(pad_old, pad_new, kept, bpt):
     """Algorithmic bytes of an in-place realign: 2 * kept_i * bpt over
     rows whose padding changed (rows with Delta_i = 0 move nothing)."""

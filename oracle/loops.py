@@ -10,7 +10,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from .align import build_batch, mask_pos_row, realign_kv, repad_tokens, unpad
+from .align import (anchor_plan, build_batch, copy_rows, mask_pos_row, realign_kv, repad_tokens,
+                    unpad)
 from .pool import admission_order, form_batches
 from .toy_lm import ToyLM, greedy_fp32
 from .verify import batch_verify
@@ -64,17 +65,22 @@ def draft_cached(model: ToyLM, tokens_row, pad: int, L: int, dkept: int, cache_r
 
 
 def eqspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, cap,
-                  noise=0.0, pad_id=0, trace=None, draft_cache=False, draft_log=None):
+                  noise=0.0, pad_id=0, trace=None, draft_cache=False, draft_log=None,
+                  anchor_slack=0):
     """Alg. 2.  Returns (outputs per prompt, rounds).  With draft_cache=True the drafter
     keeps its own KV cache, realigned every round with kept_draft (f1); draft_log, if a
-    list, receives (cached proposals, recompute proposals) per round."""
+    list, receives (cached proposals, recompute proposals) per round.  With
+    anchor_slack > 0 the target KV lives in a physical buffer of cap + slack columns whose
+    logical origin moves by align.anchor_plan (f3); the forward reads the logical view."""
     B = len(prompts)
     tokens, pad, L = build_batch(prompts, cap, pad_id)
     n = np.array([len(p) for p in prompts], np.int32)
     active = np.ones(B, np.uint8)
     gen = np.zeros(B, np.int64)
     out = [[] for _ in range(B)]
-    cache = np.zeros((target.n_planes, B, target.H, cap, target.D), np.uint16)
+    phys = np.zeros((target.n_planes, B, target.H, cap + anchor_slack, target.D), np.uint16)
+    base = anchor_slack
+    cache = phys[:, :, :, base:base + cap]          # the logical view
     mask = np.stack([mask_pos_row(int(p), L + k)[0] for p in pad])
     pos = np.stack([mask_pos_row(int(p), L + k)[1] for p in pad])
     dcache = np.zeros((drafter.n_planes, B, drafter.H, cap, drafter.D), np.uint16)
@@ -103,7 +109,18 @@ def eqspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, ca
             trace.append(dict(L=L, pad=pad.copy(), n=n.copy(), accept=v["accept"].copy(),
                               kept=v["kept"].copy(), pad_new=v["pad_new"].copy()))
         tokens, mask, pos = repad_tokens(tokens, cap, k, pad, L, v, pad_id)
-        cache, _ = realign_kv(cache, pad, v["pad_new"], v["kept"])
+        if anchor_slack:
+            base_new, col_old, col_new = anchor_plan(pad, v["pad_new"], v["kept"], v["finished"],
+                                                     v["accept"], L, v["L_new"], base,
+                                                     cap + anchor_slack, k)
+            rows = np.moveaxis(phys, 1, 0)          # [B][planes][H][cap+slack][D] view
+            copy_rows(rows, rows, v["kept"], src_col=col_old, dst_col=col_new)
+            base = base_new
+            cache = phys[:, :, :, base:base + cap]
+            if trace is not None:
+                trace[-1]["base"] = base
+        else:
+            cache, _ = realign_kv(cache, pad, v["pad_new"], v["kept"])
         if draft_cache:
             dcache, _ = realign_kv(dcache, pad, v["pad_new"], v["kept_draft"])
             dkept = v["kept_draft"]

@@ -31,7 +31,8 @@ _SIGS = {
     "specdec_last_cuda_error": ([], ctypes.c_char_p),
     "specdec_verify_workspace_size": ([_I64, _I64], ctypes.c_size_t),
     "specdec_verify": ([_P, _INT, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
-                        _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P], _INT),
+                        _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P,
+                        ctypes.c_size_t, _P], _INT),
     "specdec_rebuild_pos_mask": ([_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P,
                                   _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P], _INT),
     "specdec_realign_kv": ([_P, _P, _INT, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
@@ -103,15 +104,17 @@ def specdec_verify_workspace_size(B: int, k: int) -> int:
 
 def specdec_verify(logits, draft, n, active, accept, bonus, emit, finished, plan_L, n_new,
                    pad_new, kept, ws, *, V=None, eos_id=-1, pad_id=0, budget=None, pred=None,
-                   kept_draft=None, status=None, stream=None):
+                   kept_draft=None, anchor=None, anchor_cap=0, phys_old=None, phys_new=None,
+                   status=None, stream=None):
     """logits [B, k+1, row_stride] (fp32/fp16/bf16); see include/specdec.h."""
     B, K1, rs = logits.shape
     _check(load().specdec_verify(
         _ptr(logits), DTYPE[logits.dtype], B, K1 - 1, rs if V is None else V, logits.stride(1),
         _ptr(draft), _ptr(n), _ptr(active), eos_id, pad_id, _ptr(budget), _ptr(accept),
         _ptr(bonus), _ptr(emit), _ptr(finished), _ptr(pred), _ptr(plan_L), _ptr(n_new),
-        _ptr(pad_new), _ptr(kept), _ptr(kept_draft), _ptr(status), _ptr(ws),
-        ws.numel() * ws.element_size(), _stream(stream)), "specdec_verify")
+        _ptr(pad_new), _ptr(kept), _ptr(kept_draft), _ptr(anchor), anchor_cap, _ptr(phys_old),
+        _ptr(phys_new), _ptr(status), _ptr(ws), ws.numel() * ws.element_size(),
+        _stream(stream)), "specdec_verify")
 
 
 def specdec_rebuild_pos_mask(tokens_in, tokens_out, k, n_old, pad_old, draft, accept, bonus,

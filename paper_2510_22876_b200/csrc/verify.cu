@@ -39,6 +39,9 @@ struct VerifyParams {
     uint8_t *finished;
     int64_t *pred;
     int32_t *plan_L, *n_new, *pad_new, *kept, *kept_draft;
+    int32_t *anchor;          // f3: physical origin (in/out), NULL = off
+    int64_t anchor_cap;
+    int32_t *phys_old, *phys_new;
     uint32_t *status;
     unsigned long long *ws_keys;  // [B*(k+1)]
     unsigned int *ws_counter;      // [1]
@@ -56,13 +59,19 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 // ----------------------------------------------------------------------------- epilogue
 __device__ void verify_epilogue(const VerifyParams &p) {
     __shared__ int s_red[kVerifyThreads / kWarp];
+    __shared__ int s_nmax[kVerifyThreads / kWarp];
+    __shared__ unsigned long long s_w[kMaxK + 1];  // f3: kept rows per accept class
+    __shared__ int s_base[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const int k = static_cast<int>(p.k);
     const int K1 = k + 1;
-    int local_max = 0;
+    if (threadIdx.x <= kMaxK) s_w[threadIdx.x] = 0ull;
+    __syncthreads();
+    int local_max = 0, local_nmax = 0;
     for (int64_t i = warp; i < p.B; i += nwarps) {
         const bool act = p.active[i] != 0;
+        local_nmax = max(local_nmax, p.n[i]);  // old width L = max n (R6 held last round)
         int a = 0, m = 0, nn = 1, kp = 0;
         int64_t b = p.pad_id;
         bool fin = true;
@@ -106,16 +115,61 @@ __device__ void verify_epilogue(const VerifyParams &p) {
             // f1: a draft model that cached its own k forwards (pending token, d_1..d_{k-1})
             // keeps n + min(a, k-1) entries: d_k never had a draft KV entry
             if (p.kept_draft) p.kept_draft[i] = kp ? p.n[i] + min(a, k - 1) : 0;
+            if (p.anchor && kp) atomicAdd(&s_w[a], static_cast<unsigned long long>(kp));
         }
     }
     // L' = max n' over still-active rows (R6 minimal padding)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) local_max = max(local_max, __shfl_xor_sync(0xFFFFFFFFu, local_max, o));
-    if (lane == 0) s_red[warp] = local_max;
+    for (int o = 16; o > 0; o >>= 1) {
+        local_max = max(local_max, __shfl_xor_sync(0xFFFFFFFFu, local_max, o));
+        local_nmax = max(local_nmax, __shfl_xor_sync(0xFFFFFFFFu, local_nmax, o));
+    }
+    if (lane == 0) {
+        s_red[warp] = local_max;
+        s_nmax[warp] = local_nmax;
+    }
     __syncthreads();
-    int Lnew = 0;
-    for (int w = 0; w < nwarps; ++w) Lnew = max(Lnew, s_red[w]);
-    for (int64_t i = threadIdx.x; i < p.B; i += blockDim.x) p.pad_new[i] = Lnew > 0 ? Lnew - p.n_new[i] : 0;
+    int Lnew = 0, Lold = 0;
+    for (int w = 0; w < nwarps; ++w) {
+        Lnew = max(Lnew, s_red[w]);
+        Lold = max(Lold, s_nmax[w]);
+    }
+    if (p.anchor && threadIdx.x == 0) {
+        // f3: move the physical origin to the shift d that leaves the heaviest accept class
+        // in place (rows with a = d + (L' - L) - 1 do not move); candidates d = 0 first,
+        // then larger d; feasible iff 0 <= base + d and base + d + L' + k <= anchor_cap.
+        const int64_t base = *p.anchor;
+        unsigned long long total = 0;
+        for (int a = 0; a <= k; ++a) total += s_w[a];
+        auto saved = [&](int64_t d) -> unsigned long long {
+            const int64_t a = d + (Lnew - Lold) - 1;
+            return (a >= 0 && a <= k) ? s_w[a] : 0ull;
+        };
+        auto feasible = [&](int64_t d) { return base + d >= 0 && base + d + Lnew + k <= p.anchor_cap; };
+        int64_t best = 0;
+        unsigned long long best_cost = ~0ull;
+        if (Lnew > 0) {
+            if (feasible(0)) best_cost = total - saved(0);
+            for (int a = k; a >= 0; --a) {  // larger d first
+                const int64_t d = (a + 1) - (Lnew - Lold);
+                if (d == 0 || !feasible(d)) continue;
+                const unsigned long long c = total - s_w[a];
+                if (c < best_cost) { best_cost = c; best = d; }
+            }
+        }
+        s_base[0] = static_cast<int>(base);
+        s_base[1] = static_cast<int>(base + best);
+        *p.anchor = static_cast<int32_t>(base + best);
+    }
+    if (p.anchor) __syncthreads();
+    for (int64_t i = threadIdx.x; i < p.B; i += blockDim.x) {
+        const int32_t pn = Lnew > 0 ? Lnew - p.n_new[i] : 0;
+        p.pad_new[i] = pn;
+        if (p.anchor) {
+            p.phys_old[i] = s_base[0] + (Lold - p.n[i]);
+            p.phys_new[i] = s_base[1] + pn;
+        }
+    }
     if (threadIdx.x == 0) {
         *p.plan_L = Lnew;
         *p.ws_counter = 0u;  // self-clean
@@ -296,9 +350,12 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
                               int32_t *d_budget, int32_t *d_accept, int64_t *d_bonus,
                               int32_t *d_emit, uint8_t *d_finished, int64_t *d_pred,
                               int32_t *d_plan_L, int32_t *d_n_new, int32_t *d_pad_new,
-                              int32_t *d_kept, int32_t *d_kept_draft, uint32_t *d_status,
-                              void *d_ws, size_t ws_bytes, specdec_stream_t stream) {
+                              int32_t *d_kept, int32_t *d_kept_draft, int32_t *d_anchor,
+                              int64_t anchor_cap, int32_t *d_phys_old, int32_t *d_phys_new,
+                              uint32_t *d_status, void *d_ws, size_t ws_bytes,
+                              specdec_stream_t stream) {
     const int es = dtype_size(dtype);
+    if (d_anchor && (!d_phys_old || !d_phys_new || anchor_cap < k + 2)) return SPECDEC_ERR_ARG;
     if (es == 0) return SPECDEC_ERR_DTYPE;
     if (k < 1 || k > kMaxK) return SPECDEC_ERR_ARG;
     if (B < 1 || V < 1 || row_stride < V || V > 0x7FFFFFFFll) return SPECDEC_ERR_SHAPE;
@@ -318,6 +375,7 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
     p.accept = d_accept; p.bonus = d_bonus; p.emit = d_emit; p.finished = d_finished;
     p.pred = d_pred; p.plan_L = d_plan_L; p.n_new = d_n_new; p.pad_new = d_pad_new; p.kept = d_kept;
     p.kept_draft = d_kept_draft;
+    p.anchor = d_anchor; p.anchor_cap = anchor_cap; p.phys_old = d_phys_old; p.phys_new = d_phys_new;
     p.status = d_status;
     p.ws_keys = static_cast<unsigned long long *>(d_ws);
     p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);

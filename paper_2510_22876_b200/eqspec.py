@@ -12,6 +12,10 @@ spread over many CTAs).  The KV cache -- the only large state -- is realigned in
 `active` and the remaining `budget` are updated in place by K1.  Everything is
 capacity-sized, so the data-dependent width L' never leaves the device,
 and a round can be captured once per (parity, input buffer) as a CUDA graph.
+
+Options: `draft=(layers, H, D)` adds the draft model's own KV cache,
+realigned with kept_draft (f1); `anchor_slack=S` keeps the KV in a physical buffer of
+cap + S columns whose logical origin K1 moves to minimise the rows that must move (f3).
 """
 from __future__ import annotations
 
@@ -25,9 +29,7 @@ TORCH_DT = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16
 
 class EqSpecBatch:
     def __init__(self, B, k, cap, layers, H, D, kv_dtype="bf16", device="cuda", max_new=0,
-                 eos_id=-1, pad_id=0, with_pred=False, draft=None):
-        """draft = (layers, H, D) of a draft model that keeps its own KV cache (f1): it is
-        realigned every round with the target's p -> p' and kept_draft = n + min(a, k-1)."""
+                 eos_id=-1, pad_id=0, with_pred=False, draft=None, anchor_slack=0):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         self.B, self.k, self.cap, self.layers, self.H, self.D = B, k, cap, layers, H, D
@@ -54,13 +56,19 @@ class EqSpecBatch:
         self.moved = torch.zeros(1, dtype=i64, device=dev)
         ws = _abi.specdec_verify_workspace_size(B, k)
         self.ws = torch.zeros((ws + 7) // 8, dtype=i64, device=dev)
-        self.kv = torch.zeros((self.n_planes, B, H, cap, D), dtype=TORCH_DT[kv_dtype], device=dev)
+        # f3: physical KV columns = logical capacity + slack for the moving origin
+        self.anchor_slack = anchor_slack
+        self.cap_phys = cap + anchor_slack
+        self.anchor = torch.full((1,), anchor_slack, dtype=i32, device=dev) if anchor_slack else None
+        self.phys_old = torch.zeros(B, dtype=i32, device=dev) if anchor_slack else None
+        self.phys_new = torch.zeros(B, dtype=i32, device=dev) if anchor_slack else None
+        self.kv = torch.zeros((self.n_planes, B, H, self.cap_phys, D), dtype=TORCH_DT[kv_dtype], device=dev)
         self.dkv = None
         self.kept_draft = None
         if draft is not None:
             dl, dh, dd = draft
             self.d_dims = (2 * dl, dh, dd)
-            self.dkv = torch.zeros((2 * dl, B, dh, cap, dd), dtype=TORCH_DT[kv_dtype], device=dev)
+            self.dkv = torch.zeros((2 * dl, B, dh, self.cap_phys, dd), dtype=TORCH_DT[kv_dtype], device=dev)
             self.kept_draft = torch.zeros(B, dtype=i32, device=dev)
         self.cur = 0
         self.V = None
@@ -72,7 +80,8 @@ class EqSpecBatch:
 
     # ----------------------------------------------------------------- state I/O
     def load(self, tokens, lengths, kv=None):
-        """tokens [B, cap] left-padded at width L = max(lengths); kv [planes, B, H, cap, D]."""
+        """tokens [B, cap] left-padded at width L = max(lengths); kv [planes, B, H, cap, D]
+        (logical columns; placed at the origin when anchored)."""
         lengths = torch.as_tensor(np.asarray(lengths), dtype=torch.int32)
         L = int(lengths.max())
         self.cur = 0
@@ -85,8 +94,19 @@ class EqSpecBatch:
         self.gen.zero_()
         if self.kept_draft is not None:
             self.kept_draft.zero_()     # no draft KV yet: the drafter prefills in round 1
+        if self.anchor is not None:
+            self.anchor.fill_(self.anchor_slack)
         if kv is not None:
-            self.kv.copy_(kv)
+            self.kv_logical().copy_(kv)
+
+    def base(self) -> int:
+        """Physical column of logical column 0 (host read; 0 unless anchored)."""
+        return int(self.anchor.item()) if self.anchor is not None else 0
+
+    def kv_logical(self, kv=None):
+        kv = self.kv if kv is None else kv
+        b = self.base()
+        return kv[:, :, :, b:b + self.cap]
 
     @property
     def tokens(self):
@@ -112,8 +132,9 @@ class EqSpecBatch:
                             self.emit, self.finished, self.plan_L, self.n[nx], self.pad[nx],
                             self.kept, self.ws, V=self.V or logits.shape[2],
                             eos_id=self.eos_id, pad_id=self.pad_id, budget=self.budget,
-                            pred=self.pred, kept_draft=self.kept_draft, status=self.status,
-                            stream=stream)
+                            pred=self.pred, kept_draft=self.kept_draft, anchor=self.anchor,
+                            anchor_cap=self.cap_phys, phys_old=self.phys_old,
+                            phys_new=self.phys_new, status=self.status, stream=stream)
 
     def repad(self, draft, stream=None):
         c, nx = self.cur, 1 - self.cur
@@ -124,28 +145,29 @@ class EqSpecBatch:
                                       gen=self.gen if self.out_buf is not None else None,
                                       status=self.status, stream=stream)
 
-    def realign(self, stream=None):
-        c, nx = self.cur, 1 - self.cur
-        _abi.specdec_realign_kv(self.kv, self.kv, self.kept, n_planes=self.n_planes,
-                                n_rows=self.B, H=self.H, D=self.D, src_strides=self.kv_strides,
-                                dst_strides=self.kv_strides, cap_src=self.cap, cap_dst=self.cap,
-                                src_col=self.pad[c], dst_col=self.pad[nx],
+    def _realign_one(self, kv, count, dims, src, dst, stream):
+        planes, H, D = dims
+        s = kv.stride()
+        _abi.specdec_realign_kv(kv, kv, count, n_planes=planes, n_rows=self.B, H=H, D=D,
+                                src_strides=s[:3], dst_strides=s[:3], cap_src=self.cap_phys,
+                                cap_dst=self.cap_phys, src_col=src, dst_col=dst,
                                 flags=_abi.ZERO_PADS if self.zero_pads else 0,
                                 moved_bytes=self.moved, status=self.status, stream=stream)
+
+    def realign(self, stream=None):
+        c, nx = self.cur, 1 - self.cur
+        if self.anchor is not None:
+            src, dst = self.phys_old, self.phys_new        # f3: physical columns from K1
+        else:
+            src, dst = self.pad[c], self.pad[nx]
+        self._realign_one(self.kv, self.kept, (self.n_planes, self.H, self.D), src, dst, stream)
         if self.dkv is not None:     # f1: the draft model's own cache, same shift, kept_draft
-            dp, dh, dd = self.d_dims
-            s = self.dkv.stride()
-            _abi.specdec_realign_kv(self.dkv, self.dkv, self.kept_draft, n_planes=dp,
-                                    n_rows=self.B, H=dh, D=dd, src_strides=s[:3],
-                                    dst_strides=s[:3], cap_src=self.cap, cap_dst=self.cap,
-                                    src_col=self.pad[c], dst_col=self.pad[nx],
-                                    flags=_abi.ZERO_PADS if self.zero_pads else 0,
-                                    moved_bytes=self.moved, status=self.status, stream=stream)
+            self._realign_one(self.dkv, self.kept_draft, self.d_dims, src, dst, stream)
 
     def launch_round(self, logits, draft, stream=None):
         """Enqueue K1 -> {K3 || K2} for the current parity (does not flip it).  K3 (tokens,
         masks, positions) and K2 (KV) both depend only on K1's plan and touch disjoint
-        memory, so K3 runs on a side stream under K2; the main stream joins it at the end."""
+        memory, so with `fork` K3 runs on a side stream under K2."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         if not self.fork:
             self.verify(logits, draft, s)

@@ -44,19 +44,19 @@ def test_host_validation_without_gpu(lib):
     nz = ctypes.c_void_p(16)   # never dereferenced: validation fails first
     # k < 1 -> ERR_ARG
     rc = L.specdec_verify(nz, 2, 8, 0, 100, 100, *([nz] * 3), -1, 0, None, *([nz] * 4), None,
-                          *([nz] * 4), None, None, nz, 1 << 20, None)
+                          *([nz] * 4), None, None, 0, None, None, None, nz, 1 << 20, None)
     assert rc == _abi.ERR_ARG
     # unknown dtype
     rc = L.specdec_verify(nz, 9, 8, 5, 100, 100, *([nz] * 3), -1, 0, None, *([nz] * 4), None,
-                          *([nz] * 4), None, None, nz, 1 << 20, None)
+                          *([nz] * 4), None, None, 0, None, None, None, nz, 1 << 20, None)
     assert rc == _abi.ERR_DTYPE
     # row_stride < V
     rc = L.specdec_verify(nz, 2, 8, 5, 100, 50, *([nz] * 3), -1, 0, None, *([nz] * 4), None,
-                          *([nz] * 4), None, None, nz, 1 << 20, None)
+                          *([nz] * 4), None, None, 0, None, None, None, nz, 1 << 20, None)
     assert rc == _abi.ERR_SHAPE
     # misaligned row stride (bf16, 100 elements = 200 B, not a multiple of 16)
     rc = L.specdec_verify(nz, 2, 8, 5, 100, 100, *([nz] * 3), -1, 0, None, *([nz] * 4), None,
-                          *([nz] * 4), None, None, nz, 1 << 20, None)
+                          *([nz] * 4), None, None, 0, None, None, None, nz, 1 << 20, None)
     assert rc == _abi.ERR_ARG
     # realign: D*elem not a multiple of 16
     rc = L.specdec_realign_kv(nz, nz, 2, 2, 2, 2, 4, 64, 64, 64, 8, 64, 64, 64, 8, None, 0,

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos_id=-1,
-                zero_pads=False, full_check=True):
+                zero_pads=False, full_check=True, anchor_slack=0):
     k, V = shape.k, shape.V
     cap = W.derive_cap(shape.with_(B=B), rounds)
     lengths = W.gen_lengths(shape, seed, B)
@@ -24,8 +24,10 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
     kvshape = (shape.n_planes, B, shape.H, cap, shape.D)
     kv_bits = W.gen_kv_bits_np(seed, int(np.prod(kvshape))).reshape(kvshape)
     bt = EqSpecBatch(B, k, cap, shape.layers, shape.H, shape.D, shape.kv_dtype, cuda,
-                     max_new=max_new, eos_id=eos_id, pad_id=W.PAD_ID)
+                     max_new=max_new, eos_id=eos_id, pad_id=W.PAD_ID, anchor_slack=anchor_slack)
     bt.load(tokens, lengths, bits_to_torch(kv_bits, shape.kv_dtype, cuda))
+    base_o = anchor_slack
+    bases = []
     # oracle state
     tok_o, kv_o = tokens.copy(), kv_bits.copy()
     n_o = lengths.astype(np.int32)
@@ -42,7 +44,7 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
         fwd = W.gen_kv_bits_np(seed + 1000 + r, shape.n_planes * B * shape.H * (k + 1) * shape.D)
         fwd = fwd.reshape(shape.n_planes, B, shape.H, k + 1, shape.D)
         kv_o[:, :, :, L - 1:L + k, :] = fwd
-        bt.kv[:, :, :, L - 1:L + k, :] = bits_to_torch(fwd, shape.kv_dtype, cuda)
+        bt.kv_logical()[:, :, :, L - 1:L + k, :] = bits_to_torch(fwd, shape.kv_dtype, cuda)
         rt = W.gen_round_truth(seed, r, B, k, V, pattern)
         bits = W.gen_logits_np(seed, r, B, k, V, shape.logit_dtype)
         lg = padded_logits(bits, shape.logit_dtype, cuda, extra=16)
@@ -53,7 +55,18 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
         v = OV.batch_verify(bits, shape.logit_dtype, rt.draft, n_o, pad_o, act_o, eos_id, budget, W.PAD_ID)
         tok_n, mask_n, pos_n = OA.repad_tokens(tok_o, cap, k, pad_o, L, v, W.PAD_ID)
         kv_n, defined = OA.realign_kv(kv_o, pad_o, v["pad_new"], v["kept"])
-        moved_expect += OA.moved_bytes(pad_o, v["pad_new"], v["kept"], shape.bpt)
+        if anchor_slack:
+            b2, col_old, col_new = OA.anchor_plan(pad_o, v["pad_new"], v["kept"], v["finished"],
+                                                  v["accept"], L, v["L_new"], base_o,
+                                                  cap + anchor_slack, k)
+            moved_expect += OA.moved_bytes(col_old, col_new, v["kept"], shape.bpt)
+            assert bt.base() == b2, r
+            assert np.array_equal(bt.phys_old.cpu().numpy(), col_old)
+            assert np.array_equal(bt.phys_new.cpu().numpy(), col_new)
+            base_o = b2
+            bases.append(b2)
+        else:
+            moved_expect += OA.moved_bytes(pad_o, v["pad_new"], v["kept"], shape.bpt)
         zero_regions = OA.zero_pad_region(pad_o, v["pad_new"], v["kept"])
         for i in range(B):
             out_o[i] += v["E"][i]
@@ -73,7 +86,7 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
             assert np.array_equal(bt.mask[:, :Ln + k].cpu().numpy(), mask_n), r
             assert np.array_equal(bt.pos[:, :Ln + k].cpu().numpy(), pos_n), r
         if full_check:
-            kv_g = torch_to_bits(bt.kv)
+            kv_g = torch_to_bits(bt.kv_logical())
             for i in range(B):
                 cols = np.flatnonzero(defined[i])
                 if len(cols):
@@ -92,7 +105,7 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
         tok_o, n_o, pad_o, L = tok_n, v["n_new"], v["pad_new"], Ln
         act_o = (v["finished"] == 0).astype(np.uint8)
     assert int(bt.moved.item()) == moved_expect
-    return r + 1
+    return dict(rounds=r + 1, bases=bases, moved=moved_expect)
 
 
 SMALL = W.Shape("small", 3001, 2, 2, 64, "bf16", "bf16", 8, 5, 160, 40, 160)
@@ -104,8 +117,23 @@ def test_rounds_small(cuda, pattern):
     _run_rounds(cuda, SMALL, 8, 10, pattern)
 
 
+@pytest.mark.parametrize("pattern,slack", [("alpha", 64), ("alternating", 64), ("alpha", 3)])
+def test_rounds_anchored_origin(cuda, pattern, slack):
+    """f3: K1 moves the physical origin exactly as oracle.align.anchor_plan; the logical
+    KV equals Alg. 2's realign and fewer bytes move than with the fixed origin."""
+    anc = _run_rounds(cuda, SMALL, 8, 12, pattern, seed=3, anchor_slack=slack)
+    std = _run_rounds(cuda, SMALL, 8, 12, pattern, seed=3)          # same workload, fixed origin
+    assert anc["moved"] <= std["moved"]
+    if slack >= 64:
+        assert len(set(anc["bases"])) > 1 and anc["moved"] < std["moved"]
+
+
+def test_rounds_anchored_with_finish(cuda):
+    _run_rounds(cuda, SMALL16, 6, 14, "alpha", seed=2, max_new=33, anchor_slack=32)
+
+
 def test_rounds_toy_with_budget_and_finish(cuda):
-    n = _run_rounds(cuda, W.SHAPES["toy"], 2, 40, "alpha", max_new=20)
+    n = _run_rounds(cuda, W.SHAPES["toy"], 2, 40, "alpha", max_new=20)["rounds"]
     assert n < 40  # every row finished before the round cap
 
 

@@ -33,7 +33,7 @@ def _prompts(n, seed):
 
 
 def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, drafter=None,
-                draft_log=None):
+                draft_log=None, anchor_slack=0):
     """EqSpec with the toy LM on the host and K1/K3/K2 in libspecdec.so.  `fault` injects
     one of the paper's §2 failure classes at a module seam.  With a
     `drafter`, the draft model keeps its own KV cache on the GPU, realigned by K2 with
@@ -41,7 +41,7 @@ def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, dr
     B = len(prompts)
     tokens, pad, L = build_batch(prompts, cap)
     bt = EqSpecBatch(B, k, cap, LAYERS, H, D, "bf16", cuda, max_new=max_new, eos_id=eos,
-                     draft=None if drafter is None else (LAYERS, H, D))
+                     draft=None if drafter is None else (LAYERS, H, D), anchor_slack=anchor_slack)
     bt.load(tokens, [len(p) for p in prompts])
     if fault == "skip_kv_realign":             # DSD error (iii): KV not realigned
         bt.realign = lambda stream=None: None
@@ -81,15 +81,17 @@ def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, dr
                 if act[i]:
                     draft[i] = T.propose(list(tok[i, pad_c[i]:L]), k, noise)
         else:
-            dcache = _bits(bt.dkv).copy()
+            dview = bt.kv_logical(bt.dkv)
+            dcache = _bits(dview).copy()
             dkept = bt.kept_draft.cpu().numpy()
             for i in range(B):
                 if act[i]:
                     draft[i] = draft_cached(drafter, tok[i], int(pad_c[i]), L, int(dkept[i]),
                                             dcache[:, i], k, noise)
                     draft_log.append((list(draft[i]), drafter.propose(list(tok[i, pad_c[i]:L]), k, noise)))
-            bt.dkv.copy_(_to_dev(dcache, cuda))
-        cache = _bits(bt.kv).copy()
+            dview.copy_(_to_dev(dcache, cuda))
+        kv_view = bt.kv_logical()                # f3: logical columns start at the origin
+        cache = _bits(kv_view).copy()
         logits = np.zeros((B, k + 1, V), np.float32)
         for i in range(B):
             if not act[i]:
@@ -100,7 +102,7 @@ def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, dr
                     lg = T.token_forward(t, int(pos[i, c]), c, cache[:, i], mask[i])
                     if c >= L - 1:
                         logits[i, c - L + 1] = lg.astype(np.float32)
-        bt.kv.copy_(_to_dev(cache, cuda))
+        kv_view.copy_(_to_dev(cache, cuda))
         bt.step(torch.from_numpy(logits).to(cuda), torch.from_numpy(draft).to(cuda), V=V)
         first = False
         rounds += 1
@@ -212,3 +214,18 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg):
     assert not sp.has_active() and int(sp.status.item()) == 0
     if B > 1:
         assert kinds_seen == {0, 1}           # both lazy (same-length) and fallback batches ran
+
+
+@pytest.mark.parametrize("B,noise,slack,draft", [(3, 0.3, 48, False), (4, 0.45, 48, True), (2, 0.3, 2, False)])
+def test_anchored_origin_on_gpu_equals_greedy(cuda, B, noise, slack, draft):
+    """f3: the forward reads the KV through K1's moving origin; output == greedy, with the
+    drafter's cache (f1) sharing the same origin when enabled."""
+    T = ToyLM(V, LAYERS, H, D, seed=7)
+    Dm = ToyLM(V, LAYERS, H, D, seed=8) if draft else None
+    prompts = _prompts(B, seed=400 + B)
+    ref = [T.greedy_generate(p, 18, 1, 64) for p in prompts]
+    log = []
+    out, rounds, status = _eqspec_gpu(cuda, T, prompts, 4, 18, 1, noise, drafter=Dm, draft_log=log,
+                                      anchor_slack=slack)
+    assert out == ref and status == 0
+    assert all(c == r for c, r in log)

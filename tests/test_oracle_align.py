@@ -254,3 +254,69 @@ def test_draft_cache_realign_reproduces_recompute_drafts(noise, B):
     finally:
         oracle.verify.repad_plan = orig
     assert any(c != r for c, r in log2)
+
+
+# --------------------------------------------------------------------------- f3: anchored origin
+def _cost(d, pad_old, pad_new, kept, alive):
+    return sum(int(kept[i]) for i in range(len(kept)) if alive[i] and kept[i] > 0 and d + pad_new[i] != pad_old[i])
+
+
+def test_anchor_plan_is_the_brute_force_minimum():
+    """The chosen origin moves the fewest KV rows of ALL feasible origins (brute force over
+    every shift), never more than the standard alignment (d = 0)."""
+    rng = np.random.default_rng(1)
+    for _ in range(400):
+        B, k = int(rng.integers(1, 7)), int(rng.integers(1, 6))
+        n = rng.integers(1, 30, B)
+        a = rng.integers(0, k + 1, B)
+        fin = (rng.random(B) < 0.2).astype(np.uint8)
+        plan = V.repad_plan(n, a, fin)
+        L, Ln = int(n.max()), plan["L_new"]
+        pad_old = L - n
+        base = int(rng.integers(0, 12))
+        cap_phys = base + Ln + k + int(rng.integers(0, 12))
+        b2, col_old, col_new = A.anchor_plan(pad_old, plan["pad_new"], plan["kept"], fin, a, L, Ln,
+                                             base, cap_phys, k)
+        d = b2 - base
+        alive = fin == 0
+        feas = [x for x in range(-base, cap_phys - base - Ln - k + 1)] if Ln else [0]
+        best = min(_cost(x, pad_old, plan["pad_new"], plan["kept"], alive) for x in feas)
+        assert _cost(d, pad_old, plan["pad_new"], plan["kept"], alive) == best
+        assert best <= _cost(0, pad_old, plan["pad_new"], plan["kept"], alive)
+        assert 0 <= b2 and (Ln == 0 or b2 + Ln + k <= cap_phys)
+        assert list(col_old) == list(base + pad_old) and list(col_new) == list(b2 + plan["pad_new"])
+
+
+def test_anchor_moves_only_the_logical_origin():
+    """Physically realigned KV, read through the moved origin, equals Alg. 2's realign."""
+    rng = np.random.default_rng(2)
+    for _ in range(60):
+        B, k, slack = int(rng.integers(1, 6)), 4, 10
+        n = rng.integers(2, 20, B)
+        a = rng.integers(0, k + 1, B)
+        plan = V.repad_plan(n, a, np.zeros(B, np.uint8))
+        L, Ln = int(n.max()), plan["L_new"]
+        cap = Ln + k + 2
+        logical = rng.integers(0, 1 << 15, size=(2, B, 1, cap, 3))
+        phys = np.zeros((2, B, 1, cap + slack, 3), np.int64)
+        phys[:, :, :, slack:slack + cap] = logical
+        b2, co, cn = A.anchor_plan(L - n, plan["pad_new"], plan["kept"], np.zeros(B), a, L, Ln,
+                                   slack, cap + slack, k)
+        rows = np.moveaxis(phys, 1, 0)
+        A.copy_rows(rows, rows, plan["kept"], src_col=co, dst_col=cn)
+        ref, defined = A.realign_kv(logical, L - n, plan["pad_new"], plan["kept"])
+        view = phys[:, :, :, b2:b2 + cap]
+        for i in range(B):
+            c = np.flatnonzero(defined[i])
+            assert np.array_equal(view[:, i, :, c], ref[:, i, :, c])
+
+
+@pytest.mark.parametrize("B,noise", [(3, 0.3), (4, 0.45)])
+def test_anchored_eqspec_equals_greedy_and_moves_less(B, noise):
+    T = ToyLM(seed=7)
+    prompts = _prompts(B, seed=300 + B)
+    ref = [T.greedy_generate(p, 20, -1, 64) for p in prompts]
+    tr = []
+    out, _ = eqspec_decode(T, T, prompts, 4, 20, -1, 64, noise=noise, anchor_slack=40, trace=tr)
+    assert out == ref
+    assert any(t["base"] != 40 for t in tr)       # the origin actually moved
