@@ -147,8 +147,10 @@ def test_fault_modes_break_equivalence(cuda, fault):
     assert bad != ref
 
 
-@pytest.mark.parametrize("N,Wn,B,mg", [(10, 6, 3, 2), (8, 8, 4, 4), (7, 7, 1, 2)])
-def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg):
+@pytest.mark.parametrize("N,Wn,B,mg,alg3", [(10, 6, 3, 2, False), (8, 8, 4, 4, False), (7, 7, 1, 2, False),
+                                             (9, 6, 3, 2, True)])
+def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3):
+    """EXSpec on the GPU path; alg3=True runs Alg. 3 as printed (batch 0, then re-plan)."""
     T = ToyLM(V, LAYERS, H, D, seed=7)
     k, max_new = 3, 12
     prompts = _prompts(N, seed=N + B)
@@ -167,11 +169,11 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg):
                       device=cuda)
     sp.load(lens, tokens, order, _to_dev(kv, cuda))
     kinds_seen = set()
-    for _ in range(80):
+    for _ in range(400):
         nb, kinds, blens, sizes = sp.plan()
         if nb == 0:
             break
-        for b in range(nb):
+        for b in range(1 if alg3 else nb):
             mem = sp.members[b].cpu().numpy()
             Lb = int(blens[b])
             fallback = not kinds[b]
