@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--min-group", type=int, default=2)
     ap.add_argument("--max-new", type=int, default=256)
     ap.add_argument("--shard", default="band", choices=["band", "strided"])
+    ap.add_argument("--pool-exec", default="native", choices=["native", "python"],
+                    help="pool: per-batch launch loop in C++ (specdec_pool_epoch) or Python")
     ap.add_argument("--pool-mode", default="epoch", choices=["epoch", "alg3"],
                     help="epoch: run every batch of the window plan; alg3: batch 0 then re-plan")
     ap.add_argument("--B", type=int, default=0, help="override batch size")
@@ -465,11 +467,27 @@ def run_pool(args, rank, world, device):
 
     ran = np.zeros(8, np.int64)
 
+    if args.pool_exec == "native":
+        sp.native(list(zip(ring_lg, ring_dr)), V=V, logit_dtype=ring_lg[0].dtype)
+
     def drain(events=None):
         sp.load(local_lens, order=local_order)
         sp.moved.zero_()
         epochs = batches = 0
         ran[:] = 0
+        if args.pool_exec == "native" and events is None:
+            # the per-batch launch loop in C++ (csrc/pool_exec.cu)
+            while True:
+                r_run, r_same, m_same, m_fb = sp.epoch_native(1 if args.pool_mode == "alg3" else 0)
+                if r_run == 0:
+                    break
+                epochs += 1
+                batches += r_run
+                ran[0] += r_run
+                ran[1] += r_same
+                ran[2] += m_same
+                ran[3] += m_fb
+            return epochs, batches
         while True:
             nb, kinds, blens, sizes = sp.plan()
             if nb == 0:
@@ -549,7 +567,8 @@ def run_pool(args, rank, world, device):
         "config": {"workload": f"EXSpec pool drain: {N} seqs, prompt {args.pool_lengths} "
                                f"{'U[64,512]' if args.pool_lengths == 'random' else '256'}, max_new "
                                f"{args.max_new}, W={Wn}/rank, B={sp.B}, min_group={args.min_group}, "
-                               f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}",
+                               f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}, "
+                               f"{args.pool_exec} launch loop",
                    "cap": cap, "pool_kv_GB_per_rank": sp.kv.numel() * 2 / 1e9,
                    "parallelism": f"pool sharded x{world}", "step": "one epoch (K4 plan + its batches)"},
         "pool": {"epochs": epochs, "batch_verifications": int(cnt_all[0]),

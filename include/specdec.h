@@ -236,6 +236,72 @@ int specdec_pool_writeback(const int32_t *d_members, int64_t B, int64_t k,
                            int64_t *d_pool_tokens, int64_t cap_tok, int64_t *d_out_buf,
                            int64_t max_new, uint32_t *d_status, specdec_stream_t stream);
 
+/* ------------------------------------------------------------------------------ a4 + a5
+ * specdec_pool_epoch -- native EXSpec epoch executor (Alg. 3): the
+ * host-side launch loop of one epoch in C++ instead of one Python call per kernel.
+ *   specdec_pool_group over the window; ONE device->host copy of the plan header (the
+ *   epoch's only host synchronisation); then for each of the first `max_batches` planned
+ *   batches (<= 0: all; 1: Alg. 3 as printed -- GetBatch, verify, write-back, re-plan):
+ *     fallback batch: specdec_realign_kv gather (pool -> staging, right-aligned);
+ *     inputs: `forward(ctx, b, same_length, width, &logits, &draft)` if non-NULL (the
+ *       model's verify forward, enqueued on `stream`), else the next (logits, draft) of
+ *       the descriptor's input ring;
+ *     specdec_verify (no budget; the write-back applies max_new); specdec_pool_writeback;
+ *     fallback batch: specdec_realign_kv scatter of the a+1 new KV rows.
+ * Host outputs (nullable): batches run, same-length batches run, their members, and
+ * the members of the fallback batches run.  All device buffers are caller-owned
+ * (paper_2510_22876_b200/exspec.py allocates them); host_header is pinned, 1 + 3W int32.
+ */
+typedef void (*specdec_forward_fn)(void *ctx, int32_t batch, int32_t same_length, int32_t width,
+                                   const void **logits, const int64_t **draft);
+
+typedef struct specdec_pool_desc {
+    /* pool state */
+    int32_t *len, *gen;
+    uint8_t *active;
+    const int32_t *order;
+    int32_t N;
+    int64_t *tokens;   /* [N][cap_tok] or NULL */
+    int64_t cap_tok;
+    int64_t *out_buf;  /* [N][max_new] or NULL */
+    int64_t max_new;
+    void *kv;          /* [N][n_planes][H][cap][D] */
+    void *staging;     /* [n_planes][B][H][cap][D] */
+    int kv_dtype;
+    int64_t n_planes, H, D, cap;
+    /* K4 plan buffers (see specdec_pool_group) */
+    int32_t *window, *window_size, *batch_of, *slot_of, *members, *mlen, *mpad;
+    uint8_t *mactive;
+    int32_t *bsize;
+    uint8_t *bkind;
+    int32_t *blen, *n_batches;
+    int64_t *counters;
+    /* specdec_verify scratch, [B] each (plan_L [1]) */
+    int32_t *accept;
+    int64_t *bonus;
+    int32_t *emit;
+    uint8_t *finished;
+    int32_t *n_new, *pad_new, *kept, *plan_L;
+    void *ws;
+    size_t ws_bytes;
+    uint32_t *status;
+    unsigned long long *moved;
+    int32_t *host_header; /* pinned host, 1 + 3W int32 */
+    int32_t W, B, min_group;
+    int64_t k, V, logit_stride, eos_id, pad_id;
+    int logit_dtype;
+    /* input ring used when forward == NULL: logits [B][k+1][logit_stride], drafts [B][k] */
+    const void *const *logits_ring;
+    const int64_t *const *draft_ring;
+    int32_t ring_n;
+    int32_t *ring_pos; /* host, advanced per batch */
+} specdec_pool_desc;
+
+int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,
+                       int32_t max_batches, int32_t *h_ran, int32_t *h_same,
+                       int32_t *h_members_same, int32_t *h_members_fallback,
+                       specdec_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,8 +42,39 @@ _SIGS = {
                             _P, _P, _P, _P, _P, _P], _INT),
     "specdec_pool_writeback": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
                                 _I64, _P, _P], _INT),
+    "specdec_pool_epoch": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P], _INT),
 }
 EXPORTS = tuple(_SIGS)
+
+
+class PoolDesc(ctypes.Structure):
+    """Mirror of `specdec_pool_desc` (include/specdec.h), field for field."""
+    _fields_ = [
+        ("len", _P), ("gen", _P), ("active", _P), ("order", _P), ("N", _I32),
+        ("tokens", _P), ("cap_tok", _I64), ("out_buf", _P), ("max_new", _I64),
+        ("kv", _P), ("staging", _P), ("kv_dtype", _INT),
+        ("n_planes", _I64), ("H", _I64), ("D", _I64), ("cap", _I64),
+        ("window", _P), ("window_size", _P), ("batch_of", _P), ("slot_of", _P), ("members", _P),
+        ("mlen", _P), ("mpad", _P), ("mactive", _P), ("bsize", _P), ("bkind", _P), ("blen", _P),
+        ("n_batches", _P), ("counters", _P),
+        ("accept", _P), ("bonus", _P), ("emit", _P), ("finished", _P), ("n_new", _P),
+        ("pad_new", _P), ("kept", _P), ("plan_L", _P),
+        ("ws", _P), ("ws_bytes", ctypes.c_size_t), ("status", _P), ("moved", _P),
+        ("host_header", _P),
+        ("W", _I32), ("B", _I32), ("min_group", _I32),
+        ("k", _I64), ("V", _I64), ("logit_stride", _I64), ("eos_id", _I64), ("pad_id", _I64),
+        ("logit_dtype", _INT),
+        ("logits_ring", _P), ("draft_ring", _P), ("ring_n", _I32), ("ring_pos", _P),
+    ]
+
+
+def specdec_pool_epoch(desc: PoolDesc, max_batches=0, stream=None):
+    """Native epoch executor; returns (batches run, same-length run, members same, members fallback)."""
+    out = [ctypes.c_int32(0) for _ in range(4)]
+    _check(load().specdec_pool_epoch(ctypes.byref(desc), None, None, max_batches,
+                                     *[ctypes.byref(o) for o in out], _stream(stream)),
+           "specdec_pool_epoch")
+    return tuple(o.value for o in out)
 
 
 class SpecdecError(RuntimeError):

@@ -17,6 +17,8 @@ reads the pool slots directly (zero-copy).  Sharding over GPUs is in dist.py.
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -189,6 +191,45 @@ class SequencePool:
         lg, d = inputs(0)
         self.run_batch(0, kinds[0], blens[0], lg, d, forward, V, stream)
         return True
+
+    # ----------------------------------------------------------------- native executor
+    def native(self, ring, V, logit_dtype=torch.bfloat16):
+        """Bind a `specdec_pool_desc` to this pool and an input ring [(logits, draft)] for
+        `epoch_native` (the per-batch launch loop in C++, csrc/pool_exec.cu)."""
+        p = lambda t: t.data_ptr() if t is not None else None
+        d = _abi.PoolDesc()
+        for name in ("len", "gen", "active", "order", "tokens", "out_buf", "kv", "staging", "window",
+                     "window_size", "batch_of", "slot_of", "members", "mlen", "mpad", "mactive",
+                     "bsize", "bkind", "blen", "n_batches", "counters", "accept", "bonus", "emit",
+                     "finished", "n_new", "pad_new", "kept", "plan_L", "ws", "status", "moved"):
+            setattr(d, name, p(getattr(self, name)))
+        d.N, d.cap_tok, d.max_new = self.N, self.tokens.shape[1], self.max_new
+        d.kv_dtype = _abi.DTYPE[self.kv.dtype]
+        d.n_planes, d.H, d.D, d.cap = self.n_planes, self.H, self.D, self.cap
+        d.ws_bytes = self.ws.numel() * 8
+        self._hdr = torch.zeros(1 + 3 * self.W, dtype=torch.int32).pin_memory()
+        d.host_header = self._hdr.data_ptr()
+        d.W, d.B, d.min_group = self.W, self.B, self.min_group
+        d.k, d.V, d.eos_id, d.pad_id = self.k, V, self.eos_id, self.pad_id
+        d.logit_stride = ring[0][0].stride(1)
+        d.logit_dtype = _abi.DTYPE[logit_dtype]
+        self._ring = ring                                    # keep the tensors alive
+        self._lg_ptrs = (ctypes.c_void_p * len(ring))(*[lg.data_ptr() for lg, _ in ring])
+        self._dr_ptrs = (ctypes.c_void_p * len(ring))(*[dr.data_ptr() for _, dr in ring])
+        self._ring_pos = ctypes.c_int32(0)
+        d.logits_ring = ctypes.cast(self._lg_ptrs, ctypes.c_void_p)
+        d.draft_ring = ctypes.cast(self._dr_ptrs, ctypes.c_void_p)
+        d.ring_n = len(ring)
+        d.ring_pos = ctypes.addressof(self._ring_pos)
+        self._desc = d
+        return d
+
+    def epoch_native(self, max_batches=0, stream=None):
+        """One epoch (or, with max_batches=1, one Alg. 3 iteration) in the native executor.
+        Returns (batches run, same-length batches run, members same, members fallback)."""
+        r = _abi.specdec_pool_epoch(self._desc, max_batches, stream)
+        self.verify_calls += r[0]
+        return r
 
     def has_active(self) -> bool:
         return bool(self.active.any().item())

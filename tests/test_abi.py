@@ -82,3 +82,21 @@ def test_missing_library_fails_loudly(tmp_path):
             _abi.load(str(tmp_path / "nope.so"))
     finally:
         _abi._lib = saved
+
+
+def test_pool_desc_layout_matches_header(tmp_path):
+    """The ctypes mirror of specdec_pool_desc has the C compiler's size and offsets."""
+    import shutil
+    import subprocess
+    if not shutil.which("g++"):
+        pytest.skip("no host C++ compiler")
+    src = tmp_path / "l.cpp"
+    src.write_text('#include <cstdio>\n#include <cstddef>\n#include "specdec.h"\n'
+                   'int main(){printf("%zu %zu %zu %zu\\n", sizeof(specdec_pool_desc),'
+                   ' offsetof(specdec_pool_desc, k), offsetof(specdec_pool_desc, logits_ring),'
+                   ' offsetof(specdec_pool_desc, ring_pos));}\n')
+    exe = tmp_path / "l"
+    subprocess.run(["g++", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
+    P = _abi.PoolDesc
+    assert got == [ctypes.sizeof(P), P.k.offset, P.logits_ring.offset, P.ring_pos.offset]

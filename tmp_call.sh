@@ -1,3 +1,5 @@
-for c in qwen3 vicuna glm4; do python bench.py --config $c --anchor --no-cpu-baseline > gpurun_out/b19_${c}_anchor.json 2>&1; done
-python bench.py --anchor --draft-kv --no-cpu-baseline > gpurun_out/b19_qwen3_anchor_draft.json 2>&1
-python bench.py --config qwen3 --B 4 --anchor --no-cpu-baseline > gpurun_out/b19_qwen3B4_anchor.json 2>&1
+timeout 900 python -m pytest tests/test_gpu_pool.py -q -x 2>&1 | tail -3
+for ex in native python; do timeout 600 python bench.py --config pool --pool-exec $ex > gpurun_out/b20_pool_$ex.json 2>&1; done
+timeout 600 python bench.py --config pool --pool-mode alg3 > gpurun_out/b20_pool_alg3_native.json 2>&1
+timeout 600 python bench.py --config pool --pool-lengths uniform > gpurun_out/b20_pool_uniform_native.json 2>&1
+timeout 600 python bench.py --config pool --min-group 8 > gpurun_out/b20_pool_mg8_native.json 2>&1
