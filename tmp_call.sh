@@ -1,5 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_pool.py -q -x 2>&1 | tail -3
-for ex in native python; do timeout 600 python bench.py --config pool --pool-exec $ex > gpurun_out/b20_pool_$ex.json 2>&1; done
-timeout 600 python bench.py --config pool --pool-mode alg3 > gpurun_out/b20_pool_alg3_native.json 2>&1
-timeout 600 python bench.py --config pool --pool-lengths uniform > gpurun_out/b20_pool_uniform_native.json 2>&1
-timeout 600 python bench.py --config pool --min-group 8 > gpurun_out/b20_pool_mg8_native.json 2>&1
+for s in 20 100 300; do python bench.py --steps $s --no-cpu-baseline > gpurun_out/b22_steps$s.json 2>&1; done
+python bench.py --steps 100 --episode 0 --no-cpu-baseline > gpurun_out/b22_noepisode.json 2>&1
