@@ -171,8 +171,16 @@ int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_tokens_out, 
  * cap_src / cap_dst: position capacity of each buffer (scol+cnt <= cap_src and
  *   dcol+cnt <= cap_dst, else SPECDEC_ST_KEPT and the row is skipped).
  * flags: SPECDEC_ZERO_PADS (in place only): zero [scol, dcol) when dcol > scol.
+ * d_ws / ws_bytes: optional device workspace of specdec_realign_workspace_size(dtype,
+ *   n_planes, n_rows, H, D, cap_src) bytes (16-B aligned, contents don't-care).  With it,
+ *   every slab is cut into ~128 KB segments that any CTA can stream independently: the
+ *   rows a segment's neighbour overwrites in place (|dcol - scol| rows, <= 4 KB) are first
+ *   copied to a workspace slot by a small kernel on the same stream.  NULL: one slab per
+ *   CTA (correct, less balanced when few rows move).
  * d_moved_bytes: optional uint64 accumulator of bytes read + written by this call.
  */
+size_t specdec_realign_workspace_size(int dtype, int64_t n_planes, int64_t n_rows, int64_t H,
+                                      int64_t D, int64_t cap);
 int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtype, int64_t n_planes,
                        int64_t n_rows, int64_t H, int64_t D, int64_t src_s_plane,
                        int64_t src_s_row, int64_t src_s_head, int64_t cap_src,
@@ -180,8 +188,8 @@ int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtype, int64_t 
                        int64_t cap_dst, const int32_t *d_src_col, int32_t src_col_add,
                        const int32_t *d_dst_col, int32_t dst_col_add, const int32_t *d_count,
                        int32_t count_add, const int32_t *d_src_row_map,
-                       const int32_t *d_dst_row_map, uint32_t flags,
-                       unsigned long long *d_moved_bytes, uint32_t *d_status,
+                       const int32_t *d_dst_row_map, uint32_t flags, void *d_ws,
+                       size_t ws_bytes, unsigned long long *d_moved_bytes, uint32_t *d_status,
                        specdec_stream_t stream);
 
 /* ------------------------------------------------------------------------------ a4

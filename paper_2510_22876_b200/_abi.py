@@ -35,9 +35,10 @@ _SIGS = {
                         ctypes.c_size_t, _P], _INT),
     "specdec_rebuild_pos_mask": ([_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P,
                                   _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P], _INT),
+    "specdec_realign_workspace_size": ([_INT, _I64, _I64, _I64, _I64, _I64], ctypes.c_size_t),
     "specdec_realign_kv": ([_P, _P, _INT, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
                             _I64, _I64, _I64, _P, _I32, _P, _I32, _P, _I32, _P, _P, _U32, _P,
-                            _P, _P], _INT),
+                            ctypes.c_size_t, _P, _P, _P], _INT),
     "specdec_pool_group": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                             _P, _P, _P, _P, _P, _P], _INT),
     "specdec_pool_writeback": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
@@ -160,16 +161,23 @@ def specdec_rebuild_pos_mask(tokens_in, tokens_out, k, n_old, pad_old, draft, ac
         "specdec_rebuild_pos_mask")
 
 
+def specdec_realign_workspace_size(dtype, n_planes, n_rows, H, D, cap) -> int:
+    return load().specdec_realign_workspace_size(DTYPE[dtype], n_planes, n_rows, H, D, cap)
+
+
 def specdec_realign_kv(kv_src, kv_dst, count, *, n_planes, n_rows, H, D, src_strides,
                        dst_strides, cap_src, cap_dst, src_col=None, src_col_add=0,
                        dst_col=None, dst_col_add=0, count_add=0, src_row_map=None,
-                       dst_row_map=None, flags=0, moved_bytes=None, status=None, stream=None):
-    """src/dst_strides = (s_plane, s_row, s_head) in elements; positions are D apart."""
+                       dst_row_map=None, flags=0, ws=None, moved_bytes=None, status=None,
+                       stream=None):
+    """src/dst_strides = (s_plane, s_row, s_head) in elements; positions are D apart.
+    ws: optional workspace tensor of specdec_realign_workspace_size bytes (segmentation)."""
     _check(load().specdec_realign_kv(
         _ptr(kv_src), _ptr(kv_dst), DTYPE[kv_src.dtype], n_planes, n_rows, H, D,
         src_strides[0], src_strides[1], src_strides[2], cap_src, dst_strides[0],
         dst_strides[1], dst_strides[2], cap_dst, _ptr(src_col), src_col_add, _ptr(dst_col),
         dst_col_add, _ptr(count), count_add, _ptr(src_row_map), _ptr(dst_row_map), flags,
+        _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
         _ptr(moved_bytes), _ptr(status), _stream(stream)), "specdec_realign_kv")
 
 

@@ -59,8 +59,8 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         if (fallback) {
             rc = specdec_realign_kv(d->kv, d->staging, d->kv_dtype, d->n_planes, B, d->H, d->D,
                                     p_plane, p_row, p_head, d->cap, s_plane, s_row, s_head, d->cap,
-                                    nullptr, 0, mpad, 0, mlen, -1, members, nullptr, 0, d->moved,
-                                    d->status, stream);
+                                    nullptr, 0, mpad, 0, mlen, -1, members, nullptr, 0, nullptr, 0,
+                                    d->moved, d->status, stream);
             if (rc) return rc;
         }
         const void *logits;
@@ -86,7 +86,7 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
             rc = specdec_realign_kv(d->staging, d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D,
                                     s_plane, s_row, s_head, d->cap, p_plane, p_row, p_head, d->cap,
                                     nullptr, blens[b] - 1, mlen, -1, d->accept, 1, nullptr,
-                                    members, 0, d->moved, d->status, stream);
+                                    members, 0, nullptr, 0, d->moved, d->status, stream);
             if (rc) return rc;
             mfb += sizes[b];
         } else {

@@ -2,19 +2,26 @@
 // PAPER.md:447) and the EXSpec pool gather / write-back scatter (Alg. 3, PAPER.md:492,
 // 505) as one row-mapped KV move.
 //
-// Work item = one (plane, moving row, KV head) slab: `cnt` contiguous KV rows of D
-// elements (head_dim contiguous).  One single-warp CTA streams a slab through a ring of
-// shared-memory stages with TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP): a bulk
-// load lands a chunk and completes an mbarrier transaction, the same elected lane then
-// bulk-stores it to the destination.  In place, the slab is walked in the hazard-free
-// direction: right shifts (dst > src) from the top chunk down, left shifts from the
-// bottom up.  Chunk j's store can only overwrite bytes at or beyond its own source in
-// the walking direction -- bytes that were already loaded (chunks < j completed their
-// loads before j was stored) -- and never the source of a later chunk, so loads may run
-// STAGES-1 chunks ahead of the stores.  Slabs are disjoint, so CTAs never interact.
-// The chunk stream is continuous across a CTA's items, so small slabs (pool write-back)
-// stay pipelined too.  Rows whose source and destination coincide (Delta = 0) are
-// skipped: in place, they cost zero bytes.
+// A slab is one (plane, row, KV head): `cnt` contiguous KV rows of D elements.  Each slab
+// is cut into segments of ~kSegBytes -- the work units -- so every CTA gets the same number
+// of bytes however few rows move (a B=2 batch moves one row) and the tail is one segment,
+// not one slab.  One single-warp CTA streams its units through a ring of shared-memory
+// stages with TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP): a bulk load completes an
+// mbarrier transaction, the same elected lane bulk-stores the chunk to its destination,
+// loads run STAGES-1 chunks ahead of stores, and the chunk stream is continuous across a
+// CTA's units.
+//
+// In place (the EqSpec realign) a segment is walked in the hazard-free direction -- right
+// shifts (dst > src) top-down, left shifts bottom-up -- so a chunk's store only hits bytes
+// of its own segment that were already loaded.  The only cross-segment hazard is at
+// segment boundaries: a segment's stores overwrite the first |shift| rows of its neighbour
+// (right shift: the upper neighbour's bottom rows; left: the lower neighbour's top rows).
+// A small first kernel (realign_save_kernel) copies exactly those boundary rows of every
+// segment into a workspace slot before the main kernel starts; the owning segment then
+// takes them from its slot (as its last chunk), never from the live buffer.  Segments thus
+// need no ordering at all.  Without a workspace, or for shifts wider than a slot, a slab
+// is one segment (the PR-1 behaviour).  Rows whose source and destination coincide
+// (Delta = 0) are skipped: in place they cost zero bytes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,8 +33,11 @@
 namespace specdec {
 
 constexpr int kRealignMaxRows = 1024;
-static int g_ctas_per_sm = 0;  // tuning override (SPECDEC_REALIGN_CTAS), 0 = occupancy
 constexpr int kZeroBytes = 2048;
+constexpr int64_t kSegBytes = 128 * 1024;     // target bytes per work unit
+constexpr int64_t kSlotBytes = 4096;          // boundary slot: |shift| * row bytes <= this
+static int g_ctas_per_sm = 0;                 // tuning override (SPECDEC_REALIGN_CTAS)
+static int64_t g_seg_bytes = kSegBytes;       // tuning override (SPECDEC_REALIGN_SEG, >= default)
 
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
@@ -44,12 +54,16 @@ struct RealignParams {
     uint32_t flags;
     int inplace;
     int policy_mode;  // 0: L2 evict_first on the streamed bytes, 1: evict_normal
+    char *ws;         // boundary slots (in-place segmentation), or null
+    int64_t ws_slots;
+    int64_t seg_bytes;  // >= kSegBytes (the workspace is sized for kSegBytes)
     unsigned long long *moved;
     uint32_t *status;
 };
 
 struct RowGeom {
-    int64_t src_off, dst_off, bytes;  // row-level offsets (plane 0, head 0), slab bytes
+    int64_t src_off, dst_off, rows;  // row-level offsets (plane 0, head 0), KV rows
+    int64_t shift;                   // in place: dst - src in rows (0 for distinct buffers)
 };
 
 __device__ __forceinline__ bool row_geom(const RealignParams &p, int r, RowGeom &g, bool &bad) {
@@ -67,11 +81,178 @@ __device__ __forceinline__ bool row_geom(const RealignParams &p, int r, RowGeom 
     }
     g.src_off = sr * p.ss_row + sc * p.rb;
     g.dst_off = dr * p.ds_row + dc * p.rb;
-    g.bytes = static_cast<int64_t>(cnt) * p.rb;
+    g.rows = cnt;
+    g.shift = p.inplace ? static_cast<int64_t>(dc) - sc : 0;
     if (p.inplace && g.src_off == g.dst_off) return false;  // Delta = 0: nothing moves
     return true;
 }
 
+// Segments of one slab.  In place, a slab is segmented only when a slot can hold its
+// boundary rows (and a workspace exists); distinct buffers never have boundaries.
+__device__ __forceinline__ int64_t seg_rows(const RealignParams &p) {
+    return imax64(1, p.seg_bytes / p.rb);
+}
+__device__ __forceinline__ int64_t n_segments(const RealignParams &p, const RowGeom &g) {
+    const int64_t sr = seg_rows(p);
+    const int64_t s = g.shift < 0 ? -g.shift : g.shift;
+    const bool can = !p.inplace || (p.ws && s * p.rb <= kSlotBytes && s <= sr);
+    return can ? (g.rows + sr - 1) / sr : 1;
+}
+
+// One work unit: a segment [lo, hi) of a slab's rows, plus its boundary rows.
+struct Unit {
+    const char *s;     // slab source (row 0)
+    char *d;           // slab destination (row 0)
+    int64_t lo, hi;    // segment rows
+    int64_t main_lo, main_hi;  // rows streamed from the live buffer
+    int64_t b_lo, b_rows;      // boundary rows (taken from the slot), count 0 if none
+    bool down;
+    bool first;        // segment 0 of its slab (carries the ZERO_PADS fill)
+    int64_t slab_rows;
+};
+
+__device__ __forceinline__ void make_unit(const RealignParams &p, const RowGeom &g, int64_t plane,
+                                          int64_t head, int64_t j, int64_t nseg, Unit &u) {
+    const int64_t sr = nseg > 1 ? seg_rows(p) : g.rows;
+    u.s = p.src + plane * p.ss_plane + head * p.ss_head + g.src_off;
+    u.d = p.dst + plane * p.ds_plane + head * p.ds_head + g.dst_off;
+    u.lo = j * sr;
+    u.hi = imin64(g.rows, (j + 1) * sr);
+    u.down = u.d > u.s;
+    u.first = j == 0;
+    u.slab_rows = g.rows;
+    u.main_lo = u.lo;
+    u.main_hi = u.hi;
+    u.b_lo = 0;
+    u.b_rows = 0;
+    if (p.inplace && nseg > 1) {
+        if (g.shift > 0 && j >= 1) {             // bottom rows, overwritten by segment j-1
+            u.b_rows = imin64(g.shift, u.hi - u.lo);
+            u.b_lo = u.lo;
+            u.main_lo = u.lo + u.b_rows;
+        } else if (g.shift < 0 && j + 1 < nseg) {  // top rows, overwritten by segment j+1
+            u.b_rows = imin64(-g.shift, u.hi - u.lo);
+            u.b_lo = u.hi - u.b_rows;
+            u.main_hi = u.b_lo;
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------- shared prologue
+constexpr int kGeomCache = 128;     // moving rows whose geometry is cached in smem
+struct UnitTable {
+    int32_t rows[kRealignMaxRows];  // moving batch rows
+    int32_t pre[kRealignMaxRows + 1];  // prefix of segment counts over the moving rows
+    int32_t n_mv;
+    int64_t units_per_ph;           // units per (plane, head)
+    RowGeom geo[kGeomCache];        // the issuing lane never waits on a global load per unit
+};
+
+// Geometry of moving row mi: from the smem cache (first kGeomCache rows) or recomputed.
+__device__ __forceinline__ void unit_geom(const RealignParams &p, const UnitTable &t, int mi, RowGeom &g) {
+    if (mi < kGeomCache) {
+        g = t.geo[mi];
+    } else {
+        bool bad;
+        row_geom(p, t.rows[mi], g, bad);
+    }
+}
+
+// Warp-cooperative: moving rows (ballot compaction, row order kept) + segment prefix.
+__device__ void build_table(const RealignParams &p, UnitTable &t, bool report) {
+    const int lane = threadIdx.x & 31;
+    bool any_bad = false;
+    int n_mv = 0;
+    int32_t run = 0;
+    for (int64_t base = 0; base < p.n_rows; base += 32) {
+        const int r = static_cast<int>(base) + lane;
+        RowGeom g;
+        bool bad = false, mv = false;
+        if (r < p.n_rows) mv = row_geom(p, r, g, bad);
+        const int32_t ns = mv ? static_cast<int32_t>(n_segments(p, g)) : 0;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, mv);
+        // inclusive scan of segment counts over the lanes
+        int32_t x = ns;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (mv) {
+            const int idx = n_mv + __popc(bal & ((1u << lane) - 1u));
+            t.rows[idx] = r;
+            t.pre[idx] = run + x - ns;
+            if (idx < kGeomCache) t.geo[idx] = g;
+        }
+        run += __shfl_sync(0xFFFFFFFFu, x, 31);
+        n_mv += __popc(bal);
+        any_bad |= bad;
+    }
+    any_bad = __any_sync(0xFFFFFFFFu, any_bad);
+    if (lane == 0) {
+        t.pre[n_mv] = run;
+        t.n_mv = n_mv;
+        t.units_per_ph = run;
+        if (report && any_bad && blockIdx.x == 0 && p.status) atomicOr(p.status, SPECDEC_ST_KEPT);
+    }
+    __syncwarp();
+}
+
+// unit index -> (plane, moving row, head, segment)
+__device__ __forceinline__ void locate(const RealignParams &p, const UnitTable &t, int64_t u,
+                                      int64_t &plane, int64_t &head, int &mi, int64_t &j) {
+    const int64_t U = t.units_per_ph;
+    plane = u / (p.H * U);
+    const int64_t rem = u % (p.H * U);
+    head = rem / U;
+    const int32_t r2 = static_cast<int32_t>(rem % U);
+    int lo = 0, hi = t.n_mv - 1;  // last mi with pre[mi] <= r2
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (t.pre[mid] <= r2) lo = mid; else hi = mid - 1;
+    }
+    mi = lo;
+    j = r2 - t.pre[lo];
+}
+
+// ----------------------------------------------------------------------------- boundary save
+// Copies every in-place segment's boundary rows into its workspace slot (slot = unit id).
+// One warp per unit, 8 warps per CTA, all of a lane's 16-byte loads issued before its
+// stores (a slot is <= 4 KB = 8 vectors per lane), so the whole pass is ~one DRAM trip.
+constexpr int kSaveWarps = 8;
+__global__ void __launch_bounds__(32 * kSaveWarps) realign_save_kernel(RealignParams p) {
+    __shared__ UnitTable t;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) build_table(p, t, false);
+    __syncthreads();
+    const int64_t n_units = p.n_planes * p.H * t.units_per_ph;
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * kSaveWarps + warp; u < n_units;
+         u += static_cast<int64_t>(gridDim.x) * kSaveWarps) {
+        int64_t plane, head, j;
+        int mi;
+        locate(p, t, u, plane, head, mi, j);
+        RowGeom g;
+        unit_geom(p, t, mi, g);
+        const int64_t nseg = n_segments(p, g);
+        if (nseg <= 1) continue;
+        Unit un;
+        make_unit(p, g, plane, head, j, nseg, un);
+        if (!un.b_rows) continue;
+        const uint4 *src = reinterpret_cast<const uint4 *>(un.s + un.b_lo * p.rb);
+        uint4 *slot = reinterpret_cast<uint4 *>(p.ws + u * kSlotBytes);
+        const int nv = static_cast<int>(un.b_rows * p.rb / 16);
+        constexpr int kPer = kSlotBytes / 16 / 32;  // 8 vectors per lane at most
+        uint4 v[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q)
+            if (lane + q * 32 < nv) v[q] = ld_stream_v4(src + lane + q * 32);
+#pragma unroll
+        for (int q = 0; q < kPer; ++q)
+            if (lane + q * 32 < nv) slot[lane + q * 32] = v[q];
+    }
+}
+
+// ----------------------------------------------------------------------------- main kernel
 template <int STAGES, int CHUNK>
 struct RealignSmem {
     alignas(128) unsigned char ring[STAGES][CHUNK];
@@ -79,45 +260,39 @@ struct RealignSmem {
     uint64_t bar[STAGES];
     char *st_dst[STAGES];
     uint32_t st_bytes[STAGES];
-    char *st_zero[STAGES];      // zero-fill target after this chunk (item end), or null
+    char *st_zero[STAGES];      // zero-fill target after this chunk (slab end), or null
     int64_t st_zero_bytes[STAGES];
-    int32_t rows[kRealignMaxRows];
-    int32_t n_mv;
+    UnitTable t;
 };
 
-// Load-side iterator over this CTA's (item, chunk) stream.
+// Load-side iterator over this CTA's (unit, chunk) stream: the unit's main rows in the
+// walking direction, then its boundary rows from the slot as one last chunk.
 struct ChunkIter {
-    int64_t t, n_items, stride;
-    int64_t q, nchunks;
-    const char *s;
-    char *d;
-    int64_t bytes;
-    bool down;     // walk high -> low
-    char *zptr;    // zero-fill region at item end
+    int64_t u, n_units, stride;
+    Unit un;
+    int64_t q, nmain;      // main chunks
+    bool bnd_left;         // boundary chunk still to issue
+    char *zptr;
     int64_t zbytes;
 };
 
 template <int STAGES, int CHUNK>
-__device__ __forceinline__ void iter_item(const RealignParams &p, const RealignSmem<STAGES, CHUNK> &sm,
+__device__ __forceinline__ void iter_unit(const RealignParams &p, const RealignSmem<STAGES, CHUNK> &sm,
                                           ChunkIter &it) {
-    // item -> (plane, moving row, head); head innermost
-    const int64_t head = it.t % p.H;
-    const int64_t mi = (it.t / p.H) % sm.n_mv;
-    const int64_t plane = it.t / (p.H * sm.n_mv);
+    int64_t plane, head, j;
+    int mi;
+    locate(p, sm.t, it.u, plane, head, mi, j);
     RowGeom g;
-    bool bad;
-    row_geom(p, sm.rows[mi], g, bad);
-    it.s = p.src + plane * p.ss_plane + head * p.ss_head + g.src_off;
-    it.d = p.dst + plane * p.ds_plane + head * p.ds_head + g.dst_off;
-    it.bytes = g.bytes;
-    it.down = it.d > it.s;
-    it.nchunks = (g.bytes + CHUNK - 1) / CHUNK;
+    unit_geom(p, sm.t, mi, g);
+    make_unit(p, g, plane, head, j, n_segments(p, g), it.un);
     it.q = 0;
+    it.nmain = ((it.un.main_hi - it.un.main_lo) * p.rb + CHUNK - 1) / CHUNK;
+    it.bnd_left = it.un.b_rows > 0;
     it.zptr = nullptr;
     it.zbytes = 0;
-    if ((p.flags & SPECDEC_ZERO_PADS) && p.inplace && it.down) {
-        it.zptr = const_cast<char *>(it.s);
-        it.zbytes = it.d - it.s;
+    if ((p.flags & SPECDEC_ZERO_PADS) && p.inplace && it.un.down && it.un.first) {
+        it.zptr = const_cast<char *>(it.un.s);  // rows [0, shift) of the slab become pads
+        it.zbytes = it.un.d - it.un.s;
     }
 }
 
@@ -126,67 +301,67 @@ __global__ void __launch_bounds__(32) realign_kernel(RealignParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     auto &sm = *reinterpret_cast<RealignSmem<STAGES, CHUNK> *>(smem_raw);
     const int lane = threadIdx.x;
-
-    // ---- moving rows (warp ballot compaction, row order preserved)
-    bool any_bad = false;
-    int n_mv = 0;
-    for (int64_t base = 0; base < p.n_rows; base += 32) {
-        const int r = static_cast<int>(base) + lane;
-        RowGeom g;
-        bool bad = false, mv = false;
-        if (r < p.n_rows) mv = row_geom(p, r, g, bad);
-        const unsigned bal = __ballot_sync(0xFFFFFFFFu, mv);
-        if (mv) sm.rows[n_mv + __popc(bal & ((1u << lane) - 1u))] = r;
-        n_mv += __popc(bal);
-        any_bad |= bad;
-    }
-    any_bad = __any_sync(0xFFFFFFFFu, any_bad);
+    build_table(p, sm.t, true);
     for (int z = lane * 16; z < kZeroBytes; z += 32 * 16)
         *reinterpret_cast<uint4 *>(sm.zeros + z) = make_uint4(0, 0, 0, 0);
     if (lane == 0) {
-        sm.n_mv = n_mv;
-        if (any_bad && blockIdx.x == 0 && p.status) atomicOr(p.status, SPECDEC_ST_KEPT);
         for (int s = 0; s < STAGES; ++s) mbar_init(&sm.bar[s], 1);
         fence_mbar_init();
     }
     fence_proxy_async_smem();  // zero buffer (generic writes) visible to the bulk engine
     __syncwarp();
-    if (lane != 0 || n_mv == 0) return;
+    if (lane != 0 || sm.t.n_mv == 0) return;
 
     const uint64_t pol = p.policy_mode == 0 ? policy_evict_first() : policy_evict_normal();
     ChunkIter it;
-    it.n_items = p.n_planes * static_cast<int64_t>(n_mv) * p.H;
+    it.n_units = p.n_planes * p.H * sm.t.units_per_ph;
     it.stride = gridDim.x;
-    it.t = blockIdx.x;
-    if (it.t >= it.n_items) return;
-    iter_item<STAGES, CHUNK>(p, sm, it);
+    it.u = blockIdx.x;
+    if (it.u >= it.n_units) return;
+    iter_unit<STAGES, CHUNK>(p, sm, it);
     unsigned long long moved = 0;
 
     auto issue = [&](int stage) {
-        int64_t off, nb;
-        if (!it.down) {
-            off = it.q * CHUNK;
-            nb = imin64(CHUNK, it.bytes - off);
-        } else {
-            const int64_t end = it.bytes - it.q * CHUNK;
-            off = imax64(0, end - CHUNK);
-            nb = end - off;
+        const Unit &un = it.un;
+        const char *src;
+        char *dst;
+        int64_t nb;
+        bool last;
+        if (it.q < it.nmain) {
+            const int64_t a = un.main_lo * p.rb, b = un.main_hi * p.rb;  // byte range
+            int64_t off;
+            if (!un.down) {
+                off = a + it.q * CHUNK;
+                nb = imin64(CHUNK, b - off);
+            } else {
+                const int64_t end = b - it.q * CHUNK;
+                off = imax64(a, end - CHUNK);
+                nb = end - off;
+            }
+            src = un.s + off;
+            dst = un.d + off;
+            ++it.q;
+            last = it.q == it.nmain && !it.bnd_left;
+        } else {  // the boundary rows, saved in this unit's slot before the kernel started
+            src = p.ws + it.u * kSlotBytes;
+            dst = un.d + un.b_lo * p.rb;
+            nb = un.b_rows * p.rb;
+            it.bnd_left = false;
+            last = true;
         }
-        sm.st_dst[stage] = it.d + off;
+        sm.st_dst[stage] = dst;
         sm.st_bytes[stage] = static_cast<uint32_t>(nb);
-        const bool last = (it.q + 1 == it.nchunks);
         sm.st_zero[stage] = last ? it.zptr : nullptr;
         sm.st_zero_bytes[stage] = last ? it.zbytes : 0;
-        if (last) moved += 2ull * static_cast<unsigned long long>(it.bytes);
+        if (last) moved += 2ull * static_cast<unsigned long long>((un.hi - un.lo) * p.rb);
         mbar_arrive_expect_tx(&sm.bar[stage], static_cast<uint32_t>(nb));
-        bulk_load(sm.ring[stage], it.s + off, static_cast<uint32_t>(nb), &sm.bar[stage], pol);
-        // advance
-        if (++it.q == it.nchunks) {
-            it.t += it.stride;
-            if (it.t < it.n_items) iter_item<STAGES, CHUNK>(p, sm, it);
+        bulk_load(sm.ring[stage], src, static_cast<uint32_t>(nb), &sm.bar[stage], pol);
+        if (last) {
+            it.u += it.stride;
+            if (it.u < it.n_units) iter_unit<STAGES, CHUNK>(p, sm, it);
         }
     };
-    auto more = [&]() { return it.t < it.n_items; };
+    auto more = [&]() { return it.u < it.n_units; };
 
     int64_t issued = 0;
     while (issued < STAGES && more()) {
@@ -198,8 +373,7 @@ __global__ void __launch_bounds__(32) realign_kernel(RealignParams p) {
         mbar_wait(&sm.bar[stage], static_cast<uint32_t>((c / STAGES) & 1));
         bulk_store(sm.st_dst[stage], sm.ring[stage], sm.st_bytes[stage], pol);
         if (sm.st_zero[stage]) {
-            // ZERO_PADS: old content columns that became pads (this slab's last chunk is
-            // loaded, so its source bytes may now be overwritten)
+            // ZERO_PADS: old content rows that became pads (segment 0's rows are all loaded)
             char *z = sm.st_zero[stage];
             for (int64_t zb = sm.st_zero_bytes[stage]; zb > 0;) {
                 const uint32_t nb = static_cast<uint32_t>(imin64(zb, kZeroBytes));
@@ -222,7 +396,7 @@ __global__ void __launch_bounds__(32) realign_kernel(RealignParams p) {
 }
 
 template <int STAGES, int CHUNK>
-int launch_realign(const RealignParams &p, int64_t max_items, cudaStream_t s) {
+int launch_realign(const RealignParams &p, int64_t max_units, cudaStream_t s) {
     using Sm = RealignSmem<STAGES, CHUNK>;
     const int smem = static_cast<int>(sizeof(Sm));
     // attribute + occupancy once per process (one arch per process; also keeps these
@@ -237,107 +411,36 @@ int launch_realign(const RealignParams &p, int64_t max_items, cudaStream_t s) {
         if (e != cudaSuccess) return record_cuda_error(e);
         per_sm = std::max(1, occ);
     }
-    // CTAs per SM: with many slabs per SM, one streaming CTA per SM is fastest (fewer
-    // concurrent DRAM streams, finer tail: measured in profiles/r01/realign_sweep.txt);
-    // with few slabs, fill the SM to occupancy so every slab gets its own CTA.
+    // CTAs per SM: with many units per SM, one streaming CTA per SM is fastest (fewer
+    // concurrent DRAM streams: profiles/r01/realign_sweep.txt); with few, fill the SMs.
     const int64_t sms = device_sm_count();
-    int ctas = max_items >= 16 * sms ? 1 : per_sm;
+    int ctas = max_units >= 16 * sms ? 1 : per_sm;
     if (g_ctas_per_sm > 0) ctas = std::min(per_sm, g_ctas_per_sm);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_items, sms * ctas));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_units, sms * ctas));
+    if (p.ws && p.inplace) {
+        const int64_t save_ctas = std::min<int64_t>((max_units + kSaveWarps - 1) / kSaveWarps, sms * 16);
+        realign_save_kernel<<<static_cast<unsigned>(std::max<int64_t>(1, save_ctas)), 32 * kSaveWarps, 0, s>>>(p);
+    }
     realign_kernel<STAGES, CHUNK><<<static_cast<unsigned>(grid), 32, smem, s>>>(p);
     return check_launch();
 }
 
-// ----------------------------------------------------------------------------- LDG/STG variant
-// Register-staged alternative (SPECDEC_REALIGN_CFG=9): one 256-thread CTA per slab at a
-// time, 16 KB chunks of 128-bit coalesced loads, a CTA barrier (all loads of the chunk
-// performed) before the chunk's stores, chunks walked in the hazard-free direction.
-constexpr int kLdgThreads = 256;
-constexpr int kLdgU = 4;
-
-__global__ void __launch_bounds__(kLdgThreads) realign_ldg_kernel(RealignParams p) {
-    __shared__ int32_t rows[kRealignMaxRows];
-    __shared__ int s_n;
-    const int tid = threadIdx.x, lane = tid & 31;
-    if (tid < 32) {
-        bool any_bad = false;
-        int n_mv = 0;
-        for (int64_t base = 0; base < p.n_rows; base += 32) {
-            const int r = static_cast<int>(base) + lane;
-            RowGeom g;
-            bool bad = false, mv = false;
-            if (r < p.n_rows) mv = row_geom(p, r, g, bad);
-            const unsigned bal = __ballot_sync(0xFFFFFFFFu, mv);
-            if (mv) rows[n_mv + __popc(bal & ((1u << lane) - 1u))] = r;
-            n_mv += __popc(bal);
-            any_bad |= bad;
-        }
-        any_bad = __any_sync(0xFFFFFFFFu, any_bad);
-        if (lane == 0) {
-            s_n = n_mv;
-            if (any_bad && blockIdx.x == 0 && p.status) atomicOr(p.status, SPECDEC_ST_KEPT);
-        }
-    }
-    __syncthreads();
-    const int n_mv = s_n;
-    const int64_t n_items = p.n_planes * static_cast<int64_t>(n_mv) * p.H;
-    unsigned long long moved = 0;
-    for (int64_t t = blockIdx.x; t < n_items; t += gridDim.x) {
-        const int64_t head = t % p.H, mi = (t / p.H) % n_mv, plane = t / (p.H * n_mv);
-        RowGeom g;
-        bool bad;
-        row_geom(p, rows[mi], g, bad);
-        const uint4 *src = reinterpret_cast<const uint4 *>(p.src + plane * p.ss_plane + head * p.ss_head + g.src_off);
-        uint4 *dst = reinterpret_cast<uint4 *>(p.dst + plane * p.ds_plane + head * p.ds_head + g.dst_off);
-        const bool down = reinterpret_cast<const char *>(dst) > reinterpret_cast<const char *>(src);
-        const int64_t nvec = g.bytes / 16;
-        constexpr int CV = kLdgThreads * kLdgU;
-        const int64_t nch = (nvec + CV - 1) / CV;
-        for (int64_t q = 0; q < nch; ++q) {
-            const int64_t hi = down ? nvec - q * CV : imin64(nvec, (q + 1) * CV);
-            const int64_t lo = down ? imax64(0, hi - CV) : q * CV;
-            uint4 buf[kLdgU];
-#pragma unroll
-            for (int u = 0; u < kLdgU; ++u) {
-                const int64_t v = lo + u * kLdgThreads + tid;
-                if (v < hi) buf[u] = ld_stream_v4(src + v);
-            }
-            __syncthreads();  // every load of this chunk is performed before any store
-#pragma unroll
-            for (int u = 0; u < kLdgU; ++u) {
-                const int64_t v = lo + u * kLdgThreads + tid;
-                if (v < hi) dst[v] = buf[u];
-            }
-        }
-        if ((p.flags & SPECDEC_ZERO_PADS) && p.inplace && down) {
-            __syncthreads();
-            const int64_t zv = (reinterpret_cast<const char *>(dst) - reinterpret_cast<const char *>(src)) / 16;
-            uint4 *z = const_cast<uint4 *>(src);
-            for (int64_t v = tid; v < zv; v += kLdgThreads) z[v] = make_uint4(0, 0, 0, 0);
-        }
-        __syncthreads();
-        moved += 2ull * static_cast<unsigned long long>(g.bytes);
-    }
-    if (tid == 0 && p.moved && moved) atomicAdd(p.moved, moved);
-}
-
-int launch_realign_ldg(const RealignParams &p, int64_t max_items, cudaStream_t s) {
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        int occ = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, realign_ldg_kernel, kLdgThreads, 0);
-        if (e != cudaSuccess) return record_cuda_error(e);
-        per_sm = std::max(1, occ);
-    }
-    const int ctas = g_ctas_per_sm > 0 ? std::min(per_sm, g_ctas_per_sm) : per_sm;
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_items, static_cast<int64_t>(device_sm_count()) * ctas));
-    realign_ldg_kernel<<<static_cast<unsigned>(grid), kLdgThreads, 0, s>>>(p);
-    return check_launch();
+// Upper bound of work units: every row of every (plane, head) slab segmented at capacity.
+int64_t max_units_bound(int64_t n_planes, int64_t n_rows, int64_t H, int64_t rb, int64_t cap) {
+    const int64_t sr = std::max<int64_t>(1, kSegBytes / rb);
+    return n_planes * H * n_rows * ((cap + sr - 1) / sr);
 }
 
 }  // namespace specdec
 
 using namespace specdec;
+
+extern "C" size_t specdec_realign_workspace_size(int dtype, int64_t n_planes, int64_t n_rows,
+                                                 int64_t H, int64_t D, int64_t cap) {
+    const int es = dtype_size(dtype);
+    if (es == 0 || n_planes < 1 || n_rows < 1 || H < 1 || D < 1 || cap < 1) return 0;
+    return static_cast<size_t>(max_units_bound(n_planes, n_rows, H, D * es, cap)) * kSlotBytes;
+}
 
 extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtype, int64_t n_planes,
                                   int64_t n_rows, int64_t H, int64_t D, int64_t src_s_plane,
@@ -347,8 +450,9 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
                                   const int32_t *d_dst_col, int32_t dst_col_add,
                                   const int32_t *d_count, int32_t count_add,
                                   const int32_t *d_src_row_map, const int32_t *d_dst_row_map,
-                                  uint32_t flags, unsigned long long *d_moved_bytes,
-                                  uint32_t *d_status, specdec_stream_t stream) {
+                                  uint32_t flags, void *d_ws, size_t ws_bytes,
+                                  unsigned long long *d_moved_bytes, uint32_t *d_status,
+                                  specdec_stream_t stream) {
     const int es = dtype_size(dtype);
     if (es == 0) return SPECDEC_ERR_DTYPE;
     if (!d_kv_src || !d_kv_dst || !d_count) return SPECDEC_ERR_ARG;
@@ -365,6 +469,8 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     if (inplace && (src_s_plane != dst_s_plane || src_s_row != dst_s_row || src_s_head != dst_s_head))
         return SPECDEC_ERR_ARG;
     if ((flags & SPECDEC_ZERO_PADS) && !inplace) return SPECDEC_ERR_ARG;
+    const int64_t units = max_units_bound(n_planes, n_rows, H, rb, cap_src);
+    if (d_ws && (!aligned16(d_ws) || ws_bytes < static_cast<size_t>(units) * kSlotBytes)) return SPECDEC_ERR_ARG;
     RealignParams p;
     p.src = static_cast<const char *>(d_kv_src);
     p.dst = static_cast<char *>(d_kv_dst);
@@ -375,11 +481,11 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     p.src_map = d_src_row_map; p.dst_map = d_dst_row_map;
     p.src_col_add = src_col_add; p.dst_col_add = dst_col_add; p.count_add = count_add;
     p.flags = flags; p.inplace = inplace ? 1 : 0;
+    p.ws = static_cast<char *>(d_ws);
+    p.ws_slots = d_ws ? units : 0;
     p.moved = d_moved_bytes; p.status = d_status;
-    const int64_t max_items = n_planes * n_rows * H;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    // pipeline shape (stages x chunk bytes), L2 policy and CTAs/SM: tuning overrides for
-    // sweeps (tools/kbench.py, profiles/); the default is the measured best.
+    // pipeline shape / L2 policy / CTAs per SM: tuning overrides for sweeps (tools/kbench.py)
     static int cfg = -1, pol = 0;
     if (cfg < 0) {
         const char *e = getenv("SPECDEC_REALIGN_CFG");
@@ -388,22 +494,14 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
         pol = q ? atoi(q) : 0;
         const char *c = getenv("SPECDEC_REALIGN_CTAS");
         g_ctas_per_sm = c ? atoi(c) : 0;
+        const char *sg = getenv("SPECDEC_REALIGN_SEG");
+        g_seg_bytes = std::max<int64_t>(kSegBytes, sg ? atoll(sg) : kSegBytes);
     }
     p.policy_mode = pol;
+    p.seg_bytes = g_seg_bytes;
     switch (cfg) {
-        case 1: return launch_realign<8, 8192>(p, max_items, s);
-        case 2: return launch_realign<4, 16384>(p, max_items, s);
-        case 3: return launch_realign<6, 16384>(p, max_items, s);
-        case 4: return launch_realign<12, 8192>(p, max_items, s);
-        case 5: return launch_realign<4, 8192>(p, max_items, s);
-        case 6: return launch_realign<2, 16384>(p, max_items, s);
-        case 7: return launch_realign<3, 8192>(p, max_items, s);
-        case 9: return launch_realign_ldg(p, max_items, s);
-        case 10: return launch_realign<8, 16384>(p, max_items, s);
-        case 11: return launch_realign<12, 16384>(p, max_items, s);
-        case 12: return launch_realign<6, 32768>(p, max_items, s);
-        case 13: return launch_realign<4, 32768>(p, max_items, s);
-        case 14: return launch_realign<16, 8192>(p, max_items, s);
-        default: return launch_realign<3, 32768>(p, max_items, s);  // measured best
+        case 1: return launch_realign<4, 16384>(p, units, s);
+        case 2: return launch_realign<6, 32768>(p, units, s);
+        default: return launch_realign<3, 32768>(p, units, s);  // measured best
     }
 }

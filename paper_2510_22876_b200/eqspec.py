@@ -19,6 +19,8 @@ cap + S columns whose logical origin K1 moves to minimise the rows that must mov
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -70,6 +72,14 @@ class EqSpecBatch:
             self.d_dims = (2 * dl, dh, dd)
             self.dkv = torch.zeros((2 * dl, B, dh, self.cap_phys, dd), dtype=TORCH_DT[kv_dtype], device=dev)
             self.kept_draft = torch.zeros(B, dtype=i32, device=dev)
+        # K2 workspace: boundary-row slots that let any CTA stream any ~128 KB segment of a
+        # slab in place (load balance when few rows move); shared by the target and draft calls
+        sizes = [_abi.specdec_realign_workspace_size(self.kv.dtype, self.n_planes, B, H, D, self.cap_phys)]
+        if self.dkv is not None:
+            sizes.append(_abi.specdec_realign_workspace_size(self.dkv.dtype, *self.d_dims[:1], B,
+                                                             *self.d_dims[1:], self.cap_phys))
+        self.rws = torch.empty(max(sizes), dtype=torch.uint8, device=dev)
+        self.segment = bool(int(os.environ.get("SPECDEC_SEGMENT", "0")))  # measured: profiles/r01
         self.cur = 0
         self.V = None
         self.zero_pads = False
@@ -152,6 +162,7 @@ class EqSpecBatch:
                                 src_strides=s[:3], dst_strides=s[:3], cap_src=self.cap_phys,
                                 cap_dst=self.cap_phys, src_col=src, dst_col=dst,
                                 flags=_abi.ZERO_PADS if self.zero_pads else 0,
+                                ws=self.rws if self.segment else None,
                                 moved_bytes=self.moved, status=self.status, stream=stream)
 
     def realign(self, stream=None):

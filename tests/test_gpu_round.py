@@ -148,7 +148,8 @@ def test_rounds_zero_pads(cuda):
 
 
 # ----------------------------------------------------------------------------- K2 alone
-def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, dtype="bf16", zero=False):
+def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, dtype="bf16", zero=False,
+                  seg=False):
     B = len(kept)
     cap = cap or int(max(np.max(pad_old), np.max(pad_new)) + np.max(kept) + 4)
     shp = (planes, B, H, cap, D)
@@ -158,8 +159,12 @@ def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, 
     moved = torch.zeros(1, dtype=torch.int64, device=cuda)
     st = torch.zeros(1, dtype=torch.int32, device=cuda)
     s = kv.stride()
+    ws = None
+    if seg:   # workspace -> slabs cut in ~128 KB segments with saved boundary rows
+        ws = torch.full((_abi.specdec_realign_workspace_size(kv.dtype, planes, B, H, D, cap),), 0xAB,
+                        dtype=torch.uint8, device=cuda)
     _abi.specdec_realign_kv(kv, kv, t32(kept), n_planes=planes, n_rows=B, H=H, D=D,
-                            src_strides=s[:3], dst_strides=s[:3], cap_src=cap, cap_dst=cap,
+                            src_strides=s[:3], dst_strides=s[:3], cap_src=cap, cap_dst=cap, ws=ws,
                             src_col=t32(pad_old), dst_col=t32(pad_new),
                             flags=_abi.ZERO_PADS if zero else 0, moved_bytes=moved, status=st)
     torch.cuda.synchronize()
@@ -191,6 +196,26 @@ def test_realign_adversarial_shifts(cuda, D, dtype):
     ]
     for po, pn, kp in cases:
         _realign_case(cuda, po, pn, kp, D=D, dtype=dtype)
+
+
+@pytest.mark.parametrize("D,dtype", [(128, "bf16"), (64, "fp16"), (32, "fp32")])
+def test_realign_segmented_in_place(cuda, D, dtype):
+    """Slabs of many 128 KB segments streamed by independent CTAs: boundary rows saved to
+    the workspace first; shifts of both signs, up to a full slot (4 KB of rows), wider
+    shifts (unsegmented fallback), Delta = 0, tiny and ragged slabs."""
+    rb = D * (4 if dtype == "fp32" else 2)
+    smax = 4096 // rb                       # widest shift a slot holds
+    long = (5 * 131072) // rb + 37          # > 5 segments, ragged last one
+    cases = [
+        ([0] * 4, [5] * 4, [long, long - 3, 513, 2]),
+        ([7] * 4, [0] * 4, [long, 1000, long // 2, 1]),
+        ([0, smax, 0, smax], [smax, 0, smax, 0], [long, long, long, long]),
+        ([0, 3, 2 * smax + 3, 9], [smax + 1, 3, 0, 2], [long, 100, long, 7]),    # wide -> unsegmented
+        ([1, 0, 4, 2], [0, 1, 4, 1], [long - 1, long, long, 3]),
+    ]
+    for po, pn, kp in cases:
+        _realign_case(cuda, po, pn, kp, D=D, H=2, dtype=dtype, seg=True)
+    _realign_case(cuda, [0, 4, 0], [3, 4, 0], [long, 50, long], D=D, H=2, dtype=dtype, seg=True, zero=True)
 
 
 def test_realign_zero_pads_and_skips(cuda):

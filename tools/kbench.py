@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--H", type=int, default=8)
     ap.add_argument("--cap", type=int, default=2304)
     ap.add_argument("--kept", type=int, default=2000)
+    ap.add_argument("--seg", action="store_true", help="pass a workspace (segmented slabs)")
     a = ap.parse_args()
     dev = torch.device("cuda")
     P, B, H, cap, D = a.planes, a.B, a.H, a.cap, 128
@@ -59,9 +60,13 @@ def main():
     kept = [a.kept] * B
     slab = P * H * a.kept * D * 2
 
+    ws = torch.empty(_abi.specdec_realign_workspace_size(kv.dtype, P, B, H, D, cap), dtype=torch.uint8,
+                     device=dev) if a.seg else None
+
     def k2(src, dst, po, pn, kp):
         _abi.specdec_realign_kv(src, dst, i32(kp), n_planes=P, n_rows=B, H=H, D=D, src_strides=s,
-                                dst_strides=s, cap_src=cap, cap_dst=cap, src_col=i32(po), dst_col=i32(pn))
+                                dst_strides=s, cap_src=cap, cap_dst=cap, src_col=i32(po), dst_col=i32(pn),
+                                ws=ws)
 
     ms = timed(lambda: k2(kv, kv2, [0] * B, [0] * B, kept), a.reps)
     res["k2_oop"] = 2 * slab * B / ms / 1e6
@@ -84,7 +89,7 @@ def main():
         k2(kv, kv, po, pn, kept)
     ms = timed(mixed, a.reps)
     res["k2_mixed"] = 2 * slab * len(mv) / ms / 1e6
-    res["cfg"] = os.environ.get("SPECDEC_REALIGN_CFG", "0")
+    res["cfg"] = os.environ.get("SPECDEC_REALIGN_CFG", "0") + ("+seg" if a.seg else "")
     print(json.dumps({k: (round(v, 1) if isinstance(v, float) else v) for k, v in res.items()}))
 
 
