@@ -80,6 +80,23 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def coll_device(device):
+    """Tensors for collectives live on the GPU under NCCL, on the host under gloo."""
+    import torch
+    import torch.distributed as dist
+    return device if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
+def max_over_ranks(x: float, device, world: int) -> float:
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=coll_device(device))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def ncu_traffic(config_key):
     """dram bytes per launch of K2 from the committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -317,11 +334,8 @@ def run_ours(args, rank, world, device):
     k2 = sum(e[2].elapsed_time(e[3]) for e in evs)
     # ---- C: e2e
     e2e = None if args.no_e2e else run_e2e(rb, args, world)
-    t = torch.tensor([ms], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     logits_bytes = sh.B * (sh.k + 1) * sh.V * (4 if sh.logit_dtype == "fp32" else 2)
-    return dict(sh=sh, ms=float(t.item()), moved=moved_B, moved_A=moved_A, k1_ms=k1, k3_ms=k3,
+    return dict(sh=sh, ms=max_over_ranks(ms, device, world), moved=moved_B, moved_A=moved_A, k1_ms=k1, k3_ms=k3,
                 k2_ms=k2, status=status | int(bt.status.item()), clocks=clocks.summary(), e2e=e2e,
                 end_width=width_end, logits_bytes=logits_bytes)
 
@@ -388,11 +402,7 @@ def run_e2e(rb, args, world):
     e1.record(comp)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1), dev, world)
     # the results are the method's: every step's emit = planted accept + 1 (no EOS/budget)
     if d2h_mode != "none":
         for r in range(args.steps):
@@ -566,11 +576,10 @@ def run_pool(args, rank, world, device):
     out_loc = sp.out_buf.cpu().numpy()
     gen_loc = sp.gen.cpu().numpy()
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, device, world)
         g0 = time.perf_counter()
-        _, gen_all, cnt_all = gather_results(mine, out_loc, gen_loc, cnt, N, args.max_new, device=device)
+        _, gen_all, cnt_all = gather_results(mine, out_loc, gen_loc, cnt, N, args.max_new,
+                                             device=coll_device(device))
         gather_ms = (time.perf_counter() - g0) * 1e3
     else:
         gen_all, cnt_all, gather_ms = gen_loc, cnt, 0.0
@@ -646,8 +655,16 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    # SPECDEC_BENCH_SHARE_GPU=1 (testing only): every rank on cuda:0 over gloo, so the
+    # N > 1 code path can be exercised on a one-GPU box; the real launch uses NCCL.
+    shared = os.environ.get("SPECDEC_BENCH_SHARE_GPU") == "1"
+    if shared:
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     if args.config == "pool":
