@@ -1,4 +1,5 @@
 // abi_misc.cu -- version, error reporting and device-property cache for libspecdec.so.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -27,6 +28,15 @@ int device_sm_count() {
         cache[dev] = n;
     }
     return cache[dev];
+}
+
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("SPECDEC_PDL");
+        on = e ? atoi(e) != 0 : 1;
+    }
+    return on != 0;
 }
 
 }  // namespace specdec

@@ -34,6 +34,17 @@ __device__ __forceinline__ uint32_t unpack_idx(unsigned long long p) {
     return ~static_cast<uint32_t>(p & 0xFFFFFFFFull);
 }
 
+// ----------------------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with the programmatic-serialization
+// attribute may start while its predecessor drains; griddepcontrol.wait blocks until the
+// predecessor has completed and its writes are visible (a no-op without the attribute).
+// Every specdec kernel waits before touching any input, so ordering is unchanged; only the
+// launch latency between consecutive kernels overlaps.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ----------------------------------------------------------------------------- loads
 __device__ __forceinline__ uint4 ld_stream_v4(const void *p) {
     uint4 r;

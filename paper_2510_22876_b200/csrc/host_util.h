@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <utility>
 
 #include "specdec.h"
 
@@ -25,6 +26,27 @@ inline int dtype_size(int dtype) {
 
 inline int check_launch() {
     cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPECDEC_OK : record_cuda_error(e);
+}
+
+bool pdl_enabled();  // SPECDEC_PDL (default on)
+
+// Launch with the programmatic-stream-serialization attribute (PDL) when enabled; the
+// kernels call pdl_wait() before reading anything a predecessor may write.
+template <typename... KArgs, typename... Args>
+int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+             Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
     return e == cudaSuccess ? SPECDEC_OK : record_cuda_error(e);
 }
 

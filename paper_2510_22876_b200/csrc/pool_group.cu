@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     int32_t B, int32_t min_group, int32_t *window, int32_t *window_size, int32_t *batch_of,
     int32_t *slot_of, int32_t *members, int32_t *mlen, int32_t *mpad, uint8_t *mactive,
     int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters) {
+    pdl_wait();
+    pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PoolSmem &sm = *reinterpret_cast<PoolSmem *>(smem_raw);
     const int tid = threadIdx.x;
@@ -251,9 +253,8 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
         if (e != cudaSuccess) return record_cuda_error(e);
         attr_done = true;
     }
-    pool_group_kernel<<<1, kPoolThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
-        d_len, d_active, d_order, N, W, B, min_group, d_window, d_window_size, d_batch_of,
-        d_slot_of, d_members, d_mlen, d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches,
-        d_counters);
-    return check_launch();
+    return launch_k(pool_group_kernel, dim3(1), dim3(kPoolThreads), smem,
+                    reinterpret_cast<cudaStream_t>(stream), d_len, d_active, d_order, N, W, B,
+                    min_group, d_window, d_window_size, d_batch_of, d_slot_of, d_members, d_mlen,
+                    d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches, d_counters);
 }

@@ -43,6 +43,8 @@ __device__ __forceinline__ int64_t emitted_token(const int64_t *d, int32_t a, in
 }
 
 __global__ void __launch_bounds__(kRepadThreads) repad_kernel(RepadParams p) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int64_t i = blockIdx.x;
     const int tid = threadIdx.x;
     const int32_t Lnew = *p.plan_L;
@@ -115,6 +117,8 @@ __global__ void __launch_bounds__(kRepadThreads) repad_kernel(RepadParams p) {
 //   p' + n <= c < L'   : E[c - p' - n]                        (append A ++ [B])
 constexpr int kRepadCols = 4;  // columns per thread
 __global__ void __launch_bounds__(kRepadThreads) repad_gather_kernel(RepadParams p) {
+    pdl_wait();                // K1's plan is complete and visible
+    pdl_launch_dependents();
     const int64_t i = blockIdx.y;
     const int tid = threadIdx.x;
     const int32_t Lnew = *p.plan_L;
@@ -173,6 +177,8 @@ __global__ void pool_writeback_kernel(const int32_t *members, int64_t k, const i
                                       int32_t *pool_len, int32_t *pool_gen, uint8_t *pool_active,
                                       int64_t *pool_tokens, int64_t cap_tok, int64_t *out_buf,
                                       int64_t max_new, uint32_t *status) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int64_t r = blockIdx.x;
     const int32_t s = members[r];
     if (s < 0) return;
@@ -235,15 +241,13 @@ extern "C" int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_t
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (d_tokens_in == d_tokens_out) {
         // in place: one CTA walks each row in the hazard-free direction
-        repad_kernel<<<static_cast<unsigned>(B), kRepadThreads, 0, s>>>(p);
-    } else {
-        if (B > 65535) return SPECDEC_ERR_SHAPE;
-        const int64_t cols = std::max(cap_tok, mp_stride);
-        const int64_t per = static_cast<int64_t>(kRepadThreads) * kRepadCols;
-        dim3 grid(static_cast<unsigned>((cols + per - 1) / per), static_cast<unsigned>(B));
-        repad_gather_kernel<<<grid, kRepadThreads, 0, s>>>(p);
+        return launch_k(repad_kernel, dim3(static_cast<unsigned>(B)), dim3(kRepadThreads), 0, s, p);
     }
-    return check_launch();
+    if (B > 65535) return SPECDEC_ERR_SHAPE;
+    const int64_t cols = std::max(cap_tok, mp_stride);
+    const int64_t per = static_cast<int64_t>(kRepadThreads) * kRepadCols;
+    dim3 grid(static_cast<unsigned>((cols + per - 1) / per), static_cast<unsigned>(B));
+    return launch_k(repad_gather_kernel, grid, dim3(kRepadThreads), 0, s, p);
 }
 
 extern "C" int specdec_pool_writeback(const int32_t *d_members, int64_t B, int64_t k,
@@ -262,9 +266,8 @@ extern "C" int specdec_pool_writeback(const int32_t *d_members, int64_t B, int64
     if (d_pool_tokens && cap_tok < 1) return SPECDEC_ERR_SHAPE;
     if (max_new < 1) return SPECDEC_ERR_SHAPE;
     const int threads = static_cast<int>((k + 1 + 31) / 32 * 32);
-    pool_writeback_kernel<<<static_cast<unsigned>(B), threads, 0,
-                            reinterpret_cast<cudaStream_t>(stream)>>>(
-        d_members, k, d_draft, d_accept, d_bonus, d_emit, d_finished, d_pool_len, d_pool_gen,
-        d_pool_active, d_pool_tokens, cap_tok, d_out_buf, max_new, d_status);
-    return check_launch();
+    return launch_k(pool_writeback_kernel, dim3(static_cast<unsigned>(B)), dim3(threads), 0,
+                    reinterpret_cast<cudaStream_t>(stream), d_members, k, d_draft, d_accept,
+                    d_bonus, d_emit, d_finished, d_pool_len, d_pool_gen, d_pool_active,
+                    d_pool_tokens, cap_tok, d_out_buf, max_new, d_status);
 }

@@ -209,6 +209,8 @@ __device__ __forceinline__ void cta_merge(const VerifyParams &p, int64_t row, un
 // ----------------------------------------------------------------------------- fp32 (toy)
 // Per-element keys, strict '>' over ascending indices within a thread.
 __global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams p) {
+    pdl_wait();
+    pdl_launch_dependents();
     __shared__ unsigned long long s_red[kVerifyThreads / kWarp];
     __shared__ int s_last;
     const int tid = threadIdx.x;
@@ -264,6 +266,8 @@ constexpr int kVPT = 8;  // 16-byte vectors per thread, all in flight, kept in r
 
 template <bool BF16>
 __global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p) {
+    pdl_wait();                // the logits' producer (and the previous round) completed
+    pdl_launch_dependents();
     using T = H16<BF16>;
     __shared__ unsigned long long s_red[kVerifyThreads / kWarp];
     __shared__ uint32_t s_m[kVerifyThreads / kWarp];
@@ -395,9 +399,8 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
     dim3 grid(static_cast<unsigned>(n_chunks), static_cast<unsigned>(rows));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     switch (dtype) {
-        case SPECDEC_F32: verify_kernel_f32<<<grid, kVerifyThreads, 0, s>>>(p); break;
-        case SPECDEC_F16: verify_kernel16<false><<<grid, kVerifyThreads, 0, s>>>(p); break;
-        default: verify_kernel16<true><<<grid, kVerifyThreads, 0, s>>>(p); break;
+        case SPECDEC_F32: return launch_k(verify_kernel_f32, grid, dim3(kVerifyThreads), 0, s, p);
+        case SPECDEC_F16: return launch_k(verify_kernel16<false>, grid, dim3(kVerifyThreads), 0, s, p);
+        default: return launch_k(verify_kernel16<true>, grid, dim3(kVerifyThreads), 0, s, p);
     }
-    return check_launch();
 }
