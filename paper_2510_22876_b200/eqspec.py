@@ -167,6 +167,10 @@ class EqSpecBatch:
 
     def realign(self, stream=None):
         c, nx = self.cur, 1 - self.cur
+        if self.B == 1 and self.anchor is None:
+            # a single row is always right-aligned at L' = n': p' = p = 0, so Realign is a
+            # pure truncation that moves nothing -- no launch at all
+            return
         if self.anchor is not None:
             src, dst = self.phys_old, self.phys_new        # f3: physical columns from K1
         else:
@@ -174,6 +178,14 @@ class EqSpecBatch:
         self._realign_one(self.kv, self.kept, (self.n_planes, self.H, self.D), src, dst, stream)
         if self.dkv is not None:     # f1: the draft model's own cache, same shift, kept_draft
             self._realign_one(self.dkv, self.kept_draft, self.d_dims, src, dst, stream)
+
+    @property
+    def kernels_per_round(self) -> int:
+        """libspecdec kernels one round launches (K1, K3, K2 per cache, + save kernels)."""
+        if self.B == 1 and self.anchor is None:
+            return 2
+        per_cache = 2 if self.segment else 1
+        return 2 + per_cache * (2 if self.dkv is not None else 1)
 
     def launch_round(self, logits, draft, stream=None):
         """Enqueue K1 -> {K3 || K2} for the current parity (does not flip it).  K3 (tokens,
