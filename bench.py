@@ -683,7 +683,8 @@ def main():
         value = world * args.steps / (res["ms"] / 1e3)
         k2_launch_ms = res["k2_ms"] / args.steps
         bytes_per_launch = res["moved"] / args.steps
-        achieved = bytes_per_launch / (k2_launch_ms / 1e3) / 1e9
+        # (B=1 moves no KV: K2 is not launched and the roofline line reports 0 bytes)
+        achieved = bytes_per_launch / (k2_launch_ms / 1e3) / 1e9 if k2_launch_ms > 1e-6 else 0.0
         traffic, traffic_note = ncu_traffic(f"{sh.name}_B{sh.B}")
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
