@@ -105,3 +105,30 @@ def test_pool_desc_layout_matches_header(tmp_path):
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
     P = _abi.PoolDesc
     assert got == [ctypes.sizeof(P), P.k.offset, P.logits_ring.offset, P.ring_pos.offset]
+
+
+def test_header_is_plain_c_and_links(tmp_path, lib):
+    """include/specdec.h compiles as C99 and a C program links libspecdec.so and gets the
+    host-side argument errors back (no GPU, no torch)."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no host C compiler")
+    src = tmp_path / "c.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include "specdec.h"
+int main(void) {
+    int rc = specdec_verify((const void *)16, SPECDEC_BF16, 8, 0, 100, 104, 0, 0, 0, -1, 0, 0,
+                            0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0);
+    size_t ws = specdec_verify_workspace_size(8, 5);
+    printf("%d %d %zu\n", specdec_version(), rc, ws);
+    return 0;
+}
+''')
+    exe = tmp_path / "c"
+    libdir = os.path.dirname(_abi.lib_path())
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
+                    "-L", libdir, "-l:libspecdec.so", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    assert out == ["100", str(_abi.ERR_ARG), str(8 * 6 * 8 + 16)]
