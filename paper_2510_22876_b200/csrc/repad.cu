@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kRepadThreads) repad_kernel(RepadParams p) {
 //   c <  p'            : pad
 //   p' <= c < p' + n   : old token at column c - p' + p      (unpad + repad)
 //   p' + n <= c < L'   : E[c - p' - n]                        (append A ++ [B])
-constexpr int kRepadCols = 4;  // columns per thread
+constexpr int kRepadCols = 1;  // columns per thread: many small CTAs, the kernel is latency-bound
 __global__ void __launch_bounds__(kRepadThreads) repad_gather_kernel(RepadParams p) {
     pdl_wait();                // K1's plan is complete and visible
     pdl_launch_dependents();

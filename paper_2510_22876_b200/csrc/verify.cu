@@ -42,6 +42,7 @@ struct VerifyParams {
     int32_t *anchor;          // f3: physical origin (in/out), NULL = off
     int64_t anchor_cap;
     int32_t *phys_old, *phys_new;
+    int exp;                  // SPECDEC_K1_EXP timing experiments (0 = normal)
     uint32_t *status;
     unsigned long long *ws_keys;  // [B*(k+1)]
     unsigned int *ws_counter;      // [1]
@@ -178,6 +179,7 @@ __device__ void verify_epilogue(const VerifyParams &p) {
 
 // Arrival on the grid-wide counter; the last CTA runs the epilogue.
 __device__ __forceinline__ void arrive_and_maybe_finish(const VerifyParams &p, int *s_last) {
+    if (p.exp == 1) return;  // timing experiment only (tools/k1bench.py): argmax without epilogue
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned int total = gridDim.x * gridDim.y;
@@ -380,6 +382,12 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
     p.pred = d_pred; p.plan_L = d_plan_L; p.n_new = d_n_new; p.pad_new = d_pad_new; p.kept = d_kept;
     p.kept_draft = d_kept_draft;
     p.anchor = d_anchor; p.anchor_cap = anchor_cap; p.phys_old = d_phys_old; p.phys_new = d_phys_new;
+    static int exp = -1;
+    if (exp < 0) {
+        const char *e = getenv("SPECDEC_K1_EXP");
+        exp = e ? atoi(e) : 0;
+    }
+    p.exp = exp;
     p.status = d_status;
     p.ws_keys = static_cast<unsigned long long *>(d_ws);
     p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
