@@ -345,7 +345,10 @@ def run_e2e(rb, args, world):
     """Each step: H2D of that step's logits + drafts from pinned host memory (copy stream,
     two device buffers, so the copy of step s+1 overlaps the round of step s), the round
     (graph replay), D2H of the step's result -- the per-row emitted-token counts -- into
-    pinned host memory (SPECDEC_E2E_D2H=three also reads accept + bonus; none: no read)."""
+    pinned host memory (SPECDEC_E2E_D2H=three also reads accept + bonus; none: no read).
+    The D2H runs on a third stream while the next round computes: the batch keeps one
+    result set per state parity, and a round waits only until the set it overwrites (two
+    rounds back) has been read out."""
     import torch
     import torch.distributed as dist
     sh, dev, bt = rb.sh, rb.dev, rb.bt
@@ -360,8 +363,10 @@ def run_e2e(rb, args, world):
     bt.capture(list(zip(dlg, ddr)), V=sh.V)   # graphs on the two staging buffers
     comp = rb.stream
     copy = torch.cuda.Stream(dev)
+    d2h = torch.cuda.Stream(dev)
     ready = [torch.cuda.Event() for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]
+    fetched = [torch.cuda.Event() for _ in range(2)]  # results of parity p were read out
 
     def h2d(r):
         b = r % 2
@@ -374,20 +379,29 @@ def run_e2e(rb, args, world):
     def run(n):
         for b in range(2):
             done[b].record(comp)
+            fetched[b].record(d2h)
         h2d(0)
         for r in range(n):
             if r + 1 < n:
                 h2d(r + 1)
             b = r % 2
+            par = bt.cur
             comp.wait_event(ready[b])
+            comp.wait_event(fetched[par])  # round r-2's results (same parity set) are out
             rb.episode(r, args.episode)
             bt.replay(b)
             done[b].record(comp)
-            if d2h_mode == "three":
-                out_a[r].copy_(bt.accept, non_blocking=True)
-                out_b[r].copy_(bt.bonus, non_blocking=True)
-            if d2h_mode != "none":
+            if d2h_mode == "none":
+                continue
+            # the D2H runs on its own stream under the next round (results are per parity)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done[b])
+                if d2h_mode == "three":
+                    out_a[r].copy_(bt.accept, non_blocking=True)
+                    out_b[r].copy_(bt.bonus, non_blocking=True)
                 out_e[r].copy_(bt.emit, non_blocking=True)
+                fetched[par].record(d2h)
+        comp.wait_stream(d2h)
 
     rb.reset()
     run(min(args.warmup, args.steps))
@@ -412,7 +426,8 @@ def run_e2e(rb, args, world):
     d2h_b = {"three": sh.B * 16, "one": sh.B * 4, "none": 0}[d2h_mode]
     return {"value": world * args.steps / (ms / 1e3), "unit": "rounds/s", "h2d_bytes_per_step": h2d_b,
             "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / args.steps, "wall_s": wall,
-            "overlap": "H2D on a copy stream, double-buffered; round = CUDA graph replay"}
+            "overlap": "H2D on a copy stream, double-buffered; round = CUDA graph replay; "
+                       "D2H on a third stream from the round's parity result set"}
 
 
 # ----------------------------------------------------------------------------- oracle timing

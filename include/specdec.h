@@ -52,7 +52,8 @@ typedef struct CUstream_st *specdec_stream_t; /* == cudaStream_t */
 #define SPECDEC_ST_KEPT 4u     /* a KV row range lies outside [0, cap); the item was skipped */
 
 /* specdec_realign_kv flags */
-#define SPECDEC_ZERO_PADS 1u /* also zero the old content columns that became pads */
+#define SPECDEC_ZERO_PADS 1u    /* also zero the old content columns that became pads */
+#define SPECDEC_OVERLAP_PREV 2u /* start under the previous kernel on the stream (see below) */
 
 /* ------------------------------------------------------------------------------ misc */
 int specdec_version(void);                /* ABI version (major*100 + minor) */
@@ -171,6 +172,13 @@ int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_tokens_out, 
  * cap_src / cap_dst: position capacity of each buffer (scol+cnt <= cap_src and
  *   dcol+cnt <= cap_dst, else SPECDEC_ST_KEPT and the row is skipped).
  * flags: SPECDEC_ZERO_PADS (in place only): zero [scol, dcol) when dcol > scol.
+ *   SPECDEC_OVERLAP_PREV: the caller guarantees that the call enqueued immediately before
+ *   on `stream` is a specdec_* kernel launch that itself waited for the producer of this
+ *   call's columns / counts / KV (e.g. specdec_rebuild_pos_mask right after
+ *   specdec_verify) and that this call does not read what it writes.  The copy then
+ *   starts while that kernel runs (programmatic dependent launch) and waits for it only
+ *   before exiting, so completion order on the stream is unchanged.  Ignored with a
+ *   workspace in place (the boundary-save kernel must finish first) and with PDL off.
  * d_ws / ws_bytes: optional device workspace of specdec_realign_workspace_size(dtype,
  *   n_planes, n_rows, H, D, cap_src) bytes (16-B aligned, contents don't-care).  With it,
  *   every slab is cut into ~128 KB segments that any CTA can stream independently: the

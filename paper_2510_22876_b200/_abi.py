@@ -18,6 +18,7 @@ _lib = None
 OK, ERR_ARG, ERR_SHAPE, ERR_DTYPE, ERR_CAPACITY, ERR_CUDA = 0, -1, -2, -3, -4, -5
 ST_NAN, ST_CAPACITY, ST_KEPT = 1, 2, 4
 ZERO_PADS = 1
+OVERLAP_PREV = 2
 DTYPE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 
 _P = ctypes.c_void_p

@@ -68,13 +68,15 @@ struct RowGeom {
 
 __device__ __forceinline__ bool row_geom(const RealignParams &p, int r, RowGeom &g, bool &bad) {
     bad = false;
-    const int32_t cnt = p.count[r] + p.count_add;
+    // L2 loads: under SPECDEC_OVERLAP_PREV the plan's producer finished before this grid
+    // started but this grid never waited on it, so nothing may come from a stale L1 line
+    const int32_t cnt = __ldcg(p.count + r) + p.count_add;
     if (cnt <= 0) return false;
-    const int32_t sr = p.src_map ? p.src_map[r] : r;
-    const int32_t dr = p.dst_map ? p.dst_map[r] : r;
+    const int32_t sr = p.src_map ? __ldcg(p.src_map + r) : r;
+    const int32_t dr = p.dst_map ? __ldcg(p.dst_map + r) : r;
     if (sr < 0 || dr < 0) return false;
-    const int32_t sc = (p.src_col ? p.src_col[r] : 0) + p.src_col_add;
-    const int32_t dc = (p.dst_col ? p.dst_col[r] : 0) + p.dst_col_add;
+    const int32_t sc = (p.src_col ? __ldcg(p.src_col + r) : 0) + p.src_col_add;
+    const int32_t dc = (p.dst_col ? __ldcg(p.dst_col + r) : 0) + p.dst_col_add;
     if (sc < 0 || dc < 0 || sc + cnt > p.cap_src || dc + cnt > p.cap_dst) {
         bad = true;
         return false;
@@ -299,13 +301,8 @@ __device__ __forceinline__ void iter_unit(const RealignParams &p, const RealignS
 }
 
 template <int STAGES, int CHUNK>
-__global__ void __launch_bounds__(32) realign_kernel(RealignParams p) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    auto &sm = *reinterpret_cast<RealignSmem<STAGES, CHUNK> *>(smem_raw);
+__device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem<STAGES, CHUNK> &sm) {
     const int lane = threadIdx.x;
-    pdl_wait();                // K1's plan (counts, columns) is complete and visible
-    // (dependents are released only as CTAs finish: a next round's verify CTAs parked on
-    // the SMs during the stream cost K2 ~5 %, measured)
     build_table(p, sm.t, true);
     for (int z = lane * 16; z < kZeroBytes; z += 32 * 16)
         *reinterpret_cast<uint4 *>(sm.zeros + z) = make_uint4(0, 0, 0, 0);
@@ -401,6 +398,22 @@ __global__ void __launch_bounds__(32) realign_kernel(RealignParams p) {
 }
 
 template <int STAGES, int CHUNK>
+__global__ void __launch_bounds__(32) realign_kernel(RealignParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    auto &sm = *reinterpret_cast<RealignSmem<STAGES, CHUNK> *>(smem_raw);
+    // Normally: wait until K1's plan (counts, columns) is complete and visible.  With
+    // SPECDEC_OVERLAP_PREV the previous kernel (K3) waited on K1 before releasing this grid,
+    // so the plan is already complete: start at once, streaming under K3, and wait on K3
+    // only before exiting so this grid's completion still implies K3's.
+    // (Dependents are released only as CTAs finish: a next round's verify CTAs parked on
+    // the SMs during the stream cost K2 ~5 %, measured.)
+    const bool overlap = (p.flags & SPECDEC_OVERLAP_PREV) != 0;
+    if (!overlap) pdl_wait();
+    realign_body<STAGES, CHUNK>(p, sm);
+    if (overlap) pdl_wait();
+}
+
+template <int STAGES, int CHUNK>
 int launch_realign(const RealignParams &p, int64_t max_units, cudaStream_t s) {
     using Sm = RealignSmem<STAGES, CHUNK>;
     const int smem = static_cast<int>(sizeof(Sm));
@@ -430,12 +443,14 @@ int launch_realign(const RealignParams &p, int64_t max_units, cudaStream_t s) {
                                 dim3(32 * kSaveWarps), 0, s, p);
         if (rc) return rc;
     }
+    RealignParams pm = p;
+    if (p.ws && p.inplace) pm.flags &= ~SPECDEC_OVERLAP_PREV;  // must wait for the boundary slots
     // One streaming CTA per SM is enforced through shared memory, not left to the CTA
     // scheduler: launched early under PDL, a persistent grid could otherwise double up on
     // the SMs that are free first (measured -5..7 % before this).
     const int smem_launch = ctas == 1 ? std::max(smem, kOnePerSm) : smem;
     return launch_k(realign_kernel<STAGES, CHUNK>, dim3(static_cast<unsigned>(grid)), dim3(32),
-                    smem_launch, s, p);
+                    smem_launch, s, pm);
 }
 
 // Upper bound of work units: every row of every (plane, head) slab segmented at capacity.
@@ -471,7 +486,7 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     if (!d_kv_src || !d_kv_dst || !d_count) return SPECDEC_ERR_ARG;
     if (n_planes < 1 || n_rows < 1 || H < 1 || D < 1 || cap_src < 1 || cap_dst < 1) return SPECDEC_ERR_SHAPE;
     if (n_rows > kRealignMaxRows) return SPECDEC_ERR_SHAPE;
-    if (flags & ~SPECDEC_ZERO_PADS) return SPECDEC_ERR_ARG;
+    if (flags & ~(SPECDEC_ZERO_PADS | SPECDEC_OVERLAP_PREV)) return SPECDEC_ERR_ARG;
     const int64_t rb = D * es;
     if (rb % 16 != 0 || !aligned16(d_kv_src) || !aligned16(d_kv_dst)) return SPECDEC_ERR_ARG;
     const int64_t st[6] = {src_s_plane, src_s_row, src_s_head, dst_s_plane, dst_s_row, dst_s_head};

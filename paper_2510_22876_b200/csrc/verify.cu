@@ -24,6 +24,7 @@ namespace specdec {
 
 constexpr int kVerifyThreads = 256;
 constexpr int kMaxK = 31;  // k + 1 <= 32: one lane per slot in the epilogue
+constexpr int kEpiCache = 1024;  // rows whose n' the epilogue keeps in shared memory
 
 struct VerifyParams {
     const void *logits;
@@ -63,6 +64,7 @@ __device__ void verify_epilogue(const VerifyParams &p) {
     __shared__ int s_nmax[kVerifyThreads / kWarp];
     __shared__ unsigned long long s_w[kMaxK + 1];  // f3: kept rows per accept class
     __shared__ int s_base[2];
+    __shared__ int32_t s_nn[kEpiCache];  // n' of the first rows (no global re-read below)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     const int k = static_cast<int>(p.k);
@@ -71,14 +73,18 @@ __device__ void verify_epilogue(const VerifyParams &p) {
     __syncthreads();
     int local_max = 0, local_nmax = 0;
     for (int64_t i = warp; i < p.B; i += nwarps) {
-        const bool act = p.active[i] != 0;
-        local_nmax = max(local_nmax, p.n[i]);  // old width L = max n (R6 held last round)
+        // every load of the row first, independent of each other: one memory round trip
+        const uint8_t act_b = p.active[i];
+        const int32_t n_i = p.n[i];
+        const unsigned long long key = lane < K1 ? __ldcg(p.ws_keys + i * K1 + lane) : 0ull;
+        const int64_t d = lane < k ? p.draft[i * k + lane] : -1;
+        const int32_t bud_i = p.budget ? p.budget[i] : 0;
+        const bool act = act_b != 0;
+        local_nmax = max(local_nmax, n_i);  // old width L = max n (R6 held last round)
         int a = 0, m = 0, nn = 1, kp = 0;
         int64_t b = p.pad_id;
         bool fin = true;
-        int64_t pr = -1, d = -1;
-        if (lane < K1) pr = act ? static_cast<int64_t>(unpack_idx(__ldcg(p.ws_keys + i * K1 + lane))) : -1;
-        if (lane < k) d = p.draft[i * k + lane];
+        const int64_t pr = (act && lane < K1) ? static_cast<int64_t>(unpack_idx(key)) : -1;
         if (p.pred && lane < K1) p.pred[i * K1 + lane] = pr;
         if (act) {
             // first mismatch; R1: all k match -> a = k
@@ -94,13 +100,13 @@ __device__ void verify_epilogue(const VerifyParams &p) {
                 if (e) { m = __ffs(e); fin = true; }
             }
             if (p.budget) {  // then to the remaining budget (R10)
-                const int bud = max(p.budget[i], 0);
+                const int bud = max(bud_i, 0);
                 if (m >= bud) { m = bud; fin = true; }
                 if (lane == 0) p.budget[i] = bud - m;  // in/out
             }
             if (!fin) {
-                nn = p.n[i] + a + 1;  // accepted + bonus
-                kp = p.n[i] + a;      // the bonus has no KV yet
+                nn = n_i + a + 1;  // accepted + bonus
+                kp = n_i + a;      // the bonus has no KV yet
                 local_max = max(local_max, nn);
             }
         }
@@ -112,10 +118,11 @@ __device__ void verify_epilogue(const VerifyParams &p) {
             p.finished[i] = fin ? 1 : 0;
             p.active[i] = fin ? 0 : 1;  // in/out: rows still active after this round
             p.n_new[i] = nn;
+            if (i < kEpiCache) s_nn[i] = nn;
             p.kept[i] = kp;
             // f1: a draft model that cached its own k forwards (pending token, d_1..d_{k-1})
             // keeps n + min(a, k-1) entries: d_k never had a draft KV entry
-            if (p.kept_draft) p.kept_draft[i] = kp ? p.n[i] + min(a, k - 1) : 0;
+            if (p.kept_draft) p.kept_draft[i] = kp ? n_i + min(a, k - 1) : 0;
             if (p.anchor && kp) atomicAdd(&s_w[a], static_cast<unsigned long long>(kp));
         }
     }
@@ -164,7 +171,7 @@ __device__ void verify_epilogue(const VerifyParams &p) {
     }
     if (p.anchor) __syncthreads();
     for (int64_t i = threadIdx.x; i < p.B; i += blockDim.x) {
-        const int32_t pn = Lnew > 0 ? Lnew - p.n_new[i] : 0;
+        const int32_t pn = Lnew > 0 ? Lnew - (i < kEpiCache ? s_nn[i] : p.n_new[i]) : 0;
         p.pad_new[i] = pn;
         if (p.anchor) {
             p.phys_old[i] = s_base[0] + (Lold - p.n[i]);
@@ -181,14 +188,15 @@ __device__ void verify_epilogue(const VerifyParams &p) {
 __device__ __forceinline__ void arrive_and_maybe_finish(const VerifyParams &p, int *s_last) {
     if (p.exp == 1) return;  // timing experiment only (tools/k1bench.py): argmax without epilogue
     if (threadIdx.x == 0) {
-        __threadfence();
+        // acq_rel: releases this CTA's key atomicMax (same thread, cta_merge) and, in the
+        // last CTA, acquires every other CTA's -- no separate sequentially-consistent fences
         const unsigned int total = gridDim.x * gridDim.y;
-        const unsigned int prev = atomicAdd(p.ws_counter, 1u);
+        unsigned int prev;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.ws_counter) : "memory");
         *s_last = (prev == total - 1);
     }
     __syncthreads();
     if (!*s_last) return;
-    __threadfence();
     verify_epilogue(p);
 }
 
@@ -270,6 +278,7 @@ template <bool BF16>
 __global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p) {
     pdl_wait();                // the logits' producer (and the previous round) completed
     pdl_launch_dependents();
+    if (p.exp == 2) return;    // timing experiment only: the launch floor of this grid
     using T = H16<BF16>;
     __shared__ unsigned long long s_red[kVerifyThreads / kWarp];
     __shared__ uint32_t s_m[kVerifyThreads / kWarp];
@@ -382,26 +391,43 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
     p.pred = d_pred; p.plan_L = d_plan_L; p.n_new = d_n_new; p.pad_new = d_pad_new; p.kept = d_kept;
     p.kept_draft = d_kept_draft;
     p.anchor = d_anchor; p.anchor_cap = anchor_cap; p.phys_old = d_phys_old; p.phys_new = d_phys_new;
-    static int exp = -1;
+    static int exp = -1, cta_mult = 4, vpt = 0;
     if (exp < 0) {
         const char *e = getenv("SPECDEC_K1_EXP");
         exp = e ? atoi(e) : 0;
+        const char *c = getenv("SPECDEC_K1_CTAS");  // tuning override: target CTAs per SM
+        if (c && atoi(c) > 0) cta_mult = atoi(c);
+        const char *v = getenv("SPECDEC_K1_VPT");   // tuning override: 16-B vectors per thread
+        if (v && atoi(v) > 0) vpt = std::min(atoi(v), kVPT);
     }
     p.exp = exp;
     p.status = d_status;
     p.ws_keys = static_cast<unsigned long long *>(d_ws);
     p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
 
-    // one wave: about 4 CTAs per SM over the whole logits tail, chunks in multiples of
-    // one 16-byte vector per thread, so there is no tail wave and every SM streams.
     const int VE = 16 / es;
     const int64_t rows = B * (k + 1);
     const int64_t quantum = static_cast<int64_t>(kVerifyThreads) * VE;
-    const int64_t target_ctas = 4ll * device_sm_count();
-    const int64_t per_row = std::max<int64_t>(1, target_ctas / rows);  // CTAs per (row, slot)
-    int64_t chunk = (V + per_row - 1) / per_row;
-    chunk = std::max<int64_t>(quantum, (chunk + quantum - 1) / quantum * quantum);
-    if (es == 2) chunk = std::min<int64_t>(chunk, quantum * kVPT);  // register-resident
+    const int64_t sms = device_sm_count();
+    int64_t chunk;
+    if (es == 2) {
+        // 16-bit logits, register-resident: as many 16-B vectors per thread as possible (fewer
+        // CTAs = fewer merges and arrivals on the latency-bound path) while the grid still
+        // covers >= 3/4 of the SMs.  Sweep (profiles/r01/k1_sweep.txt): best or within 3 %
+        // of best at B = 1, 2, 4, 8, 16.
+        int v = kVPT;
+        for (const int c : {8, 6, 4, 3, 2, 1}) {
+            v = c;
+            if (rows * ((V + quantum * c - 1) / (quantum * c)) * 4 >= 3 * sms) break;
+        }
+        if (vpt > 0) v = vpt;
+        chunk = quantum * v;
+    } else {
+        // fp32 (strided loop): about cta_mult CTAs per SM in one wave, no tail wave
+        const int64_t per_row = std::max<int64_t>(1, cta_mult * sms / rows);  // CTAs per (row, slot)
+        chunk = (V + per_row - 1) / per_row;
+        chunk = std::max<int64_t>(quantum, (chunk + quantum - 1) / quantum * quantum);
+    }
     p.chunk = chunk;
     const int64_t n_chunks = (V + chunk - 1) / chunk;
     dim3 grid(static_cast<unsigned>(n_chunks), static_cast<unsigned>(rows));

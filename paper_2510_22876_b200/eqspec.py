@@ -47,10 +47,13 @@ class EqSpecBatch:
         self.budget = torch.full((B,), max_new, dtype=i32, device=dev) if max_new else None
         self.gen = torch.zeros(B, dtype=i32, device=dev)
         self.out_buf = torch.zeros((B, max_new), dtype=i64, device=dev) if max_new else None
-        self.accept = torch.zeros(B, dtype=i32, device=dev)
-        self.bonus = torch.zeros(B, dtype=i64, device=dev)
-        self.emit = torch.zeros(B, dtype=i32, device=dev)
-        self.finished = torch.zeros(B, dtype=u8, device=dev)
+        # per-round results, one set per state parity: a round's results stay readable
+        # (e.g. by an asynchronous D2H on another stream) while the next round runs
+        self._accept = torch.zeros((2, B), dtype=i32, device=dev)
+        self._bonus = torch.zeros((2, B), dtype=i64, device=dev)
+        self._emit = torch.zeros((2, B), dtype=i32, device=dev)
+        self._finished = torch.zeros((2, B), dtype=u8, device=dev)
+        self._last = 0  # parity of the last launched round
         self.kept = torch.zeros(B, dtype=i32, device=dev)
         self.plan_L = torch.zeros(1, dtype=i32, device=dev)
         self.pred = torch.zeros((B, k + 1), dtype=i64, device=dev) if with_pred else None
@@ -86,6 +89,8 @@ class EqSpecBatch:
         # K3 on a side stream under K2: a small win for direct launches, a loss inside a
         # CUDA graph (measured: profiles/r01/round_modes.txt), so off by default
         self.fork = False
+        # K2 starts under K3 (SPECDEC_OVERLAP_PREV; serial launch order only)
+        self.overlap = bool(int(os.environ.get("SPECDEC_OVERLAP", "1")))
         self._graphs = {}
 
     # ----------------------------------------------------------------- state I/O
@@ -130,6 +135,23 @@ class EqSpecBatch:
     def pad_cur(self):
         return self.pad[self.cur]
 
+    # results of the last launched round (its parity's set)
+    @property
+    def accept(self):
+        return self._accept[self._last]
+
+    @property
+    def bonus(self):
+        return self._bonus[self._last]
+
+    @property
+    def emit(self):
+        return self._emit[self._last]
+
+    @property
+    def finished(self):
+        return self._finished[self._last]
+
     @property
     def kv_strides(self):
         s = self.kv.stride()
@@ -138,6 +160,7 @@ class EqSpecBatch:
     # ----------------------------------------------------------------- the three calls
     def verify(self, logits, draft, stream=None):
         c, nx = self.cur, 1 - self.cur
+        self._last = c
         _abi.specdec_verify(logits, draft, self.n[c], self.active, self.accept, self.bonus,
                             self.emit, self.finished, self.plan_L, self.n[nx], self.pad[nx],
                             self.kept, self.ws, V=self.V or logits.shape[2],
@@ -155,14 +178,14 @@ class EqSpecBatch:
                                       gen=self.gen if self.out_buf is not None else None,
                                       status=self.status, stream=stream)
 
-    def _realign_one(self, kv, count, dims, src, dst, stream):
+    def _realign_one(self, kv, count, dims, src, dst, stream, overlap=False):
         planes, H, D = dims
         s = kv.stride()
+        flags = (_abi.ZERO_PADS if self.zero_pads else 0) | (_abi.OVERLAP_PREV if overlap else 0)
         _abi.specdec_realign_kv(kv, kv, count, n_planes=planes, n_rows=self.B, H=H, D=D,
                                 src_strides=s[:3], dst_strides=s[:3], cap_src=self.cap_phys,
                                 cap_dst=self.cap_phys, src_col=src, dst_col=dst,
-                                flags=_abi.ZERO_PADS if self.zero_pads else 0,
-                                ws=self.rws if self.segment else None,
+                                flags=flags, ws=self.rws if self.segment else None,
                                 moved_bytes=self.moved, status=self.status, stream=stream)
 
     def realign(self, stream=None):
@@ -175,7 +198,9 @@ class EqSpecBatch:
             src, dst = self.phys_old, self.phys_new        # f3: physical columns from K1
         else:
             src, dst = self.pad[c], self.pad[nx]
-        self._realign_one(self.kv, self.kept, (self.n_planes, self.H, self.D), src, dst, stream)
+        # serial order K1 -> K3 -> K2: K3 waited on K1, so the first K2 may start under it
+        self._realign_one(self.kv, self.kept, (self.n_planes, self.H, self.D), src, dst, stream,
+                          overlap=self.overlap and not self.fork)
         if self.dkv is not None:     # f1: the draft model's own cache, same shift, kept_draft
             self._realign_one(self.dkv, self.kept_draft, self.d_dims, src, dst, stream)
 
@@ -237,4 +262,5 @@ class EqSpecBatch:
     def replay(self, j):
         """One EqSpec round from input pair j via its captured graph; flips the parity."""
         self._graphs[(self.cur, j)].replay()
+        self._last = self.cur
         self.cur = 1 - self.cur
