@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--min-group", type=int, default=2)
     ap.add_argument("--max-new", type=int, default=256)
     ap.add_argument("--shard", default="band", choices=["band", "strided"])
+    ap.add_argument("--pool-consumer", default="zero-copy", choices=["zero-copy", "dense"],
+                    help="pool: same-length batches run on the pool slots (zero-copy) or are "
+                         "gathered into a dense staging rectangle too (PAPER.md:537)")
     ap.add_argument("--pool-exec", default="native", choices=["native", "python"],
                     help="pool: per-batch launch loop in C++ (specdec_pool_epoch) or Python")
     ap.add_argument("--pool-mode", default="epoch", choices=["epoch", "alg3"],
@@ -66,6 +69,8 @@ def parse():
                     help="f3: anchored-origin realign (K1 moves the KV origin to minimise moved rows)")
     ap.add_argument("--draft-kv", action="store_true",
                     help="f1: the draft model keeps its own KV cache, realigned every round too")
+    ap.add_argument("--kv-mode", default="inplace", choices=["inplace", "pingpong"],
+                    help="K2 in place, or out of place between two KV buffers (copies Delta=0 rows too)")
     ap.add_argument("--round-mode", default="graph-serial",
                     choices=["graph-fork", "graph-serial", "direct-fork", "direct-serial"],
                     help="value region: CUDA-graph replay or direct launches; K3 forked under K2 or serial")
@@ -178,6 +183,7 @@ DRAFT_DIMS = {"vicuna": (2, 12, 64), "qwen3": (28, 8, 128), "glm4": (28, 8, 128)
 def workload_name(sh, args):
     d = f", draft KV {DRAFT_DIMS[sh.name]} realigned too" if getattr(args, "draft_kv", False) else ""
     d += ", anchored origin (f3)" if getattr(args, "anchor", False) else ""
+    d += ", ping-pong KV (out of place)" if getattr(args, "kv_mode", "inplace") == "pingpong" else ""
     return (f"{sh.name} EqSpec round: B={sh.B} k={sh.k} V={sh.V} KV {sh.layers}x{sh.H}x{sh.D} "
             f"{sh.kv_dtype}, n~U[{sh.len_lo},{sh.len_hi}], accept={args.pattern}{d}")
 
@@ -199,7 +205,10 @@ class RoundBench:
         # f3: slack for the moving origin: at most k+1 columns of drift per round
         slack = (k + 1) * total_rounds if args.anchor else 0
         self.bt = EqSpecBatch(B, k, self.cap, sh.layers, sh.H, sh.D, sh.kv_dtype, device, draft=draft,
-                              anchor_slack=slack)
+                              anchor_slack=slack, kv_mode=args.kv_mode)
+        # ping-pong: the method's (algorithmic) KV bytes are those of the rows that shift;
+        # K2 also copies the Delta = 0 rows (counted by the device `moved` counter)
+        self.alg_rows = torch.zeros(1, dtype=torch.int64, device=device)
         if draft is not None:
             self.bt.dkv.copy_(W.gen_kv_torch(args.seed + 1, self.bt.dkv.shape, self.bt.dkv.dtype, device))
         self.bt.load(self.tokens, self.lengths)
@@ -246,6 +255,9 @@ class RoundBench:
         bt.realign()
         if ev is not None:
             ev[3].record(self.stream)
+            if bt.kv_mode == "pingpong":
+                c = bt.cur
+                self.alg_rows += (bt.kept.long() * (bt.pad[c] != bt.pad[1 - c])).sum()
         bt.cur = 1 - bt.cur
 
     def mean_width(self):
@@ -329,13 +341,17 @@ def run_ours(args, rank, world, device):
         rb.step(r, evs[r])
     sync()
     moved_B = int(bt.moved.item()) - moved0
+    # algorithmic K2 bytes of region B: in place = the device counter (only shifting rows
+    # move); ping-pong = the shifting rows' bytes, although every kept row is copied
+    alg_B = moved_B if bt.kv_mode == "inplace" else int(rb.alg_rows.item()) * 2 * sh.bpt
     k1 = sum(e[0].elapsed_time(e[1]) for e in evs)
     k3 = sum(e[1].elapsed_time(e[2]) for e in evs)
     k2 = sum(e[2].elapsed_time(e[3]) for e in evs)
     # ---- C: e2e
     e2e = None if args.no_e2e else run_e2e(rb, args, world)
     logits_bytes = sh.B * (sh.k + 1) * sh.V * (4 if sh.logit_dtype == "fp32" else 2)
-    return dict(sh=sh, ms=max_over_ranks(ms, device, world), moved=moved_B, moved_A=moved_A, k1_ms=k1, k3_ms=k3,
+    return dict(sh=sh, ms=max_over_ranks(ms, device, world), moved=alg_B, copied=moved_B, moved_A=moved_A,
+                k1_ms=k1, k3_ms=k3,
                 kernels_per_round=bt.kernels_per_round,
                 k2_ms=k2, status=status | int(bt.status.item()), clocks=clocks.summary(), e2e=e2e,
                 end_width=width_end, logits_bytes=logits_bytes)
@@ -504,7 +520,8 @@ def run_pool(args, rank, world, device):
     cap = ((int(lens.max()) + args.max_new + k + 1) + 15) // 16 * 16
     Wn = min(args.pool_W or n_loc, 2048, n_loc)
     sp = SequencePool(n_loc, cap, sh.layers, sh.H, sh.D, k, W=Wn, B=min(B, Wn),
-                      min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False)
+                      min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False,
+                      dense_consumer=args.pool_consumer == "dense")
     local_lens = lens[mine]
     local_order = np.arange(n_loc)            # `mine` is already in admission order
     ring_lg = [W.gen_logits_torch(args.seed, r, sp.B, k, V, sh.logit_dtype, device) for r in range(RING)]
@@ -554,7 +571,7 @@ def run_pool(args, rank, world, device):
                 ran[1 if kinds[b] else 3] += 1 if kinds[b] else int(sizes[b])
                 ran[2] += int(sizes[b]) if kinds[b] else 0
                 lg, d = inputs(b)
-                if events is not None and not kinds[b]:
+                if events is not None and (not kinds[b] or sp.dense_consumer):
                     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                     e[0].record()
                     sp.gather(b)
@@ -618,7 +635,7 @@ def run_pool(args, rank, world, device):
         "config": {"workload": f"EXSpec pool drain: {N} seqs, prompt {args.pool_lengths} "
                                f"{'U[64,512]' if args.pool_lengths == 'random' else '256'}, max_new "
                                f"{args.max_new}, W={Wn}/rank, B={sp.B}, min_group={args.min_group}, "
-                               f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}, "
+                               f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}, {args.pool_consumer} consumer, "
                                f"{args.pool_exec} launch loop",
                    "cap": cap, "pool_kv_GB_per_rank": sp.kv.numel() * 2 / 1e9,
                    "parallelism": f"pool sharded x{world}", "step": "one epoch (K4 plan + its batches)"},
@@ -631,7 +648,11 @@ def run_pool(args, rank, world, device):
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_src},
         "clocks": clocks.summary(), "status": status,
-        "gpu_launches": None, "e2e": None, "cpu_baseline": None,
+        # libspecdec launches in the timed drain: K4 per plan (the epochs + the final empty
+        # plan), K1 + write-back per batch, gather + scatter per fallback batch
+        "gpu_launches": (epochs + 1) + 2 * int(cnt[0])
+        + 2 * (int(cnt[0]) if sp.dense_consumer else int(cnt[0]) - int(cnt[1])),
+        "e2e": None, "cpu_baseline": None,
     }
 
 
@@ -700,7 +721,7 @@ def main():
         bytes_per_launch = res["moved"] / args.steps
         # (B=1 moves no KV: K2 is not launched and the roofline line reports 0 bytes)
         achieved = bytes_per_launch / (k2_launch_ms / 1e3) / 1e9 if k2_launch_ms > 1e-6 else 0.0
-        traffic, traffic_note = ncu_traffic(f"{sh.name}_B{sh.B}")
+        traffic, traffic_note = ncu_traffic(f"{sh.name}_B{sh.B}" + ("_pingpong" if args.kv_mode == "pingpong" else ""))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             rps, parts = oracle_round_sample(sh, args, rounds=2)
@@ -725,7 +746,10 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "specdec_realign_kv (K2)", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "traffic_note": traffic_note, "peak_source": peak_src,
-                         "bytes_per_launch": bytes_per_launch, "launch_ms": k2_launch_ms},
+                         "bytes_per_launch": bytes_per_launch, "launch_ms": k2_launch_ms,
+                         "kv_mode": args.kv_mode,
+                         "copied_GBps": res["copied"] / args.steps / (k2_launch_ms / 1e3) / 1e9
+                         if k2_launch_ms > 1e-6 else 0.0},
             "kernels_ms_per_step": {"verify_K1": res["k1_ms"] / args.steps,
                                     "repad_K3": res["k3_ms"] / args.steps,
                                     "realign_K2": k2_launch_ms},
@@ -734,7 +758,7 @@ def main():
             "e2e": res["e2e"],
             "gpu_launches": res["kernels_per_round"] * args.steps,
             "launch_mode": args.round_mode + " (graph: one CUDA graph per (parity, ring slot), 3 kernels per replay)",
-            "bytes_moved_check": {"value_region": res["moved_A"], "kernel_region": res["moved"]},
+            "bytes_moved_check": {"value_region": res["moved_A"], "kernel_region": res["copied"]},
             "status": res["status"],
             "cpu_baseline": cpu,
         }

@@ -50,6 +50,7 @@ typedef struct CUstream_st *specdec_stream_t; /* == cudaStream_t */
 #define SPECDEC_ST_NAN 1u      /* a NaN logit was seen (the argmax is still defined: first NaN) */
 #define SPECDEC_ST_CAPACITY 2u /* a width / buffer bound would be exceeded; the row was skipped */
 #define SPECDEC_ST_KEPT 4u     /* a KV row range lies outside [0, cap); the item was skipped */
+#define SPECDEC_ST_BOUND 8u    /* a row's count exceeded the caller's count_bound; row skipped */
 
 /* specdec_realign_kv flags */
 #define SPECDEC_ZERO_PADS 1u    /* also zero the old content columns that became pads */
@@ -185,6 +186,11 @@ int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_tokens_out, 
  *   rows a segment's neighbour overwrites in place (|dcol - scol| rows, <= 4 KB) are first
  *   copied to a workspace slot by a small kernel on the same stream.  NULL: one slab per
  *   CTA (correct, less balanced when few rows move).
+ * count_bound: the caller's upper bound on count[r] + count_add over all rows, or 0 for
+ *   none (then cap_src).  Tight bounds let the host size the launch: slabs of at most
+ *   4 KB (e.g. the pool write-back scatter, a + 1 <= k + 1 rows) are moved by a
+ *   register-staged warp-per-slab kernel with every slab in flight at once instead of
+ *   the TMA ring.  A row above the bound is skipped and sets SPECDEC_ST_BOUND.
  * d_moved_bytes: optional uint64 accumulator of bytes read + written by this call.
  */
 size_t specdec_realign_workspace_size(int dtype, int64_t n_planes, int64_t n_rows, int64_t H,
@@ -195,7 +201,7 @@ int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtype, int64_t 
                        int64_t dst_s_plane, int64_t dst_s_row, int64_t dst_s_head,
                        int64_t cap_dst, const int32_t *d_src_col, int32_t src_col_add,
                        const int32_t *d_dst_col, int32_t dst_col_add, const int32_t *d_count,
-                       int32_t count_add, const int32_t *d_src_row_map,
+                       int32_t count_add, int32_t count_bound, const int32_t *d_src_row_map,
                        const int32_t *d_dst_row_map, uint32_t flags, void *d_ws,
                        size_t ws_bytes, unsigned long long *d_moved_bytes, uint32_t *d_status,
                        specdec_stream_t stream);
@@ -311,6 +317,10 @@ typedef struct specdec_pool_desc {
     const int64_t *const *draft_ring;
     int32_t ring_n;
     int32_t *ring_pos; /* host, advanced per batch */
+    /* 1: gather / scatter every batch, same-length ones too -- a consumer that needs a
+     * dense rectangle ("concatenate directly"); 0: same-length batches run
+     * zero-copy on the pool slots (forward kind = 1) */
+    int32_t dense_consumer;
 } specdec_pool_desc;
 
 int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,

@@ -16,7 +16,7 @@ _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspecdec
 _lib = None
 
 OK, ERR_ARG, ERR_SHAPE, ERR_DTYPE, ERR_CAPACITY, ERR_CUDA = 0, -1, -2, -3, -4, -5
-ST_NAN, ST_CAPACITY, ST_KEPT = 1, 2, 4
+ST_NAN, ST_CAPACITY, ST_KEPT, ST_BOUND = 1, 2, 4, 8
 ZERO_PADS = 1
 OVERLAP_PREV = 2
 DTYPE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
@@ -38,7 +38,7 @@ _SIGS = {
                                   _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P], _INT),
     "specdec_realign_workspace_size": ([_INT, _I64, _I64, _I64, _I64, _I64], ctypes.c_size_t),
     "specdec_realign_kv": ([_P, _P, _INT, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _I64,
-                            _I64, _I64, _I64, _P, _I32, _P, _I32, _P, _I32, _P, _P, _U32, _P,
+                            _I64, _I64, _I64, _P, _I32, _P, _I32, _P, _I32, _I32, _P, _P, _U32, _P,
                             ctypes.c_size_t, _P, _P, _P], _INT),
     "specdec_pool_group": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                             _P, _P, _P, _P, _P, _P], _INT),
@@ -67,6 +67,7 @@ class PoolDesc(ctypes.Structure):
         ("k", _I64), ("V", _I64), ("logit_stride", _I64), ("eos_id", _I64), ("pad_id", _I64),
         ("logit_dtype", _INT),
         ("logits_ring", _P), ("draft_ring", _P), ("ring_n", _I32), ("ring_pos", _P),
+        ("dense_consumer", _I32),
     ]
 
 
@@ -168,16 +169,17 @@ def specdec_realign_workspace_size(dtype, n_planes, n_rows, H, D, cap) -> int:
 
 def specdec_realign_kv(kv_src, kv_dst, count, *, n_planes, n_rows, H, D, src_strides,
                        dst_strides, cap_src, cap_dst, src_col=None, src_col_add=0,
-                       dst_col=None, dst_col_add=0, count_add=0, src_row_map=None,
-                       dst_row_map=None, flags=0, ws=None, moved_bytes=None, status=None,
-                       stream=None):
+                       dst_col=None, dst_col_add=0, count_add=0, count_bound=0,
+                       src_row_map=None, dst_row_map=None, flags=0, ws=None, moved_bytes=None,
+                       status=None, stream=None):
     """src/dst_strides = (s_plane, s_row, s_head) in elements; positions are D apart.
-    ws: optional workspace tensor of specdec_realign_workspace_size bytes (segmentation)."""
+    ws: optional workspace tensor of specdec_realign_workspace_size bytes (segmentation).
+    count_bound: upper bound on count + count_add (0 = none)."""
     _check(load().specdec_realign_kv(
         _ptr(kv_src), _ptr(kv_dst), DTYPE[kv_src.dtype], n_planes, n_rows, H, D,
         src_strides[0], src_strides[1], src_strides[2], cap_src, dst_strides[0],
         dst_strides[1], dst_strides[2], cap_dst, _ptr(src_col), src_col_add, _ptr(dst_col),
-        dst_col_add, _ptr(count), count_add, _ptr(src_row_map), _ptr(dst_row_map), flags,
+        dst_col_add, _ptr(count), count_add, count_bound, _ptr(src_row_map), _ptr(dst_row_map), flags,
         _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
         _ptr(moved_bytes), _ptr(status), _stream(stream)), "specdec_realign_kv")
 

@@ -51,7 +51,8 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     (void)es;
     int32_t ran = 0, same = 0, msame = 0, mfb = 0;
     for (int32_t b = 0; b < run; ++b) {
-        const bool fallback = kinds[b] == 0;
+        const bool same_len = kinds[b] != 0;
+        const bool fallback = !same_len || d->dense_consumer;  // moves KV through the staging
         int32_t *members = d->members + static_cast<int64_t>(b) * B;
         int32_t *mlen = d->mlen + static_cast<int64_t>(b) * B;
         int32_t *mpad = d->mpad + static_cast<int64_t>(b) * B;
@@ -59,7 +60,7 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         if (fallback) {
             rc = specdec_realign_kv(d->kv, d->staging, d->kv_dtype, d->n_planes, B, d->H, d->D,
                                     p_plane, p_row, p_head, d->cap, s_plane, s_row, s_head, d->cap,
-                                    nullptr, 0, mpad, 0, mlen, -1, members, nullptr, 0, nullptr, 0,
+                                    nullptr, 0, mpad, 0, mlen, -1, 0, members, nullptr, 0, nullptr, 0,
                                     d->moved, d->status, stream);
             if (rc) return rc;
         }
@@ -85,13 +86,16 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         if (fallback) {
             rc = specdec_realign_kv(d->staging, d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D,
                                     s_plane, s_row, s_head, d->cap, p_plane, p_row, p_head, d->cap,
-                                    nullptr, blens[b] - 1, mlen, -1, d->accept, 1, nullptr,
-                                    members, 0, nullptr, 0, d->moved, d->status, stream);
+                                    nullptr, blens[b] - 1, mlen, -1, d->accept, 1,
+                                    static_cast<int32_t>(d->k + 1),  // a + 1 <= k + 1 rows
+                                    nullptr, members, 0, nullptr, 0, d->moved, d->status, stream);
             if (rc) return rc;
-            mfb += sizes[b];
-        } else {
+        }
+        if (same_len) {
             ++same;
             msame += sizes[b];
+        } else {
+            mfb += sizes[b];
         }
         ++ran;
     }

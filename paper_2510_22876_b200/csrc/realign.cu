@@ -51,6 +51,7 @@ struct RealignParams {
     int64_t ds_plane, ds_row, ds_head, cap_dst;  // dst strides in bytes
     const int32_t *src_col, *dst_col, *count, *src_map, *dst_map;
     int32_t src_col_add, dst_col_add, count_add;
+    int32_t count_bound;  // caller's bound on the rows per slab (0 = none)
     uint32_t flags;
     int inplace;
     int policy_mode;  // 0: L2 evict_first on the streamed bytes, 1: evict_normal
@@ -66,8 +67,10 @@ struct RowGeom {
     int64_t shift;                   // in place: dst - src in rows (0 for distinct buffers)
 };
 
-__device__ __forceinline__ bool row_geom(const RealignParams &p, int r, RowGeom &g, bool &bad) {
-    bad = false;
+// bad: SPECDEC_ST_KEPT (column range outside the capacity) / SPECDEC_ST_BOUND (count above
+// the caller's bound) -- the row is skipped
+__device__ __forceinline__ bool row_geom(const RealignParams &p, int r, RowGeom &g, uint32_t &bad) {
+    bad = 0u;
     // L2 loads: under SPECDEC_OVERLAP_PREV the plan's producer finished before this grid
     // started but this grid never waited on it, so nothing may come from a stale L1 line
     const int32_t cnt = __ldcg(p.count + r) + p.count_add;
@@ -78,7 +81,11 @@ __device__ __forceinline__ bool row_geom(const RealignParams &p, int r, RowGeom 
     const int32_t sc = (p.src_col ? __ldcg(p.src_col + r) : 0) + p.src_col_add;
     const int32_t dc = (p.dst_col ? __ldcg(p.dst_col + r) : 0) + p.dst_col_add;
     if (sc < 0 || dc < 0 || sc + cnt > p.cap_src || dc + cnt > p.cap_dst) {
-        bad = true;
+        bad = SPECDEC_ST_KEPT;
+        return false;
+    }
+    if (p.count_bound > 0 && cnt > p.count_bound) {
+        bad = SPECDEC_ST_BOUND;
         return false;
     }
     g.src_off = sr * p.ss_row + sc * p.rb;
@@ -155,7 +162,7 @@ __device__ __forceinline__ void unit_geom(const RealignParams &p, const UnitTabl
     if (mi < kGeomCache) {
         g = t.geo[mi];
     } else {
-        bool bad;
+        uint32_t bad;
         row_geom(p, t.rows[mi], g, bad);
     }
 }
@@ -163,13 +170,14 @@ __device__ __forceinline__ void unit_geom(const RealignParams &p, const UnitTabl
 // Warp-cooperative: moving rows (ballot compaction, row order kept) + segment prefix.
 __device__ void build_table(const RealignParams &p, UnitTable &t, bool report) {
     const int lane = threadIdx.x & 31;
-    bool any_bad = false;
+    uint32_t any_bad = 0u;
     int n_mv = 0;
     int32_t run = 0;
     for (int64_t base = 0; base < p.n_rows; base += 32) {
         const int r = static_cast<int>(base) + lane;
         RowGeom g;
-        bool bad = false, mv = false;
+        uint32_t bad = 0u;
+        bool mv = false;
         if (r < p.n_rows) mv = row_geom(p, r, g, bad);
         const int32_t ns = mv ? static_cast<int32_t>(n_segments(p, g)) : 0;
         const unsigned bal = __ballot_sync(0xFFFFFFFFu, mv);
@@ -190,17 +198,19 @@ __device__ void build_table(const RealignParams &p, UnitTable &t, bool report) {
         n_mv += __popc(bal);
         any_bad |= bad;
     }
-    any_bad = __any_sync(0xFFFFFFFFu, any_bad);
+    any_bad = __reduce_or_sync(0xFFFFFFFFu, any_bad);
     if (lane == 0) {
         t.pre[n_mv] = run;
         t.n_mv = n_mv;
         t.units_per_ph = run;
-        if (report && any_bad && blockIdx.x == 0 && p.status) atomicOr(p.status, SPECDEC_ST_KEPT);
+        if (report && any_bad && blockIdx.x == 0 && p.status) atomicOr(p.status, any_bad);
     }
     __syncwarp();
 }
 
-// unit index -> (plane, moving row, head, segment)
+// unit index -> (plane, moving row, head, segment); the row is the fastest index, so the
+// units processed together (one grid-wide round, below) lie in one contiguous span of
+// planes -- measured 5-7 % faster than the row as the slowest index (tools/kbench.py).
 __device__ __forceinline__ void locate(const RealignParams &p, const UnitTable &t, int64_t u,
                                       int64_t &plane, int64_t &head, int &mi, int64_t &j) {
     const int64_t U = t.units_per_ph;
@@ -215,6 +225,15 @@ __device__ __forceinline__ void locate(const RealignParams &p, const UnitTable &
     }
     mi = lo;
     j = r2 - t.pre[lo];
+}
+
+// The ring kernel's CTA b takes, in round r, unit r*G + ((b + r) mod G) (G = grid size):
+// every round still covers one contiguous block of G units (DRAM locality), but a CTA's
+// row residue advances by G + 1 per round instead of G, so it sweeps all rows even when
+// G and the number of rows share a factor (148 = 4 * 37: with 4 or 8 moving rows a plain
+// grid stride handed each CTA one or two rows, and rows of unequal length left CTAs idle).
+__device__ __forceinline__ int64_t unit_of_round(int64_t r, int64_t b, int64_t G) {
+    return r * G + (b + r) % G;
 }
 
 // ----------------------------------------------------------------------------- boundary save
@@ -256,6 +275,55 @@ __global__ void __launch_bounds__(32 * kSaveWarps) realign_save_kernel(RealignPa
     }
 }
 
+// ----------------------------------------------------------------------------- small slabs
+// Slabs of at most kSmallBytes (the caller's count_bound says so; e.g. the pool write-back
+// scatter moves a + 1 <= k + 1 rows): one warp per slab, every 16-byte vector of the slab
+// loaded into registers before any is stored -- in place too, since a slab's source and
+// destination lie inside the slab's own row -- and 8 warps per CTA, ~8 CTAs per SM, so
+// nearly every slab of the call is in flight at once.  The TMA ring would hold 3 slabs
+// per SM and pay a DRAM round trip for each.
+constexpr int64_t kSmallBytes = 4096;
+constexpr int kSmallWarps = 8;
+constexpr int kSmallVec = kSmallBytes / 16 / 32;  // 16-B vectors per lane
+
+__global__ void __launch_bounds__(32 * kSmallWarps) realign_small_kernel(RealignParams p) {
+    __shared__ UnitTable t;
+    const bool overlap = (p.flags & SPECDEC_OVERLAP_PREV) != 0;
+    if (!overlap) pdl_wait();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) build_table(p, t, true);
+    __syncthreads();
+    const int64_t n_units = p.n_planes * p.H * t.units_per_ph;  // one segment per slab here
+    unsigned long long moved = 0;
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * kSmallWarps + warp; u < n_units;
+         u += static_cast<int64_t>(gridDim.x) * kSmallWarps) {
+        int64_t plane, head, j;
+        int mi;
+        locate(p, t, u, plane, head, mi, j);
+        RowGeom g;
+        unit_geom(p, t, mi, g);
+        const char *src = p.src + plane * p.ss_plane + head * p.ss_head + g.src_off;
+        char *dst = p.dst + plane * p.ds_plane + head * p.ds_head + g.dst_off;
+        const int64_t nb = g.rows * p.rb;  // <= kSmallBytes: the host checked count_bound
+        const int nv = static_cast<int>(nb / 16);
+        uint4 v[kSmallVec];
+#pragma unroll
+        for (int q = 0; q < kSmallVec; ++q)  // plain (coherent) loads: in place, dst aliases src
+            if (lane + q * 32 < nv) v[q] = reinterpret_cast<const uint4 *>(src)[lane + q * 32];
+#pragma unroll
+        for (int q = 0; q < kSmallVec; ++q)
+            if (lane + q * 32 < nv) reinterpret_cast<uint4 *>(dst)[lane + q * 32] = v[q];
+        if ((p.flags & SPECDEC_ZERO_PADS) && p.inplace && dst > src) {
+            // old content rows [scol, dcol) became pads (all of them were loaded above)
+            for (int64_t z = lane * 16; z < dst - src; z += 32 * 16)
+                *reinterpret_cast<uint4 *>(const_cast<char *>(src) + z) = make_uint4(0, 0, 0, 0);
+        }
+        moved += 2ull * static_cast<unsigned long long>(nb);
+    }
+    if (p.moved && lane == 0 && moved) atomicAdd(p.moved, moved);
+    if (overlap) pdl_wait();
+}
+
 // ----------------------------------------------------------------------------- main kernel
 template <int STAGES, int CHUNK>
 struct RealignSmem {
@@ -272,7 +340,7 @@ struct RealignSmem {
 // Load-side iterator over this CTA's (unit, chunk) stream: the unit's main rows in the
 // walking direction, then its boundary rows from the slot as one last chunk.
 struct ChunkIter {
-    int64_t u, n_units, stride;
+    int64_t u, n_units, stride, round;
     Unit un;
     int64_t q, nmain;      // main chunks
     bool bnd_left;         // boundary chunk still to issue
@@ -318,7 +386,8 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
     ChunkIter it;
     it.n_units = p.n_planes * p.H * sm.t.units_per_ph;
     it.stride = gridDim.x;
-    it.u = blockIdx.x;
+    it.round = 0;
+    it.u = unit_of_round(0, blockIdx.x, it.stride);
     if (it.u >= it.n_units) return;
     iter_unit<STAGES, CHUNK>(p, sm, it);
     unsigned long long moved = 0;
@@ -359,7 +428,7 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
         mbar_arrive_expect_tx(&sm.bar[stage], static_cast<uint32_t>(nb));
         bulk_load(sm.ring[stage], src, static_cast<uint32_t>(nb), &sm.bar[stage], pol);
         if (last) {
-            it.u += it.stride;
+            it.u = unit_of_round(++it.round, blockIdx.x, it.stride);
             if (it.u < it.n_units) iter_unit<STAGES, CHUNK>(p, sm, it);
         }
     };
@@ -459,6 +528,20 @@ int64_t max_units_bound(int64_t n_planes, int64_t n_rows, int64_t H, int64_t rb,
     return n_planes * H * n_rows * ((cap + sr - 1) / sr);
 }
 
+int launch_realign_small(const RealignParams &p, cudaStream_t s) {
+    static int per_sm = 0;  // resident CTAs per SM: one wave, grid-strided
+    if (per_sm == 0) {
+        const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, realign_small_kernel,
+                                                                            32 * kSmallWarps, 0);
+        if (e != cudaSuccess) return record_cuda_error(e);
+        per_sm = std::max(1, per_sm);
+    }
+    const int64_t slabs = p.n_planes * p.H * p.n_rows;
+    const int64_t grid = std::max<int64_t>(
+        1, std::min<int64_t>((slabs + kSmallWarps - 1) / kSmallWarps, static_cast<int64_t>(per_sm) * device_sm_count()));
+    return launch_k(realign_small_kernel, dim3(static_cast<unsigned>(grid)), dim3(32 * kSmallWarps), 0, s, p);
+}
+
 }  // namespace specdec
 
 using namespace specdec;
@@ -476,7 +559,7 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
                                   int64_t dst_s_plane, int64_t dst_s_row, int64_t dst_s_head,
                                   int64_t cap_dst, const int32_t *d_src_col, int32_t src_col_add,
                                   const int32_t *d_dst_col, int32_t dst_col_add,
-                                  const int32_t *d_count, int32_t count_add,
+                                  const int32_t *d_count, int32_t count_add, int32_t count_bound,
                                   const int32_t *d_src_row_map, const int32_t *d_dst_row_map,
                                   uint32_t flags, void *d_ws, size_t ws_bytes,
                                   unsigned long long *d_moved_bytes, uint32_t *d_status,
@@ -497,6 +580,7 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     if (inplace && (src_s_plane != dst_s_plane || src_s_row != dst_s_row || src_s_head != dst_s_head))
         return SPECDEC_ERR_ARG;
     if ((flags & SPECDEC_ZERO_PADS) && !inplace) return SPECDEC_ERR_ARG;
+    if (count_bound < 0) return SPECDEC_ERR_ARG;
     const int64_t units = max_units_bound(n_planes, n_rows, H, rb, cap_src);
     if (d_ws && (!aligned16(d_ws) || ws_bytes < static_cast<size_t>(units) * kSlotBytes)) return SPECDEC_ERR_ARG;
     RealignParams p;
@@ -508,6 +592,7 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     p.src_col = d_src_col; p.dst_col = d_dst_col; p.count = d_count;
     p.src_map = d_src_row_map; p.dst_map = d_dst_row_map;
     p.src_col_add = src_col_add; p.dst_col_add = dst_col_add; p.count_add = count_add;
+    p.count_bound = count_bound;
     p.flags = flags; p.inplace = inplace ? 1 : 0;
     p.ws = static_cast<char *>(d_ws);
     p.ws_slots = d_ws ? units : 0;
@@ -527,9 +612,18 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     }
     p.policy_mode = pol;
     p.seg_bytes = g_seg_bytes;
+    if (count_bound > 0 && count_bound * rb <= kSmallBytes) {
+        p.ws = nullptr;  // small slabs are never segmented
+        p.ws_slots = 0;
+        return launch_realign_small(p, s);
+    }
+    // a tight bound also sizes the ring kernel's grid (work units actually possible)
+    const int64_t units_launch = count_bound > 0
+        ? std::min(units, max_units_bound(n_planes, n_rows, H, rb, std::min<int64_t>(cap_src, count_bound)))
+        : units;
     switch (cfg) {
-        case 1: return launch_realign<4, 16384>(p, units, s);
-        case 2: return launch_realign<6, 32768>(p, units, s);
-        default: return launch_realign<3, 32768>(p, units, s);  // measured best
+        case 1: return launch_realign<4, 16384>(p, units_launch, s);
+        case 2: return launch_realign<6, 32768>(p, units_launch, s);
+        default: return launch_realign<3, 32768>(p, units_launch, s);  // measured best
     }
 }

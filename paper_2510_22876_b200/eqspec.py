@@ -15,7 +15,10 @@ and a round can be captured once per (parity, input buffer) as a CUDA graph.
 
 Options: `draft=(layers, H, D)` adds the draft model's own KV cache,
 realigned with kept_draft (f1); `anchor_slack=S` keeps the KV in a physical buffer of
-cap + S columns whose logical origin K1 moves to minimise the rows that must move (f3).
+cap + S columns whose logical origin K1 moves to minimise the rows that must move (f3);
+`kv_mode="pingpong"` keeps two KV buffers and realigns out of place from the current into
+the other one every round -- rows with Delta = 0 are copied too (the SURVEY §8d ping-pong
+cell, the analog of the paper's fresh-tensor realignment).
 """
 from __future__ import annotations
 
@@ -31,7 +34,15 @@ TORCH_DT = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16
 
 class EqSpecBatch:
     def __init__(self, B, k, cap, layers, H, D, kv_dtype="bf16", device="cuda", max_new=0,
-                 eos_id=-1, pad_id=0, with_pred=False, draft=None, anchor_slack=0):
+                 eos_id=-1, pad_id=0, with_pred=False, draft=None, anchor_slack=0,
+                 kv_mode="inplace"):
+        if kv_mode not in ("inplace", "pingpong"):
+            raise ValueError(f"kv_mode {kv_mode!r}")
+        if kv_mode == "pingpong" and anchor_slack:
+            raise ValueError("the anchored origin (f3) is an in-place scheme")
+        self.kv_mode = kv_mode
+        nbuf = 2 if kv_mode == "pingpong" else 1
+        self.cur = 0  # state parity: round r reads slot cur and writes slot 1 - cur
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         self.B, self.k, self.cap, self.layers, self.H, self.D = B, k, cap, layers, H, D
@@ -67,13 +78,16 @@ class EqSpecBatch:
         self.anchor = torch.full((1,), anchor_slack, dtype=i32, device=dev) if anchor_slack else None
         self.phys_old = torch.zeros(B, dtype=i32, device=dev) if anchor_slack else None
         self.phys_new = torch.zeros(B, dtype=i32, device=dev) if anchor_slack else None
-        self.kv = torch.zeros((self.n_planes, B, H, self.cap_phys, D), dtype=TORCH_DT[kv_dtype], device=dev)
-        self.dkv = None
+        # KV buffers: one (in place) or two (ping-pong: the current one is buffer [cur])
+        self._kvbuf = [torch.zeros((self.n_planes, B, H, self.cap_phys, D), dtype=TORCH_DT[kv_dtype], device=dev)
+                       for _ in range(nbuf)]
+        self._dkvbuf = None
         self.kept_draft = None
         if draft is not None:
             dl, dh, dd = draft
             self.d_dims = (2 * dl, dh, dd)
-            self.dkv = torch.zeros((2 * dl, B, dh, self.cap_phys, dd), dtype=TORCH_DT[kv_dtype], device=dev)
+            self._dkvbuf = [torch.zeros((2 * dl, B, dh, self.cap_phys, dd), dtype=TORCH_DT[kv_dtype], device=dev)
+                            for _ in range(nbuf)]
             self.kept_draft = torch.zeros(B, dtype=i32, device=dev)
         # K2 workspace: boundary-row slots that let any CTA stream any ~128 KB segment of a
         # slab in place (load balance when few rows move); shared by the target and draft calls
@@ -83,7 +97,6 @@ class EqSpecBatch:
                                                              *self.d_dims[1:], self.cap_phys))
         self.rws = torch.empty(max(sizes), dtype=torch.uint8, device=dev)
         self.segment = bool(int(os.environ.get("SPECDEC_SEGMENT", "0")))  # measured: profiles/r01
-        self.cur = 0
         self.V = None
         self.zero_pads = False
         # K3 on a side stream under K2: a small win for direct launches, a loss inside a
@@ -152,6 +165,15 @@ class EqSpecBatch:
     def finished(self):
         return self._finished[self._last]
 
+    # the current KV buffers (ping-pong: the one the next round reads)
+    @property
+    def kv(self):
+        return self._kvbuf[self.cur % len(self._kvbuf)]
+
+    @property
+    def dkv(self):
+        return None if self._dkvbuf is None else self._dkvbuf[self.cur % len(self._dkvbuf)]
+
     @property
     def kv_strides(self):
         s = self.kv.stride()
@@ -178,11 +200,15 @@ class EqSpecBatch:
                                       gen=self.gen if self.out_buf is not None else None,
                                       status=self.status, stream=stream)
 
-    def _realign_one(self, kv, count, dims, src, dst, stream, overlap=False):
+    def _realign_one(self, bufs, count, dims, src, dst, stream, overlap=False):
         planes, H, D = dims
+        c, nx = self.cur, 1 - self.cur
+        kv, kv_dst = (bufs[c], bufs[nx]) if len(bufs) == 2 else (bufs[0], bufs[0])
         s = kv.stride()
+        if self.zero_pads and kv_dst is not kv:
+            raise ValueError("ZERO_PADS is an in-place option (ping-pong pads are don't-care, R8)")
         flags = (_abi.ZERO_PADS if self.zero_pads else 0) | (_abi.OVERLAP_PREV if overlap else 0)
-        _abi.specdec_realign_kv(kv, kv, count, n_planes=planes, n_rows=self.B, H=H, D=D,
+        _abi.specdec_realign_kv(kv, kv_dst, count, n_planes=planes, n_rows=self.B, H=H, D=D,
                                 src_strides=s[:3], dst_strides=s[:3], cap_src=self.cap_phys,
                                 cap_dst=self.cap_phys, src_col=src, dst_col=dst,
                                 flags=flags, ws=self.rws if self.segment else None,
@@ -190,7 +216,7 @@ class EqSpecBatch:
 
     def realign(self, stream=None):
         c, nx = self.cur, 1 - self.cur
-        if self.B == 1 and self.anchor is None:
+        if self.B == 1 and self.anchor is None and self.kv_mode == "inplace":
             # a single row is always right-aligned at L' = n': p' = p = 0, so Realign is a
             # pure truncation that moves nothing -- no launch at all
             return
@@ -199,17 +225,17 @@ class EqSpecBatch:
         else:
             src, dst = self.pad[c], self.pad[nx]
         # serial order K1 -> K3 -> K2: K3 waited on K1, so the first K2 may start under it
-        self._realign_one(self.kv, self.kept, (self.n_planes, self.H, self.D), src, dst, stream,
+        self._realign_one(self._kvbuf, self.kept, (self.n_planes, self.H, self.D), src, dst, stream,
                           overlap=self.overlap and not self.fork)
-        if self.dkv is not None:     # f1: the draft model's own cache, same shift, kept_draft
-            self._realign_one(self.dkv, self.kept_draft, self.d_dims, src, dst, stream)
+        if self._dkvbuf is not None:     # f1: the draft model's own cache, same shift, kept_draft
+            self._realign_one(self._dkvbuf, self.kept_draft, self.d_dims, src, dst, stream)
 
     @property
     def kernels_per_round(self) -> int:
         """libspecdec kernels one round launches (K1, K3, K2 per cache, + save kernels)."""
-        if self.B == 1 and self.anchor is None:
+        if self.B == 1 and self.anchor is None and self.kv_mode == "inplace":
             return 2
-        per_cache = 2 if self.segment else 1
+        per_cache = 2 if self.segment and self.kv_mode == "inplace" else 1
         return 2 + per_cache * (2 if self.dkv is not None else 1)
 
     def launch_round(self, logits, draft, stream=None):

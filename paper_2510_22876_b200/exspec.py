@@ -28,7 +28,8 @@ from .eqspec import TORCH_DT
 
 class SequencePool:
     def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
-                 max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True):
+                 max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True,
+                 dense_consumer=False):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         if B > W:
@@ -38,6 +39,8 @@ class SequencePool:
         self.W, self.B, self.min_group = W, B, min_group
         self.max_new, self.eos_id, self.pad_id = max_new, eos_id, pad_id
         self.device = dev
+        # gather / scatter same-length batches too (a dense-rectangle consumer)
+        self.dense_consumer = bool(dense_consumer)
         self.cap_tok = cap_tok or cap
         # pool state
         self.len = torch.zeros(N, dtype=i32, device=dev)
@@ -138,7 +141,7 @@ class SequencePool:
     def scatter(self, b, blen, stream=None):
         """Write-back Pool.KV[i] <- KV[i]: the a+1 new rows
         staging [L_b-1, L_b+a) -> pool [len-1, len+a)."""
-        _abi.specdec_realign_kv(self.staging, self.kv, self.accept, count_add=1,
+        _abi.specdec_realign_kv(self.staging, self.kv, self.accept, count_add=1, count_bound=self.k + 1,
                                 n_planes=self.n_planes, n_rows=self.B, H=self.H, D=self.D,
                                 src_strides=self.staging_strides, dst_strides=self.kv_strides,
                                 cap_src=self.cap, cap_dst=self.cap, src_col_add=int(blen) - 1,
@@ -160,11 +163,11 @@ class SequencePool:
                                     out_buf=self.out_buf, status=self.status, stream=stream)
 
     def run_batch(self, b, kind, blen, logits, draft, forward=None, V=None, stream=None):
-        fallback = not kind
+        fallback = not kind or self.dense_consumer
         if fallback:
             self.gather(b, stream)
         if forward is not None:
-            forward(self, b, bool(kind), int(blen))
+            forward(self, b, not fallback, int(blen))
         self.verify(b, logits, draft, V, stream)
         self.writeback(b, draft, stream)
         if fallback:
@@ -221,6 +224,7 @@ class SequencePool:
         d.draft_ring = ctypes.cast(self._dr_ptrs, ctypes.c_void_p)
         d.ring_n = len(ring)
         d.ring_pos = ctypes.addressof(self._ring_pos)
+        d.dense_consumer = 1 if self.dense_consumer else 0
         self._desc = d
         return d
 

@@ -60,15 +60,19 @@ def test_host_validation_without_gpu(lib):
     assert rc == _abi.ERR_ARG
     # realign: D*elem not a multiple of 16
     rc = L.specdec_realign_kv(nz, nz, 2, 2, 2, 2, 4, 64, 64, 64, 8, 64, 64, 64, 8, None, 0,
-                              None, 0, nz, 0, None, None, 0, None, 0, None, None, None)
+                              None, 0, nz, 0, 0, None, None, 0, None, 0, None, None, None)
     assert rc == _abi.ERR_ARG
     # in place with row maps -> ERR_ARG
     rc = L.specdec_realign_kv(nz, nz, 2, 2, 2, 2, 8, 64, 64, 64, 8, 64, 64, 64, 8, None, 0,
-                              None, 0, nz, 0, nz, None, 0, None, 0, None, None, None)
+                              None, 0, nz, 0, 0, nz, None, 0, None, 0, None, None, None)
     assert rc == _abi.ERR_ARG
     # workspace too small for the segment slots -> ERR_ARG
     rc = L.specdec_realign_kv(nz, nz, 2, 2, 2, 2, 8, 64, 64, 64, 8, 64, 64, 64, 8, None, 0,
-                              None, 0, nz, 0, None, None, 0, nz, 16, None, None, None)
+                              None, 0, nz, 0, 0, None, None, 0, nz, 16, None, None, None)
+    assert rc == _abi.ERR_ARG
+    # negative count_bound -> ERR_ARG
+    rc = L.specdec_realign_kv(nz, nz, 2, 2, 2, 2, 8, 64, 64, 64, 8, 64, 64, 64, 8, None, 0,
+                              None, 0, nz, 0, -1, None, None, 0, None, 0, None, None, None)
     assert rc == _abi.ERR_ARG
     assert _abi.specdec_realign_workspace_size(__import__("torch").bfloat16, 72, 8, 8, 128, 2736) > 0
     # pool_group: B > W

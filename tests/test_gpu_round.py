@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos_id=-1,
-                zero_pads=False, full_check=True, anchor_slack=0):
+                zero_pads=False, full_check=True, anchor_slack=0, kv_mode="inplace"):
     k, V = shape.k, shape.V
     cap = W.derive_cap(shape.with_(B=B), rounds)
     lengths = W.gen_lengths(shape, seed, B)
@@ -24,7 +24,8 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
     kvshape = (shape.n_planes, B, shape.H, cap, shape.D)
     kv_bits = W.gen_kv_bits_np(seed, int(np.prod(kvshape))).reshape(kvshape)
     bt = EqSpecBatch(B, k, cap, shape.layers, shape.H, shape.D, shape.kv_dtype, cuda,
-                     max_new=max_new, eos_id=eos_id, pad_id=W.PAD_ID, anchor_slack=anchor_slack)
+                     max_new=max_new, eos_id=eos_id, pad_id=W.PAD_ID, anchor_slack=anchor_slack,
+                     kv_mode=kv_mode)
     bt.load(tokens, lengths, bits_to_torch(kv_bits, shape.kv_dtype, cuda))
     base_o = anchor_slack
     bases = []
@@ -65,6 +66,8 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
             assert np.array_equal(bt.phys_new.cpu().numpy(), col_new)
             base_o = b2
             bases.append(b2)
+        elif kv_mode == "pingpong":   # out of place: every kept row is copied, Delta = 0 too
+            moved_expect += 2 * int(np.asarray(v["kept"], np.int64).sum()) * shape.bpt
         else:
             moved_expect += OA.moved_bytes(pad_o, v["pad_new"], v["kept"], shape.bpt)
         zero_regions = OA.zero_pad_region(pad_o, v["pad_new"], v["kept"])
@@ -143,13 +146,21 @@ def test_rounds_budget_staggered_finish(cuda, B):
     _run_rounds(cuda, SMALL16, B, 14, "alpha", seed=B, max_new=33)
 
 
+@pytest.mark.parametrize("pattern", ["alpha", "alternating"])
+def test_rounds_pingpong(cuda, pattern):
+    """kv_mode="pingpong": K2 out of place between two KV buffers every round."""
+    _run_rounds(cuda, SMALL, 8, 10, pattern, kv_mode="pingpong")
+    _run_rounds(cuda, SMALL16, 3, 14, pattern, seed=4, max_new=33, kv_mode="pingpong")
+    _run_rounds(cuda, SMALL, 1, 5, pattern, kv_mode="pingpong")   # B=1 copies too
+
+
 def test_rounds_zero_pads(cuda):
     _run_rounds(cuda, SMALL, 8, 6, "alternating", zero_pads=True, seed=5)
 
 
 # ----------------------------------------------------------------------------- K2 alone
 def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, dtype="bf16", zero=False,
-                  seg=False):
+                  seg=False, bound=0):
     B = len(kept)
     cap = cap or int(max(np.max(pad_old), np.max(pad_new)) + np.max(kept) + 4)
     shp = (planes, B, H, cap, D)
@@ -166,7 +177,8 @@ def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, 
     _abi.specdec_realign_kv(kv, kv, t32(kept), n_planes=planes, n_rows=B, H=H, D=D,
                             src_strides=s[:3], dst_strides=s[:3], cap_src=cap, cap_dst=cap, ws=ws,
                             src_col=t32(pad_old), dst_col=t32(pad_new),
-                            flags=_abi.ZERO_PADS if zero else 0, moved_bytes=moved, status=st)
+                            flags=_abi.ZERO_PADS if zero else 0, moved_bytes=moved, status=st,
+                            count_bound=bound)
     torch.cuda.synchronize()
     g = torch_to_bits(kv)
     o, defined = OA.realign_kv(bits, pad_old, pad_new, kept)
@@ -222,9 +234,57 @@ def test_realign_zero_pads_and_skips(cuda):
     _realign_case(cuda, [0, 4, 2, 0], [3, 4, 0, 9], [50, 0, 70, 1000], zero=True)
 
 
-def test_realign_gather_scatter(cuda):
+@pytest.mark.parametrize("D,dtype", [(128, "bf16"), (8, "fp16"), (16, "fp32")])
+def test_realign_small_slabs_in_place(cuda, D, dtype):
+    """count_bound * row bytes <= 4 KB selects the register-staged warp-per-slab kernel:
+    in-place shifts of both signs wider and narrower than the slab, Delta = 0, empty rows,
+    ZERO_PADS, many rows (more slabs than one CTA's warps)."""
+    rb = D * (4 if dtype == "fp32" else 2)
+    bmax = 4096 // rb
+    cases = [
+        ([0] * 4, [5] * 4, [bmax, 6, 1, 0]),
+        ([9] * 4, [0] * 4, [bmax, bmax - 1, 3, 2]),
+        ([0, 7, 3, 0], [40, 7, 0, 1], [bmax, 5, 6, bmax]),
+    ]
+    for po, pn, kp in cases:
+        _realign_case(cuda, po, pn, kp, D=D, dtype=dtype, bound=bmax)
+        _realign_case(cuda, po, pn, kp, D=D, dtype=dtype, bound=bmax, zero=True)
+    rng = np.random.default_rng(5)
+    B = 40
+    po, pn = rng.integers(0, 30, B), rng.integers(0, 30, B)
+    _realign_case(cuda, po, pn, rng.integers(0, 7, B), D=D, dtype=dtype, H=5, planes=3, bound=6)
+
+
+def test_realign_count_bound_violation(cuda):
+    """A row above count_bound is skipped and reported (SPECDEC_ST_BOUND), small and ring
+    kernels alike; the other rows move."""
+    for bound in (4, 64):       # 4 * 256 B -> small kernel; 64 * 256 B -> TMA ring kernel
+        planes, B, H, cap, D = 2, 3, 2, 200, 128
+        shp = (planes, B, H, cap, D)
+        bits = W.gen_kv_bits_np(9, int(np.prod(shp))).reshape(shp)
+        kv = bits_to_torch(bits, "bf16", cuda)
+        t32 = lambda x: torch.as_tensor(np.asarray(x, np.int32), device=cuda)
+        st = torch.zeros(1, dtype=torch.int32, device=cuda)
+        kept = [bound, bound + 1, 2]
+        s = kv.stride()
+        _abi.specdec_realign_kv(kv, kv, t32(kept), n_planes=planes, n_rows=B, H=H, D=D,
+                                src_strides=s[:3], dst_strides=s[:3], cap_src=cap, cap_dst=cap,
+                                src_col=t32([0, 0, 0]), dst_col=t32([3, 3, 3]), status=st,
+                                count_bound=bound)
+        torch.cuda.synchronize()
+        assert int(st.item()) == _abi.ST_BOUND
+        g = torch_to_bits(kv)
+        assert np.array_equal(g[:, 1], bits[:, 1])          # skipped
+        o, _ = OA.realign_kv(bits, np.zeros(B, np.int32), np.full(B, 3, np.int32), np.array(kept))
+        for i in (0, 2):
+            assert np.array_equal(g[:, i, :, 3:3 + kept[i]], o[:, i, :, 3:3 + kept[i]])
+
+
+@pytest.mark.parametrize("bound", [0, 6])
+def test_realign_gather_scatter(cuda, bound):
     """Pool mode (a5): gather from a sequence-major pool into a plane-major staging
-    rectangle at right-aligned columns, then scatter a tail back (distinct buffers)."""
+    rectangle at right-aligned columns, then scatter a tail back (distinct buffers);
+    bound = 6 = k + 1 sends the scatter through the small-slab kernel, as the pool does."""
     N, planes, H, cap, D = 6, 4, 2, 90, 64
     B, cap_b = 3, 100
     pool_bits = W.gen_kv_bits_np(11, N * planes * H * cap * D).reshape(N, planes, H, cap, D)
@@ -255,7 +315,7 @@ def test_realign_gather_scatter(cuda):
     _abi.specdec_realign_kv(stage, pool, t32(acc), count_add=1, n_planes=planes, n_rows=B, H=H, D=D,
                             src_strides=ss[:3], dst_strides=(ps[1], ps[0], ps[2]), cap_src=cap_b,
                             cap_dst=cap, src_col_add=Lb - 1, dst_col=t32(lens), dst_col_add=-1,
-                            dst_row_map=t32(members))
+                            dst_row_map=t32(members), count_bound=bound)
     torch.cuda.synchronize()
     pg = torch_to_bits(pool)
     for i, s in enumerate(members):

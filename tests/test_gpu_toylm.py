@@ -33,7 +33,7 @@ def _prompts(n, seed):
 
 
 def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, drafter=None,
-                draft_log=None, anchor_slack=0):
+                draft_log=None, anchor_slack=0, kv_mode="inplace"):
     """EqSpec with the toy LM on the host and K1/K3/K2 in libspecdec.so.  `fault` injects
     one of the paper's §2 failure classes at a module seam.  With a
     `drafter`, the draft model keeps its own KV cache on the GPU, realigned by K2 with
@@ -41,7 +41,8 @@ def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, dr
     B = len(prompts)
     tokens, pad, L = build_batch(prompts, cap)
     bt = EqSpecBatch(B, k, cap, LAYERS, H, D, "bf16", cuda, max_new=max_new, eos_id=eos,
-                     draft=None if drafter is None else (LAYERS, H, D), anchor_slack=anchor_slack)
+                     draft=None if drafter is None else (LAYERS, H, D), anchor_slack=anchor_slack,
+                     kv_mode=kv_mode)
     bt.load(tokens, [len(p) for p in prompts])
     if fault == "skip_kv_realign":             # DSD error (iii): KV not realigned
         bt.realign = lambda stream=None: None
@@ -120,6 +121,22 @@ def test_eqspec_on_gpu_equals_greedy(cuda, B, noise, eos, k):
     assert out == ref and status == 0
 
 
+@pytest.mark.parametrize("B,noise,draft", [(3, 0.3, False), (4, 0.45, True), (1, 0.2, False)])
+def test_pingpong_kv_on_gpu_equals_greedy(cuda, B, noise, draft):
+    """kv_mode="pingpong": each round's realign writes the other KV buffer, which the next
+    forward reads; output == greedy (with the draft cache ping-ponged too)."""
+    T = ToyLM(V, LAYERS, H, D, seed=7)
+    Dm = ToyLM(V, LAYERS, H, D, seed=8) if draft else None
+    prompts = _prompts(B, seed=300 + B)
+    ref = [T.greedy_generate(p, 18, 1, 64) for p in prompts]
+    log = []
+    out, rounds, status = _eqspec_gpu(cuda, T, prompts, 4, 18, 1, noise, drafter=Dm,
+                                      draft_log=log if draft else None, kv_mode="pingpong")
+    assert out == ref and status == 0
+    if draft:
+        assert len(log) >= rounds and all(c == r for c, r in log)
+
+
 @pytest.mark.parametrize("B,noise", [(3, 0.3), (4, 0.0), (2, 0.5)])
 def test_draft_kv_realign_on_gpu(cuda, B, noise):
     """f1: the drafter's own KV cache, realigned on the GPU with kept_draft = n + min(a, k-1),
@@ -147,10 +164,12 @@ def test_fault_modes_break_equivalence(cuda, fault):
     assert bad != ref
 
 
-@pytest.mark.parametrize("N,Wn,B,mg,alg3", [(10, 6, 3, 2, False), (8, 8, 4, 4, False), (7, 7, 1, 2, False),
-                                             (9, 6, 3, 2, True)])
-def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3):
-    """EXSpec on the GPU path; alg3=True runs Alg. 3 as printed (batch 0, then re-plan)."""
+@pytest.mark.parametrize("N,Wn,B,mg,alg3,dense", [(10, 6, 3, 2, False, False), (8, 8, 4, 4, False, False),
+                                                   (7, 7, 1, 2, False, False), (9, 6, 3, 2, True, False),
+                                                   (10, 6, 3, 2, False, True)])
+def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3, dense):
+    """EXSpec on the GPU path; alg3=True runs Alg. 3 as printed (batch 0, then re-plan);
+    dense=True gathers / scatters same-length batches too (a dense-rectangle consumer)."""
     T = ToyLM(V, LAYERS, H, D, seed=7)
     k, max_new = 3, 12
     prompts = _prompts(N, seed=N + B)
@@ -166,7 +185,7 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3):
         for c, t in enumerate(p[:-1]):                    # prefill all but the pending token
             T.token_forward(t, c, c, kv[s], ones)
     sp = SequencePool(N, cap, LAYERS, H, D, k, W=Wn, B=B, min_group=mg, max_new=max_new, eos_id=1,
-                      device=cuda)
+                      device=cuda, dense_consumer=dense)
     sp.load(lens, tokens, order, _to_dev(kv, cuda))
     kinds_seen = set()
     for _ in range(400):
@@ -176,7 +195,7 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3):
         for b in range(1 if alg3 else nb):
             mem = sp.members[b].cpu().numpy()
             Lb = int(blens[b])
-            fallback = not kinds[b]
+            fallback = not kinds[b] or dense
             kinds_seen.add(int(kinds[b]))
             if fallback:
                 sp.gather(b)
