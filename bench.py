@@ -59,6 +59,8 @@ def parse():
                     help="epoch: run every batch of the window plan; alg3: batch 0 then re-plan")
     ap.add_argument("--B", type=int, default=0, help="override batch size")
     ap.add_argument("--pattern", default="alpha", choices=list(W.ACCEPT_PATTERNS))
+    ap.add_argument("--alpha", type=float, default=0.7, help="acceptance rate of --pattern fixed")
+    ap.add_argument("--ctx", type=int, default=0, help="override the context: n ~ U[ctx-512, ctx]")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -172,6 +174,8 @@ def shape_for(args):
     sh = W.SHAPES[args.config]
     if args.B:
         sh = sh.with_(B=args.B)
+    if args.ctx:   # SURVEY §8d ctx sweep: n ~ U[ctx - 512, ctx]
+        sh = sh.with_(ctx=args.ctx, len_lo=max(1, args.ctx - 512), len_hi=args.ctx)
     return sh
 
 
@@ -185,7 +189,8 @@ def workload_name(sh, args):
     d += ", anchored origin (f3)" if getattr(args, "anchor", False) else ""
     d += ", ping-pong KV (out of place)" if getattr(args, "kv_mode", "inplace") == "pingpong" else ""
     return (f"{sh.name} EqSpec round: B={sh.B} k={sh.k} V={sh.V} KV {sh.layers}x{sh.H}x{sh.D} "
-            f"{sh.kv_dtype}, n~U[{sh.len_lo},{sh.len_hi}], accept={args.pattern}{d}")
+            f"{sh.kv_dtype}, n~U[{sh.len_lo},{sh.len_hi}], accept={args.pattern}"
+            f"{f' alpha={args.alpha}' if args.pattern == 'fixed' else ''}{d}")
 
 
 class RoundBench:
@@ -215,7 +220,7 @@ class RoundBench:
         self.bt.kv.copy_(W.gen_kv_torch(args.seed, self.bt.kv.shape, self.bt.kv.dtype, device))
         self.logits = [W.gen_logits_torch(args.seed, r, B, k, sh.V, sh.logit_dtype, device)
                        for r in range(RING)]
-        self.truth = [W.gen_round_truth(args.seed, r, B, k, sh.V, args.pattern) for r in range(RING)]
+        self.truth = [W.gen_round_truth(args.seed, r, B, k, sh.V, args.pattern, alpha=args.alpha) for r in range(RING)]
         self.drafts = [torch.from_numpy(t.draft).to(device) for t in self.truth]
         self.stream = torch.cuda.current_stream(device)
 
@@ -467,7 +472,7 @@ def oracle_round_sample(sh, args, plane_sample=2, rounds=2, seed=0):
     tv = tr = tk = 0.0
     for r in range(rounds):
         bits = W.gen_logits_np(seed, r, B, k, sh.V, sh.logit_dtype)
-        rt = W.gen_round_truth(seed, r, B, k, sh.V, args.pattern)
+        rt = W.gen_round_truth(seed, r, B, k, sh.V, args.pattern, alpha=args.alpha)
         a = time.perf_counter()
         v = OV.batch_verify(bits, sh.logit_dtype, rt.draft, n, pad, act)
         b = time.perf_counter()
@@ -525,7 +530,7 @@ def run_pool(args, rank, world, device):
     local_lens = lens[mine]
     local_order = np.arange(n_loc)            # `mine` is already in admission order
     ring_lg = [W.gen_logits_torch(args.seed, r, sp.B, k, V, sh.logit_dtype, device) for r in range(RING)]
-    ring_dr = [torch.from_numpy(W.gen_round_truth(args.seed, r, sp.B, k, V, args.pattern).draft).to(device)
+    ring_dr = [torch.from_numpy(W.gen_round_truth(args.seed, r, sp.B, k, V, args.pattern, alpha=args.alpha).draft).to(device)
                for r in range(RING)]
     ctr = {"i": 0}
 

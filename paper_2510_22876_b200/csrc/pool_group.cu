@@ -3,10 +3,12 @@
 //
 // One CTA of 1024 threads plans the whole window on device:
 //   1. RefillWindow: stable compaction of d_order by d_active (block scan), first W ids;
-//   2. per member: group count and rank among equal lengths (the length histogram,
-//      computed by all-pairs comparison of the <= 2048 window lengths held in smem);
-//   3. groups ordered by (-count, length); each group yields same-length batches of
-//      min(B, remaining) while remaining >= min_group; group offsets by an ordered sum;
+//   2. the length histogram: a block-wide bitonic sort of the (length, window position)
+//      keys puts every group contiguous and in window order, so a member's group is a
+//      scan over segment heads and its rank its offset in the segment;
+//   3. groups ordered by (-count, length) -- a second bitonic sort over the group keys;
+//      each group yields same-length batches of min(B, remaining) while remaining >=
+//      min_group; group offsets by an exclusive scan in that order;
 //   4. leftovers keep window order (block scan) and fill fallback batches of B.
 // Every step is a deterministic function of the inputs, so the plan is bit-identical to
 // the oracle's (tests/test_gpu_pool.py).
@@ -47,20 +49,45 @@ __device__ int block_exclusive_scan(int v, int *s_warp, int &total) {
 }
 
 struct PoolSmem {
+    unsigned long long key[kPoolMaxW];  // sort buffer (member keys, then group keys)
     int wid[kPoolMaxW];     // window member ids
     int wlen[kPoolMaxW];    // their lengths
-    int cnt[kPoolMaxW];     // group size of the member's length
-    int rank[kPoolMaxW];    // rank within its group (window order)
-    int lead[kPoolMaxW];    // window index of the group's first member
-    int gbase[kPoolMaxW];   // (leaders) first batch index of the group
-    int nsb[kPoolMaxW];     // (leaders) number of same-length batches
-    int matched[kPoolMaxW]; // (leaders) members placed in same-length batches
+    int grp[kPoolMaxW];     // member -> group (groups numbered by ascending length)
+    int rank[kPoolMaxW];    // member -> rank within its group (window order); later: flat slot
+    int gstart[kPoolMaxW + 1];  // group -> first position in the sorted member order
+    int nsb[kPoolMaxW];     // group -> number of same-length batches
+    int matched[kPoolMaxW]; // group -> members placed in same-length batches
+    int gbase[kPoolMaxW];   // group -> first batch index
     int bmax[kPoolMaxW];    // per batch: max length
     int bmin[kPoolMaxW];    // per batch: min length
     int bcnt[kPoolMaxW];    // per batch: member count
     int warp[32];
-    int scalars[8];
 };
+
+// Ascending bitonic sort of key[0, n) (n a power of two <= 2 * blockDim.x, padded with ~0).
+// Keys are unique, so the result is unique whatever the thread schedule.  Thread p owns
+// compare-exchange pair p; for j <= 32 the pairs of warp w all lie in key[64w, 64w + 64),
+// so those substeps need only a warp barrier -- a block barrier is paid only before a
+// substep with j >= 64 (15 of the 66 substeps at n = 2048, none for n <= 64).
+__device__ void block_bitonic_sort(unsigned long long *key, int n) {
+    const int p = threadIdx.x;
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (p < (n >> 1)) {
+                const int i = 2 * j * (p / j) + (p % j), l = i + j;
+                const unsigned long long a = key[i], b = key[l];
+                const bool up = (i & k) == 0;
+                if ((a > b) == up) {
+                    key[i] = b;
+                    key[l] = a;
+                }
+            }
+            const int jn = j > 1 ? j >> 1 : k;  // the next substep's j (k: next stage's first)
+            if (jn >= 64 && (j > 1 || k < n)) __syncthreads(); else __syncwarp();
+        }
+    }
+    __syncthreads();
+}
 
 __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     const int32_t *len, const uint8_t *active, const int32_t *order, int32_t N, int32_t W,
@@ -97,63 +124,82 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     }
     const int Wn = min(filled, W);
     __syncthreads();
-    // ---- 2. group counts / ranks / leaders (length histogram over the window)
-    for (int w = tid; w < Wn; w += T) {
-        const int l = sm.wlen[w];
-        int c = 0, r = 0, first = w;
-        for (int u = 0; u < Wn; ++u) {
-            if (sm.wlen[u] == l) {
-                ++c;
-                if (u < w) ++r;
-                first = min(first, u);
-            }
-        }
-        sm.cnt[w] = c;
-        sm.rank[w] = r;
-        sm.lead[w] = first;
-    }
+    // ---- 2. length histogram: sort (length, window position), groups = equal-length runs
+    int n2 = 1;
+    while (n2 < Wn) n2 <<= 1;
+    for (int i = tid; i < n2; i += T)
+        sm.key[i] = i < Wn ? (static_cast<unsigned long long>(static_cast<uint32_t>(sm.wlen[i])) << 32) |
+                                 static_cast<uint32_t>(i)
+                           : ~0ull;
     __syncthreads();
-    // ---- 3. same-length batches per group (leaders), groups ordered by (-count, length)
+    block_bitonic_sort(sm.key, n2);
+    int n_groups = 0;
+    for (int base = 0; base < Wn; base += T) {  // group id = number of run heads before
+        const int i = base + tid;
+        int head = 0;
+        if (i < Wn) head = (i == 0 || (sm.key[i] >> 32) != (sm.key[i - 1] >> 32)) ? 1 : 0;
+        int tot;
+        const int g = n_groups + block_exclusive_scan(head, sm.warp, tot);
+        if (head) sm.gstart[g] = i;
+        n_groups += tot;
+    }
+    if (tid == 0) sm.gstart[n_groups] = Wn;
+    __syncthreads();
+    // member -> (group, rank): binary search of its sorted position among the group starts
+    for (int i = tid; i < Wn; i += T) {
+        int lo = 0, hi = n_groups - 1;  // last g with gstart[g] <= i
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sm.gstart[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        const int w = static_cast<int>(sm.key[i] & 0xFFFFFFFFull);
+        sm.grp[w] = lo;
+        sm.rank[w] = i - sm.gstart[lo];
+    }
+    // ---- 3. same-length batches per group; groups ordered by (-count, length)
     const int mg = B == 1 ? 1 : min_group;
-    for (int w = tid; w < Wn; w += T) {
-        if (sm.rank[w] != 0) continue;
-        const int c = sm.cnt[w];
+    for (int g = tid; g < n_groups; g += T) {
+        const int c = sm.gstart[g + 1] - sm.gstart[g];
         int nb = 0, m = 0;
         if (c >= mg) {
             const int full = c / B, rem = c % B;
             nb = full + (rem >= mg ? 1 : 0);
             m = full * B + (rem >= mg ? rem : 0);
         }
-        sm.nsb[w] = nb;
-        sm.matched[w] = m;
+        sm.nsb[g] = nb;
+        sm.matched[g] = m;
     }
     __syncthreads();
-    int local_same = 0, local_groups = 0;
-    for (int w = tid; w < Wn; w += T) {
-        if (sm.rank[w] != 0) continue;
-        ++local_groups;
-        local_same += sm.nsb[w];
-        const int c = sm.cnt[w], l = sm.wlen[w];
-        int base = 0;
-        for (int u = 0; u < Wn; ++u) {
-            if (sm.rank[u] != 0) continue;
-            const int cu = sm.cnt[u], lu = sm.wlen[u];
-            if (cu > c || (cu == c && lu < l)) base += sm.nsb[u];
-        }
-        sm.gbase[w] = base;
+    int g2 = 1;
+    while (g2 < n_groups) g2 <<= 1;
+    for (int g = tid; g < g2; g += T)   // key: (-count, length) ascending; group id in the low bits
+        sm.key[g] = g < n_groups
+            ? (static_cast<unsigned long long>(kPoolMaxW - (sm.gstart[g + 1] - sm.gstart[g])) << 32) |
+                  static_cast<unsigned long long>(g)  // ids ascend with the length: (-count, length)
+            : ~0ull;
+    __syncthreads();
+    block_bitonic_sort(sm.key, g2);
+    int run = 0;
+    for (int base = 0; base < n_groups; base += T) {  // gbase: exclusive scan of nsb in that order
+        const int q = base + tid;
+        const int g = q < n_groups ? static_cast<int>(sm.key[q] & 0xFFFFFFFFull) : 0;
+        const int v = q < n_groups ? sm.nsb[g] : 0;
+        int tot;
+        const int before = run + block_exclusive_scan(v, sm.warp, tot);
+        if (q < n_groups) sm.gbase[g] = before;
+        run += tot;
     }
-    int tot_same, n_groups;
-    block_exclusive_scan(local_same, sm.warp, tot_same);
-    block_exclusive_scan(local_groups, sm.warp, n_groups);
+    const int tot_same = run;
+    __syncthreads();
     // ---- 4. place members: same-length slots, then leftovers in window order
     int n_left = 0;
     for (int base = 0; base < Wn; base += T) {
         const int w = base + tid;
         int unmatched = 0, bi = -1, sl = -1;
         if (w < Wn) {
-            const int ld = sm.lead[w], r = sm.rank[w];
-            if (r < sm.matched[ld]) {
-                bi = sm.gbase[ld] + r / B;
+            const int g = sm.grp[w], r = sm.rank[w];
+            if (r < sm.matched[g]) {
+                bi = sm.gbase[g] + r / B;
                 sl = r % B;
             } else {
                 unmatched = 1;

@@ -1,0 +1,74 @@
+"""SURVEY §8d bench matrix: runs bench.py over the cells and prints one summary line per
+cell (plus the raw JSON lines to --jsonl).
+
+    python tools/bench_matrix.py [--quick] [--jsonl out.jsonl]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+ROUND = ["--no-cpu-baseline", "--no-e2e"]
+CELLS = (
+    # (label, args)
+    [(f"Q{B} {m}", ["--B", str(B), "--kv-mode", m]) for B in (1, 2, 4, 8) for m in ("inplace", "pingpong")]
+    + [(f"Q8 ctx{c}", ["--ctx", str(c)]) for c in (512, 1024, 2048, 4096)]
+    + [(f"Q8 alpha{a}", ["--pattern", "fixed", "--alpha", str(a)]) for a in (0.3, 0.5, 0.8)]
+    + [(f"Q8 {p}", ["--pattern", p]) for p in ("all_k", "all_0", "alternating", "one_zero")]
+    + [("Q8 anchored", ["--anchor"]), ("Q8 draft-kv", ["--draft-kv"])]
+    + [(f"V8 {m}", ["--config", "vicuna", "--kv-mode", m]) for m in ("inplace", "pingpong")]
+    + [(f"G8 {m}", ["--config", "glm4", "--kv-mode", m]) for m in ("inplace", "pingpong")]
+    + [("T toy", ["--config", "toy"])]
+)
+POOL = (
+    [(f"P N{n} {ln}", ["--config", "pool", "--pool-n", str(n), "--pool-lengths", ln])
+     for n in (64, 256, 1024) for ln in ("random", "uniform")]
+    + [(f"P N1024 W{w}", ["--config", "pool", "--pool-W", str(w)]) for w in (8, 16, 32)]
+    + [("P N1024 min_group 8", ["--config", "pool", "--min-group", "8"]),
+       ("P N1024 alg3", ["--config", "pool", "--pool-mode", "alg3"]),
+       ("P N1024 dense consumer", ["--config", "pool", "--pool-consumer", "dense"])]
+)
+
+
+def summary(label, d):
+    if "pool" in d:
+        p = d["pool"]
+        return (f"{label:26s} {d['value']:10.1f} seq/s  grouping {p['grouping_rate']:.3f}  "
+                f"batches {p['batch_verifications']:6d}  mean_batch {p['mean_batch']:.2f}  "
+                f"KV {p['kv_bytes_moved_rank0'] / 1e9:8.1f} GB  K2 {d['roofline']['achieved']:7.1f} GB/s")
+    r = d["roofline"]
+    k = d["kernels_ms_per_step"]
+    return (f"{label:26s} {d['value']:10.1f} rounds/s  {d['ms_per_step'] * 1e3:8.1f} us  "
+            f"K2 {r['achieved']:7.1f} GB/s (frac {r['frac']:.3f}, copied {r.get('copied_GBps', 0):7.1f})  "
+            f"K1 {k['verify_K1'] * 1e3:5.1f} K3 {k['repad_K3'] * 1e3:5.1f} K2 {k['realign_K2'] * 1e3:7.1f} us")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true", help="round cells only")
+    ap.add_argument("--jsonl", default="")
+    a = ap.parse_args()
+    cells = [(lbl, ROUND + args) for lbl, args in CELLS]
+    if not a.quick:
+        cells += [(lbl, ["--no-cpu-baseline"] + args) for lbl, args in POOL]
+    out = open(a.jsonl, "w") if a.jsonl else None
+    for lbl, args in cells:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, capture_output=True,
+                           text=True, timeout=900)
+        lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+        if r.returncode or not lines:
+            print(f"{lbl:26s} FAILED rc={r.returncode} {r.stderr.strip().splitlines()[-1:]}", flush=True)
+            continue
+        d = json.loads(lines[-1])
+        if out:
+            out.write(json.dumps({"cell": lbl, **d}) + "\n")
+        print(summary(lbl, d), flush=True)
+
+
+if __name__ == "__main__":
+    main()
