@@ -581,8 +581,7 @@ def run_pool(args, rank, world, device):
                     e[0].record()
                     sp.gather(b)
                     e[1].record()
-                    sp.verify(b, lg, d, V)
-                    sp.writeback(b, d)
+                    sp.verify_writeback(b, lg, d, V)
                     e[2].record()
                     sp.scatter(b, blens[b])
                     e[3].record()
@@ -651,11 +650,14 @@ def run_pool(args, rank, world, device):
                  "kv_bytes_moved_rank0": moved, "gather_ms": gather_ms},
         "roofline": {"bound": "hbm", "kernel": "specdec_realign_kv gather+scatter (fallback batches)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src},
+                     "frac": achieved / peak, "traffic": None,
+                     # launches differ in size (one per fallback batch): no single per-launch
+                     # figure; the note gives the ncu traffic of one representative gather
+                     "traffic_note": ncu_traffic("pool_gather")[1], "peak_source": peak_src},
         "clocks": clocks.summary(), "status": status,
         # libspecdec launches in the timed drain: K4 per plan (the epochs + the final empty
-        # plan), K1 + write-back per batch, gather + scatter per fallback batch
-        "gpu_launches": (epochs + 1) + 2 * int(cnt[0])
+        # plan), K1 with the fused write-back per batch, gather + scatter per fallback batch
+        "gpu_launches": (epochs + 1) + (1 if sp.fused else 2) * int(cnt[0])
         + 2 * (int(cnt[0]) if sp.dense_consumer else int(cnt[0]) - int(cnt[1])),
         "e2e": None, "cpu_baseline": None,
     }

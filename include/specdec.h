@@ -258,6 +258,26 @@ int specdec_pool_writeback(const int32_t *d_members, int64_t B, int64_t k,
                            int64_t *d_pool_tokens, int64_t cap_tok, int64_t *d_out_buf,
                            int64_t max_new, uint32_t *d_status, specdec_stream_t stream);
 
+/* ------------------------------------------------------------------------------ a1 + a5
+ * specdec_pool_verify -- one EXSpec batch's Alg. 1 BatchVerify with
+ * the Alg. 3 Phase 4 write-back fused into its epilogue: exactly
+ * specdec_verify(n = d_mlen, active = d_mactive, budget = NULL, no plan outputs) followed
+ * by specdec_pool_writeback(d_members, ...), in one launch (the pool's per-batch path is
+ * latency-bound: one launch and one dependent kernel fewer per batch).
+ * Arguments as in those two calls; d_mlen / d_mactive / d_members are one batch's rows of
+ * specdec_pool_group's outputs.  Errors: as specdec_verify (logits / shape / workspace)
+ * and specdec_pool_writeback (pool pointers, cap_tok, max_new); SPECDEC_ST_CAPACITY if a
+ * pool token row would overflow (that row's write-back is skipped).
+ */
+int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, int64_t k, int64_t V,
+                        int64_t row_stride, const int64_t *d_draft, const int32_t *d_members,
+                        const int32_t *d_mlen, uint8_t *d_mactive, int64_t eos_id,
+                        int64_t pad_id, int32_t *d_accept, int64_t *d_bonus, int32_t *d_emit,
+                        uint8_t *d_finished, int32_t *d_pool_len, int32_t *d_pool_gen,
+                        uint8_t *d_pool_active, int64_t *d_pool_tokens, int64_t cap_tok,
+                        int64_t *d_out_buf, int64_t max_new, uint32_t *d_status, void *d_ws,
+                        size_t ws_bytes, specdec_stream_t stream);
+
 /* ------------------------------------------------------------------------------ a4 + a5
  * specdec_pool_epoch -- native EXSpec epoch executor (Alg. 3): the
  * host-side launch loop of one epoch in C++ instead of one Python call per kernel.

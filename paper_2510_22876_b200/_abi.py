@@ -45,6 +45,8 @@ _SIGS = {
     "specdec_pool_writeback": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
                                 _I64, _P, _P], _INT),
     "specdec_pool_epoch": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P], _INT),
+    "specdec_pool_verify": ([_P, _INT, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _P,
+                             _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P], _INT),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -182,6 +184,20 @@ def specdec_realign_kv(kv_src, kv_dst, count, *, n_planes, n_rows, H, D, src_str
         dst_col_add, _ptr(count), count_add, count_bound, _ptr(src_row_map), _ptr(dst_row_map), flags,
         _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
         _ptr(moved_bytes), _ptr(status), _stream(stream)), "specdec_realign_kv")
+
+
+def specdec_pool_verify(logits, draft, members, mlen, mactive, accept, bonus, emit, finished,
+                        pool_len, pool_gen, pool_active, ws, *, V=None, eos_id=-1, pad_id=0,
+                        max_new, pool_tokens=None, out_buf=None, status=None, stream=None):
+    """K1 + the pool write-back in one launch (include/specdec.h)."""
+    B, K1, _ = logits.shape
+    _check(load().specdec_pool_verify(
+        _ptr(logits), DTYPE[logits.dtype], B, K1 - 1, V or logits.shape[2], logits.stride(1),
+        _ptr(draft), _ptr(members), _ptr(mlen), _ptr(mactive), eos_id, pad_id, _ptr(accept),
+        _ptr(bonus), _ptr(emit), _ptr(finished), _ptr(pool_len), _ptr(pool_gen),
+        _ptr(pool_active), _ptr(pool_tokens), 0 if pool_tokens is None else pool_tokens.shape[1],
+        _ptr(out_buf), max_new, _ptr(status), _ptr(ws), ws.numel() * ws.element_size(),
+        _stream(stream)), "specdec_pool_verify")
 
 
 def specdec_pool_group(length, active, order, W, B, min_group, window, window_size, batch_of,

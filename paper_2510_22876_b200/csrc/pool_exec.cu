@@ -5,8 +5,8 @@
 // host synchronisation), then for every planned batch (or only batch 0: Alg. 3 as printed):
 //   fallback batches:  specdec_realign_kv gather (pool -> right-aligned staging)
 //   forward callback   (the model's verify forward; may be NULL for synthetic inputs)
-//   specdec_verify     (logits / drafts from the callback or from the input ring)
-//   specdec_pool_writeback
+//   specdec_pool_verify (Alg. 1 + the Phase 4 write-back in one launch; logits / drafts
+//                       from the callback or from the input ring)
 //   fallback batches:  specdec_realign_kv scatter (the a+1 new KV rows back to the pool)
 // Every launch goes through the same C ABI entry points the Python driver uses.
 #include <cuda_runtime.h>
@@ -73,15 +73,11 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
             logits = d->logits_ring[j];
             draft = d->draft_ring[j];
         }
-        rc = specdec_verify(logits, d->logit_dtype, B, d->k, d->V, d->logit_stride, draft, mlen, mact,
-                            d->eos_id, d->pad_id, nullptr, d->accept, d->bonus, d->emit,
-                            d->finished, nullptr, d->plan_L, d->n_new, d->pad_new, d->kept,
-                            nullptr, nullptr, 0, nullptr, nullptr, d->status, d->ws, d->ws_bytes,
-                            stream);
-        if (rc) return rc;
-        rc = specdec_pool_writeback(members, B, d->k, draft, d->accept, d->bonus, d->emit,
-                                    d->finished, d->len, d->gen, d->active, d->tokens, d->cap_tok,
-                                    d->out_buf, d->max_new, d->status, stream);
+        // K1 with the Phase 4 write-back fused into its epilogue
+        rc = specdec_pool_verify(logits, d->logit_dtype, B, d->k, d->V, d->logit_stride, draft, members,
+                                 mlen, mact, d->eos_id, d->pad_id, d->accept, d->bonus, d->emit,
+                                 d->finished, d->len, d->gen, d->active, d->tokens, d->cap_tok,
+                                 d->out_buf, d->max_new, d->status, d->ws, d->ws_bytes, stream);
         if (rc) return rc;
         if (fallback) {
             rc = specdec_realign_kv(d->staging, d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D,

@@ -43,6 +43,11 @@ struct VerifyParams {
     int32_t *anchor;          // f3: physical origin (in/out), NULL = off
     int64_t anchor_cap;
     int32_t *phys_old, *phys_new;
+    // pool mode (specdec_pool_verify): Alg. 3 Phase 4 write-back fused into the epilogue
+    const int32_t *wb_members;  // [B] pool sequence of each row (-1 = empty), NULL = off
+    int32_t *wb_len, *wb_gen;
+    uint8_t *wb_active;
+    int64_t *wb_tokens, wb_cap_tok, *wb_out_buf, wb_max_new;
     int exp;                  // SPECDEC_K1_EXP timing experiments (0 = normal)
     uint32_t *status;
     unsigned long long *ws_keys;  // [B*(k+1)]
@@ -86,13 +91,14 @@ __device__ void verify_epilogue(const VerifyParams &p) {
         bool fin = true;
         const int64_t pr = (act && lane < K1) ? static_cast<int64_t>(unpack_idx(key)) : -1;
         if (p.pred && lane < K1) p.pred[i * K1 + lane] = pr;
+        int64_t tok = -1;
         if (act) {
             // first mismatch; R1: all k match -> a = k
             const unsigned mism = __ballot_sync(0xFFFFFFFFu, lane < k && pr != d);
             a = mism ? __ffs(mism) - 1 : k;
             b = __shfl_sync(0xFFFFFFFFu, pr, a);  // bonus = pred at the first mismatch (R2)
             // E = D[:a] ++ [b]: lane t < a holds D[t], lane a holds b; cut after the first EOS
-            const int64_t tok = lane < a ? d : b;
+            tok = lane < a ? d : b;
             m = a + 1;
             fin = false;
             if (p.eos_id >= 0) {
@@ -111,15 +117,39 @@ __device__ void verify_epilogue(const VerifyParams &p) {
             }
         }
         if (lane < K1) p.ws_keys[i * K1 + lane] = 0ull;  // self-clean
+        if (p.wb_members) {
+            // Alg. 3 Phase 4, as specdec_pool_writeback: E cut to the
+            // sequence's remaining budget, appended to its pool tokens / output, len and gen
+            // advanced, deactivated when finished
+            const int32_t sq = p.wb_members[i];
+            if (sq >= 0) {
+                const int32_t len = p.wb_len[sq], g = p.wb_gen[sq];
+                const int32_t em = min(m, static_cast<int32_t>(max(static_cast<int64_t>(0), p.wb_max_new - g)));
+                const bool fin2 = fin || g + em >= p.wb_max_new;
+                if (p.wb_tokens && len + em > p.wb_cap_tok) {
+                    if (lane == 0 && p.status) atomicOr(p.status, SPECDEC_ST_CAPACITY);
+                } else {
+                    if (lane < em) {
+                        if (p.wb_tokens) p.wb_tokens[static_cast<int64_t>(sq) * p.wb_cap_tok + len + lane] = tok;
+                        if (p.wb_out_buf) p.wb_out_buf[static_cast<int64_t>(sq) * p.wb_max_new + g + lane] = tok;
+                    }
+                    if (lane == 0) {
+                        p.wb_len[sq] = len + em;
+                        p.wb_gen[sq] = g + em;
+                        if (fin2) p.wb_active[sq] = 0;
+                    }
+                }
+            }
+        }
         if (lane == 0) {
             p.accept[i] = a;
             p.bonus[i] = b;
             p.emit[i] = m;
             p.finished[i] = fin ? 1 : 0;
             p.active[i] = fin ? 0 : 1;  // in/out: rows still active after this round
-            p.n_new[i] = nn;
+            if (p.n_new) p.n_new[i] = nn;
             if (i < kEpiCache) s_nn[i] = nn;
-            p.kept[i] = kp;
+            if (p.kept) p.kept[i] = kp;
             // f1: a draft model that cached its own k forwards (pending token, d_1..d_{k-1})
             // keeps n + min(a, k-1) entries: d_k never had a draft KV entry
             if (p.kept_draft) p.kept_draft[i] = kp ? n_i + min(a, k - 1) : 0;
@@ -170,7 +200,7 @@ __device__ void verify_epilogue(const VerifyParams &p) {
         *p.anchor = static_cast<int32_t>(base + best);
     }
     if (p.anchor) __syncthreads();
-    for (int64_t i = threadIdx.x; i < p.B; i += blockDim.x) {
+    for (int64_t i = threadIdx.x; i < p.B && p.pad_new; i += blockDim.x) {
         const int32_t pn = Lnew > 0 ? Lnew - (i < kEpiCache ? s_nn[i] : p.n_new[i]) : 0;
         p.pad_new[i] = pn;
         if (p.anchor) {
@@ -179,7 +209,7 @@ __device__ void verify_epilogue(const VerifyParams &p) {
         }
     }
     if (threadIdx.x == 0) {
-        *p.plan_L = Lnew;
+        if (p.plan_L) *p.plan_L = Lnew;
         *p.ws_counter = 0u;  // self-clean
     }
 }
@@ -359,38 +389,11 @@ extern "C" size_t specdec_verify_workspace_size(int64_t B, int64_t k) {
     return static_cast<size_t>(B * (k + 1)) * sizeof(unsigned long long) + 16;
 }
 
-extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_t k, int64_t V,
-                              int64_t row_stride, const int64_t *d_draft, const int32_t *d_n,
-                              uint8_t *d_active, int64_t eos_id, int64_t pad_id,
-                              int32_t *d_budget, int32_t *d_accept, int64_t *d_bonus,
-                              int32_t *d_emit, uint8_t *d_finished, int64_t *d_pred,
-                              int32_t *d_plan_L, int32_t *d_n_new, int32_t *d_pad_new,
-                              int32_t *d_kept, int32_t *d_kept_draft, int32_t *d_anchor,
-                              int64_t anchor_cap, int32_t *d_phys_old, int32_t *d_phys_new,
-                              uint32_t *d_status, void *d_ws, size_t ws_bytes,
-                              specdec_stream_t stream) {
-    const int es = dtype_size(dtype);
-    if (d_anchor && (!d_phys_old || !d_phys_new || anchor_cap < k + 2)) return SPECDEC_ERR_ARG;
-    if (es == 0) return SPECDEC_ERR_DTYPE;
-    if (k < 1 || k > kMaxK) return SPECDEC_ERR_ARG;
-    if (B < 1 || V < 1 || row_stride < V || V > 0x7FFFFFFFll) return SPECDEC_ERR_SHAPE;
-    if (B * (k + 1) > 65535) return SPECDEC_ERR_SHAPE;  // gridDim.y
-    if (!d_logits || !d_draft || !d_n || !d_active || !d_accept || !d_bonus || !d_emit ||
-        !d_finished || !d_plan_L || !d_n_new || !d_pad_new || !d_kept || !d_ws)
-        return SPECDEC_ERR_ARG;
-    if (!aligned16(d_logits) || (row_stride * es) % 16 != 0 || (reinterpret_cast<uintptr_t>(d_ws) & 7u))
-        return SPECDEC_ERR_ARG;
-    if (ws_bytes < specdec_verify_workspace_size(B, k)) return SPECDEC_ERR_ARG;
+namespace specdec {
 
-    VerifyParams p;
-    p.logits = d_logits;
-    p.B = B; p.k = k; p.V = V; p.row_stride = row_stride;
-    p.draft = d_draft; p.n = d_n; p.active = d_active;
-    p.eos_id = eos_id; p.pad_id = pad_id; p.budget = d_budget;
-    p.accept = d_accept; p.bonus = d_bonus; p.emit = d_emit; p.finished = d_finished;
-    p.pred = d_pred; p.plan_L = d_plan_L; p.n_new = d_n_new; p.pad_new = d_pad_new; p.kept = d_kept;
-    p.kept_draft = d_kept_draft;
-    p.anchor = d_anchor; p.anchor_cap = anchor_cap; p.phys_old = d_phys_old; p.phys_new = d_phys_new;
+// Common host path of specdec_verify / specdec_pool_verify: shape checks done by the
+// callers, p filled except the launch geometry.
+static int launch_verify(VerifyParams &p, int dtype, int es, specdec_stream_t stream) {
     static int exp = -1, cta_mult = 4, vpt = 0;
     if (exp < 0) {
         const char *e = getenv("SPECDEC_K1_EXP");
@@ -401,10 +404,7 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
         if (v && atoi(v) > 0) vpt = std::min(atoi(v), kVPT);
     }
     p.exp = exp;
-    p.status = d_status;
-    p.ws_keys = static_cast<unsigned long long *>(d_ws);
-    p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
-
+    const int64_t B = p.B, k = p.k, V = p.V;
     const int VE = 16 / es;
     const int64_t rows = B * (k + 1);
     const int64_t quantum = static_cast<int64_t>(kVerifyThreads) * VE;
@@ -437,4 +437,83 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
         case SPECDEC_F16: return launch_k(verify_kernel16<false>, grid, dim3(kVerifyThreads), 0, s, p);
         default: return launch_k(verify_kernel16<true>, grid, dim3(kVerifyThreads), 0, s, p);
     }
+}
+
+// shape / pointer checks shared by both entry points
+static int check_verify(const void *d_logits, int es, int64_t B, int64_t k, int64_t V,
+                        int64_t row_stride, void *d_ws, size_t ws_bytes) {
+    if (es == 0) return SPECDEC_ERR_DTYPE;
+    if (k < 1 || k > kMaxK) return SPECDEC_ERR_ARG;
+    if (B < 1 || V < 1 || row_stride < V || V > 0x7FFFFFFFll) return SPECDEC_ERR_SHAPE;
+    if (B * (k + 1) > 65535) return SPECDEC_ERR_SHAPE;  // gridDim.y
+    if (!d_logits || !d_ws) return SPECDEC_ERR_ARG;
+    if (!aligned16(d_logits) || (row_stride * es) % 16 != 0 || (reinterpret_cast<uintptr_t>(d_ws) & 7u))
+        return SPECDEC_ERR_ARG;
+    if (ws_bytes < specdec_verify_workspace_size(B, k)) return SPECDEC_ERR_ARG;
+    return SPECDEC_OK;
+}
+
+}  // namespace specdec
+
+extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_t k, int64_t V,
+                              int64_t row_stride, const int64_t *d_draft, const int32_t *d_n,
+                              uint8_t *d_active, int64_t eos_id, int64_t pad_id,
+                              int32_t *d_budget, int32_t *d_accept, int64_t *d_bonus,
+                              int32_t *d_emit, uint8_t *d_finished, int64_t *d_pred,
+                              int32_t *d_plan_L, int32_t *d_n_new, int32_t *d_pad_new,
+                              int32_t *d_kept, int32_t *d_kept_draft, int32_t *d_anchor,
+                              int64_t anchor_cap, int32_t *d_phys_old, int32_t *d_phys_new,
+                              uint32_t *d_status, void *d_ws, size_t ws_bytes,
+                              specdec_stream_t stream) {
+    const int es = dtype_size(dtype);
+    if (d_anchor && (!d_phys_old || !d_phys_new || anchor_cap < k + 2)) return SPECDEC_ERR_ARG;
+    const int rc = check_verify(d_logits, es, B, k, V, row_stride, d_ws, ws_bytes);
+    if (rc) return rc;
+    if (!d_draft || !d_n || !d_active || !d_accept || !d_bonus || !d_emit || !d_finished ||
+        !d_plan_L || !d_n_new || !d_pad_new || !d_kept)
+        return SPECDEC_ERR_ARG;
+    VerifyParams p{};
+    p.logits = d_logits;
+    p.B = B; p.k = k; p.V = V; p.row_stride = row_stride;
+    p.draft = d_draft; p.n = d_n; p.active = d_active;
+    p.eos_id = eos_id; p.pad_id = pad_id; p.budget = d_budget;
+    p.accept = d_accept; p.bonus = d_bonus; p.emit = d_emit; p.finished = d_finished;
+    p.pred = d_pred; p.plan_L = d_plan_L; p.n_new = d_n_new; p.pad_new = d_pad_new; p.kept = d_kept;
+    p.kept_draft = d_kept_draft;
+    p.anchor = d_anchor; p.anchor_cap = anchor_cap; p.phys_old = d_phys_old; p.phys_new = d_phys_new;
+    p.status = d_status;
+    p.ws_keys = static_cast<unsigned long long *>(d_ws);
+    p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
+    return launch_verify(p, dtype, es, stream);
+}
+
+extern "C" int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, int64_t k,
+                                   int64_t V, int64_t row_stride, const int64_t *d_draft,
+                                   const int32_t *d_members, const int32_t *d_mlen,
+                                   uint8_t *d_mactive, int64_t eos_id, int64_t pad_id,
+                                   int32_t *d_accept, int64_t *d_bonus, int32_t *d_emit,
+                                   uint8_t *d_finished, int32_t *d_pool_len, int32_t *d_pool_gen,
+                                   uint8_t *d_pool_active, int64_t *d_pool_tokens, int64_t cap_tok,
+                                   int64_t *d_out_buf, int64_t max_new, uint32_t *d_status,
+                                   void *d_ws, size_t ws_bytes, specdec_stream_t stream) {
+    const int es = dtype_size(dtype);
+    const int rc = check_verify(d_logits, es, B, k, V, row_stride, d_ws, ws_bytes);
+    if (rc) return rc;
+    if (!d_draft || !d_members || !d_mlen || !d_mactive || !d_accept || !d_bonus || !d_emit ||
+        !d_finished || !d_pool_len || !d_pool_gen || !d_pool_active)
+        return SPECDEC_ERR_ARG;
+    if (d_pool_tokens && cap_tok < 1) return SPECDEC_ERR_SHAPE;
+    if (max_new < 1) return SPECDEC_ERR_SHAPE;
+    VerifyParams p{};
+    p.logits = d_logits;
+    p.B = B; p.k = k; p.V = V; p.row_stride = row_stride;
+    p.draft = d_draft; p.n = d_mlen; p.active = d_mactive;
+    p.eos_id = eos_id; p.pad_id = pad_id;
+    p.accept = d_accept; p.bonus = d_bonus; p.emit = d_emit; p.finished = d_finished;
+    p.wb_members = d_members; p.wb_len = d_pool_len; p.wb_gen = d_pool_gen; p.wb_active = d_pool_active;
+    p.wb_tokens = d_pool_tokens; p.wb_cap_tok = cap_tok; p.wb_out_buf = d_out_buf; p.wb_max_new = max_new;
+    p.status = d_status;
+    p.ws_keys = static_cast<unsigned long long *>(d_ws);
+    p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
+    return launch_verify(p, dtype, es, stream);
 }

@@ -41,6 +41,8 @@ class SequencePool:
         self.device = dev
         # gather / scatter same-length batches too (a dense-rectangle consumer)
         self.dense_consumer = bool(dense_consumer)
+        # verify + write-back in one launch (specdec_pool_verify); False: the two calls
+        self.fused = True
         self.cap_tok = cap_tok or cap
         # pool state
         self.len = torch.zeros(N, dtype=i32, device=dev)
@@ -80,7 +82,9 @@ class SequencePool:
         self.status = torch.zeros(1, dtype=i32, device=dev)
         self.moved = torch.zeros(1, dtype=i64, device=dev)
         self.verify_calls = 0
-        self._pinned = torch.zeros(1 + 3 * W, dtype=i32).pin_memory()
+        self._pinned = torch.zeros(1 + 3 * W, dtype=i32)   # plan header, host side
+        if dev.type == "cuda":
+            self._pinned = self._pinned.pin_memory()
 
     # ----------------------------------------------------------------- state
     def load(self, prompts_lens, tokens=None, order=None, kv=None):
@@ -162,14 +166,27 @@ class SequencePool:
                                     max_new=self.max_new, pool_tokens=self.tokens,
                                     out_buf=self.out_buf, status=self.status, stream=stream)
 
+    def verify_writeback(self, b, logits, draft, V=None, stream=None):
+        """Alg. 1 on batch b and the Phase 4 write-back: one fused launch, or the two calls."""
+        if not self.fused:
+            self.verify(b, logits, draft, V, stream)
+            self.writeback(b, draft, stream)
+            return
+        _abi.specdec_pool_verify(logits, draft, self.members[b], self.mlen[b], self.mactive[b],
+                                 self.accept, self.bonus, self.emit, self.finished, self.len,
+                                 self.gen, self.active, self.ws, V=V or logits.shape[2],
+                                 eos_id=self.eos_id, pad_id=self.pad_id, max_new=self.max_new,
+                                 pool_tokens=self.tokens, out_buf=self.out_buf,
+                                 status=self.status, stream=stream)
+        self.verify_calls += 1
+
     def run_batch(self, b, kind, blen, logits, draft, forward=None, V=None, stream=None):
         fallback = not kind or self.dense_consumer
         if fallback:
             self.gather(b, stream)
         if forward is not None:
             forward(self, b, not fallback, int(blen))
-        self.verify(b, logits, draft, V, stream)
-        self.writeback(b, draft, stream)
+        self.verify_writeback(b, logits, draft, V, stream)
         if fallback:
             self.scatter(b, blen, stream)
 

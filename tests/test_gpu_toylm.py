@@ -187,6 +187,7 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3, dense):
     sp = SequencePool(N, cap, LAYERS, H, D, k, W=Wn, B=B, min_group=mg, max_new=max_new, eos_id=1,
                       device=cuda, dense_consumer=dense)
     sp.load(lens, tokens, order, _to_dev(kv, cuda))
+    sp.fused = not dense          # the dense case also covers the unfused verify + write-back
     kinds_seen = set()
     for _ in range(400):
         nb, kinds, blens, sizes = sp.plan()
@@ -225,8 +226,7 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3, dense):
                 sp.staging.copy_(_to_dev(src, cuda))
             else:
                 sp.kv.copy_(_to_dev(pool_kv, cuda))
-            sp.verify(b, torch.from_numpy(logits).to(cuda), torch.from_numpy(draft).to(cuda), V=V)
-            sp.writeback(b, torch.from_numpy(draft).to(cuda))
+            sp.verify_writeback(b, torch.from_numpy(logits).to(cuda), torch.from_numpy(draft).to(cuda), V=V)
             if fallback:
                 sp.scatter(b, Lb)
     gen = sp.gen.cpu().numpy()
