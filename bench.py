@@ -499,6 +499,78 @@ def cpu_info():
     return model
 
 
+def pool_workload(args):
+    """Prompt lengths (incl. the pending token) and admission order of the pool workload."""
+    N = args.pool_n
+    rng_h = W.hash_np(args.seed, W.S_POOL, np.arange(N))
+    if args.pool_lengths == "uniform":
+        lens = np.full(N, 256, np.int32)                      # All-Mean analog (PAPER.md:700)
+    else:
+        lens = (64 + (rng_h % np.uint64(512 - 64 + 1)).astype(np.int64)).astype(np.int32)
+    order = np.array(sorted(range(N), key=lambda s: (int(lens[s]), s)), np.int32)  # sort on
+    return lens, order
+
+
+def oracle_pool_sample(args, verify_samples=2):
+    """The CPU oracle on the pool workload, as a bounded sample: the oracle's own GetBatch
+    plan (oracle.pool.form_batches, timed in full) drives the whole drain with the planted
+    accept lengths; the per-batch Alg. 1 verify (oracle.verify.batch_verify over the full
+    B x (k+1) x V logits) and the KV gather / scatter copy rate (oracle.align.copy_rows on
+    2 of the 72 planes of one member) are timed on samples and extrapolated to the drain's
+    batch count and algorithmic KV bytes.  Returns (sequences/s, parts)."""
+    from oracle import align as OA
+    from oracle import pool as OP
+    from oracle import verify as OV
+    sh = W.SHAPES["qwen3"]
+    k, V, B = sh.k, sh.V, sh.B
+    lens, order = pool_workload(args)
+    N = len(lens)
+    Wn = min(args.pool_W or N, 2048, N)
+    o_len, gen, act = lens.astype(np.int64), np.zeros(N, np.int64), np.ones(N, np.uint8)
+    truth = [W.gen_round_truth(args.seed, r, B, k, V, args.pattern, alpha=args.alpha) for r in range(RING)]
+    t_plan = 0.0
+    n_batches = 0
+    kv_bytes = 0
+    dense = args.pool_consumer == "dense"
+    while act.any():
+        t0 = time.perf_counter()
+        plan = OP.form_batches(o_len, act, order, Wn, B, args.min_group)
+        t_plan += time.perf_counter() - t0
+        nb = 1 if args.pool_mode == "alg3" else len(plan["batches"])
+        for b in range(nb):
+            mem = plan["batches"][b]
+            acc = truth[n_batches % RING].accept
+            for j, s in enumerate(mem):
+                e = min(int(acc[j]) + 1, args.max_new - int(gen[s]))
+                if dense or not plan["kind"][b]:
+                    kv_bytes += 2 * (int(o_len[s]) - 1) * sh.bpt + 2 * (int(acc[j]) + 1) * sh.bpt
+                o_len[s] += e
+                gen[s] += e
+                if gen[s] >= args.max_new:
+                    act[s] = 0
+            n_batches += 1
+    # per-batch verify, timed on samples of the same logits
+    t_ver = []
+    for r in range(verify_samples):
+        bits = W.gen_logits_np(args.seed, r, B, k, V, sh.logit_dtype)
+        n = np.full(B, 300, np.int32)
+        t0 = time.perf_counter()
+        OV.batch_verify(bits, sh.logit_dtype, truth[r].draft, n, np.zeros(B, np.int32), np.ones(B, np.uint8))
+        t_ver.append(time.perf_counter() - t0)
+    # KV copy rate of the oracle's gather (2 planes of one 300-token member)
+    P, cap = 2, 320
+    src = W.gen_kv_bits_np(args.seed, 1 * P * sh.H * cap * sh.D).reshape(1, P, sh.H, cap, sh.D)
+    dst = np.zeros((1, P, sh.H, cap, sh.D), np.uint16)
+    t0 = time.perf_counter()
+    OA.copy_rows(src, dst, count=np.array([299]), src_row=np.array([0]), dst_col=np.array([1]))
+    t_cp = time.perf_counter() - t0
+    kv_rate = 2 * 299 * P * sh.H * sh.D * 2 / max(t_cp, 1e-9)   # bytes read + written per s
+    t_total = t_plan + n_batches * float(np.mean(t_ver)) + kv_bytes / kv_rate
+    parts = {"plan_s": t_plan, "verify_s_per_batch": float(np.mean(t_ver)), "batches": n_batches,
+             "kv_bytes": kv_bytes, "kv_copy_GBps": kv_rate / 1e9, "total_s": t_total}
+    return N / t_total, parts
+
+
 def run_pool(args, rank, world, device):
     """EXSpec pool (BASELINE.json configs[4]): N Qwen3-shaped sequences, band-sharded over
     the ranks; each rank drains its shard (K4 plan, per batch gather / verify / write-back
@@ -513,12 +585,7 @@ def run_pool(args, rank, world, device):
     sh = W.SHAPES["qwen3"]
     k, V, B = sh.k, sh.V, sh.B
     N = args.pool_n
-    rng_h = W.hash_np(args.seed, W.S_POOL, np.arange(N))
-    if args.pool_lengths == "uniform":
-        lens = np.full(N, 256, np.int32)                      # All-Mean analog
-    else:
-        lens = (64 + (rng_h % np.uint64(512 - 64 + 1)).astype(np.int64)).astype(np.int32)
-    order = np.array(sorted(range(N), key=lambda s: (int(lens[s]), s)), np.int32)  # sort on
+    lens, order = pool_workload(args)
     shards = (shard_bands if args.shard == "band" else shard_strided)(order, world)
     mine = shards[rank]
     n_loc = len(mine)
@@ -667,6 +734,22 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle as it stands, rank 0 only."""
     if rank != 0:
         return None
+    if args.config == "pool":
+        t0 = time.perf_counter()
+        sps, parts = oracle_pool_sample(args)
+        wall = time.perf_counter() - t0
+        sample = (f"the oracle's GetBatch plan over the whole {args.pool_n}-sequence drain "
+                  f"({parts['batches']} batches, timed in full); per-batch oracle verify timed on 2 "
+                  f"batches and KV copies on 2 of 72 planes of one member, extrapolated to the "
+                  f"drain's batches and {parts['kv_bytes'] / 1e9:.0f} GB; numpy single-threaded on {cpu_info()}")
+        return {"impl": "reference", "metric": "EXSpec pool sequences/s (Qwen3-8B shape, N=%d, B=8, k=5)"
+                % args.pool_n, "value": sps, "unit": "sequences/s", "n_gpus": world, "steps": 1,
+                "warmup": 0, "ms_per_step": parts["total_s"] * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": f"EXSpec pool drain: {args.pool_n} seqs, prompt {args.pool_lengths}"},
+                "cpu_baseline": {"value": sps, "unit": "sequences/s", "cores": 1, "kind": "oracle",
+                                 "sample": sample, "parts": parts, "wall_s": wall},
+                "e2e": {"value": sps, "unit": "sequences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     sh = shape_for(args)
     for _ in range(max(0, min(args.warmup, 1))):
         oracle_round_sample(sh, args, rounds=1)

@@ -67,8 +67,8 @@ struct PoolSmem {
 // Ascending bitonic sort of key[0, n) (n a power of two <= 2 * blockDim.x, padded with ~0).
 // Keys are unique, so the result is unique whatever the thread schedule.  Thread p owns
 // compare-exchange pair p; for j <= 32 the pairs of warp w all lie in key[64w, 64w + 64),
-// so those substeps need only a warp barrier -- a block barrier is paid only before a
-// substep with j >= 64 (15 of the 66 substeps at n = 2048, none for n <= 64).
+// so two consecutive such substeps need only a warp barrier -- a block barrier is paid
+// around every substep with j >= 64 (none for n <= 64).
 __device__ void block_bitonic_sort(unsigned long long *key, int n) {
     const int p = threadIdx.x;
     for (int k = 2; k <= n; k <<= 1) {
@@ -82,8 +82,10 @@ __device__ void block_bitonic_sort(unsigned long long *key, int n) {
                     key[l] = a;
                 }
             }
-            const int jn = j > 1 ? j >> 1 : k;  // the next substep's j (k: next stage's first)
-            if (jn >= 64 && (j > 1 || k < n)) __syncthreads(); else __syncwarp();
+            // a block barrier when this or the next substep crosses warps (j >= 64);
+            // jn = the next substep's j (k: the next stage's first)
+            const int jn = j > 1 ? j >> 1 : k;
+            if ((j >= 64 || jn >= 64) && (j > 1 || k < n)) __syncthreads(); else __syncwarp();
         }
     }
     __syncthreads();

@@ -4,7 +4,8 @@ graph, per-launch time from CUDA events.
     python tools/k1bench.py [--B 8] [--k 5] [--V 151936] [--n 50]
 
 SPECDEC_K1_EXP=1 times the argmax phase alone (no grid-wide arrival / epilogue), =2 an empty
-kernel on the same grid (the launch floor) -- results invalid, for splitting the latency.
+kernel on the same grid (the launch floor), =3 the loads and per-thread max only (no CTA
+reduction) -- results invalid, for splitting the latency.
 """
 from __future__ import annotations
 
