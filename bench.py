@@ -55,6 +55,9 @@ def parse():
                          "gathered into a dense staging rectangle too (PAPER.md:537)")
     ap.add_argument("--pool-exec", default="native", choices=["native", "python"],
                     help="pool: per-batch launch loop in C++ (specdec_pool_epoch) or Python")
+    ap.add_argument("--pool-staging", type=int, default=2,
+                    help="pool, native executor: staging buffers; >= 2 overlaps the fallback "
+                         "gathers (copy stream) with the same-length batches, 1 = serial")
     ap.add_argument("--pool-mode", default="epoch", choices=["epoch", "alg3"],
                     help="epoch: run every batch of the window plan; alg3: batch 0 then re-plan")
     ap.add_argument("--B", type=int, default=0, help="override batch size")
@@ -593,7 +596,8 @@ def run_pool(args, rank, world, device):
     Wn = min(args.pool_W or n_loc, 2048, n_loc)
     sp = SequencePool(n_loc, cap, sh.layers, sh.H, sh.D, k, W=Wn, B=min(B, Wn),
                       min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False,
-                      dense_consumer=args.pool_consumer == "dense")
+                      dense_consumer=args.pool_consumer == "dense",
+                      n_staging=args.pool_staging if args.pool_exec == "native" else 1)
     local_lens = lens[mine]
     local_order = np.arange(n_loc)            # `mine` is already in admission order
     ring_lg = [W.gen_logits_torch(args.seed, r, sp.B, k, V, sh.logit_dtype, device) for r in range(RING)]
@@ -707,7 +711,9 @@ def run_pool(args, rank, world, device):
                                f"{'U[64,512]' if args.pool_lengths == 'random' else '256'}, max_new "
                                f"{args.max_new}, W={Wn}/rank, B={sp.B}, min_group={args.min_group}, "
                                f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}, {args.pool_consumer} consumer, "
-                               f"{args.pool_exec} launch loop",
+                               f"{args.pool_exec} launch loop"
+                               + (f", fallback gathers overlapped ({sp.n_staging} staging buffers)"
+                                  if args.pool_exec == "native" and sp.n_staging >= 2 else ""),
                    "cap": cap, "pool_kv_GB_per_rank": sp.kv.numel() * 2 / 1e9,
                    "parallelism": f"pool sharded x{world}", "step": "one epoch (K4 plan + its batches)"},
         "pool": {"epochs": epochs, "batch_verifications": int(cnt_all[0]),

@@ -290,6 +290,11 @@ int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, int64_t k, i
  *       the descriptor's input ring;
  *     specdec_verify (no budget; the write-back applies max_new); specdec_pool_writeback;
  *     fallback batch: specdec_realign_kv scatter of the a+1 new KV rows.
+ *   With desc->n_staging >= 2 the fallback gathers are overlapped with the same-length
+ *   batches (see the descriptor's last fields); results are identical.
+ * Errors: SPECDEC_ERR_ARG for a NULL desc / header, W or B < 1, no input ring without a
+ * forward callback, or an incomplete overlap configuration (ring, stream or events
+ * missing); any error of the calls it makes is returned as is.
  * Host outputs (nullable): batches run, same-length batches run, their members, and
  * the members of the fallback batches run.  All device buffers are caller-owned
  * (paper_2510_22876_b200/exspec.py allocates them); host_header is pinned, 1 + 3W int32.
@@ -341,6 +346,25 @@ typedef struct specdec_pool_desc {
      * dense rectangle ("concatenate directly"); 0: same-length batches run
      * zero-copy on the pool slots (forward kind = 1) */
     int32_t dense_consumer;
+    /* Overlapped fallback gathers (n_staging >= 2; 0 or 1 = off, the serial loop above).
+     * The batches of one epoch have disjoint members and are planned from one window
+     * state, so the order they run in does not change any result (the input-ring slot of
+     * batch b stays ring_pos + b).  With overlap on, every fallback batch's gather runs on
+     * `copy_stream` into staging_ring[f % n_staging] (f = its rank among the epoch's
+     * fallback batches), and the fallback batches are spread evenly among the
+     * same-length ones on `stream`, so the bandwidth-bound gathers stream under the
+     * latency-bound same-length verifies.  Ordering: the verify of fallback batch f waits
+     * for its gather (events[f % n_staging]); the gather of f + n_staging waits for the
+     * scatter of f (events[n_staging + f % n_staging]).  `stream` waits on every gather,
+     * so the epoch is complete when `stream` is.  The caller owns the buffers and the
+     * 2 * n_staging events (cudaEvent_t, timing disabled).  staging_ring[0] may be
+     * `staging`.  If `cur_staging` is non-NULL the executor stores the staging buffer of
+     * a fallback batch there before calling forward() (NULL for same-length batches). */
+    int32_t n_staging;
+    void *const *staging_ring; /* host array of n_staging device pointers, layout of `staging` */
+    specdec_stream_t copy_stream;
+    void *const *events;       /* host array of 2 * n_staging cudaEvent_t */
+    void **cur_staging;        /* host, nullable */
 } specdec_pool_desc;
 
 int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,

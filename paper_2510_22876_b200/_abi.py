@@ -70,6 +70,8 @@ class PoolDesc(ctypes.Structure):
         ("logit_dtype", _INT),
         ("logits_ring", _P), ("draft_ring", _P), ("ring_n", _I32), ("ring_pos", _P),
         ("dense_consumer", _I32),
+        ("n_staging", _I32), ("staging_ring", _P), ("copy_stream", _P), ("events", _P),
+        ("cur_staging", _P),
     ]
 
 

@@ -11,6 +11,8 @@
 // Every launch goes through the same C ABI entry points the Python driver uses.
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "host_util.h"
 #include "specdec.h"
 
@@ -23,6 +25,11 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     if (!d || !d->host_header || d->W < 1 || d->B < 1) return SPECDEC_ERR_ARG;
     if (!forward && (!d->logits_ring || !d->draft_ring || d->ring_n < 1 || !d->ring_pos))
         return SPECDEC_ERR_ARG;
+    if (d->n_staging >= 2 && (!d->staging_ring || !d->copy_stream || !d->events))
+        return SPECDEC_ERR_ARG;
+    if (d->n_staging >= 2)
+        for (int32_t i = 0; i < d->n_staging; ++i)
+            if (!d->staging_ring[i] || !d->events[i] || !d->events[d->n_staging + i]) return SPECDEC_ERR_ARG;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int32_t W = d->W, B = d->B;
     int rc = specdec_pool_group(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
@@ -49,27 +56,74 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     const int64_t p_plane = hcd, p_row = d->n_planes * hcd, p_head = d->cap * d->D;
     const int64_t s_plane = B * hcd, s_row = hcd, s_head = d->cap * d->D;
     (void)es;
+    // Processing order.  Serial: plan order.  Overlapped (n_staging >= 2): the fallback
+    // batches are spread evenly among the same-length ones, so that while the copy stream
+    // gathers fallback f the main stream keeps verifying same-length batches.
+    const int32_t NS = d->n_staging >= 2 ? d->n_staging : 0;
+    const bool overlap = NS > 0 && run > 1;
+    std::vector<int32_t> seq, fb_rank(run, -1);
+    std::vector<int32_t> fbs;
+    seq.reserve(run);
+    for (int32_t b = 0; b < run; ++b)
+        if (kinds[b] == 0 || d->dense_consumer) fb_rank[b] = static_cast<int32_t>(fbs.size()), fbs.push_back(b);
+    if (!overlap) {
+        for (int32_t b = 0; b < run; ++b) seq.push_back(b);
+    } else {
+        const int64_t nf = static_cast<int64_t>(fbs.size()), ns = run - nf;
+        int64_t f = 0;
+        for (int32_t b = 0, si = 0; b < run; ++b) {
+            if (fb_rank[b] >= 0) continue;
+            // fallback f goes after floor((f + 1) * ns / (nf + 1)) same-length batches
+            while (f < nf && (f + 1) * ns / (nf + 1) <= si) seq.push_back(fbs[f++]);
+            seq.push_back(b);
+            ++si;
+        }
+        while (f < nf) seq.push_back(fbs[f++]);
+    }
+    cudaStream_t cs = overlap ? reinterpret_cast<cudaStream_t>(d->copy_stream) : nullptr;
+    auto ev = [&](int i) { return reinterpret_cast<cudaEvent_t>(d->events[i]); };
+    auto stg = [&](int32_t b) -> void * {
+        return overlap ? d->staging_ring[fb_rank[b] % NS] : d->staging;
+    };
+    auto gather = [&](int32_t b, cudaStream_t on) {
+        const int64_t o = static_cast<int64_t>(b) * B;
+        return specdec_realign_kv(d->kv, stg(b), d->kv_dtype, d->n_planes, B, d->H, d->D, p_plane,
+                                  p_row, p_head, d->cap, s_plane, s_row, s_head, d->cap, nullptr, 0,
+                                  d->mpad + o, 0, d->mlen + o, -1, 0, d->members + o, nullptr, 0,
+                                  nullptr, 0, d->moved, d->status,
+                                  reinterpret_cast<specdec_stream_t>(on));
+    };
+    // the first NS gathers: the plan is complete (host sync above) and so is every
+    // scatter of the previous epoch, so nothing to wait for
+    if (overlap) {
+        for (int32_t f = 0; f < NS && f < static_cast<int32_t>(fbs.size()); ++f) {
+            if ((rc = gather(fbs[f], cs))) return rc;
+            if ((e = cudaEventRecord(ev(f % NS), cs)) != cudaSuccess) return record_cuda_error(e);
+        }
+    }
+    const int32_t ring_base = d->ring_pos ? *d->ring_pos : 0;
     int32_t ran = 0, same = 0, msame = 0, mfb = 0;
-    for (int32_t b = 0; b < run; ++b) {
+    for (const int32_t b : seq) {
         const bool same_len = kinds[b] != 0;
-        const bool fallback = !same_len || d->dense_consumer;  // moves KV through the staging
+        const bool fallback = fb_rank[b] >= 0;  // moves KV through the staging
         int32_t *members = d->members + static_cast<int64_t>(b) * B;
         int32_t *mlen = d->mlen + static_cast<int64_t>(b) * B;
-        int32_t *mpad = d->mpad + static_cast<int64_t>(b) * B;
         uint8_t *mact = d->mactive + static_cast<int64_t>(b) * B;
         if (fallback) {
-            rc = specdec_realign_kv(d->kv, d->staging, d->kv_dtype, d->n_planes, B, d->H, d->D,
-                                    p_plane, p_row, p_head, d->cap, s_plane, s_row, s_head, d->cap,
-                                    nullptr, 0, mpad, 0, mlen, -1, 0, members, nullptr, 0, nullptr, 0,
-                                    d->moved, d->status, stream);
-            if (rc) return rc;
+            if (overlap) {
+                e = cudaStreamWaitEvent(s, ev(fb_rank[b] % NS), 0);
+                if (e != cudaSuccess) return record_cuda_error(e);
+            } else if ((rc = gather(b, s))) {
+                return rc;
+            }
         }
         const void *logits;
         const int64_t *draft;
         if (forward) {
+            if (d->cur_staging) *d->cur_staging = fallback ? stg(b) : nullptr;
             forward(ctx, b, fallback ? 0 : 1, blens[b], &logits, &draft);
         } else {
-            const int32_t j = (*d->ring_pos)++ % d->ring_n;
+            const int32_t j = (ring_base + b) % d->ring_n;  // the plan index picks the slot
             logits = d->logits_ring[j];
             draft = d->draft_ring[j];
         }
@@ -80,12 +134,20 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
                                  d->out_buf, d->max_new, d->status, d->ws, d->ws_bytes, stream);
         if (rc) return rc;
         if (fallback) {
-            rc = specdec_realign_kv(d->staging, d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D,
+            rc = specdec_realign_kv(stg(b), d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D,
                                     s_plane, s_row, s_head, d->cap, p_plane, p_row, p_head, d->cap,
                                     nullptr, blens[b] - 1, mlen, -1, d->accept, 1,
                                     static_cast<int32_t>(d->k + 1),  // a + 1 <= k + 1 rows
                                     nullptr, members, 0, nullptr, 0, d->moved, d->status, stream);
             if (rc) return rc;
+            const int32_t nxt = fb_rank[b] + NS;  // the gather that reuses this staging buffer
+            if (overlap && nxt < static_cast<int32_t>(fbs.size())) {
+                if ((e = cudaEventRecord(ev(NS + fb_rank[b] % NS), s)) != cudaSuccess ||
+                    (e = cudaStreamWaitEvent(cs, ev(NS + fb_rank[b] % NS), 0)) != cudaSuccess)
+                    return record_cuda_error(e);
+                if ((rc = gather(fbs[nxt], cs))) return rc;
+                if ((e = cudaEventRecord(ev(nxt % NS), cs)) != cudaSuccess) return record_cuda_error(e);
+            }
         }
         if (same_len) {
             ++same;
@@ -95,6 +157,7 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         }
         ++ran;
     }
+    if (!forward && d->ring_pos) *d->ring_pos = ring_base + run;
     if (h_ran) *h_ran = ran;
     if (h_same) *h_same = same;
     if (h_members_same) *h_members_same = msame;

@@ -29,7 +29,7 @@ from .eqspec import TORCH_DT
 class SequencePool:
     def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
                  max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True,
-                 dense_consumer=False):
+                 dense_consumer=False, n_staging=1):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         if B > W:
@@ -54,6 +54,11 @@ class SequencePool:
         alloc = torch.zeros if kv_init else torch.empty
         self.kv = alloc((N, self.n_planes, H, cap, D), dtype=TORCH_DT[kv_dtype], device=dev)
         self.staging = alloc((self.n_planes, B, H, cap, D), dtype=TORCH_DT[kv_dtype], device=dev)
+        # native executor only: n_staging >= 2 overlaps the fallback gathers (copy stream,
+        # ring of staging buffers) with the same-length batches (specdec_pool_desc)
+        self.n_staging = int(n_staging)
+        self.staging_ring = [self.staging] + [alloc(self.staging.shape, dtype=self.staging.dtype, device=dev)
+                                              for _ in range(max(self.n_staging, 1) - 1)]
         # plan (K4 outputs)
         self.window = torch.zeros(W, dtype=i32, device=dev)
         self.window_size = torch.zeros(1, dtype=i32, device=dev)
@@ -242,6 +247,18 @@ class SequencePool:
         d.ring_n = len(ring)
         d.ring_pos = ctypes.addressof(self._ring_pos)
         d.dense_consumer = 1 if self.dense_consumer else 0
+        if self.n_staging >= 2:
+            ns = self.n_staging
+            self._copy_stream = torch.cuda.Stream(self.device)
+            self._events = [torch.cuda.Event(enable_timing=False) for _ in range(2 * ns)]
+            for e in self._events:
+                e.record(torch.cuda.current_stream(self.device))   # materialise the handle
+            self._stg_ptrs = (ctypes.c_void_p * ns)(*[t.data_ptr() for t in self.staging_ring])
+            self._ev_ptrs = (ctypes.c_void_p * (2 * ns))(*[e.cuda_event for e in self._events])
+            d.n_staging = ns
+            d.staging_ring = ctypes.cast(self._stg_ptrs, ctypes.c_void_p)
+            d.copy_stream = self._copy_stream.cuda_stream
+            d.events = ctypes.cast(self._ev_ptrs, ctypes.c_void_p)
         self._desc = d
         return d
 

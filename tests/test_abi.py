@@ -100,15 +100,16 @@ def test_pool_desc_layout_matches_header(tmp_path):
     if not shutil.which("g++"):
         pytest.skip("no host C++ compiler")
     src = tmp_path / "l.cpp"
+    P = _abi.PoolDesc
+    names = [f[0] for f in P._fields_]
+    body = "".join(f' printf("%zu\\n", offsetof(specdec_pool_desc, {n}));' for n in names)
     src.write_text('#include <cstdio>\n#include <cstddef>\n#include "specdec.h"\n'
-                   'int main(){printf("%zu %zu %zu %zu\\n", sizeof(specdec_pool_desc),'
-                   ' offsetof(specdec_pool_desc, k), offsetof(specdec_pool_desc, logits_ring),'
-                   ' offsetof(specdec_pool_desc, ring_pos));}\n')
+                   'int main(){printf("%zu\\n", sizeof(specdec_pool_desc));' + body + '}\n')
     exe = tmp_path / "l"
     subprocess.run(["g++", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))
-    P = _abi.PoolDesc
-    assert got == [ctypes.sizeof(P), P.k.offset, P.logits_ring.offset, P.ring_pos.offset]
+    # every field, in order, at the C compiler's offset
+    assert got == [ctypes.sizeof(P)] + [getattr(P, n).offset for n in names]
 
 
 def test_header_is_plain_c_and_links(tmp_path, lib):
