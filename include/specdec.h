@@ -351,10 +351,11 @@ typedef struct specdec_pool_desc {
      * state, so the order they run in does not change any result (the input-ring slot of
      * batch b stays ring_pos + b).  With overlap on, every fallback batch's gather runs on
      * `copy_stream` into staging_ring[f % n_staging] (f = its rank among the epoch's
-     * fallback batches), and the fallback batches are spread evenly among the
-     * same-length ones on `stream`, so the bandwidth-bound gathers stream under the
-     * latency-bound same-length verifies.  Ordering: the verify of fallback batch f waits
-     * for its gather (events[f % n_staging]); the gather of f + n_staging waits for the
+     * fallback batches), and the fallback batches are interleaved with the same-length
+     * ones on `stream` by a list schedule on the estimates below (a fallback batch runs
+     * as soon as its gather is expected to be complete), so the bandwidth-bound gathers
+     * stream under the latency-bound same-length verifies.  Ordering: the verify of
+     * fallback batch f waits for its gather (events[f % n_staging]); the gather of f + n_staging waits for the
      * scatter of f (events[n_staging + f % n_staging]).  `stream` waits on every gather,
      * so the epoch is complete when `stream` is.  The caller owns the buffers and the
      * 2 * n_staging events (cudaEvent_t, timing disabled).  staging_ring[0] may be
@@ -365,6 +366,9 @@ typedef struct specdec_pool_desc {
     specdec_stream_t copy_stream;
     void *const *events;       /* host array of 2 * n_staging cudaEvent_t */
     void **cur_staging;        /* host, nullable */
+    /* scheduling hints for the overlapped order (<= 0: 5500 GB/s, 10 us): the gather rate
+     * and the duration of one batch verify; they change the order, never a result */
+    double est_gather_GBps, est_verify_us;
 } specdec_pool_desc;
 
 int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,

@@ -71,7 +71,7 @@ class PoolDesc(ctypes.Structure):
         ("logits_ring", _P), ("draft_ring", _P), ("ring_n", _I32), ("ring_pos", _P),
         ("dense_consumer", _I32),
         ("n_staging", _I32), ("staging_ring", _P), ("copy_stream", _P), ("events", _P),
-        ("cur_staging", _P),
+        ("cur_staging", _P), ("est_gather_GBps", ctypes.c_double), ("est_verify_us", ctypes.c_double),
     ]
 
 

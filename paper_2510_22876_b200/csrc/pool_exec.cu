@@ -11,6 +11,7 @@
 // Every launch goes through the same C ABI entry points the Python driver uses.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "host_util.h"
@@ -57,7 +58,7 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     const int64_t s_plane = B * hcd, s_row = hcd, s_head = d->cap * d->D;
     (void)es;
     // Processing order.  Serial: plan order.  Overlapped (n_staging >= 2): the fallback
-    // batches are spread evenly among the same-length ones, so that while the copy stream
+    // batches are interleaved with the same-length ones, so that while the copy stream
     // gathers fallback f the main stream keeps verifying same-length batches.
     const int32_t NS = d->n_staging >= 2 ? d->n_staging : 0;
     const bool overlap = NS > 0 && run > 1;
@@ -69,25 +70,49 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     if (!overlap) {
         for (int32_t b = 0; b < run; ++b) seq.push_back(b);
     } else {
-        const int64_t nf = static_cast<int64_t>(fbs.size()), ns = run - nf;
-        int64_t f = 0;
-        for (int32_t b = 0, si = 0; b < run; ++b) {
-            if (fb_rank[b] >= 0) continue;
-            // fallback f goes after floor((f + 1) * ns / (nf + 1)) same-length batches
-            while (f < nf && (f + 1) * ns / (nf + 1) <= si) seq.push_back(fbs[f++]);
-            seq.push_back(b);
-            ++si;
+        // List schedule on estimated durations: a fallback batch goes next as soon as its
+        // gather is expected to be done, else the next same-length batch; gathers run back
+        // to back, the one into staging slot f % NS after the scatter of f - NS.  Only the
+        // order (i.e. the timing) depends on the estimates, never a result.
+        const double gbps = d->est_gather_GBps > 0 ? d->est_gather_GBps : 5500.0;
+        const double tv = d->est_verify_us > 0 ? d->est_verify_us : 10.0;  // K1 (+ scatter)
+        const double row_bytes = static_cast<double>(d->n_planes) * d->H * d->D * dtype_size(d->kv_dtype);
+        auto gather_us = [&](int32_t b) {  // read + write of <= size * (width - 1) rows
+            return 2.0 * sizes[b] * std::max(blens[b] - 1, 0) * row_bytes / (gbps * 1e3);
+        };
+        std::vector<int32_t> sames;
+        for (int32_t b = 0; b < run; ++b)
+            if (fb_rank[b] < 0) sames.push_back(b);
+        const size_t nf = fbs.size(), ns = sames.size();
+        std::vector<double> g_end(nf, 0.0), s_end(nf, 0.0);
+        for (size_t f = 0; f < nf && f < static_cast<size_t>(NS); ++f)
+            g_end[f] = (f ? g_end[f - 1] : 0.0) + gather_us(fbs[f]);
+        double t = 0.0;
+        size_t fi = 0, si = 0;
+        while (fi < nf || si < ns) {
+            if (fi < nf && (g_end[fi] <= t || si == ns)) {
+                t = std::max(t, g_end[fi]) + 2.0 * tv;  // verify + scatter
+                s_end[fi] = t;
+                const size_t nx = fi + NS;
+                if (nx < nf) g_end[nx] = std::max(g_end[nx - 1], s_end[fi]) + gather_us(fbs[nx]);
+                seq.push_back(fbs[fi++]);
+            } else {
+                t += tv;
+                seq.push_back(sames[si++]);
+            }
         }
-        while (f < nf) seq.push_back(fbs[f++]);
     }
     cudaStream_t cs = overlap ? reinterpret_cast<cudaStream_t>(d->copy_stream) : nullptr;
     auto ev = [&](int i) { return reinterpret_cast<cudaEvent_t>(d->events[i]); };
     auto stg = [&](int32_t b) -> void * {
         return overlap ? d->staging_ring[fb_rank[b] % NS] : d->staging;
     };
+    // a batch's members fill its first sizes[b] slots (the rest are -1): every launch of
+    // the batch covers those rows only
+    auto rows = [&](int32_t b) -> int32_t { return sizes[b] > 0 && sizes[b] < B ? sizes[b] : B; };
     auto gather = [&](int32_t b, cudaStream_t on) {
         const int64_t o = static_cast<int64_t>(b) * B;
-        return specdec_realign_kv(d->kv, stg(b), d->kv_dtype, d->n_planes, B, d->H, d->D, p_plane,
+        return specdec_realign_kv(d->kv, stg(b), d->kv_dtype, d->n_planes, rows(b), d->H, d->D, p_plane,
                                   p_row, p_head, d->cap, s_plane, s_row, s_head, d->cap, nullptr, 0,
                                   d->mpad + o, 0, d->mlen + o, -1, 0, d->members + o, nullptr, 0,
                                   nullptr, 0, d->moved, d->status,
@@ -128,13 +153,13 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
             draft = d->draft_ring[j];
         }
         // K1 with the Phase 4 write-back fused into its epilogue
-        rc = specdec_pool_verify(logits, d->logit_dtype, B, d->k, d->V, d->logit_stride, draft, members,
+        rc = specdec_pool_verify(logits, d->logit_dtype, rows(b), d->k, d->V, d->logit_stride, draft, members,
                                  mlen, mact, d->eos_id, d->pad_id, d->accept, d->bonus, d->emit,
                                  d->finished, d->len, d->gen, d->active, d->tokens, d->cap_tok,
                                  d->out_buf, d->max_new, d->status, d->ws, d->ws_bytes, stream);
         if (rc) return rc;
         if (fallback) {
-            rc = specdec_realign_kv(stg(b), d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D,
+            rc = specdec_realign_kv(stg(b), d->kv, d->kv_dtype, d->n_planes, rows(b), d->H, d->D,
                                     s_plane, s_row, s_head, d->cap, p_plane, p_row, p_head, d->cap,
                                     nullptr, blens[b] - 1, mlen, -1, d->accept, 1,
                                     static_cast<int32_t>(d->k + 1),  // a + 1 <= k + 1 rows

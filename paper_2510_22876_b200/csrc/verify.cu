@@ -298,6 +298,13 @@ struct H16 {
             return *reinterpret_cast<uint32_t *>(&r);
         }
     }
+    // 0xFFFF in each half where a == b (native packed compare, set.eq.u32.{bf16x2,f16x2})
+    __device__ static uint32_t eq2(uint32_t a, uint32_t b) {
+        if constexpr (BF16)
+            return __heq2_mask(*reinterpret_cast<__nv_bfloat162 *>(&a), *reinterpret_cast<__nv_bfloat162 *>(&b));
+        else
+            return __heq2_mask(*reinterpret_cast<__half2 *>(&a), *reinterpret_cast<__half2 *>(&b));
+    }
     static constexpr uint32_t kExp = BF16 ? 0x7F80u : 0x7C00u;
     static constexpr uint32_t kNegInf2 = BF16 ? 0xFF80FF80u : 0xFC00FC00u;
 };
@@ -356,27 +363,52 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p
 #pragma unroll
         for (int q = 1; q < kVerifyThreads / kWarp; ++q) m = T::max2(m | (m << 16), s_m[q] | (s_m[q] << 16)) & 0xFFFFu;
         const uint32_t kM = key16(m, T::kExp);
+        if (p.exp == 4) {  // timing experiment only: stream + CTA maximum, no pass 2 / merge
+            if (kM == 0xFFFFFFFFu && p.status) atomicOr(p.status, 0x80000000u);
+            return;
+        }
         uint32_t first = 0xFFFFFFFFu;
         if (key16(my_m, T::kExp) == kM) {
-            // pass 2 over the registers, ascending index; an ordinary M (not NaN, not +-0)
-            // matches by exact bits, the special cases by key
+            // pass 2 over the registers, without a serial scan: per vector u, one packed
+            // compare per word (0xFFFF per equal half) and two byte permutes give 8 flag
+            // bytes, byte j set iff half j of the vector equals M; the lowest u with a flag
+            // and its lowest flag byte are the first match (ascending u, then j = ascending
+            // index).  Every warp with a matching lane executes this, and with ties (common
+            // on bf16's coarse grid) that is most warps: it must be short.  An ordinary M
+            // (not NaN, not +-0) matches by value == by bits; the special cases by key.
             const bool plain = (m & 0x7FFFu) != 0 && (m & 0x7FFFu) <= T::kExp;
+            int code = -1;  // 8 u + j of the first match
+            if (plain) {
+                const uint32_t mm = m | (m << 16);
 #pragma unroll
-            for (int u = 0; u < kVPT; ++u) {
-                if (u >= mine || first != 0xFFFFFFFFu) break;
-                const uint32_t e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-                const uint32_t base = static_cast<uint32_t>((vec0 + tid + u * kVerifyThreads) * 8);
+                for (int u = kVPT - 1; u >= 0; --u) {
+                    const uint32_t r0 = T::eq2(w[u].x, mm), r1 = T::eq2(w[u].y, mm);
+                    const uint32_t r2 = T::eq2(w[u].z, mm), r3 = T::eq2(w[u].w, mm);
+                    const uint32_t lo = __byte_perm(r0, r1, 0x6420), hi = __byte_perm(r2, r3, 0x6420);
+                    if (u < mine && (lo | hi))
+                        code = 8 * u + (lo ? (__ffs(lo) - 1) >> 3 : 4 + ((__ffs(hi) - 1) >> 3));
+                }
+            } else {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t lo = e[q] & 0xFFFFu, hi = e[q] >> 16;
-                    const bool mlo = plain ? lo == m : key16(lo, T::kExp) == kM;
-                    const bool mhi = plain ? hi == m : key16(hi, T::kExp) == kM;
-                    if (first == 0xFFFFFFFFu && mlo) first = base + 2 * q;
-                    if (first == 0xFFFFFFFFu && mhi) first = base + 2 * q + 1;
+                for (int u = kVPT - 1; u >= 0; --u) {
+                    const uint32_t e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+                    int j = -1;
+#pragma unroll
+                    for (int q = 3; q >= 0; --q) {
+                        if (key16(e[q] >> 16, T::kExp) == kM) j = 2 * q + 1;
+                        if (key16(e[q] & 0xFFFFu, T::kExp) == kM) j = 2 * q;
+                    }
+                    if (u < mine && j >= 0) code = 8 * u + j;
                 }
             }
+            if (code >= 0)
+                first = static_cast<uint32_t>((vec0 + tid + (code >> 3) * kVerifyThreads) * 8 + (code & 7));
             for (int64_t v = tail0 + tid; v < v1 && first == 0xFFFFFFFFu; v += kVerifyThreads)
                 if (key16(reinterpret_cast<const uint16_t *>(rowp)[v], T::kExp) == kM) first = static_cast<uint32_t>(v);
+        }
+        if (p.exp == 5) {  // timing experiment only: up to pass 2, no merge
+            if (first == 0xFFFFFFFEu && p.status) atomicOr(p.status, 0x80000000u);
+            return;
         }
         // every thread holding M contributes (key(M), ~first); the max picks the lowest index
         cta_merge(p, row, first != 0xFFFFFFFFu ? pack_key(kM, first) : 0ull, s_red);

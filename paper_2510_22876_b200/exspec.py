@@ -218,7 +218,7 @@ class SequencePool:
         return True
 
     # ----------------------------------------------------------------- native executor
-    def native(self, ring, V, logit_dtype=torch.bfloat16):
+    def native(self, ring, V, logit_dtype=torch.bfloat16, est_gather_GBps=0.0, est_verify_us=0.0):
         """Bind a `specdec_pool_desc` to this pool and an input ring [(logits, draft)] for
         `epoch_native` (the per-batch launch loop in C++, csrc/pool_exec.cu)."""
         p = lambda t: t.data_ptr() if t is not None else None
@@ -259,6 +259,7 @@ class SequencePool:
             d.staging_ring = ctypes.cast(self._stg_ptrs, ctypes.c_void_p)
             d.copy_stream = self._copy_stream.cuda_stream
             d.events = ctypes.cast(self._ev_ptrs, ctypes.c_void_p)
+            d.est_gather_GBps, d.est_verify_us = float(est_gather_GBps), float(est_verify_us)
         self._desc = d
         return d
 

@@ -5,7 +5,8 @@ graph, per-launch time from CUDA events.
 
 SPECDEC_K1_EXP=1 times the argmax phase alone (no grid-wide arrival / epilogue), =2 an empty
 kernel on the same grid (the launch floor), =3 the loads and per-thread max only (no CTA
-reduction) -- results invalid, for splitting the latency.
+reduction), =4 up to the CTA maximum (no pass 2), =5 up to pass 2 (no merge) -- results
+invalid, for splitting the latency.
 """
 from __future__ import annotations
 
@@ -29,10 +30,11 @@ def main():
     ap.add_argument("--k", type=int, default=5)
     ap.add_argument("--V", type=int, default=151936)
     ap.add_argument("--n", type=int, default=50)
+    ap.add_argument("--ring", type=int, default=8, help="logits buffers (16 at Qwen3 B=8 > L2)")
     a = ap.parse_args()
     dev = torch.device("cuda")
     B, k, V = a.B, a.k, a.V
-    ring = [W.gen_logits_torch(0, r, B, k, V, "bf16", dev) for r in range(8)]
+    ring = [W.gen_logits_torch(0, r, B, k, V, "bf16", dev) for r in range(a.ring)]
     draft = torch.from_numpy(W.gen_round_truth(0, 0, B, k, V, "alpha").draft).to(dev)
     i32, i64, u8 = torch.int32, torch.int64, torch.uint8
     n = torch.full((B,), 100, dtype=i32, device=dev)
@@ -43,7 +45,7 @@ def main():
 
     def one(j):
         act.fill_(1)
-        _abi.specdec_verify(ring[j % 8], draft, n, act, *out, plan[0], plan[1], plan[2], plan[3], ws)
+        _abi.specdec_verify(ring[j % len(ring)], draft, n, act, *out, plan[0], plan[1], plan[2], plan[3], ws)
     for j in range(3):
         one(j)
     torch.cuda.synchronize()
@@ -52,7 +54,7 @@ def main():
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
         for j in range(a.n):
-            _abi.specdec_verify(ring[j % 8], draft, n, act, *out, plan[0], plan[1], plan[2], plan[3], ws,
+            _abi.specdec_verify(ring[j % len(ring)], draft, n, act, *out, plan[0], plan[1], plan[2], plan[3], ws,
                                 stream=s)
     torch.cuda.current_stream().wait_stream(s)
     g.replay()
@@ -67,7 +69,7 @@ def main():
         best = min(best, e0.elapsed_time(e1) / a.n * 1e3)
     mb = B * (k + 1) * V * 2 / 1e6
     print(json.dumps({"B": B, "k": k, "V": V, "us_per_launch": round(best, 2), "logits_MB": round(mb, 2),
-                      "GBps": round(mb * 1e3 / best, 1), "exp": os.environ.get("SPECDEC_K1_EXP", "0"),
+                      "GBps": round(mb * 1e3 / best, 1), "ring_MB": round(mb * len(ring), 1), "exp": os.environ.get("SPECDEC_K1_EXP", "0"),
                       "pdl": os.environ.get("SPECDEC_PDL", "1")}))
 
 
