@@ -354,10 +354,13 @@ typedef struct specdec_pool_desc {
      * fallback batches), and the fallback batches are interleaved with the same-length
      * ones on `stream` by a list schedule on the estimates below (a fallback batch runs
      * as soon as its gather is expected to be complete), so the bandwidth-bound gathers
-     * stream under the latency-bound same-length verifies.  Ordering: the verify of
-     * fallback batch f waits for its gather (events[f % n_staging]); the gather of f + n_staging waits for the
-     * scatter of f (events[n_staging + f % n_staging]).  `stream` waits on every gather,
-     * so the epoch is complete when `stream` is.  The caller owns the buffers and the
+     * stream under the latency-bound same-length verifies.  The scatters run on
+     * `copy_stream` too.  Ordering: the verify of fallback batch f waits for its gather
+     * (events[f % n_staging]); its scatter waits for that verify (events[n_staging +
+     * f % n_staging]) and reads the batch's accept lengths from accept_ring[f % n_staging];
+     * the gather of f + n_staging follows that scatter in copy-stream order; `stream`
+     * waits for the copy stream at the end, so the epoch is complete when `stream` is.
+     * The caller owns the buffers and the
      * 2 * n_staging events (cudaEvent_t, timing disabled).  staging_ring[0] may be
      * `staging`.  If `cur_staging` is non-NULL the executor stores the staging buffer of
      * a fallback batch there before calling forward() (NULL for same-length batches). */
@@ -366,6 +369,7 @@ typedef struct specdec_pool_desc {
     specdec_stream_t copy_stream;
     void *const *events;       /* host array of 2 * n_staging cudaEvent_t */
     void **cur_staging;        /* host, nullable */
+    int32_t *accept_ring;      /* device [n_staging][B]: accept lengths of the fallback batch in each slot */
     /* scheduling hints for the overlapped order (<= 0: 5500 GB/s, 10 us): the gather rate
      * and the duration of one batch verify; they change the order, never a result */
     double est_gather_GBps, est_verify_us;

@@ -71,14 +71,21 @@ class PoolDesc(ctypes.Structure):
         ("logits_ring", _P), ("draft_ring", _P), ("ring_n", _I32), ("ring_pos", _P),
         ("dense_consumer", _I32),
         ("n_staging", _I32), ("staging_ring", _P), ("copy_stream", _P), ("events", _P),
-        ("cur_staging", _P), ("est_gather_GBps", ctypes.c_double), ("est_verify_us", ctypes.c_double),
+        ("cur_staging", _P), ("accept_ring", _P),
+        ("est_gather_GBps", ctypes.c_double), ("est_verify_us", ctypes.c_double),
     ]
 
 
-def specdec_pool_epoch(desc: PoolDesc, max_batches=0, stream=None):
-    """Native epoch executor; returns (batches run, same-length run, members same, members fallback)."""
+# specdec_forward_fn: (ctx, batch, same_length, width, const void **logits, const int64_t **draft)
+FORWARD_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                              ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p))
+
+
+def specdec_pool_epoch(desc: PoolDesc, max_batches=0, stream=None, forward=None):
+    """Native epoch executor; returns (batches run, same-length run, members same, members fallback).
+    `forward`: an optional FORWARD_FN (the model's verify forward), else the descriptor's ring."""
     out = [ctypes.c_int32(0) for _ in range(4)]
-    _check(load().specdec_pool_epoch(ctypes.byref(desc), None, None, max_batches,
+    _check(load().specdec_pool_epoch(ctypes.byref(desc), forward, None, max_batches,
                                      *[ctypes.byref(o) for o in out], _stream(stream)),
            "specdec_pool_epoch")
     return tuple(o.value for o in out)

@@ -26,7 +26,7 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     if (!d || !d->host_header || d->W < 1 || d->B < 1) return SPECDEC_ERR_ARG;
     if (!forward && (!d->logits_ring || !d->draft_ring || d->ring_n < 1 || !d->ring_pos))
         return SPECDEC_ERR_ARG;
-    if (d->n_staging >= 2 && (!d->staging_ring || !d->copy_stream || !d->events))
+    if (d->n_staging >= 2 && (!d->staging_ring || !d->copy_stream || !d->events || !d->accept_ring))
         return SPECDEC_ERR_ARG;
     if (d->n_staging >= 2)
         for (int32_t i = 0; i < d->n_staging; ++i)
@@ -71,8 +71,9 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         for (int32_t b = 0; b < run; ++b) seq.push_back(b);
     } else {
         // List schedule on estimated durations: a fallback batch goes next as soon as its
-        // gather is expected to be done, else the next same-length batch; gathers run back
-        // to back, the one into staging slot f % NS after the scatter of f - NS.  Only the
+        // gather is expected to be done, else the next same-length batch; the copy stream
+        // runs gathers back to back, the one into staging slot f % NS after the scatter of
+        // f - NS (which follows that batch's verify).  Only the
         // order (i.e. the timing) depends on the estimates, never a result.
         const double gbps = d->est_gather_GBps > 0 ? d->est_gather_GBps : 5500.0;
         const double tv = d->est_verify_us > 0 ? d->est_verify_us : 10.0;  // K1 (+ scatter)
@@ -91,10 +92,11 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         size_t fi = 0, si = 0;
         while (fi < nf || si < ns) {
             if (fi < nf && (g_end[fi] <= t || si == ns)) {
-                t = std::max(t, g_end[fi]) + 2.0 * tv;  // verify + scatter
+                t = std::max(t, g_end[fi]) + tv;  // its verify
                 s_end[fi] = t;
+                // copy stream: ..., gather nx - 1, [verify fi], scatter fi (~ tv), gather nx
                 const size_t nx = fi + NS;
-                if (nx < nf) g_end[nx] = std::max(g_end[nx - 1], s_end[fi]) + gather_us(fbs[nx]);
+                if (nx < nf) g_end[nx] = std::max(g_end[nx - 1], s_end[fi]) + tv + gather_us(fbs[nx]);
                 seq.push_back(fbs[fi++]);
             } else {
                 t += tv;
@@ -152,24 +154,36 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
             logits = d->logits_ring[j];
             draft = d->draft_ring[j];
         }
-        // K1 with the Phase 4 write-back fused into its epilogue
+        // K1 with the Phase 4 write-back fused into its epilogue; with overlap, a fallback
+        // batch's accept lengths go to its staging slot's row of accept_ring, read by its
+        // scatter on the copy stream after later batches have reused d->accept
+        const int32_t slot = fallback && overlap ? fb_rank[b] % NS : -1;
+        int32_t *acc = slot >= 0 ? d->accept_ring + static_cast<int64_t>(slot) * B : d->accept;
         rc = specdec_pool_verify(logits, d->logit_dtype, rows(b), d->k, d->V, d->logit_stride, draft, members,
-                                 mlen, mact, d->eos_id, d->pad_id, d->accept, d->bonus, d->emit,
+                                 mlen, mact, d->eos_id, d->pad_id, acc, d->bonus, d->emit,
                                  d->finished, d->len, d->gen, d->active, d->tokens, d->cap_tok,
                                  d->out_buf, d->max_new, d->status, d->ws, d->ws_bytes, stream);
         if (rc) return rc;
         if (fallback) {
+            // scatter of the a+1 new KV rows back to the pool: on `stream` (serial) or on the
+            // copy stream after this verify (overlap), where stream order also keeps the
+            // next gather into this staging slot behind it
+            cudaStream_t on = stream ? reinterpret_cast<cudaStream_t>(stream) : nullptr;
+            if (overlap) {
+                if ((e = cudaEventRecord(ev(NS + slot), s)) != cudaSuccess ||
+                    (e = cudaStreamWaitEvent(cs, ev(NS + slot), 0)) != cudaSuccess)
+                    return record_cuda_error(e);
+                on = cs;
+            }
             rc = specdec_realign_kv(stg(b), d->kv, d->kv_dtype, d->n_planes, rows(b), d->H, d->D,
                                     s_plane, s_row, s_head, d->cap, p_plane, p_row, p_head, d->cap,
-                                    nullptr, blens[b] - 1, mlen, -1, d->accept, 1,
+                                    nullptr, blens[b] - 1, mlen, -1, acc, 1,
                                     static_cast<int32_t>(d->k + 1),  // a + 1 <= k + 1 rows
-                                    nullptr, members, 0, nullptr, 0, d->moved, d->status, stream);
+                                    nullptr, members, 0, nullptr, 0, d->moved, d->status,
+                                    reinterpret_cast<specdec_stream_t>(on));
             if (rc) return rc;
             const int32_t nxt = fb_rank[b] + NS;  // the gather that reuses this staging buffer
             if (overlap && nxt < static_cast<int32_t>(fbs.size())) {
-                if ((e = cudaEventRecord(ev(NS + fb_rank[b] % NS), s)) != cudaSuccess ||
-                    (e = cudaStreamWaitEvent(cs, ev(NS + fb_rank[b] % NS), 0)) != cudaSuccess)
-                    return record_cuda_error(e);
                 if ((rc = gather(fbs[nxt], cs))) return rc;
                 if ((e = cudaEventRecord(ev(nxt % NS), cs)) != cudaSuccess) return record_cuda_error(e);
             }
@@ -181,6 +195,12 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
             mfb += sizes[b];
         }
         ++ran;
+    }
+    if (overlap && !fbs.empty()) {
+        // the epoch ends on `stream`: it waits for the copy stream's last scatter (events[0]
+        // is free again -- every wait on its earlier records has been enqueued)
+        if ((e = cudaEventRecord(ev(0), cs)) != cudaSuccess || (e = cudaStreamWaitEvent(s, ev(0), 0)) != cudaSuccess)
+            return record_cuda_error(e);
     }
     if (!forward && d->ring_pos) *d->ring_pos = ring_base + run;
     if (h_ran) *h_ran = ran;

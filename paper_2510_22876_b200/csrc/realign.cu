@@ -37,6 +37,7 @@ constexpr int kZeroBytes = 2048;
 constexpr int64_t kSegBytes = 128 * 1024;     // target bytes per work unit
 constexpr int64_t kSlotBytes = 4096;          // boundary slot: |shift| * row bytes <= this
 static int g_ctas_per_sm = 0;                 // tuning override (SPECDEC_REALIGN_CTAS)
+static int64_t g_grid_cap = 0;                // tuning override (SPECDEC_REALIGN_GRID): max CTAs
 static int64_t g_seg_bytes = kSegBytes;       // tuning override (SPECDEC_REALIGN_SEG, >= default)
 
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -505,7 +506,8 @@ int launch_realign(const RealignParams &p, int64_t max_units, cudaStream_t s) {
     const int64_t sms = device_sm_count();
     int ctas = max_units >= 16 * sms ? 1 : per_sm;
     if (g_ctas_per_sm > 0) ctas = std::min(per_sm, g_ctas_per_sm);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_units, sms * ctas));
+    int64_t grid = std::max<int64_t>(1, std::min<int64_t>(max_units, sms * ctas));
+    if (g_grid_cap > 0) grid = std::min(grid, g_grid_cap);
     if (p.ws && p.inplace) {
         const int64_t save_ctas = std::min<int64_t>((max_units + kSaveWarps - 1) / kSaveWarps, sms * 16);
         const int rc = launch_k(realign_save_kernel, dim3(static_cast<unsigned>(std::max<int64_t>(1, save_ctas))),
@@ -607,6 +609,8 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
         pol = q ? atoi(q) : 0;
         const char *c = getenv("SPECDEC_REALIGN_CTAS");
         g_ctas_per_sm = c ? atoi(c) : 0;
+        const char *gc = getenv("SPECDEC_REALIGN_GRID");
+        g_grid_cap = gc ? atoll(gc) : 0;
         const char *sg = getenv("SPECDEC_REALIGN_SEG");
         g_seg_bytes = std::max<int64_t>(kSegBytes, sg ? atoll(sg) : kSegBytes);
     }

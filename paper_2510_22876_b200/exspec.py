@@ -259,14 +259,17 @@ class SequencePool:
             d.staging_ring = ctypes.cast(self._stg_ptrs, ctypes.c_void_p)
             d.copy_stream = self._copy_stream.cuda_stream
             d.events = ctypes.cast(self._ev_ptrs, ctypes.c_void_p)
+            self._accept_ring = torch.zeros((ns, self.B), dtype=torch.int32, device=self.device)
+            d.accept_ring = self._accept_ring.data_ptr()
             d.est_gather_GBps, d.est_verify_us = float(est_gather_GBps), float(est_verify_us)
         self._desc = d
         return d
 
-    def epoch_native(self, max_batches=0, stream=None):
+    def epoch_native(self, max_batches=0, stream=None, forward=None):
         """One epoch (or, with max_batches=1, one Alg. 3 iteration) in the native executor.
+        `forward`: optional _abi.FORWARD_FN called per batch for its (logits, draft).
         Returns (batches run, same-length batches run, members same, members fallback)."""
-        r = _abi.specdec_pool_epoch(self._desc, max_batches, stream)
+        r = _abi.specdec_pool_epoch(self._desc, max_batches, stream, forward)
         self.verify_calls += r[0]
         return r
 
