@@ -60,6 +60,9 @@ def parse():
                          "gathers (copy stream) with the same-length batches, 1 = serial")
     ap.add_argument("--pool-est", type=float, nargs=2, default=(0.0, 0.0), metavar=("GBPS", "VERIFY_US"),
                     help="pool, overlapped executor: scheduling estimates (0 = library defaults)")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="pool, 1 GPU: drain each of G band shards alone and report the predicted "
+                         "G-GPU throughput (slowest shard); a prediction, not a measurement")
     ap.add_argument("--pool-mode", default="epoch", choices=["epoch", "alg3"],
                     help="epoch: run every batch of the window plan; alg3: batch 0 then re-plan")
     ap.add_argument("--B", type=int, default=0, help="override batch size")
@@ -579,7 +582,7 @@ def oracle_pool_sample(args, verify_samples=2):
 SLEEP_CYCLES = 200_000     # ~0.1 ms at 1.965 GHz: longer than Python's enqueue of one batch
 
 
-def run_pool(args, rank, world, device):
+def run_pool(args, rank, world, device, emulate=False):
     """EXSpec pool (BASELINE.json configs[4]): N Qwen3-shaped sequences, band-sharded over
     the ranks; each rank drains its shard (K4 plan, per batch gather / verify / write-back
     / scatter); one NCCL all-gather of outputs + counters at the end.  value = sequences/s
@@ -675,7 +678,7 @@ def run_pool(args, rank, world, device):
         return epochs, batches
 
     drain()                                   # warm-up drain (attributes, allocator)
-    if world > 1:
+    if world > 1 and not emulate:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(device.index if device.index is not None else 0)
@@ -695,6 +698,12 @@ def run_pool(args, rank, world, device):
     status = int(sp.status.item())
     out_loc = sp.out_buf.cpu().numpy()
     gen_loc = sp.gen.cpu().numpy()
+    if emulate:
+        # one rank's shard drained alone on this GPU (no collectives): see run_pool_emulated
+        assert int((gen_loc == args.max_new).sum()) == n_loc, "every sequence reaches max_new (EOS off)"
+        return {"rank": rank, "ms": ms, "seqs": n_loc, "epochs": epochs, "batches": int(cnt[0]),
+                "same_length_batches": int(cnt[1]), "kv_bytes": moved, "status": status,
+                "clocks": clocks.summary()}
     if world > 1:
         ms = max_over_ranks(ms, device, world)
         g0 = time.perf_counter()
@@ -751,6 +760,39 @@ def run_pool(args, rank, world, device):
         "gpu_launches": (epochs + 1) + (1 if sp.fused else 2) * int(cnt[0])
         + 2 * (int(cnt[0]) if sp.dense_consumer else int(cnt[0]) - int(cnt[1])),
         "e2e": None, "cpu_baseline": None,
+    }
+
+
+def run_pool_emulated(args, device):
+    """--emulate-ranks G on one GPU: drain each of the G band shards alone, one after the
+    other, exactly as rank r of a G-GPU run would (same shard, same executor, no
+    collective inside the drain).  The G-GPU job time is the slowest shard (the ranks
+    share nothing until the end-of-run all-gather of ~2 MB), so the predicted whole-job
+    throughput is N / max_r(ms_r).  This is a prediction from measured per-shard times,
+    not a multi-GPU measurement."""
+    import torch
+    G = args.emulate_ranks
+    per = []
+    for r in range(G):
+        per.append(run_pool(args, r, G, device, emulate=True))
+        torch.cuda.empty_cache()
+    mx = max(p["ms"] for p in per)
+    N = args.pool_n
+    return {
+        "metric": "EXSpec pool sequences/s (Qwen3-8B shape, N=%d, B=8, k=5)" % N,
+        "value": N / (mx / 1e3), "unit": "sequences/s", "n_gpus": 1, "steps": sum(p["epochs"] for p in per),
+        "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"EXSpec pool drain: {N} seqs, prompt {args.pool_lengths}, {args.shard} shards",
+                   "parallelism": f"pool sharded x{G}, EMULATED: each shard drained alone on one B200"},
+        "emulated": {"ranks": G, "predicted_seq_per_s": N / (mx / 1e3),
+                     "per_rank_ms": [p["ms"] for p in per], "per_rank_seqs": [p["seqs"] for p in per],
+                     "per_rank_batches": [p["batches"] for p in per],
+                     "per_rank_kv_GB": [p["kv_bytes"] / 1e9 for p in per],
+                     "imbalance_max_over_mean": mx / (sum(p["ms"] for p in per) / G),
+                     "note": "prediction: job time = slowest shard; the end-of-run all-gather (~2 MB over "
+                             "NVLink) is not included"},
+        "clocks": per[0]["clocks"], "status": max(p["status"] for p in per), "e2e": None, "cpu_baseline": None,
     }
 
 
@@ -818,6 +860,9 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
+    if args.config == "pool" and args.emulate_ranks > 1 and world == 1:
+        print(json.dumps(run_pool_emulated(args, device)))
+        return
     if args.config == "pool":
         out = run_pool(args, rank, world, device)
         if rank == 0:
