@@ -371,66 +371,29 @@ def run_ours(args, rank, world, device):
 
 
 def run_e2e(rb, args, world):
-    """Each step: H2D of that step's logits + drafts from pinned host memory (copy stream,
-    two device buffers, so the copy of step s+1 overlaps the round of step s), the round
-    (graph replay), D2H of the step's result -- the per-row emitted-token counts -- into
-    pinned host memory (SPECDEC_E2E_D2H=three also reads accept + bonus; none: no read).
-    The D2H runs on a third stream while the next round computes: the batch keeps one
-    result set per state parity, and a round waits only until the set it overwrites (two
-    rounds back) has been read out."""
+    """End to end through the C ABI with HOST buffers: every step is one
+    specdec_eqspec_round_host call (eqspec.py step_host) that copies the step's logits +
+    drafts from pinned host memory into a device staging slot (copy stream), runs the
+    round (K1 -> K3 -> K2) on the compute stream and copies the step's result -- the
+    per-row emitted-token counts -- back into pinned host memory (third stream).  Two
+    staging slots and one result set per state parity let the copies of step s+1 run
+    under the round of step s; nothing synchronises the host inside the timed region."""
     import torch
     import torch.distributed as dist
     sh, dev, bt = rb.sh, rb.dev, rb.bt
     d2h_mode = os.environ.get("SPECDEC_E2E_D2H", "one")
     host_lg = [lg.cpu().pin_memory() for lg in rb.logits]
     host_dr = [d.cpu().pin_memory() for d in rb.drafts]
-    dlg = [torch.empty_like(rb.logits[0]) for _ in range(2)]
-    ddr = [torch.empty_like(rb.drafts[0]) for _ in range(2)]
-    out_a = torch.empty((args.steps, sh.B), dtype=torch.int32).pin_memory()
-    out_b = torch.empty((args.steps, sh.B), dtype=torch.int64).pin_memory()
     out_e = torch.empty((args.steps, sh.B), dtype=torch.int32).pin_memory()
-    bt.capture(list(zip(dlg, ddr)), V=sh.V)   # graphs on the two staging buffers
     comp = rb.stream
-    copy = torch.cuda.Stream(dev)
-    d2h = torch.cuda.Stream(dev)
-    ready = [torch.cuda.Event() for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]
-    fetched = [torch.cuda.Event() for _ in range(2)]  # results of parity p were read out
-
-    def h2d(r):
-        b = r % 2
-        with torch.cuda.stream(copy):
-            copy.wait_event(done[b])
-            dlg[b].copy_(host_lg[r % RING], non_blocking=True)
-            ddr[b].copy_(host_dr[r % RING], non_blocking=True)
-            ready[b].record(copy)
+    bt.host_io(host_lg[0], host_dr[0])
 
     def run(n):
-        for b in range(2):
-            done[b].record(comp)
-            fetched[b].record(d2h)
-        h2d(0)
         for r in range(n):
-            if r + 1 < n:
-                h2d(r + 1)
-            b = r % 2
-            par = bt.cur
-            comp.wait_event(ready[b])
-            comp.wait_event(fetched[par])  # round r-2's results (same parity set) are out
             rb.episode(r, args.episode)
-            bt.replay(b)
-            done[b].record(comp)
-            if d2h_mode == "none":
-                continue
-            # the D2H runs on its own stream under the next round (results are per parity)
-            with torch.cuda.stream(d2h):
-                d2h.wait_event(done[b])
-                if d2h_mode == "three":
-                    out_a[r].copy_(bt.accept, non_blocking=True)
-                    out_b[r].copy_(bt.bonus, non_blocking=True)
-                out_e[r].copy_(bt.emit, non_blocking=True)
-                fetched[par].record(d2h)
-        comp.wait_stream(d2h)
+            bt.step_host(host_lg[r % RING], host_dr[r % RING],
+                         None if d2h_mode == "none" else out_e[r], V=sh.V, stream=comp)
+        comp.wait_stream(bt._io_streams[1])
 
     rb.reset()
     run(min(args.warmup, args.steps))
@@ -452,10 +415,11 @@ def run_e2e(rb, args, world):
         for r in range(args.steps):
             assert np.array_equal(out_e[r].numpy(), rb.truth[r % RING].accept + 1), "e2e emit mismatch"
     h2d_b = rb.logits[0].numel() * rb.logits[0].element_size() + rb.drafts[0].numel() * 8
-    d2h_b = {"three": sh.B * 16, "one": sh.B * 4, "none": 0}[d2h_mode]
+    d2h_b = {"one": sh.B * 4, "none": 0}[d2h_mode]
     return {"value": world * args.steps / (ms / 1e3), "unit": "rounds/s", "h2d_bytes_per_step": h2d_b,
             "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / args.steps, "wall_s": wall,
-            "overlap": "H2D on a copy stream, double-buffered; round = CUDA graph replay; "
+            "api": "specdec_eqspec_round_host (one C call per step: H2D + K1/K3/K2 + D2H)",
+            "overlap": "H2D on a copy stream into two staging slots; round on the compute stream; "
                        "D2H on a third stream from the round's parity result set"}
 
 

@@ -380,6 +380,90 @@ int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, v
                        int32_t *h_members_same, int32_t *h_members_fallback,
                        specdec_stream_t stream);
 
+/* ------------------------------------------------------------------------------ a1-a3
+ * specdec_eqspec_round -- one whole EqSpec round after the verify forward (Alg. 2's loop
+ * body): specdec_verify -> specdec_rebuild_pos_mask ->
+ * specdec_realign_kv (target cache, then the draft cache if any), enqueued on `stream`
+ * with no host synchronisation, exactly the calls paper_2510_22876_b200/eqspec.py makes.
+ * The batch state is double-buffered by `parity` p: the round reads n[p], pad[p],
+ * tokens[p] and writes n[1-p], pad[1-p], tokens[1-p]; its results go to the result set
+ * of parity p (accept[p], ...), so a reader of round r's results (e.g. a D2H on another
+ * stream) only has to finish before round r+2.  KV: kv[0] == kv[1] realigns in place;
+ * two buffers ping-pong (round p reads kv[p], writes kv[1-p]).  B == 1 in place moves no
+ * KV (a single row stays right-aligned): no realign launch.  The anchored
+ * origin (f3) is driven from eqspec.py only (anchor fields are not part of this call).
+ * Errors: SPECDEC_ERR_ARG for a NULL desc / logits / draft or parity not 0/1; any error of
+ * the three calls as is.
+ */
+typedef struct specdec_round_desc {
+    int64_t B, k, V, logit_stride;
+    int logit_dtype;
+    int64_t eos_id, pad_id;
+    /* per-row state, [2] = by parity */
+    int32_t *n[2], *pad[2];
+    int64_t *tokens[2];        /* [B][cap_tok] each */
+    int64_t cap_tok;
+    int64_t *mask, *pos;       /* [B][mp_stride] */
+    int64_t mp_stride;
+    uint8_t *active;           /* [B] in/out */
+    int32_t *budget;           /* [B] in/out remaining new tokens, or NULL */
+    int32_t *gen;              /* [B], with out_buf, or NULL */
+    int64_t *out_buf;          /* [B][max_new] or NULL */
+    int64_t max_new;
+    /* results, one set per parity */
+    int32_t *accept[2], *emit[2];
+    int64_t *bonus[2];
+    uint8_t *finished[2];
+    int64_t *pred;             /* [B][k+1] or NULL */
+    int32_t *kept, *plan_L, *kept_draft /* NULL unless a draft cache */;
+    void *ws;                  /* specdec_verify workspace */
+    size_t ws_bytes;
+    uint32_t *status;
+    unsigned long long *moved;
+    /* target KV [planes][B][H][cap_kv][D] (element strides s_plane, s_row, s_head) */
+    void *kv[2];
+    int kv_dtype;
+    int64_t n_planes, H, D, cap_kv, s_plane, s_row, s_head;
+    /* draft-model KV (f1), same layout rules; dkv[0] == NULL: none */
+    void *dkv[2];
+    int64_t d_planes, d_H, d_D, d_s_plane, d_s_row, d_s_head;
+    /* realign: SPECDEC_ZERO_PADS / SPECDEC_OVERLAP_PREV for the target call; an optional
+     * segment workspace (specdec_realign_workspace_size) */
+    uint32_t realign_flags;
+    void *realign_ws;
+    size_t realign_ws_bytes;
+} specdec_round_desc;
+
+int specdec_eqspec_round(const specdec_round_desc *d, int parity, const void *d_logits,
+                         const int64_t *d_draft, specdec_stream_t stream);
+
+/* specdec_eqspec_round_host -- the same round from HOST inputs, with the host<->device
+ * copies inside the call (the end-to-end path of a caller whose logits live in host
+ * memory).  On `io->copy_stream`: wait io->ev_done[slot] (the last round that read
+ * staging slot `slot`), copy h_logits [B][k+1][logit_stride] and h_draft [B][k] (pinned
+ * host memory, for the copies to be asynchronous) into io->d_logits[slot] /
+ * io->d_draft[slot], record io->ev_ready[slot].  On `stream`: wait ev_ready[slot] and
+ * io->ev_fetched[parity] (the read-out of the result set this round overwrites), run
+ * specdec_eqspec_round, record ev_done[slot].  If h_emit (pinned [B] int32) is non-NULL:
+ * on io->d2h_stream wait ev_done[slot], copy emit[parity] -> h_emit, record
+ * ev_fetched[parity].  Nothing synchronises the host: successive calls with alternating
+ * slot and parity overlap the copies of round r+1 with round r.  The events are the
+ * caller's (cudaEvent_t, timing disabled; a never-recorded event does not block).
+ * Errors: as specdec_eqspec_round; SPECDEC_ERR_ARG for a NULL io / host pointer or slot
+ * not 0/1; SPECDEC_ERR_CUDA for a failed copy or event call.
+ */
+typedef struct specdec_host_io {
+    void *d_logits[2];         /* device staging, [B][k+1][logit_stride] each */
+    int64_t *d_draft[2];       /* device staging, [B][k] each */
+    specdec_stream_t copy_stream, d2h_stream;
+    void *ev_ready[2], *ev_done[2], *ev_fetched[2];
+} specdec_host_io;
+
+int specdec_eqspec_round_host(const specdec_round_desc *d, const specdec_host_io *io,
+                              int parity, int slot, const void *h_logits,
+                              const int64_t *h_draft, int32_t *h_emit,
+                              specdec_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,8 @@ _SIGS = {
     "specdec_pool_writeback": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
                                 _I64, _P, _P], _INT),
     "specdec_pool_epoch": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P], _INT),
+    "specdec_eqspec_round": ([_P, _INT, _P, _P, _P], _INT),
+    "specdec_eqspec_round_host": ([_P, _P, _INT, _INT, _P, _P, _P, _P], _INT),
     "specdec_pool_verify": ([_P, _INT, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _P,
                              _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P], _INT),
 }
@@ -74,6 +76,53 @@ class PoolDesc(ctypes.Structure):
         ("cur_staging", _P), ("accept_ring", _P),
         ("est_gather_GBps", ctypes.c_double), ("est_verify_us", ctypes.c_double),
     ]
+
+
+_P2 = _P * 2
+
+
+class RoundDesc(ctypes.Structure):
+    """Mirror of `specdec_round_desc` (include/specdec.h), field for field."""
+    _fields_ = [
+        ("B", _I64), ("k", _I64), ("V", _I64), ("logit_stride", _I64), ("logit_dtype", _INT),
+        ("eos_id", _I64), ("pad_id", _I64),
+        ("n", _P2), ("pad", _P2), ("tokens", _P2), ("cap_tok", _I64),
+        ("mask", _P), ("pos", _P), ("mp_stride", _I64),
+        ("active", _P), ("budget", _P), ("gen", _P), ("out_buf", _P), ("max_new", _I64),
+        ("accept", _P2), ("emit", _P2), ("bonus", _P2), ("finished", _P2),
+        ("pred", _P), ("kept", _P), ("plan_L", _P), ("kept_draft", _P),
+        ("ws", _P), ("ws_bytes", ctypes.c_size_t), ("status", _P), ("moved", _P),
+        ("kv", _P2), ("kv_dtype", _INT),
+        ("n_planes", _I64), ("H", _I64), ("D", _I64), ("cap_kv", _I64),
+        ("s_plane", _I64), ("s_row", _I64), ("s_head", _I64),
+        ("dkv", _P2), ("d_planes", _I64), ("d_H", _I64), ("d_D", _I64),
+        ("d_s_plane", _I64), ("d_s_row", _I64), ("d_s_head", _I64),
+        ("realign_flags", _U32), ("realign_ws", _P), ("realign_ws_bytes", ctypes.c_size_t),
+    ]
+
+
+class HostIO(ctypes.Structure):
+    """Mirror of `specdec_host_io` (include/specdec.h)."""
+    _fields_ = [("d_logits", _P2), ("d_draft", _P2), ("copy_stream", _P), ("d2h_stream", _P),
+                ("ev_ready", _P2), ("ev_done", _P2), ("ev_fetched", _P2)]
+
+
+def specdec_eqspec_round(desc: RoundDesc, parity, logits, draft, stream=None):
+    """One EqSpec round (K1 -> K3 -> K2) in the native driver."""
+    _check(load().specdec_eqspec_round(ctypes.byref(desc), parity, _ptr(logits), _ptr(draft),
+                                       _stream(stream)), "specdec_eqspec_round")
+
+
+def specdec_eqspec_round_host(desc: RoundDesc, io: HostIO, parity, slot, h_logits, h_draft,
+                              h_emit=None, stream=None):
+    """One EqSpec round from pinned HOST logits / drafts (H2D + round + D2H of emit)."""
+    hp = lambda t: None if t is None else t.data_ptr()
+    for t in (h_logits, h_draft, h_emit):
+        if t is not None and (t.is_cuda or not t.is_pinned()):
+            raise SpecdecError("pinned host tensor expected")
+    _check(load().specdec_eqspec_round_host(ctypes.byref(desc), ctypes.byref(io), parity, slot,
+                                            hp(h_logits), hp(h_draft), hp(h_emit), _stream(stream)),
+           "specdec_eqspec_round_host")
 
 
 # specdec_forward_fn: (ctx, batch, same_length, width, const void **logits, const int64_t **draft)

@@ -22,6 +22,7 @@ cell, the analog of the paper's fresh-tensor realignment).
 """
 from __future__ import annotations
 
+import ctypes
 import os
 
 import numpy as np
@@ -105,6 +106,9 @@ class EqSpecBatch:
         # K2 starts under K3 (SPECDEC_OVERLAP_PREV; serial launch order only)
         self.overlap = bool(int(os.environ.get("SPECDEC_OVERLAP", "1")))
         self._graphs = {}
+        # launch the round through the native driver (specdec_eqspec_round: one C call for
+        # K1 -> K3 -> K2) instead of the three calls from Python; same kernels, same order
+        self.native_round = False
 
     # ----------------------------------------------------------------- state I/O
     def load(self, tokens, lengths, kv=None):
@@ -238,11 +242,102 @@ class EqSpecBatch:
         per_cache = 2 if self.segment and self.kv_mode == "inplace" else 1
         return 2 + per_cache * (2 if self.dkv is not None else 1)
 
+    # ----------------------------------------------------------------- native round driver
+    def round_desc(self, logits):
+        """The `specdec_round_desc` of this batch for logits shaped like `logits`
+        [B, k+1, >= V] (specdec_eqspec_round / specdec_eqspec_round_host).  The anchored
+        origin (f3) is not part of the native driver."""
+        if self.anchor is not None:
+            raise ValueError("the native round driver does not take the anchored origin (f3)")
+        key = (logits.stride(1), logits.dtype, self.V or logits.shape[2])
+        if getattr(self, "_rdesc_key", None) == key:
+            d = self._rdesc
+        else:
+            p = lambda t: None if t is None else t.data_ptr()
+            two = lambda a, b: (ctypes.c_void_p * 2)(p(a), p(b))
+            d = _abi.RoundDesc()
+            d.B, d.k, d.V, d.logit_stride = self.B, self.k, key[2], key[0]
+            d.logit_dtype = _abi.DTYPE[logits.dtype]
+            d.eos_id, d.pad_id = self.eos_id, self.pad_id
+            d.n, d.pad, d.tokens = two(self.n[0], self.n[1]), two(self.pad[0], self.pad[1]), two(self.tok[0], self.tok[1])
+            d.cap_tok = self.tok.shape[2]
+            d.mask, d.pos, d.mp_stride = p(self.mask), p(self.pos), self.mask.stride(0)
+            d.active, d.budget = p(self.active), p(self.budget)
+            d.gen = p(self.gen) if self.out_buf is not None else None
+            d.out_buf, d.max_new = p(self.out_buf), self.max_new
+            d.accept = two(self._accept[0], self._accept[1])
+            d.emit = two(self._emit[0], self._emit[1])
+            d.bonus = two(self._bonus[0], self._bonus[1])
+            d.finished = two(self._finished[0], self._finished[1])
+            d.pred, d.kept, d.plan_L, d.kept_draft = p(self.pred), p(self.kept), p(self.plan_L), p(self.kept_draft)
+            d.ws, d.ws_bytes = p(self.ws), self.ws.numel() * 8
+            d.status, d.moved = p(self.status), p(self.moved)
+            kb = self._kvbuf
+            d.kv = two(kb[0], kb[-1])
+            d.kv_dtype = _abi.DTYPE[kb[0].dtype]
+            d.n_planes, d.H, d.D, d.cap_kv = self.n_planes, self.H, self.D, self.cap_phys
+            d.s_plane, d.s_row, d.s_head = kb[0].stride()[:3]
+            if self._dkvbuf is not None:
+                db = self._dkvbuf
+                d.dkv = two(db[0], db[-1])
+                d.d_planes, d.d_H, d.d_D = self.d_dims
+                d.d_s_plane, d.d_s_row, d.d_s_head = db[0].stride()[:3]
+            self._rdesc, self._rdesc_key = d, key
+        d.realign_flags = ((_abi.ZERO_PADS if self.zero_pads else 0)
+                           | (_abi.OVERLAP_PREV if self.overlap else 0))
+        d.realign_ws = self.rws.data_ptr() if self.segment else None
+        d.realign_ws_bytes = self.rws.numel() if self.segment else 0
+        return d
+
+    def launch_round_native(self, logits, draft, stream=None):
+        """The same round through the native driver (one C call, specdec_eqspec_round)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._last = self.cur
+        _abi.specdec_eqspec_round(self.round_desc(logits), self.cur, logits, draft, s)
+
+    def host_io(self, like_logits, like_draft):
+        """Device staging (two slots), copy / D2H streams and events for step_host: the
+        end-to-end round from pinned host inputs (specdec_eqspec_round_host)."""
+        io = _abi.HostIO()
+        self._io_lg = [torch.empty_like(like_logits, device=self.device) for _ in range(2)]
+        self._io_dr = [torch.empty_like(like_draft, device=self.device) for _ in range(2)]
+        self._io_streams = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
+        self._io_events = [torch.cuda.Event() for _ in range(6)]
+        cur = torch.cuda.current_stream(self.device)
+        for e in self._io_events:          # materialise the handles (recorded once, idle)
+            e.record(cur)
+        two = lambda a, b: (ctypes.c_void_p * 2)(a, b)
+        io.d_logits = two(self._io_lg[0].data_ptr(), self._io_lg[1].data_ptr())
+        io.d_draft = two(self._io_dr[0].data_ptr(), self._io_dr[1].data_ptr())
+        io.copy_stream = self._io_streams[0].cuda_stream
+        io.d2h_stream = self._io_streams[1].cuda_stream
+        ev = [e.cuda_event for e in self._io_events]
+        io.ev_ready, io.ev_done, io.ev_fetched = two(ev[0], ev[1]), two(ev[2], ev[3]), two(ev[4], ev[5])
+        self._io, self._io_slot = io, 0
+        return io
+
+    def step_host(self, h_logits, h_draft, h_emit=None, V=None, zero_pads=False, stream=None):
+        """One round from pinned host logits [B, k+1, >= V] / drafts [B, k]: H2D, the round
+        and (if h_emit) the D2H of the emitted counts, all enqueued by one C call
+        (specdec_eqspec_round_host); alternates the staging slot and flips the parity."""
+        self.V, self.zero_pads = V, zero_pads
+        if getattr(self, "_io", None) is None:
+            self.host_io(h_logits, h_draft)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._last = self.cur
+        _abi.specdec_eqspec_round_host(self.round_desc(h_logits), self._io, self.cur, self._io_slot,
+                                       h_logits, h_draft, h_emit, s)
+        self._io_slot ^= 1
+        self.cur = 1 - self.cur
+
     def launch_round(self, logits, draft, stream=None):
         """Enqueue K1 -> {K3 || K2} for the current parity (does not flip it).  K3 (tokens,
         masks, positions) and K2 (KV) both depend only on K1's plan and touch disjoint
         memory, so with `fork` K3 runs on a side stream under K2."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if self.native_round and not self.fork and self.anchor is None:
+            self.launch_round_native(logits, draft, s)
+            return
         if not self.fork:
             self.verify(logits, draft, s)
             self.repad(draft, s)

@@ -93,18 +93,21 @@ def test_missing_library_fails_loudly(tmp_path):
         _abi._lib = saved
 
 
-def test_pool_desc_layout_matches_header(tmp_path):
-    """The ctypes mirror of specdec_pool_desc has the C compiler's size and offsets."""
+@pytest.mark.parametrize("cname,pyname", [("specdec_pool_desc", "PoolDesc"),
+                                           ("specdec_round_desc", "RoundDesc"),
+                                           ("specdec_host_io", "HostIO")])
+def test_desc_layout_matches_header(tmp_path, cname, pyname):
+    """The ctypes mirrors of the descriptor structs have the C compiler's size and offsets."""
     import shutil
     import subprocess
     if not shutil.which("g++"):
         pytest.skip("no host C++ compiler")
     src = tmp_path / "l.cpp"
-    P = _abi.PoolDesc
+    P = getattr(_abi, pyname)
     names = [f[0] for f in P._fields_]
-    body = "".join(f' printf("%zu\\n", offsetof(specdec_pool_desc, {n}));' for n in names)
+    body = "".join(f' printf("%zu\\n", offsetof({cname}, {n}));' for n in names)
     src.write_text('#include <cstdio>\n#include <cstddef>\n#include "specdec.h"\n'
-                   'int main(){printf("%zu\\n", sizeof(specdec_pool_desc));' + body + '}\n')
+                   'int main(){printf("%zu\\n", sizeof(' + cname + '));' + body + '}\n')
     exe = tmp_path / "l"
     subprocess.run(["g++", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()))

@@ -16,7 +16,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos_id=-1,
-                zero_pads=False, full_check=True, anchor_slack=0, kv_mode="inplace"):
+                zero_pads=False, full_check=True, anchor_slack=0, kv_mode="inplace", drive="python"):
+    """drive: "python" (the three calls from eqspec.py), "native" (specdec_eqspec_round)
+    or "host" (specdec_eqspec_round_host from pinned host logits / drafts)."""
     k, V = shape.k, shape.V
     cap = W.derive_cap(shape.with_(B=B), rounds)
     lengths = W.gen_lengths(shape, seed, B)
@@ -27,6 +29,8 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
                      max_new=max_new, eos_id=eos_id, pad_id=W.PAD_ID, anchor_slack=anchor_slack,
                      kv_mode=kv_mode)
     bt.load(tokens, lengths, bits_to_torch(kv_bits, shape.kv_dtype, cuda))
+    bt.native_round = drive == "native"
+    h_emit = torch.zeros(B, dtype=torch.int32).pin_memory() if drive == "host" else None
     base_o = anchor_slack
     bases = []
     # oracle state
@@ -50,7 +54,11 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
         bits = W.gen_logits_np(seed, r, B, k, V, shape.logit_dtype)
         lg = padded_logits(bits, shape.logit_dtype, cuda, extra=16)
         draft = torch.from_numpy(rt.draft).to(cuda)
-        bt.step(lg, draft, V=V, zero_pads=zero_pads)
+        if drive == "host":
+            bt.step_host(lg.cpu().pin_memory(), torch.from_numpy(rt.draft).pin_memory(), h_emit,
+                         V=V, zero_pads=zero_pads)
+        else:
+            bt.step(lg, draft, V=V, zero_pads=zero_pads)
         # oracle
         budget = None if not max_new else (max_new - gen_o)
         v = OV.batch_verify(bits, shape.logit_dtype, rt.draft, n_o, pad_o, act_o, eos_id, budget, W.PAD_ID)
@@ -79,6 +87,8 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
         for key, g in (("accept", bt.accept), ("bonus", bt.bonus), ("emit", bt.emit),
                        ("finished", bt.finished), ("kept", bt.kept)):
             assert np.array_equal(g.cpu().numpy(), v[key]), (r, key)
+        if h_emit is not None:
+            assert np.array_equal(h_emit.numpy(), v["emit"]), r     # the D2H of the host call
         Ln = v["L_new"]
         assert int(bt.plan_L.item()) == Ln
         assert np.array_equal(bt.pad_cur.cpu().numpy(), v["pad_new"]), r
@@ -364,3 +374,19 @@ def test_full_size_sampled(cuda, name):
             assert np.array_equal(new[pn:pn + kp], old[po:po + kp]), (r, pl, i, h)
         n_o, pad_o = v["n_new"], v["pad_new"]
     assert int(bt.status.item()) == 0
+
+
+@pytest.mark.parametrize("drive", ["native", "host"])
+@pytest.mark.parametrize("pattern", ["alpha", "alternating", "all_k"])
+def test_rounds_native_driver(cuda, drive, pattern):
+    """specdec_eqspec_round (one C call per round) and specdec_eqspec_round_host (H2D +
+    round + D2H) against the oracle, like the Python-driven rounds."""
+    _run_rounds(cuda, SMALL, 8, 12, pattern, drive=drive)
+
+
+@pytest.mark.parametrize("drive", ["native", "host"])
+def test_rounds_native_driver_modes(cuda, drive):
+    _run_rounds(cuda, SMALL16, 5, 10, "alpha", seed=3, kv_mode="pingpong", drive=drive)
+    _run_rounds(cuda, W.SHAPES["toy"], 2, 30, "alpha", max_new=24, eos_id=7, drive=drive)
+    _run_rounds(cuda, SMALL, 1, 6, "alpha", drive=drive)
+    _run_rounds(cuda, SMALL, 6, 6, "one_zero", zero_pads=True, drive=drive)
