@@ -390,8 +390,8 @@ int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, v
  * of parity p (accept[p], ...), so a reader of round r's results (e.g. a D2H on another
  * stream) only has to finish before round r+2.  KV: kv[0] == kv[1] realigns in place;
  * two buffers ping-pong (round p reads kv[p], writes kv[1-p]).  B == 1 in place moves no
- * KV (a single row stays right-aligned): no realign launch.  The anchored
- * origin (f3) is driven from eqspec.py only (anchor fields are not part of this call).
+ * KV (a single row stays right-aligned): no realign launch (unless the
+ * anchored origin (f3) is on: then the realign follows K1's physical columns).
  * Errors: SPECDEC_ERR_ARG for a NULL desc / logits / draft or parity not 0/1; any error of
  * the three calls as is.
  */
@@ -432,6 +432,9 @@ typedef struct specdec_round_desc {
     uint32_t realign_flags;
     void *realign_ws;
     size_t realign_ws_bytes;
+    /* anchored origin (f3, see specdec_verify): anchor [1] in/out, NULL = off; the realign
+     * then moves KV from phys_old to phys_new columns (cap_kv is the physical capacity) */
+    int32_t *anchor, *phys_old, *phys_new;
 } specdec_round_desc;
 
 int specdec_eqspec_round(const specdec_round_desc *d, int parity, const void *d_logits,

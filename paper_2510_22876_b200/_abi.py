@@ -98,6 +98,7 @@ class RoundDesc(ctypes.Structure):
         ("dkv", _P2), ("d_planes", _I64), ("d_H", _I64), ("d_D", _I64),
         ("d_s_plane", _I64), ("d_s_row", _I64), ("d_s_head", _I64),
         ("realign_flags", _U32), ("realign_ws", _P), ("realign_ws_bytes", ctypes.c_size_t),
+        ("anchor", _P), ("phys_old", _P), ("phys_new", _P),
     ]
 
 

@@ -17,7 +17,8 @@ extern "C" int specdec_eqspec_round(const specdec_round_desc *d, int parity, con
     int rc = specdec_verify(d_logits, d->logit_dtype, d->B, d->k, d->V, d->logit_stride, d_draft,
                             d->n[c], d->active, d->eos_id, d->pad_id, d->budget, d->accept[c],
                             d->bonus[c], d->emit[c], d->finished[c], d->pred, d->plan_L, d->n[nx],
-                            d->pad[nx], d->kept, d->kept_draft, nullptr, 0, nullptr, nullptr,
+                            d->pad[nx], d->kept, d->kept_draft, d->anchor, d->anchor ? d->cap_kv : 0,
+                            d->phys_old, d->phys_new,
                             d->status, d->ws, d->ws_bytes, stream);
     if (rc) return rc;
     // K3: tokens' / mask / positions (+ output buffer)
@@ -29,20 +30,23 @@ extern "C" int specdec_eqspec_round(const specdec_round_desc *d, int parity, con
     if (rc) return rc;
     // K2: KV[p'_i + c] = KV[p_i + c], c < kept_i (target, then the draft model's cache)
     const bool inplace = d->kv[0] == d->kv[1];
-    if (d->B == 1 && inplace) return SPECDEC_OK;  // one row: p = p' = 0, nothing moves
+    if (d->B == 1 && inplace && !d->anchor) return SPECDEC_OK;  // one row: p = p' = 0, nothing moves
+    // source / destination columns: the pads, or K1's physical columns (anchored origin)
+    const int32_t *col_src = d->anchor ? d->phys_old : d->pad[c];
+    const int32_t *col_dst = d->anchor ? d->phys_new : d->pad[nx];
     const void *src = d->kv[inplace ? 0 : c];
     void *dst = d->kv[inplace ? 0 : nx];
     const uint32_t flags = d->realign_flags;
     rc = specdec_realign_kv(src, dst, d->kv_dtype, d->n_planes, d->B, d->H, d->D, d->s_plane, d->s_row,
-                            d->s_head, d->cap_kv, d->s_plane, d->s_row, d->s_head, d->cap_kv, d->pad[c], 0,
-                            d->pad[nx], 0, d->kept, 0, 0, nullptr, nullptr, flags, d->realign_ws,
+                            d->s_head, d->cap_kv, d->s_plane, d->s_row, d->s_head, d->cap_kv, col_src, 0,
+                            col_dst, 0, d->kept, 0, 0, nullptr, nullptr, flags, d->realign_ws,
                             d->realign_ws_bytes, d->moved, d->status, stream);
     if (rc || !d->dkv[0]) return rc;
     if (!d->kept_draft) return SPECDEC_ERR_ARG;
     const bool dinplace = d->dkv[0] == d->dkv[1];
     return specdec_realign_kv(d->dkv[dinplace ? 0 : c], d->dkv[dinplace ? 0 : nx], d->kv_dtype, d->d_planes,
                               d->B, d->d_H, d->d_D, d->d_s_plane, d->d_s_row, d->d_s_head, d->cap_kv,
-                              d->d_s_plane, d->d_s_row, d->d_s_head, d->cap_kv, d->pad[c], 0, d->pad[nx], 0,
+                              d->d_s_plane, d->d_s_row, d->d_s_head, d->cap_kv, col_src, 0, col_dst, 0,
                               d->kept_draft, 0, 0, nullptr, nullptr, flags & SPECDEC_ZERO_PADS,
                               d->realign_ws, d->realign_ws_bytes, d->moved, d->status, stream);
 }

@@ -245,10 +245,7 @@ class EqSpecBatch:
     # ----------------------------------------------------------------- native round driver
     def round_desc(self, logits):
         """The `specdec_round_desc` of this batch for logits shaped like `logits`
-        [B, k+1, >= V] (specdec_eqspec_round / specdec_eqspec_round_host).  The anchored
-        origin (f3) is not part of the native driver."""
-        if self.anchor is not None:
-            raise ValueError("the native round driver does not take the anchored origin (f3)")
+        [B, k+1, >= V] (specdec_eqspec_round / specdec_eqspec_round_host)."""
         key = (logits.stride(1), logits.dtype, self.V or logits.shape[2])
         if getattr(self, "_rdesc_key", None) == key:
             d = self._rdesc
@@ -282,6 +279,7 @@ class EqSpecBatch:
                 d.dkv = two(db[0], db[-1])
                 d.d_planes, d.d_H, d.d_D = self.d_dims
                 d.d_s_plane, d.d_s_row, d.d_s_head = db[0].stride()[:3]
+            d.anchor, d.phys_old, d.phys_new = p(self.anchor), p(self.phys_old), p(self.phys_new)
             self._rdesc, self._rdesc_key = d, key
         d.realign_flags = ((_abi.ZERO_PADS if self.zero_pads else 0)
                            | (_abi.OVERLAP_PREV if self.overlap else 0))
@@ -335,7 +333,7 @@ class EqSpecBatch:
         masks, positions) and K2 (KV) both depend only on K1's plan and touch disjoint
         memory, so with `fork` K3 runs on a side stream under K2."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        if self.native_round and not self.fork and self.anchor is None:
+        if self.native_round and not self.fork:
             self.launch_round_native(logits, draft, s)
             return
         if not self.fork:

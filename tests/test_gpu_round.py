@@ -390,3 +390,13 @@ def test_rounds_native_driver_modes(cuda, drive):
     _run_rounds(cuda, W.SHAPES["toy"], 2, 30, "alpha", max_new=24, eos_id=7, drive=drive)
     _run_rounds(cuda, SMALL, 1, 6, "alpha", drive=drive)
     _run_rounds(cuda, SMALL, 6, 6, "one_zero", zero_pads=True, drive=drive)
+
+
+@pytest.mark.parametrize("drive", ["native", "host"])
+def test_rounds_native_driver_anchored(cuda, drive):
+    """The round drivers with the anchored origin (f3): K1's physical columns drive K2."""
+    py = _run_rounds(cuda, SMALL, 8, 12, "alpha", seed=3, anchor_slack=96)
+    nat = _run_rounds(cuda, SMALL, 8, 12, "alpha", seed=3, anchor_slack=96, drive=drive)
+    assert nat["bases"] == py["bases"] and nat["moved"] == py["moved"]
+    _run_rounds(cuda, SMALL16, 6, 14, "alpha", seed=2, max_new=33, anchor_slack=32, drive=drive)
+    _run_rounds(cuda, SMALL, 1, 6, "alpha", anchor_slack=16, drive=drive)
