@@ -49,7 +49,9 @@ def parse():
     ap.add_argument("--pool-W", type=int, default=0, help="pool: window (0 = whole shard, <= 2048)")
     ap.add_argument("--min-group", type=int, default=2)
     ap.add_argument("--max-new", type=int, default=256)
-    ap.add_argument("--shard", default="band", choices=["band", "strided"])
+    ap.add_argument("--shard", default="balanced", choices=["band", "strided", "balanced"],
+                    help="pool sharding over ranks: equal-count bands, strided, or bands of "
+                         "equal estimated cost (prompt length + max_new per sequence)")
     ap.add_argument("--pool-consumer", default="zero-copy", choices=["zero-copy", "dense"],
                     help="pool: same-length batches run on the pool slots (zero-copy) or are "
                          "gathered into a dense staging rectangle too (PAPER.md:537)")
@@ -63,6 +65,8 @@ def parse():
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="pool, 1 GPU: drain each of G band shards alone and report the predicted "
                          "G-GPU throughput (slowest shard); a prediction, not a measurement")
+    ap.add_argument("--shard-c", type=float, default=1.0,
+                    help="--shard balanced: per-sequence weight = prompt length + c * max_new")
     ap.add_argument("--pool-mode", default="epoch", choices=["epoch", "alg3"],
                     help="epoch: run every batch of the window plan; alg3: batch 0 then re-plan")
     ap.add_argument("--B", type=int, default=0, help="override batch size")
@@ -554,14 +558,17 @@ def run_pool(args, rank, world, device, emulate=False):
     import torch
     import torch.distributed as dist
 
-    from paper_2510_22876_b200.dist import gather_results, shard_bands, shard_strided
+    from paper_2510_22876_b200.dist import gather_results, shard_balanced, shard_bands, shard_strided
     from paper_2510_22876_b200.exspec import SequencePool
 
     sh = W.SHAPES["qwen3"]
     k, V, B = sh.k, sh.V, sh.B
     N = args.pool_n
     lens, order = pool_workload(args)
-    shards = (shard_bands if args.shard == "band" else shard_strided)(order, world)
+    if args.shard == "balanced":
+        shards = shard_balanced(order, world, np.asarray(lens, np.float64) + args.shard_c * args.max_new)
+    else:
+        shards = (shard_bands if args.shard == "band" else shard_strided)(order, world)
     mine = shards[rank]
     n_loc = len(mine)
     cap = ((int(lens.max()) + args.max_new + k + 1) + 15) // 16 * 16

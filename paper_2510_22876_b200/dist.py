@@ -25,6 +25,21 @@ def shard_bands(order, world: int):
     return [order[cuts[g]:cuts[g + 1]].copy() for g in range(world)]
 
 
+def shard_balanced(order, world: int, weights):
+    """Contiguous bands of the admission order with equal total weight instead of equal
+    counts: band g ends at the first position whose cumulative weight reaches (g+1)/G of
+    the total.  With weights = a per-sequence cost estimate (bench.py: prompt length +
+    max_new -- KV bytes grow with the length, plus a per-sequence latency share), the
+    long-prompt bands get fewer sequences and the slowest rank finishes sooner."""
+    order = np.asarray(order)
+    w = np.asarray(weights, np.float64)[order]
+    cum = np.cumsum(w)
+    tot = cum[-1] if len(cum) else 0.0
+    cuts = [0] + [int(np.searchsorted(cum, tot * (g + 1) / world - 1e-9) + 1) for g in range(world - 1)] + [len(order)]
+    cuts = np.maximum.accumulate(np.minimum(cuts, len(order)))
+    return [order[cuts[g]:cuts[g + 1]].copy() for g in range(world)]
+
+
 def shard_strided(order, world: int):
     order = np.asarray(order)
     return [order[g::world].copy() for g in range(world)]

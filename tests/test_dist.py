@@ -11,7 +11,7 @@ import torch.multiprocessing as mp
 from oracle.loops import exspec_decode
 from oracle.pool import admission_order
 from oracle.toy_lm import ToyLM
-from paper_2510_22876_b200.dist import gather_results, shard_bands, shard_strided
+from paper_2510_22876_b200.dist import gather_results, shard_balanced, shard_bands, shard_strided
 
 MAX_NEW, K, CAP = 10, 3, 64
 
@@ -80,3 +80,18 @@ def test_gloo_world2_matches_single_process():
     got = [list(out[s, :gen[s]]) for s in range(len(prompts))]
     assert got == ref            # sharded EXSpec == per-sequence greedy, token for token
     assert cnt[0] > 0
+
+
+def test_balanced_bands():
+    """Equal-weight contiguous bands: a partition of the admission order, in order, whose
+    band weights differ by at most one element's weight."""
+    rng = np.random.default_rng(3)
+    for N, G in ((1024, 8), (37, 4), (5, 8), (8, 2)):
+        w = rng.integers(64, 512, N).astype(np.float64) + 256
+        order = np.argsort(w, kind="stable")
+        sh = shard_balanced(order, G, w)
+        assert len(sh) == G and np.array_equal(np.concatenate(sh), order)
+        tot = [w[s].sum() for s in sh if len(s)]
+        if N >= G:
+            assert max(tot) - min(tot) <= 2 * w.max()
+    assert [list(s) for s in shard_balanced(np.arange(4), 2, [1, 1, 1, 3])] == [[0, 1, 2], [3]]
