@@ -55,6 +55,8 @@ typedef struct CUstream_st *specdec_stream_t; /* == cudaStream_t */
 /* specdec_realign_kv flags */
 #define SPECDEC_ZERO_PADS 1u    /* also zero the old content columns that became pads */
 #define SPECDEC_OVERLAP_PREV 2u /* start under the previous kernel on the stream (see below) */
+#define SPECDEC_DYNAMIC 4u      /* dynamic work tickets from the workspace header (see below) */
+#define SPECDEC_SEGMENTED 8u    /* in place: cut slabs into segments (workspace slots) */
 
 /* ------------------------------------------------------------------------------ misc */
 int specdec_version(void);                /* ABI version (major*100 + minor) */
@@ -178,14 +180,23 @@ int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_tokens_out, 
  *   call's columns / counts / KV (e.g. specdec_rebuild_pos_mask right after
  *   specdec_verify) and that this call does not read what it writes.  The copy then
  *   starts while that kernel runs (programmatic dependent launch) and waits for it only
- *   before exiting, so completion order on the stream is unchanged.  Ignored with a
- *   workspace in place (the boundary-save kernel must finish first) and with PDL off.
- * d_ws / ws_bytes: optional device workspace of specdec_realign_workspace_size(dtype,
- *   n_planes, n_rows, H, D, cap_src) bytes (16-B aligned, contents don't-care).  With it,
- *   every slab is cut into ~128 KB segments that any CTA can stream independently: the
- *   rows a segment's neighbour overwrites in place (|dcol - scol| rows, <= 4 KB) are first
- *   copied to a workspace slot by a small kernel on the same stream.  NULL: one slab per
- *   CTA (correct, less balanced when few rows move).
+ *   before exiting, so completion order on the stream is unchanged.  Ignored with
+ *   SPECDEC_SEGMENTED in place (the boundary-save kernel must finish first) and with PDL
+ *   off.
+ *   SPECDEC_DYNAMIC: the streaming CTAs take work units from a ticket counter in the
+ *   workspace header instead of a static assignment, so CTAs that stream faster take more
+ *   units (measured +1 % at Qwen3 B=8, +1.2 % Vicuna).  Needs d_ws.
+ *   SPECDEC_SEGMENTED (in place): every slab is cut into ~128 KB segments that any CTA can
+ *   stream independently: the rows a segment's neighbour overwrites (|dcol - scol| rows,
+ *   <= 4 KB) are first copied to a workspace slot by a small kernel on the same stream.
+ *   Without it a slab is one unit in place (correct; less balanced when few rows move).
+ *   Needs d_ws.  Distinct buffers are always segmented (no slots needed).
+ * d_ws / ws_bytes: device workspace (16-B aligned) for SPECDEC_DYNAMIC / SPECDEC_SEGMENTED:
+ *   a 128-byte header -- the dynamic-schedule counters, which must be ZERO before the first
+ *   call and are left zero by every call -- then the segment slots.  Size: 128 bytes for
+ *   SPECDEC_DYNAMIC alone, specdec_realign_workspace_size(dtype, n_planes, n_rows, H, D,
+ *   cap_src) with SPECDEC_SEGMENTED.  Calls that share a workspace must not run
+ *   concurrently (stream-ordered calls are fine).  NULL: static assignment, no segments.
  * count_bound: the caller's upper bound on count[r] + count_add over all rows, or 0 for
  *   none (then cap_src).  Tight bounds let the host size the launch: slabs of at most
  *   4 KB (e.g. the pool write-back scatter, a + 1 <= k + 1 rows) are moved by a
@@ -427,8 +438,9 @@ typedef struct specdec_round_desc {
     /* draft-model KV (f1), same layout rules; dkv[0] == NULL: none */
     void *dkv[2];
     int64_t d_planes, d_H, d_D, d_s_plane, d_s_row, d_s_head;
-    /* realign: SPECDEC_ZERO_PADS / SPECDEC_OVERLAP_PREV for the target call; an optional
-     * segment workspace (specdec_realign_workspace_size) */
+    /* realign: SPECDEC_ZERO_PADS / SPECDEC_OVERLAP_PREV / SPECDEC_DYNAMIC /
+     * SPECDEC_SEGMENTED for the target call (the draft call takes all but OVERLAP_PREV);
+     * the workspace both calls share, stream-ordered (see specdec_realign_kv) */
     uint32_t realign_flags;
     void *realign_ws;
     size_t realign_ws_bytes;

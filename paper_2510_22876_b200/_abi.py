@@ -19,6 +19,8 @@ OK, ERR_ARG, ERR_SHAPE, ERR_DTYPE, ERR_CAPACITY, ERR_CUDA = 0, -1, -2, -3, -4, -
 ST_NAN, ST_CAPACITY, ST_KEPT, ST_BOUND = 1, 2, 4, 8
 ZERO_PADS = 1
 OVERLAP_PREV = 2
+DYNAMIC = 4
+SEGMENTED = 8
 DTYPE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 
 _P = ctypes.c_void_p

@@ -37,13 +37,15 @@ constexpr int kZeroBytes = 2048;
 constexpr int64_t kSegBytes = 128 * 1024;     // target bytes per work unit
 constexpr int64_t kSlotBytes = 4096;          // boundary slot: |shift| * row bytes <= this
 static int g_ctas_per_sm = 0;                 // tuning override (SPECDEC_REALIGN_CTAS)
-static int64_t g_grid_cap = 0;                // tuning override (SPECDEC_REALIGN_GRID): max CTAs
+static int64_t g_grid_cap = 0;
+constexpr int64_t kWsHeader = 128;            // workspace header: the dynamic-schedule counters                // tuning override (SPECDEC_REALIGN_GRID): max CTAs
 static int64_t g_seg_bytes = kSegBytes;       // tuning override (SPECDEC_REALIGN_SEG, >= default)
 
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 struct RealignParams {
+    unsigned int *sched;  // SPECDEC_DYNAMIC: [0] next unit ticket, [1] CTAs done (or null)
     const char *src;
     char *dst;
     int64_t n_planes, n_rows, H;
@@ -369,6 +371,19 @@ __device__ __forceinline__ void iter_unit(const RealignParams &p, const RealignS
     }
 }
 
+// SPECDEC_DYNAMIC: every CTA takes its next unit from a ticket counter in the caller's
+// workspace (one ticket prefetched, so the L2 round trip hides under the current unit):
+// CTAs that stream faster take more units and all finish within about one unit of each
+// other.  Each CTA reports once when done; the last one leaves both counters zero for
+// the next call, so a workspace is reusable by stream-ordered calls.
+__device__ __forceinline__ void dyn_done(const RealignParams &p) {
+    if (!p.sched) return;
+    if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+        atomicExch(p.sched, 0u);
+        atomicExch(p.sched + 1, 0u);
+    }
+}
+
 template <int STAGES, int CHUNK>
 __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem<STAGES, CHUNK> &sm) {
     const int lane = threadIdx.x;
@@ -381,15 +396,22 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
     }
     fence_proxy_async_smem();  // zero buffer (generic writes) visible to the bulk engine
     __syncwarp();
-    if (lane != 0 || sm.t.n_mv == 0) return;
+    if (lane != 0) return;
+    if (sm.t.n_mv == 0) { dyn_done(p); return; }
 
     const uint64_t pol = p.policy_mode == 0 ? policy_evict_first() : policy_evict_normal();
     ChunkIter it;
     it.n_units = p.n_planes * p.H * sm.t.units_per_ph;
     it.stride = gridDim.x;
     it.round = 0;
-    it.u = unit_of_round(0, blockIdx.x, it.stride);
-    if (it.u >= it.n_units) return;
+    unsigned int next_ticket = 0;
+    if (p.sched) {
+        it.u = atomicAdd(p.sched, 1u);
+        next_ticket = atomicAdd(p.sched, 1u);
+    } else {
+        it.u = unit_of_round(0, blockIdx.x, it.stride);
+    }
+    if (it.u >= it.n_units) { dyn_done(p); return; }
     iter_unit<STAGES, CHUNK>(p, sm, it);
     unsigned long long moved = 0;
 
@@ -429,7 +451,12 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
         mbar_arrive_expect_tx(&sm.bar[stage], static_cast<uint32_t>(nb));
         bulk_load(sm.ring[stage], src, static_cast<uint32_t>(nb), &sm.bar[stage], pol);
         if (last) {
-            it.u = unit_of_round(++it.round, blockIdx.x, it.stride);
+            if (p.sched) {
+                it.u = next_ticket;
+                if (it.u < it.n_units) next_ticket = atomicAdd(p.sched, 1u);
+            } else {
+                it.u = unit_of_round(++it.round, blockIdx.x, it.stride);
+            }
             if (it.u < it.n_units) iter_unit<STAGES, CHUNK>(p, sm, it);
         }
     };
@@ -465,6 +492,7 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
     }
     bulk_wait_all<0>();
     if (p.moved && moved) atomicAdd(p.moved, moved);
+    dyn_done(p);
 }
 
 template <int STAGES, int CHUNK>
@@ -552,7 +580,7 @@ extern "C" size_t specdec_realign_workspace_size(int dtype, int64_t n_planes, in
                                                  int64_t H, int64_t D, int64_t cap) {
     const int es = dtype_size(dtype);
     if (es == 0 || n_planes < 1 || n_rows < 1 || H < 1 || D < 1 || cap < 1) return 0;
-    return static_cast<size_t>(max_units_bound(n_planes, n_rows, H, D * es, cap)) * kSlotBytes;
+    return static_cast<size_t>(kWsHeader + max_units_bound(n_planes, n_rows, H, D * es, cap) * kSlotBytes);
 }
 
 extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtype, int64_t n_planes,
@@ -571,7 +599,8 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     if (!d_kv_src || !d_kv_dst || !d_count) return SPECDEC_ERR_ARG;
     if (n_planes < 1 || n_rows < 1 || H < 1 || D < 1 || cap_src < 1 || cap_dst < 1) return SPECDEC_ERR_SHAPE;
     if (n_rows > kRealignMaxRows) return SPECDEC_ERR_SHAPE;
-    if (flags & ~(SPECDEC_ZERO_PADS | SPECDEC_OVERLAP_PREV)) return SPECDEC_ERR_ARG;
+    if (flags & ~(SPECDEC_ZERO_PADS | SPECDEC_OVERLAP_PREV | SPECDEC_DYNAMIC | SPECDEC_SEGMENTED))
+        return SPECDEC_ERR_ARG;
     const int64_t rb = D * es;
     if (rb % 16 != 0 || !aligned16(d_kv_src) || !aligned16(d_kv_dst)) return SPECDEC_ERR_ARG;
     const int64_t st[6] = {src_s_plane, src_s_row, src_s_head, dst_s_plane, dst_s_row, dst_s_head};
@@ -584,7 +613,11 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     if ((flags & SPECDEC_ZERO_PADS) && !inplace) return SPECDEC_ERR_ARG;
     if (count_bound < 0) return SPECDEC_ERR_ARG;
     const int64_t units = max_units_bound(n_planes, n_rows, H, rb, cap_src);
-    if (d_ws && (!aligned16(d_ws) || ws_bytes < static_cast<size_t>(units) * kSlotBytes)) return SPECDEC_ERR_ARG;
+    const bool segmented = (flags & SPECDEC_SEGMENTED) && inplace;
+    if ((flags & (SPECDEC_DYNAMIC | SPECDEC_SEGMENTED)) && !d_ws) return SPECDEC_ERR_ARG;
+    if (d_ws && (!aligned16(d_ws) ||
+                 ws_bytes < static_cast<size_t>(kWsHeader + (segmented ? units * kSlotBytes : 0))))
+        return SPECDEC_ERR_ARG;
     RealignParams p;
     p.src = static_cast<const char *>(d_kv_src);
     p.dst = static_cast<char *>(d_kv_dst);
@@ -596,8 +629,10 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     p.src_col_add = src_col_add; p.dst_col_add = dst_col_add; p.count_add = count_add;
     p.count_bound = count_bound;
     p.flags = flags; p.inplace = inplace ? 1 : 0;
-    p.ws = static_cast<char *>(d_ws);
-    p.ws_slots = d_ws ? units : 0;
+    // in-place segmentation slots after the header (distinct buffers need none)
+    p.ws = segmented ? static_cast<char *>(d_ws) + kWsHeader : nullptr;
+    p.ws_slots = segmented ? units : 0;
+    p.sched = (flags & SPECDEC_DYNAMIC) ? static_cast<unsigned int *>(d_ws) : nullptr;
     p.moved = d_moved_bytes; p.status = d_status;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     // pipeline shape / L2 policy / CTAs per SM: tuning overrides for sweeps (tools/kbench.py)

@@ -47,7 +47,8 @@ extern "C" int specdec_eqspec_round(const specdec_round_desc *d, int parity, con
     return specdec_realign_kv(d->dkv[dinplace ? 0 : c], d->dkv[dinplace ? 0 : nx], d->kv_dtype, d->d_planes,
                               d->B, d->d_H, d->d_D, d->d_s_plane, d->d_s_row, d->d_s_head, d->cap_kv,
                               d->d_s_plane, d->d_s_row, d->d_s_head, d->cap_kv, col_src, 0, col_dst, 0,
-                              d->kept_draft, 0, 0, nullptr, nullptr, flags & SPECDEC_ZERO_PADS,
+                              d->kept_draft, 0, 0, nullptr, nullptr,
+                              flags & (SPECDEC_ZERO_PADS | SPECDEC_DYNAMIC | SPECDEC_SEGMENTED),
                               d->realign_ws, d->realign_ws_bytes, d->moved, d->status, stream);
 }
 

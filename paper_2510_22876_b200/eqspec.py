@@ -96,8 +96,10 @@ class EqSpecBatch:
         if self.dkv is not None:
             sizes.append(_abi.specdec_realign_workspace_size(self.dkv.dtype, *self.d_dims[:1], B,
                                                              *self.d_dims[1:], self.cap_phys))
-        self.rws = torch.empty(max(sizes), dtype=torch.uint8, device=dev)
+        self.rws = torch.zeros(max(sizes), dtype=torch.uint8, device=dev)   # header zero (specdec.h)
         self.segment = bool(int(os.environ.get("SPECDEC_SEGMENT", "0")))  # measured: profiles/r01
+        # K2 work tickets (SPECDEC_DYNAMIC) from rws's header: +1 % at Qwen3 B=8
+        self.dynamic = bool(int(os.environ.get("SPECDEC_DYNAMIC", "1")))
         self.V = None
         self.zero_pads = False
         # K3 on a side stream under K2: a small win for direct launches, a loss inside a
@@ -211,12 +213,16 @@ class EqSpecBatch:
         s = kv.stride()
         if self.zero_pads and kv_dst is not kv:
             raise ValueError("ZERO_PADS is an in-place option (ping-pong pads are don't-care, R8)")
-        flags = (_abi.ZERO_PADS if self.zero_pads else 0) | (_abi.OVERLAP_PREV if overlap else 0)
+        flags = (_abi.ZERO_PADS if self.zero_pads else 0) | (_abi.OVERLAP_PREV if overlap else 0) \
+            | self._ws_flags()
         _abi.specdec_realign_kv(kv, kv_dst, count, n_planes=planes, n_rows=self.B, H=H, D=D,
                                 src_strides=s[:3], dst_strides=s[:3], cap_src=self.cap_phys,
                                 cap_dst=self.cap_phys, src_col=src, dst_col=dst,
-                                flags=flags, ws=self.rws if self.segment else None,
+                                flags=flags, ws=self.rws if self._ws_flags() else None,
                                 moved_bytes=self.moved, status=self.status, stream=stream)
+
+    def _ws_flags(self) -> int:
+        return (_abi.SEGMENTED if self.segment else 0) | (_abi.DYNAMIC if self.dynamic else 0)
 
     def realign(self, stream=None):
         c, nx = self.cur, 1 - self.cur
@@ -282,9 +288,9 @@ class EqSpecBatch:
             d.anchor, d.phys_old, d.phys_new = p(self.anchor), p(self.phys_old), p(self.phys_new)
             self._rdesc, self._rdesc_key = d, key
         d.realign_flags = ((_abi.ZERO_PADS if self.zero_pads else 0)
-                           | (_abi.OVERLAP_PREV if self.overlap else 0))
-        d.realign_ws = self.rws.data_ptr() if self.segment else None
-        d.realign_ws_bytes = self.rws.numel() if self.segment else 0
+                           | (_abi.OVERLAP_PREV if self.overlap else 0) | self._ws_flags())
+        d.realign_ws = self.rws.data_ptr() if self._ws_flags() else None
+        d.realign_ws_bytes = self.rws.numel() if self._ws_flags() else 0
         return d
 
     def launch_round_native(self, logits, draft, stream=None):

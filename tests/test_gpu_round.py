@@ -170,7 +170,7 @@ def test_rounds_zero_pads(cuda):
 
 # ----------------------------------------------------------------------------- K2 alone
 def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, dtype="bf16", zero=False,
-                  seg=False, bound=0):
+                  seg=False, bound=0, dyn=False):
     B = len(kept)
     cap = cap or int(max(np.max(pad_old), np.max(pad_new)) + np.max(kept) + 4)
     shp = (planes, B, H, cap, D)
@@ -181,15 +181,24 @@ def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, 
     st = torch.zeros(1, dtype=torch.int32, device=cuda)
     s = kv.stride()
     ws = None
-    if seg:   # workspace -> slabs cut in ~128 KB segments with saved boundary rows
+    flags = _abi.ZERO_PADS if zero else 0
+    if seg:   # SEGMENTED: slabs cut in ~128 KB segments with saved boundary rows
         ws = torch.full((_abi.specdec_realign_workspace_size(kv.dtype, planes, B, H, D, cap),), 0xAB,
-                        dtype=torch.uint8, device=cuda)
+                        dtype=torch.uint8, device=cuda)          # slot contents are don't-care
+        flags |= _abi.SEGMENTED
+    if dyn:   # DYNAMIC: work tickets from the (zeroed) 128-byte header
+        if ws is None:
+            ws = torch.zeros(128, dtype=torch.uint8, device=cuda)
+        ws[:128] = 0
+        flags |= _abi.DYNAMIC
     _abi.specdec_realign_kv(kv, kv, t32(kept), n_planes=planes, n_rows=B, H=H, D=D,
                             src_strides=s[:3], dst_strides=s[:3], cap_src=cap, cap_dst=cap, ws=ws,
                             src_col=t32(pad_old), dst_col=t32(pad_new),
-                            flags=_abi.ZERO_PADS if zero else 0, moved_bytes=moved, status=st,
+                            flags=flags, moved_bytes=moved, status=st,
                             count_bound=bound)
     torch.cuda.synchronize()
+    if dyn:
+        assert not ws[:128].any(), "the schedule counters are left zero"
     g = torch_to_bits(kv)
     o, defined = OA.realign_kv(bits, pad_old, pad_new, kept)
     for i in range(B):
@@ -206,7 +215,8 @@ def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, 
 
 
 @pytest.mark.parametrize("D,dtype", [(128, "bf16"), (8, "bf16"), (64, "fp16"), (4, "fp32")])
-def test_realign_adversarial_shifts(cuda, D, dtype):
+@pytest.mark.parametrize("dyn", [False, True])
+def test_realign_adversarial_shifts(cuda, D, dtype, dyn):
     k = 5
     big = 700  # 700 rows x 256 B = 175 KB -> many 16 KB chunks
     cases = [
@@ -217,7 +227,7 @@ def test_realign_adversarial_shifts(cuda, D, dtype):
         ([1, 2, 3, 4], [2, 3, 4, 5], [1, 2, 3, 4]),            # tiny slabs
     ]
     for po, pn, kp in cases:
-        _realign_case(cuda, po, pn, kp, D=D, dtype=dtype)
+        _realign_case(cuda, po, pn, kp, D=D, dtype=dtype, dyn=dyn)
 
 
 @pytest.mark.parametrize("D,dtype", [(128, "bf16"), (64, "fp16"), (32, "fp32")])
@@ -237,11 +247,14 @@ def test_realign_segmented_in_place(cuda, D, dtype):
     ]
     for po, pn, kp in cases:
         _realign_case(cuda, po, pn, kp, D=D, H=2, dtype=dtype, seg=True)
+        _realign_case(cuda, po, pn, kp, D=D, H=2, dtype=dtype, seg=True, dyn=True)
     _realign_case(cuda, [0, 4, 0], [3, 4, 0], [long, 50, long], D=D, H=2, dtype=dtype, seg=True, zero=True)
 
 
 def test_realign_zero_pads_and_skips(cuda):
     _realign_case(cuda, [0, 4, 2, 0], [3, 4, 0, 9], [50, 0, 70, 1000], zero=True)
+    _realign_case(cuda, [0, 4, 2, 0], [3, 4, 0, 9], [50, 0, 70, 1000], zero=True, dyn=True)
+    _realign_case(cuda, [3, 3], [3, 3], [10, 10], dyn=True)      # nothing moves: every CTA exits early
 
 
 @pytest.mark.parametrize("D,dtype", [(128, "bf16"), (8, "fp16"), (16, "fp32")])

@@ -46,7 +46,8 @@ def main():
     ap.add_argument("--H", type=int, default=8)
     ap.add_argument("--cap", type=int, default=2304)
     ap.add_argument("--kept", type=int, default=2000)
-    ap.add_argument("--seg", action="store_true", help="pass a workspace (segmented slabs)")
+    ap.add_argument("--seg", action="store_true", help="SPECDEC_SEGMENTED (in-place segmented slabs)")
+    ap.add_argument("--dyn", action="store_true", help="SPECDEC_DYNAMIC (work tickets)")
     ap.add_argument("--gather", type=int, default=0,
                     help="EXSpec pool gather/scatter geometry instead: pool of N sequences")
     a = ap.parse_args()
@@ -65,13 +66,14 @@ def main():
     kept = [a.kept] * B
     slab = P * H * a.kept * D * 2
 
-    ws = torch.empty(_abi.specdec_realign_workspace_size(kv.dtype, P, B, H, D, cap), dtype=torch.uint8,
-                     device=dev) if a.seg else None
+    ws = torch.zeros(_abi.specdec_realign_workspace_size(kv.dtype, P, B, H, D, cap), dtype=torch.uint8,
+                     device=dev) if (a.seg or a.dyn) else None
+    kflags = (_abi.SEGMENTED if a.seg else 0) | (_abi.DYNAMIC if a.dyn else 0)
 
     def k2(src, dst, po, pn, kp):
         _abi.specdec_realign_kv(src, dst, i32(kp), n_planes=P, n_rows=B, H=H, D=D, src_strides=s,
                                 dst_strides=s, cap_src=cap, cap_dst=cap, src_col=i32(po), dst_col=i32(pn),
-                                ws=ws)
+                                ws=ws, flags=kflags)
 
     ms = timed(lambda: k2(kv, kv2, [0] * B, [0] * B, kept), a.reps)
     res["k2_oop"] = 2 * slab * B / ms / 1e6
