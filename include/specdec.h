@@ -384,6 +384,9 @@ typedef struct specdec_pool_desc {
     /* scheduling hints for the overlapped order (<= 0: 5500 GB/s, 10 us): the gather rate
      * and the duration of one batch verify; they change the order, never a result */
     double est_gather_GBps, est_verify_us;
+    /* optional >= 128-byte zeroed workspace: the fallback gathers take SPECDEC_DYNAMIC
+     * work tickets from it (they run one after another on one stream); NULL = static */
+    void *gather_ws;
 } specdec_pool_desc;
 
 int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,

@@ -77,6 +77,7 @@ class PoolDesc(ctypes.Structure):
         ("n_staging", _I32), ("staging_ring", _P), ("copy_stream", _P), ("events", _P),
         ("cur_staging", _P), ("accept_ring", _P),
         ("est_gather_GBps", ctypes.c_double), ("est_verify_us", ctypes.c_double),
+        ("gather_ws", _P),
     ]
 
 

@@ -116,8 +116,9 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         const int64_t o = static_cast<int64_t>(b) * B;
         return specdec_realign_kv(d->kv, stg(b), d->kv_dtype, d->n_planes, rows(b), d->H, d->D, p_plane,
                                   p_row, p_head, d->cap, s_plane, s_row, s_head, d->cap, nullptr, 0,
-                                  d->mpad + o, 0, d->mlen + o, -1, 0, d->members + o, nullptr, 0,
-                                  nullptr, 0, d->moved, d->status,
+                                  d->mpad + o, 0, d->mlen + o, -1, 0, d->members + o, nullptr,
+                                  d->gather_ws ? SPECDEC_DYNAMIC : 0u, d->gather_ws, d->gather_ws ? 128 : 0,
+                                  d->moved, d->status,
                                   reinterpret_cast<specdec_stream_t>(on));
     };
     // the first NS gathers: the plan is complete (host sync above) and so is every

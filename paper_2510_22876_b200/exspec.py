@@ -247,6 +247,9 @@ class SequencePool:
         d.ring_n = len(ring)
         d.ring_pos = ctypes.addressof(self._ring_pos)
         d.dense_consumer = 1 if self.dense_consumer else 0
+        # the gathers take K2 work tickets (SPECDEC_DYNAMIC) from a zeroed 128-byte header
+        self._gather_ws = torch.zeros(128, dtype=torch.uint8, device=self.device)
+        d.gather_ws = self._gather_ws.data_ptr()
         if self.n_staging >= 2:
             ns = self.n_staging
             self._copy_stream = torch.cuda.Stream(self.device)
