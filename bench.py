@@ -260,8 +260,13 @@ class RoundBench:
             self.reset_fast()
 
     def step(self, r, ev=None):
+        import torch
         bt, lg, d = self.bt, self.logits[r % RING], self.drafts[r % RING]
         if ev is not None:
+            # keep the GPU busy while Python enqueues this round, so that the event
+            # intervals hold kernel time only (short rounds: no host launch gaps)
+            with torch.cuda.stream(self.stream):
+                torch.cuda._sleep(SLEEP_CYCLES)
             ev[0].record(self.stream)
         bt.verify(lg, d)
         if ev is not None:

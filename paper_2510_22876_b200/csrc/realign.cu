@@ -544,6 +544,10 @@ int launch_realign(const RealignParams &p, int64_t max_units, cudaStream_t s) {
     }
     RealignParams pm = p;
     if (p.ws && p.inplace) pm.flags &= ~SPECDEC_OVERLAP_PREV;  // must wait for the boundary slots
+    // dynamic tickets pay an L2 round trip before the first unit and at exit: with fewer
+    // than ~8 units per CTA the static rotation is as balanced and faster (measured: toy
+    // rounds 12.2 vs 10.6 us, Qwen3 B=2 -0.6 %; B >= 4 and GLM/Vicuna gain 0.4-1.2 %)
+    if (max_units < 8 * grid) pm.sched = nullptr;
     // One streaming CTA per SM is enforced through shared memory, not left to the CTA
     // scheduler: launched early under PDL, a persistent grid could otherwise double up on
     // the SMs that are free first (measured -5..7 % before this).

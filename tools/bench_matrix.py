@@ -31,11 +31,19 @@ POOL = (
     + [(f"P N1024 W{w}", ["--config", "pool", "--pool-W", str(w)]) for w in (8, 16, 32)]
     + [("P N1024 min_group 8", ["--config", "pool", "--min-group", "8"]),
        ("P N1024 alg3", ["--config", "pool", "--pool-mode", "alg3"]),
-       ("P N1024 dense consumer", ["--config", "pool", "--pool-consumer", "dense"])]
+       ("P N1024 dense consumer", ["--config", "pool", "--pool-consumer", "dense"]),
+       ("P N1024 serial executor", ["--config", "pool", "--pool-staging", "1"]),
+       ("P N1024 emul x8 count bands", ["--config", "pool", "--emulate-ranks", "8", "--shard", "band"])]
+    + [(f"P N1024 emulated x{g}", ["--config", "pool", "--emulate-ranks", str(g)]) for g in (2, 4, 8)]
 )
 
 
 def summary(label, d):
+    if "emulated" in d:
+        e = d["emulated"]
+        return (f"{label:26s} {d['value']:10.1f} seq/s predicted (slowest of {e['ranks']} shards, each drained "
+                f"alone)  per-rank ms {[round(x, 1) for x in e['per_rank_ms']]}  max/mean "
+                f"{e['imbalance_max_over_mean']:.3f}")
     if "pool" in d:
         p = d["pool"]
         return (f"{label:26s} {d['value']:10.1f} seq/s  grouping {p['grouping_rate']:.3f}  "
