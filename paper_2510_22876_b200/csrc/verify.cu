@@ -64,7 +64,10 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 }
 
 // ----------------------------------------------------------------------------- epilogue
-__device__ void verify_epilogue(const VerifyParams &p) {
+// pre_sq: the pool sequence of this warp's first row (pool mode), loaded before the
+// arrival so that the row's pool length / generated count loads issue together with the
+// key loads instead of one dependent round trip later.
+__device__ void verify_epilogue(const VerifyParams &p, int32_t pre_sq) {
     __shared__ int s_red[kVerifyThreads / kWarp];
     __shared__ int s_nmax[kVerifyThreads / kWarp];
     __shared__ unsigned long long s_w[kMaxK + 1];  // f3: kept rows per accept class
@@ -84,6 +87,8 @@ __device__ void verify_epilogue(const VerifyParams &p) {
         const unsigned long long key = lane < K1 ? __ldcg(p.ws_keys + i * K1 + lane) : 0ull;
         const int64_t d = lane < k ? p.draft[i * k + lane] : -1;
         const int32_t bud_i = p.budget ? p.budget[i] : 0;
+        const int32_t sq = p.wb_members ? (i == warp ? pre_sq : p.wb_members[i]) : -1;
+        const int32_t wb_len0 = sq >= 0 ? p.wb_len[sq] : 0, wb_gen0 = sq >= 0 ? p.wb_gen[sq] : 0;
         const bool act = act_b != 0;
         local_nmax = max(local_nmax, n_i);  // old width L = max n (R6 held last round)
         int a = 0, m = 0, nn = 1, kp = 0;
@@ -121,9 +126,8 @@ __device__ void verify_epilogue(const VerifyParams &p) {
             // Alg. 3 Phase 4, as specdec_pool_writeback: E cut to the
             // sequence's remaining budget, appended to its pool tokens / output, len and gen
             // advanced, deactivated when finished
-            const int32_t sq = p.wb_members[i];
             if (sq >= 0) {
-                const int32_t len = p.wb_len[sq], g = p.wb_gen[sq];
+                const int32_t len = wb_len0, g = wb_gen0;
                 const int32_t em = min(m, static_cast<int32_t>(max(static_cast<int64_t>(0), p.wb_max_new - g)));
                 const bool fin2 = fin || g + em >= p.wb_max_new;
                 if (p.wb_tokens && len + em > p.wb_cap_tok) {
@@ -217,6 +221,10 @@ __device__ void verify_epilogue(const VerifyParams &p) {
 // Arrival on the grid-wide counter; the last CTA runs the epilogue.
 __device__ __forceinline__ void arrive_and_maybe_finish(const VerifyParams &p, int *s_last) {
     if (p.exp == 1) return;  // timing experiment only (tools/k1bench.py): argmax without epilogue
+    // pool mode: every warp loads its first row's pool sequence now (not written by this
+    // grid), under the arrival round trip; only the last CTA uses it
+    const int32_t w = static_cast<int32_t>(threadIdx.x >> 5);
+    const int32_t pre_sq = (p.wb_members && w < p.B) ? p.wb_members[w] : -1;
     if (threadIdx.x == 0) {
         // acq_rel: releases this CTA's key atomicMax (same thread, cta_merge) and, in the
         // last CTA, acquires every other CTA's -- no separate sequentially-consistent fences
@@ -227,7 +235,7 @@ __device__ __forceinline__ void arrive_and_maybe_finish(const VerifyParams &p, i
     }
     __syncthreads();
     if (!*s_last) return;
-    verify_epilogue(p);
+    verify_epilogue(p, pre_sq);
 }
 
 __device__ __forceinline__ void cta_merge(const VerifyParams &p, int64_t row, unsigned long long best,
