@@ -292,8 +292,10 @@ int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, int64_t k, i
 /* ------------------------------------------------------------------------------ a4 + a5
  * specdec_pool_epoch -- native EXSpec epoch executor (Alg. 3): the
  * host-side launch loop of one epoch in C++ instead of one Python call per kernel.
- *   specdec_pool_group over the window; ONE device->host copy of the plan header (the
- *   epoch's only host synchronisation); then for each of the first `max_batches` planned
+ *   specdec_pool_group over the window; a device->host copy of the plan header (the
+ *   epoch's only host synchronisation: ONE copy if n_batches, bkind, blen and bsize are laid
+ *   out like host_header in one buffer -- bkind's W bytes in the W int32 slots after
+ *   n_batches, then blen, then bsize -- else four); then for each of the first `max_batches` planned
  *   batches (<= 0: all; 1: Alg. 3 as printed -- GetBatch, verify, write-back, re-plan):
  *     fallback batch: specdec_realign_kv gather (pool -> staging, right-aligned);
  *     inputs: `forward(ctx, b, same_length, width, &logits, &draft)` if non-NULL (the

@@ -40,11 +40,21 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     if (rc) return rc;
     // plan header -> pinned host: n_batches, kind, width, size (W each)
     int32_t *hh = d->host_header;
-    cudaError_t e = cudaMemcpyAsync(hh, d->n_batches, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hh + 1 + W, d->blen, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(hh + 1 + 2 * W, d->bsize, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(reinterpret_cast<uint8_t *>(hh + 1), d->bkind, W, cudaMemcpyDeviceToHost, s);
+    cudaError_t e;
+    // one copy when the four device arrays are laid out like host_header in one buffer
+    // (n_batches, bkind in the next W int32 slots, blen, bsize), else four
+    const bool packed = reinterpret_cast<const char *>(d->bkind) == reinterpret_cast<const char *>(d->n_batches + 1) &&
+                        d->blen == d->n_batches + 1 + W && d->bsize == d->n_batches + 1 + 2 * W;
+    if (packed) {
+        e = cudaMemcpyAsync(hh, d->n_batches, (1 + 3 * static_cast<size_t>(W)) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, s);
+    } else {
+        e = cudaMemcpyAsync(hh, d->n_batches, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hh + 1 + W, d->blen, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hh + 1 + 2 * W, d->bsize, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(reinterpret_cast<uint8_t *>(hh + 1), d->bkind, W, cudaMemcpyDeviceToHost, s);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return record_cuda_error(e);
     const int32_t nb = hh[0];

@@ -68,10 +68,13 @@ class SequencePool:
         self.mlen = torch.zeros((W, B), dtype=i32, device=dev)
         self.mpad = torch.zeros((W, B), dtype=i32, device=dev)
         self.mactive = torch.zeros((W, B), dtype=u8, device=dev)
-        self.bsize = torch.zeros(W, dtype=i32, device=dev)
-        self.bkind = torch.zeros(W, dtype=u8, device=dev)
-        self.blen = torch.zeros(W, dtype=i32, device=dev)
-        self.n_batches = torch.zeros(1, dtype=i32, device=dev)
+        # the plan header arrays share one buffer laid out like the pinned host header
+        # (n_batches | bkind in W int32 slots | blen | bsize): one D2H copy per epoch
+        self._hdr_dev = torch.zeros(1 + 3 * W, dtype=i32, device=dev)
+        self.n_batches = self._hdr_dev[0:1]
+        self.bkind = self._hdr_dev[1:1 + W].view(u8)[:W]
+        self.blen = self._hdr_dev[1 + W:1 + 2 * W]
+        self.bsize = self._hdr_dev[1 + 2 * W:1 + 3 * W]
         self.counters = torch.zeros(8, dtype=i64, device=dev)
         # per-batch verify scratch
         self.accept = torch.zeros(B, dtype=i32, device=dev)
