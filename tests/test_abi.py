@@ -140,3 +140,38 @@ int main(void) {
                     "-L", libdir, "-l:libspecdec.so", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
     assert out == ["100", str(_abi.ERR_ARG), str(8 * 6 * 8 + 16)]
+
+
+def test_host_validation_drivers_and_flags(lib):
+    """Argument errors of the realign flags, the round drivers and the pool executor's
+    overlap configuration are caught on the host (nothing launched, no GPU needed)."""
+    L = lib
+    nz = ctypes.c_void_p(16)
+    real = lambda flags, ws, wsb: L.specdec_realign_kv(nz, nz, 2, 2, 2, 2, 8, 64, 64, 64, 8, 64, 64, 64, 8,
+                                                       None, 0, None, 0, nz, 0, 0, None, None, flags, ws,
+                                                       wsb, None, None, None)
+    assert real(_abi.DYNAMIC, None, 0) == _abi.ERR_ARG          # tickets need the workspace header
+    assert real(_abi.SEGMENTED, None, 0) == _abi.ERR_ARG        # segment slots need a workspace
+    assert real(16, None, 0) == _abi.ERR_ARG                    # unknown flag
+    assert real(_abi.DYNAMIC, nz, 64) == _abi.ERR_ARG           # header is 128 bytes
+    d = _abi.RoundDesc()
+    assert L.specdec_eqspec_round(None, 0, nz, nz, None) == _abi.ERR_ARG
+    assert L.specdec_eqspec_round(ctypes.byref(d), 2, nz, nz, None) == _abi.ERR_ARG
+    assert L.specdec_eqspec_round(ctypes.byref(d), 0, None, nz, None) == _abi.ERR_ARG
+    io = _abi.HostIO()
+    assert L.specdec_eqspec_round_host(ctypes.byref(d), None, 0, 0, nz, nz, None, None) == _abi.ERR_ARG
+    assert L.specdec_eqspec_round_host(ctypes.byref(d), ctypes.byref(io), 0, 2, nz, nz, None, None) == _abi.ERR_ARG
+    assert L.specdec_eqspec_round_host(ctypes.byref(d), ctypes.byref(io), 0, 0, nz, nz, None, None) == _abi.ERR_ARG
+    p = _abi.PoolDesc()
+    p.host_header, p.W, p.B = 16, 4, 2
+    p.logits_ring, p.draft_ring, p.ring_n, p.ring_pos = 16, 16, 1, 16
+    p.n_staging = 2                                              # overlap without ring / stream / events
+    assert L.specdec_pool_epoch(ctypes.byref(p), None, None, 0, None, None, None, None, None) == _abi.ERR_ARG
+    assert L.specdec_pool_epoch(None, None, None, 0, None, None, None, None, None) == _abi.ERR_ARG
+
+
+def test_host_round_binding_rejects_unpinned(lib):
+    """specdec_eqspec_round_host's binding takes pinned host tensors only (no silent sync copy)."""
+    import torch
+    with pytest.raises(_abi.SpecdecError):
+        _abi.specdec_eqspec_round_host(_abi.RoundDesc(), _abi.HostIO(), 0, 0, torch.zeros(4), torch.zeros(4))
