@@ -85,9 +85,10 @@ def parse():
                     help="f1: the draft model keeps its own KV cache, realigned every round too")
     ap.add_argument("--kv-mode", default="inplace", choices=["inplace", "pingpong"],
                     help="K2 in place, or out of place between two KV buffers (copies Delta=0 rows too)")
-    ap.add_argument("--round-mode", default="graph-serial",
-                    choices=["graph-fork", "graph-serial", "direct-fork", "direct-serial"],
-                    help="value region: CUDA-graph replay or direct launches; K3 forked under K2 or serial")
+    ap.add_argument("--round-mode", default="graph-block",
+                    choices=["graph-block", "graph-fork", "graph-serial", "direct-fork", "direct-serial"],
+                    help="value region: CUDA graphs of one episode of rounds (block), one graph per "
+                         "round, or direct launches; K3 forked under K2 or serial")
     return ap.parse_args()
 
 
@@ -318,6 +319,24 @@ def run_ours(args, rank, world, device):
     bt.V = sh.V
     if use_graph:
         bt.capture(list(zip(rb.logits, rb.drafts)), V=sh.V)
+    # graph-block: one CUDA graph per episode -- the episode's state reset (3 device copies)
+    # and its `episode` rounds (ring slot r % RING, parity alternating; an even count, so the
+    # graph ends at the parity it starts from) -- so short rounds are not bound by one host
+    # replay call each.  Same kernels, same order, same bytes as the per-round graphs.
+    block = None
+    blk = args.episode
+    if args.round_mode == "graph-block" and blk and blk % RING == 0 and blk % 2 == 0:
+        rb.reset()
+        cs = torch.cuda.Stream(device)
+        cs.wait_stream(rb.stream)
+        block = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cs), torch.cuda.graph(block, stream=cs):
+            rb.reset_fast()
+            for r in range(blk):
+                bt.launch_round(rb.logits[r % RING], rb.drafts[r % RING], stream=cs)
+                bt.cur = 1 - bt.cur
+        rb.stream.wait_stream(cs)
+        torch.cuda.synchronize()
 
     def one_round(r):
         if use_graph:
@@ -326,6 +345,17 @@ def run_ours(args, rank, world, device):
             bt.launch_round(rb.logits[r % RING], rb.drafts[r % RING])
             bt.cur = 1 - bt.cur
 
+    def run_rounds(n):
+        r = 0
+        if block is not None:
+            while r + blk <= n:
+                block.replay()           # reset + blk rounds; bt.cur is back where it started
+                bt._last = 1 - bt.cur
+                r += blk
+        for q in range(r, n):
+            rb.episode(q, args.episode)
+            one_round(q)
+
     def sync():
         if world > 1:
             dist.barrier()
@@ -333,9 +363,7 @@ def run_ours(args, rank, world, device):
 
     # ---- A: value (graphs)
     rb.reset()
-    for r in range(args.warmup):
-        rb.episode(r, args.episode)
-        one_round(r)
+    run_rounds(args.warmup)
     rb.reset()
     moved0 = int(bt.moved.item())
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -343,9 +371,7 @@ def run_ours(args, rank, world, device):
     clocks = ClockSampler(device.index if device.index is not None else 0)
     with clocks:
         t0.record(rb.stream)
-        for r in range(args.steps):
-            rb.episode(r, args.episode)
-            one_round(r)
+        run_rounds(args.steps)
         t1.record(rb.stream)
         torch.cuda.synchronize()
     sync()
@@ -892,7 +918,10 @@ def main():
             "clocks": res["clocks"],
             "e2e": res["e2e"],
             "gpu_launches": res["kernels_per_round"] * args.steps,
-            "launch_mode": args.round_mode + " (graph: one CUDA graph per (parity, ring slot), 3 kernels per replay)",
+            "launch_mode": args.round_mode + (f" (one CUDA graph per {args.episode}-round episode: the "
+                                              f"episode's state reset + its rounds; remainder rounds from "
+                                              f"per-round graphs)" if args.round_mode == "graph-block" else
+                                              " (graph: one CUDA graph per (parity, ring slot), 3 kernels per replay)"),
             "bytes_moved_check": {"value_region": res["moved_A"], "kernel_region": res["copied"]},
             "status": res["status"],
             "cpu_baseline": cpu,
