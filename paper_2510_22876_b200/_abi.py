@@ -117,15 +117,25 @@ def specdec_eqspec_round(desc: RoundDesc, parity, logits, draft, stream=None):
                                        _stream(stream)), "specdec_eqspec_round")
 
 
+_PINNED_OK: set = set()   # (data_ptr, nbytes) of host buffers already checked to be pinned
+
+
 def specdec_eqspec_round_host(desc: RoundDesc, io: HostIO, parity, slot, h_logits, h_draft,
                               h_emit=None, stream=None):
     """One EqSpec round from pinned HOST logits / drafts (H2D + round + D2H of emit)."""
-    hp = lambda t: None if t is None else t.data_ptr()
+    ptrs = []
     for t in (h_logits, h_draft, h_emit):
-        if t is not None and (t.is_cuda or not t.is_pinned()):
-            raise SpecdecError("pinned host tensor expected")
+        if t is None:
+            ptrs.append(None)
+            continue
+        key = (t.data_ptr(), t.numel() * t.element_size())
+        if key not in _PINNED_OK:    # the pinned check costs a driver query: once per buffer
+            if t.is_cuda or not t.is_pinned():
+                raise SpecdecError("pinned host tensor expected")
+            _PINNED_OK.add(key)
+        ptrs.append(key[0])
     _check(load().specdec_eqspec_round_host(ctypes.byref(desc), ctypes.byref(io), parity, slot,
-                                            hp(h_logits), hp(h_draft), hp(h_emit), _stream(stream)),
+                                            ptrs[0], ptrs[1], ptrs[2], _stream(stream)),
            "specdec_eqspec_round_host")
 
 

@@ -12,6 +12,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "repad_cols.cuh"
 #include "host_util.h"
 
 namespace specdec {
@@ -37,10 +38,6 @@ struct RepadParams {
     uint32_t *status;
 };
 
-// E_i[t] for t < emit_i: draft tokens, then the bonus
-__device__ __forceinline__ int64_t emitted_token(const int64_t *d, int32_t a, int64_t b, int t) {
-    return t < a ? d[t] : b;
-}
 
 __global__ void __launch_bounds__(kRepadThreads) repad_kernel(RepadParams p) {
     pdl_wait();
@@ -155,17 +152,7 @@ __global__ void __launch_bounds__(kRepadThreads) repad_gather_kernel(RepadParams
     for (int u = 0; u < kRepadCols; ++u) {
         const int c = c0 + u * kRepadThreads;
         if (c >= W) break;
-        const bool content = c >= pn;
-        mrow[c] = content ? 1 : 0;
-        prow[c] = content ? c - pn : 0;
-        if (c < Lnew) {
-            int64_t t = p.pad_id;           // pads, and the dummy row of a finished row (R9)
-            if (!fin && content) {
-                const int32_t j = c - pn;
-                t = j < n ? src[po + j] : emitted_token(d, a, b, j - n);
-            }
-            dst[c] = t;
-        }
+        repad_col(c, Lnew, pn, fin, po, n, src, dst, mrow, prow, d, a, b, p.pad_id);
     }
 }
 

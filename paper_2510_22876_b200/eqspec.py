@@ -109,8 +109,9 @@ class EqSpecBatch:
         self.overlap = bool(int(os.environ.get("SPECDEC_OVERLAP", "1")))
         self._graphs = {}
         # launch the round through the native driver (specdec_eqspec_round: one C call for
-        # K1 -> K3 -> K2) instead of the three calls from Python; same kernels, same order
-        self.native_round = False
+        # K1 -> K3 -> K2; default) or as the three calls from Python (False); same kernels,
+        # same order, same results
+        self.native_round = True
 
     # ----------------------------------------------------------------- state I/O
     def load(self, tokens, lengths, kv=None):

@@ -44,6 +44,8 @@ def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, dr
                      draft=None if drafter is None else (LAYERS, H, D), anchor_slack=anchor_slack,
                      kv_mode=kv_mode)
     bt.load(tokens, [len(p) for p in prompts])
+    if fault is not None:
+        bt.native_round = False    # the faults patch the Python-side calls of the round
     if fault == "skip_kv_realign":             # DSD error (iii): KV not realigned
         bt.realign = lambda stream=None: None
     if fault == "bonus_from_draft":            # DSD error (i): bonus from the draft
