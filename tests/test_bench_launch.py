@@ -53,3 +53,32 @@ def test_two_ranks_share_one_gpu(config):
         assert d["scaling"] == "strong"
     else:
         assert d["scaling"] == "weak" and d["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_default_line_has_the_contract_keys():
+    """`python bench.py` (N=1) prints one JSON line with every key the driver reads:
+    value / unit / timing fields, roofline (bound, achieved, peak, unit, frac, traffic),
+    cpu_baseline (oracle), e2e (host-buffer copies counted), gpu_launches, clocks."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "6", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
+                "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 6 and d["warmup"] == 3 and d["higher_is_better"] is True
+    assert d["config"]["workload"] and d["data"] == "synthetic" and d["dtype"] == "bf16"
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and rf["peak"] > 0
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9 and 0.5 < rf["frac"] < 1.2
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 14_000_000 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] == 3 * 6
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+    assert d["bytes_moved_check"]["value_region"] == d["bytes_moved_check"]["kernel_region"]
