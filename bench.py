@@ -761,8 +761,26 @@ def run_pool(args, rank, world, device, emulate=False):
         # plan), K1 with the fused write-back per batch, gather + scatter per fallback batch
         "gpu_launches": (epochs + 1) + (1 if sp.fused else 2) * int(cnt[0])
         + 2 * (int(cnt[0]) if sp.dense_consumer else int(cnt[0]) - int(cnt[1])),
-        "e2e": None, "cpu_baseline": None,
+        "e2e": None,
+        "e2e_note": "pool: the per-batch logits come from the model's forward on the device (the "
+                    "executor's forward callback); the host-buffer end-to-end path is the default "
+                    "(EqSpec round) line's e2e",
+        "cpu_baseline": pool_cpu_baseline(args) if (world == 1 and rank == 0) else None,
     }
+
+
+def pool_cpu_baseline(args):
+    """The oracle on the same pool workload (bounded sample, a few seconds; see
+    oracle_pool_sample), for the pool line's cpu_baseline."""
+    if args.no_cpu_baseline:
+        return None
+    sps, parts = oracle_pool_sample(args)
+    return {"value": sps, "unit": "sequences/s", "cores": 1, "kind": "oracle",
+            "sample": (f"the oracle's GetBatch plan over the whole {args.pool_n}-sequence drain "
+                       f"({parts['batches']} batches, timed in full); per-batch oracle verify timed on 2 "
+                       f"batches and KV copies on 2 of 72 planes of one member, extrapolated to the drain's "
+                       f"batches and {parts['kv_bytes'] / 1e9:.0f} GB; numpy single-threaded on {cpu_info()}"),
+            "parts": parts}
 
 
 def run_pool_emulated(args, device):
