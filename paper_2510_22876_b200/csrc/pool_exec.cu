@@ -61,12 +61,10 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     const uint8_t *kinds = reinterpret_cast<const uint8_t *>(hh + 1);
     const int32_t *blens = hh + 1 + W, *sizes = hh + 1 + 2 * W;
     const int32_t run = max_batches > 0 && max_batches < nb ? max_batches : nb;
-    const int es = dtype_size(d->kv_dtype);
     // strides in elements: pool [N][planes][H][cap][D], staging [planes][B][H][cap][D]
     const int64_t hcd = d->H * d->cap * d->D;
     const int64_t p_plane = hcd, p_row = d->n_planes * hcd, p_head = d->cap * d->D;
     const int64_t s_plane = B * hcd, s_row = hcd, s_head = d->cap * d->D;
-    (void)es;
     // Processing order.  Serial: plan order.  Overlapped (n_staging >= 2): the fallback
     // batches are interleaved with the same-length ones, so that while the copy stream
     // gathers fallback f the main stream keeps verifying same-length batches.
@@ -83,8 +81,8 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         // List schedule on estimated durations: a fallback batch goes next as soon as its
         // gather is expected to be done, else the next same-length batch; the copy stream
         // runs gathers back to back, the one into staging slot f % NS after the scatter of
-        // f - NS (which follows that batch's verify).  Only the
-        // order (i.e. the timing) depends on the estimates, never a result.
+        // f - NS (which follows that batch's verify).  Only the order (i.e. the timing)
+        // depends on the estimates, never a result.
         const double gbps = d->est_gather_GBps > 0 ? d->est_gather_GBps : 5500.0;
         const double tv = d->est_verify_us > 0 ? d->est_verify_us : 10.0;  // K1 (+ scatter)
         const double row_bytes = static_cast<double>(d->n_planes) * d->H * d->D * dtype_size(d->kv_dtype);
