@@ -9,6 +9,10 @@
 //                       from the callback or from the input ring)
 //   fallback batches:  specdec_realign_kv scatter (the a+1 new KV rows back to the pool)
 // Every launch goes through the same C ABI entry points the Python driver uses.
+// With n_staging >= 2 (specdec.h) the fallback batches' gathers and scatters run on a
+// copy stream into a ring of staging buffers, interleaved by a list schedule with the
+// same-length batches' verifies on the main stream (reading R21: the batches of one plan
+// are independent, so their order cannot change a result).
 #include <cuda_runtime.h>
 
 #include <algorithm>
