@@ -17,6 +17,7 @@ written from the paper's definitions in the paper's order:
                 per-sequence autoregressive greedy reference
     metrics.py  §3.1 closed form, §4.1 exact/partial match
 
-Shares no code with the CUDA path.  Pins live in tests/test_oracle_*.py.
+Shares no code with the CUDA path.  Pins live in tests/test_oracle_*.py and
+tests/test_golden.py (hand-worked fixtures in tests/golden/).
 Parity pin status per function is listed in DESIGN.md §"Oracle pins".
 """
