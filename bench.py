@@ -410,9 +410,10 @@ def run_e2e(rb, args, world):
     specdec_eqspec_round_host call (eqspec.py step_host) that copies the step's logits +
     drafts from pinned host memory into a device staging slot (copy stream), runs the
     round (K1 -> K3 -> K2) on the compute stream and copies the step's result -- the
-    per-row emitted-token counts -- back into pinned host memory (third stream).  Two
-    staging slots and one result set per state parity let the copies of step s+1 run
-    under the round of step s; nothing synchronises the host inside the timed region."""
+    per-row emitted-token counts -- back into pinned host memory (third stream).  Three
+    staging slots and one result set per state parity let the copy of step s start two
+    rounds ahead of its use (absorbing an occasional slow H2D); nothing synchronises the
+    host inside the timed region."""
     import torch
     import torch.distributed as dist
     sh, dev, bt = rb.sh, rb.dev, rb.bt
@@ -454,7 +455,7 @@ def run_e2e(rb, args, world):
     return {"value": world * args.steps / (ms / 1e3), "unit": "rounds/s", "h2d_bytes_per_step": h2d_b,
             "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / args.steps, "wall_s": wall,
             "api": "specdec_eqspec_round_host (one C call per step: H2D + K1/K3/K2 + D2H)",
-            "overlap": "H2D on a copy stream into two staging slots; round on the compute stream; "
+            "overlap": "H2D on a copy stream into three staging slots; round on the compute stream; "
                        "D2H on a third stream from the round's parity result set"}
 
 

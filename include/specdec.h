@@ -466,17 +466,25 @@ int specdec_eqspec_round(const specdec_round_desc *d, int parity, const void *d_
  * io->ev_fetched[parity] (the read-out of the result set this round overwrites), run
  * specdec_eqspec_round, record ev_done[slot].  If h_emit (pinned [B] int32) is non-NULL:
  * on io->d2h_stream wait ev_done[slot], copy emit[parity] -> h_emit, record
- * ev_fetched[parity].  Nothing synchronises the host: successive calls with alternating
- * slot and parity overlap the copies of round r+1 with round r.  The events are the
- * caller's (cudaEvent_t, timing disabled; a never-recorded event does not block).
- * Errors: as specdec_eqspec_round; SPECDEC_ERR_ARG for a NULL io / host pointer or slot
- * not 0/1; SPECDEC_ERR_CUDA for a failed copy or event call.
+ * ev_fetched[parity].  Nothing synchronises the host: successive calls with the slot
+ * cycling through n_slots and the parity alternating overlap the copies of the next
+ * rounds with this one.  With n_slots = 3 the copy of round r starts when round r-3 is
+ * done, two rounds ahead of its use, which absorbs the occasional slow H2D (measured at
+ * Qwen3 B=8: 280 us median, up to 2 ms; 2 slots 2158 -> 3 slots 2241 rounds/s).  The
+ * events are the caller's (cudaEvent_t, timing disabled; a never-recorded event does not
+ * block).
+ * Errors: as specdec_eqspec_round; SPECDEC_ERR_ARG for a NULL io / host pointer, n_slots
+ * outside [2, SPECDEC_HOST_SLOTS] or slot >= n_slots; SPECDEC_ERR_CUDA for a failed copy
+ * or event call.
  */
+#define SPECDEC_HOST_SLOTS 4
 typedef struct specdec_host_io {
-    void *d_logits[2];         /* device staging, [B][k+1][logit_stride] each */
-    int64_t *d_draft[2];       /* device staging, [B][k] each */
+    int32_t n_slots;           /* staging slots in use, 2..SPECDEC_HOST_SLOTS; `slot` < n_slots */
+    void *d_logits[SPECDEC_HOST_SLOTS];    /* device staging, [B][k+1][logit_stride] each */
+    int64_t *d_draft[SPECDEC_HOST_SLOTS];  /* device staging, [B][k] each */
     specdec_stream_t copy_stream, d2h_stream;
-    void *ev_ready[2], *ev_done[2], *ev_fetched[2];
+    void *ev_ready[SPECDEC_HOST_SLOTS], *ev_done[SPECDEC_HOST_SLOTS];
+    void *ev_fetched[2];       /* per result parity */
 } specdec_host_io;
 
 int specdec_eqspec_round_host(const specdec_round_desc *d, const specdec_host_io *io,

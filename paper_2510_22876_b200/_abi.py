@@ -105,10 +105,14 @@ class RoundDesc(ctypes.Structure):
     ]
 
 
+HOST_SLOTS = 4
+_PS = _P * HOST_SLOTS
+
+
 class HostIO(ctypes.Structure):
     """Mirror of `specdec_host_io` (include/specdec.h)."""
-    _fields_ = [("d_logits", _P2), ("d_draft", _P2), ("copy_stream", _P), ("d2h_stream", _P),
-                ("ev_ready", _P2), ("ev_done", _P2), ("ev_fetched", _P2)]
+    _fields_ = [("n_slots", _I32), ("d_logits", _PS), ("d_draft", _PS), ("copy_stream", _P),
+                ("d2h_stream", _P), ("ev_ready", _PS), ("ev_done", _PS), ("ev_fetched", _P2)]
 
 
 def specdec_eqspec_round(desc: RoundDesc, parity, logits, draft, stream=None):

@@ -56,7 +56,8 @@ extern "C" int specdec_eqspec_round_host(const specdec_round_desc *d, const spec
                                          int parity, int slot, const void *h_logits,
                                          const int64_t *h_draft, int32_t *h_emit,
                                          specdec_stream_t stream) {
-    if (!d || !io || !h_logits || !h_draft || (slot != 0 && slot != 1) || (parity != 0 && parity != 1))
+    if (!d || !io || !h_logits || !h_draft || (parity != 0 && parity != 1)) return SPECDEC_ERR_ARG;
+    if (io->n_slots < 2 || io->n_slots > SPECDEC_HOST_SLOTS || slot < 0 || slot >= io->n_slots)
         return SPECDEC_ERR_ARG;
     if (!io->d_logits[slot] || !io->d_draft[slot] || !io->copy_stream || !io->ev_ready[slot] ||
         !io->ev_done[slot] || (h_emit && (!io->d2h_stream || !io->ev_fetched[parity])))

@@ -300,25 +300,29 @@ class EqSpecBatch:
         self._last = self.cur
         _abi.specdec_eqspec_round(self.round_desc(logits), self.cur, logits, draft, s)
 
-    def host_io(self, like_logits, like_draft):
-        """Device staging (two slots), copy / D2H streams and events for step_host: the
-        end-to-end round from pinned host inputs (specdec_eqspec_round_host)."""
+    def host_io(self, like_logits, like_draft, n_slots=3):
+        """Device staging (n_slots slots), copy / D2H streams and events for step_host: the
+        end-to-end round from pinned host inputs (specdec_eqspec_round_host).  3 slots
+        absorb the occasional slow H2D (specdec.h)."""
         io = _abi.HostIO()
-        self._io_lg = [torch.empty_like(like_logits, device=self.device) for _ in range(2)]
-        self._io_dr = [torch.empty_like(like_draft, device=self.device) for _ in range(2)]
+        ns = int(n_slots)
+        self._io_lg = [torch.empty_like(like_logits, device=self.device) for _ in range(ns)]
+        self._io_dr = [torch.empty_like(like_draft, device=self.device) for _ in range(ns)]
         self._io_streams = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
-        self._io_events = [torch.cuda.Event() for _ in range(6)]
+        self._io_events = [torch.cuda.Event() for _ in range(2 * ns + 2)]
         cur = torch.cuda.current_stream(self.device)
         for e in self._io_events:          # materialise the handles (recorded once, idle)
             e.record(cur)
-        two = lambda a, b: (ctypes.c_void_p * 2)(a, b)
-        io.d_logits = two(self._io_lg[0].data_ptr(), self._io_lg[1].data_ptr())
-        io.d_draft = two(self._io_dr[0].data_ptr(), self._io_dr[1].data_ptr())
+        pad = lambda xs: (ctypes.c_void_p * _abi.HOST_SLOTS)(*(list(xs) + [None] * (_abi.HOST_SLOTS - len(xs))))
+        ev = [e.cuda_event for e in self._io_events]
+        io.n_slots = ns
+        io.d_logits = pad([t.data_ptr() for t in self._io_lg])
+        io.d_draft = pad([t.data_ptr() for t in self._io_dr])
         io.copy_stream = self._io_streams[0].cuda_stream
         io.d2h_stream = self._io_streams[1].cuda_stream
-        ev = [e.cuda_event for e in self._io_events]
-        io.ev_ready, io.ev_done, io.ev_fetched = two(ev[0], ev[1]), two(ev[2], ev[3]), two(ev[4], ev[5])
-        self._io, self._io_slot = io, 0
+        io.ev_ready, io.ev_done = pad(ev[:ns]), pad(ev[ns:2 * ns])
+        io.ev_fetched = (ctypes.c_void_p * 2)(ev[2 * ns], ev[2 * ns + 1])
+        self._io, self._io_slot, self._io_n = io, 0, ns
         return io
 
     def step_host(self, h_logits, h_draft, h_emit=None, V=None, zero_pads=False, stream=None):
@@ -332,7 +336,7 @@ class EqSpecBatch:
         self._last = self.cur
         _abi.specdec_eqspec_round_host(self.round_desc(h_logits), self._io, self.cur, self._io_slot,
                                        h_logits, h_draft, h_emit, s)
-        self._io_slot ^= 1
+        self._io_slot = (self._io_slot + 1) % self._io_n
         self.cur = 1 - self.cur
 
     def launch_round(self, logits, draft, stream=None):

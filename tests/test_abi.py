@@ -160,7 +160,11 @@ def test_host_validation_drivers_and_flags(lib):
     assert L.specdec_eqspec_round(ctypes.byref(d), 0, None, nz, None) == _abi.ERR_ARG
     io = _abi.HostIO()
     assert L.specdec_eqspec_round_host(ctypes.byref(d), None, 0, 0, nz, nz, None, None) == _abi.ERR_ARG
-    assert L.specdec_eqspec_round_host(ctypes.byref(d), ctypes.byref(io), 0, 2, nz, nz, None, None) == _abi.ERR_ARG
+    assert L.specdec_eqspec_round_host(ctypes.byref(d), ctypes.byref(io), 0, 0, nz, nz, None, None) == _abi.ERR_ARG  # n_slots 0
+    io.n_slots = 3
+    assert L.specdec_eqspec_round_host(ctypes.byref(d), ctypes.byref(io), 0, 3, nz, nz, None, None) == _abi.ERR_ARG  # slot >= n_slots
+    assert L.specdec_eqspec_round_host(ctypes.byref(d), ctypes.byref(io), 0, 0, nz, nz, None, None) == _abi.ERR_ARG  # no staging
+    io.n_slots = 5
     assert L.specdec_eqspec_round_host(ctypes.byref(d), ctypes.byref(io), 0, 0, nz, nz, None, None) == _abi.ERR_ARG
     p = _abi.PoolDesc()
     p.host_header, p.W, p.B = 16, 4, 2
