@@ -418,8 +418,9 @@ def run_e2e(rb, args, world):
     import torch.distributed as dist
     sh, dev, bt = rb.sh, rb.dev, rb.bt
     d2h_mode = os.environ.get("SPECDEC_E2E_D2H", "one")
-    host_lg = [lg.cpu().pin_memory() for lg in rb.logits]
-    host_dr = [d.cpu().pin_memory() for d in rb.drafts]
+    from paper_2510_22876_b200.eqspec import pack_host_inputs
+    # each step's logits + drafts in one pinned buffer: one H2D per step
+    host_lg, host_dr = zip(*[pack_host_inputs(lg, d) for lg, d in zip(rb.logits, rb.drafts)])
     out_e = torch.empty((args.steps, sh.B), dtype=torch.int32).pin_memory()
     comp = rb.stream
     bt.host_io(host_lg[0], host_dr[0])

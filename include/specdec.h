@@ -466,7 +466,9 @@ int specdec_eqspec_round(const specdec_round_desc *d, int parity, const void *d_
  * io->ev_fetched[parity] (the read-out of the result set this round overwrites), run
  * specdec_eqspec_round, record ev_done[slot].  If h_emit (pinned [B] int32) is non-NULL:
  * on io->d2h_stream wait ev_done[slot], copy emit[parity] -> h_emit, record
- * ev_fetched[parity].  Nothing synchronises the host: successive calls with the slot
+ * ev_fetched[parity].  If the drafts directly follow the logits in memory on both sides
+ * (h_draft == h_logits + logits bytes, and the same for the slot's staging), the inputs go
+ * in one copy instead of two.  Nothing synchronises the host: successive calls with the slot
  * cycling through n_slots and the parity alternating overlap the copies of the next
  * rounds with this one.  With n_slots = 3 the copy of round r starts when round r-3 is
  * done, two rounds ahead of its use, which absorbs the occasional slow H2D (measured at

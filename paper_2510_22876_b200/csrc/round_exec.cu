@@ -70,8 +70,15 @@ extern "C" int specdec_eqspec_round_host(const specdec_round_desc *d, const spec
     const size_t lg_bytes = static_cast<size_t>(d->B * (d->k + 1) * d->logit_stride) * es;
     const size_t dr_bytes = static_cast<size_t>(d->B * d->k) * sizeof(int64_t);
     cudaError_t e = cudaStreamWaitEvent(cp, ev(io->ev_done[slot]), 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(io->d_logits[slot], h_logits, lg_bytes, cudaMemcpyHostToDevice, cp);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(io->d_draft[slot], h_draft, dr_bytes, cudaMemcpyHostToDevice, cp);
+    // one DMA when the drafts directly follow the logits on both sides (packed buffers)
+    const bool packed = reinterpret_cast<const char *>(h_draft) == static_cast<const char *>(h_logits) + lg_bytes &&
+                        reinterpret_cast<const char *>(io->d_draft[slot]) ==
+                            static_cast<const char *>(io->d_logits[slot]) + lg_bytes;
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(io->d_logits[slot], h_logits, packed ? lg_bytes + dr_bytes : lg_bytes,
+                            cudaMemcpyHostToDevice, cp);
+    if (e == cudaSuccess && !packed)
+        e = cudaMemcpyAsync(io->d_draft[slot], h_draft, dr_bytes, cudaMemcpyHostToDevice, cp);
     if (e == cudaSuccess) e = cudaEventRecord(ev(io->ev_ready[slot]), cp);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev(io->ev_ready[slot]), 0);
     if (e == cudaSuccess && io->ev_fetched[parity]) e = cudaStreamWaitEvent(s, ev(io->ev_fetched[parity]), 0);

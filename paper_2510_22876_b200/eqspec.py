@@ -33,6 +33,29 @@ from . import _abi
 TORCH_DT = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}
 
 
+def pack_inputs_like(logits, draft, device, pin=False):
+    """One buffer holding a logits tensor (shape / dtype / strides of `logits`, contiguous)
+    followed by a drafts tensor like `draft`: returns the two views.  On the host
+    (device='cpu', pin=True) it is pinned memory; specdec_eqspec_round_host then copies a
+    step's inputs with one DMA."""
+    lg_bytes = logits.numel() * logits.element_size()
+    dr_bytes = draft.numel() * draft.element_size()
+    buf = torch.empty(lg_bytes + dr_bytes, dtype=torch.uint8, device=device)
+    if pin:
+        buf = buf.pin_memory()
+    lg = buf[:lg_bytes].view(logits.dtype).view(logits.shape)
+    dr = buf[lg_bytes:].view(draft.dtype).view(draft.shape)
+    return lg, dr
+
+
+def pack_host_inputs(logits, draft):
+    """Pinned host copies of (logits, draft) packed into one buffer (see pack_inputs_like)."""
+    lg, dr = pack_inputs_like(logits, draft, "cpu", pin=True)
+    lg.copy_(logits)
+    dr.copy_(draft)
+    return lg, dr
+
+
 class EqSpecBatch:
     def __init__(self, B, k, cap, layers, H, D, kv_dtype="bf16", device="cuda", max_new=0,
                  eos_id=-1, pad_id=0, with_pred=False, draft=None, anchor_slack=0,
@@ -306,13 +329,15 @@ class EqSpecBatch:
         absorb the occasional slow H2D (specdec.h)."""
         io = _abi.HostIO()
         ns = int(n_slots)
-        self._io_lg = [torch.empty_like(like_logits, device=self.device) for _ in range(ns)]
-        self._io_dr = [torch.empty_like(like_draft, device=self.device) for _ in range(ns)]
         self._io_streams = [torch.cuda.Stream(self.device), torch.cuda.Stream(self.device)]
         self._io_events = [torch.cuda.Event() for _ in range(2 * ns + 2)]
         cur = torch.cuda.current_stream(self.device)
         for e in self._io_events:          # materialise the handles (recorded once, idle)
             e.record(cur)
+        # each slot is one device buffer: the logits, then the drafts (one H2D per step when
+        # the host inputs are packed the same way, see pack_host_inputs)
+        self._io_lg, self._io_dr = zip(*[pack_inputs_like(like_logits, like_draft, self.device)
+                                         for _ in range(ns)])
         pad = lambda xs: (ctypes.c_void_p * _abi.HOST_SLOTS)(*(list(xs) + [None] * (_abi.HOST_SLOTS - len(xs))))
         ev = [e.cuda_event for e in self._io_events]
         io.n_slots = ns

@@ -8,7 +8,7 @@ import torch
 from oracle import align as OA
 from oracle import verify as OV
 from paper_2510_22876_b200 import _abi
-from paper_2510_22876_b200.eqspec import EqSpecBatch
+from paper_2510_22876_b200.eqspec import EqSpecBatch, pack_host_inputs
 from synth import workloads as W
 from tests.gpu_helpers import bits_to_torch, padded_logits, torch_to_bits
 
@@ -30,7 +30,8 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
                      kv_mode=kv_mode)
     bt.load(tokens, lengths, bits_to_torch(kv_bits, shape.kv_dtype, cuda))
     bt.native_round = drive == "native"
-    h_emit = torch.zeros(B, dtype=torch.int32).pin_memory() if drive == "host" else None
+    host = drive in ("host", "host_packed")
+    h_emit = torch.zeros(B, dtype=torch.int32).pin_memory() if host else None
     base_o = anchor_slack
     bases = []
     # oracle state
@@ -54,9 +55,12 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
         bits = W.gen_logits_np(seed, r, B, k, V, shape.logit_dtype)
         lg = padded_logits(bits, shape.logit_dtype, cuda, extra=16)
         draft = torch.from_numpy(rt.draft).to(cuda)
-        if drive == "host":
+        if drive == "host":           # separate pinned buffers: two H2D copies
             bt.step_host(lg.cpu().pin_memory(), torch.from_numpy(rt.draft).pin_memory(), h_emit,
                          V=V, zero_pads=zero_pads)
+        elif drive == "host_packed":  # logits + drafts in one pinned buffer: one copy
+            hl, hd = pack_host_inputs(lg.cpu(), torch.from_numpy(rt.draft))
+            bt.step_host(hl, hd, h_emit, V=V, zero_pads=zero_pads)
         else:
             bt.step(lg, draft, V=V, zero_pads=zero_pads)
         # oracle
@@ -389,7 +393,7 @@ def test_full_size_sampled(cuda, name):
     assert int(bt.status.item()) == 0
 
 
-@pytest.mark.parametrize("drive", ["native", "host"])
+@pytest.mark.parametrize("drive", ["native", "host", "host_packed"])
 @pytest.mark.parametrize("pattern", ["alpha", "alternating", "all_k"])
 def test_rounds_native_driver(cuda, drive, pattern):
     """specdec_eqspec_round (one C call per round) and specdec_eqspec_round_host (H2D +
@@ -397,7 +401,7 @@ def test_rounds_native_driver(cuda, drive, pattern):
     _run_rounds(cuda, SMALL, 8, 12, pattern, drive=drive)
 
 
-@pytest.mark.parametrize("drive", ["native", "host"])
+@pytest.mark.parametrize("drive", ["native", "host", "host_packed"])
 def test_rounds_native_driver_modes(cuda, drive):
     _run_rounds(cuda, SMALL16, 5, 10, "alpha", seed=3, kv_mode="pingpong", drive=drive)
     _run_rounds(cuda, W.SHAPES["toy"], 2, 30, "alpha", max_new=24, eos_id=7, drive=drive)
