@@ -95,3 +95,27 @@ def test_balanced_bands():
         if N >= G:
             assert max(tot) - min(tot) <= 2 * w.max()
     assert [list(s) for s in shard_balanced(np.arange(4), 2, [1, 1, 1, 3])] == [[0, 1, 2], [3]]
+
+
+@pytest.mark.gpu
+def test_nccl_gather_results_world1():
+    """The NCCL path of the end-of-run exchange (CUDA tensors, all_gather_into_tensor,
+    all_reduce) and bench's max-over-ranks, in a one-rank NCCL group on the one GPU: the
+    gathered outputs equal the local ones."""
+    import torch
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        ids = np.array([3, 0, 2], np.int64)
+        out_loc = np.arange(3 * 5, dtype=np.int64).reshape(3, 5)
+        gen_loc = np.array([5, 1, 3], np.int64)
+        out, gen, cnt = gather_results(ids, out_loc, gen_loc, [7, 1, 0, 0, 0, 0, 0, 0], 4, 5, device=dev)
+        assert np.array_equal(out[ids], out_loc) and np.array_equal(gen[ids], gen_loc) and gen[1] == 0
+        assert list(cnt[:2]) == [7, 1]
+        assert bench.max_over_ranks(3.5, dev, 2) == 3.5          # the NCCL all_reduce(MAX) path
+        assert bench.coll_device(dev) == dev
+    finally:
+        dist.destroy_process_group()
