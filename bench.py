@@ -405,6 +405,17 @@ def run_ours(args, rank, world, device):
                 end_width=width_end, logits_bytes=logits_bytes)
 
 
+def round_bandwidth(res, sh, args, peak):
+    k2 = res["moved_A"] / args.steps if args.kv_mode == "inplace" else res["moved"] / args.steps
+    width = res["end_width"]
+    k3 = sh.B * width * 8 * 2 + 2 * sh.B * (width + sh.k) * 8     # tokens read + written, mask + pos
+    tot = res["logits_bytes"] + k2 + k3
+    gbps = tot / (res["ms"] / args.steps / 1e3) / 1e9
+    return {"bytes_per_round": tot, "GBps": gbps, "frac": gbps / peak,
+            "note": "K1 logits + K2 algorithmic KV bytes + K3 token/mask/pos bytes per round, over the "
+                    "value region's round time (K1/K3 latency included)"}
+
+
 def run_e2e(rb, args, world):
     """End to end through the C ABI with HOST buffers: every step is one
     specdec_eqspec_round_host call (eqspec.py step_host) that copies the step's logits +
@@ -935,6 +946,10 @@ def main():
                                     "repad_K3": res["k3_ms"] / args.steps,
                                     "realign_K2": k2_launch_ms},
             "verify_logits_GBps": res["logits_bytes"] / (res["k1_ms"] / args.steps / 1e3) / 1e9,
+            # the whole round against the same peak: algorithmic bytes of K1 (logits) + K2
+            # (region A's device counter: shifting rows only, in place) + K3 (tokens, masks,
+            # positions at the mean width) per value-region round time
+            "round_bandwidth": round_bandwidth(res, sh, args, peak),
             "clocks": res["clocks"],
             "e2e": res["e2e"],
             "gpu_launches": res["kernels_per_round"] * args.steps,
