@@ -592,6 +592,7 @@ def oracle_pool_sample(args, verify_samples=2):
 
 
 SLEEP_CYCLES = 200_000     # ~0.1 ms at 1.965 GHz: longer than Python's enqueue of one batch
+ALG3_CHUNK = 64            # Alg. 3 device-loop iterations between host checks of the drain
 
 
 def run_pool(args, rank, world, device, emulate=False):
@@ -634,6 +635,7 @@ def run_pool(args, rank, world, device, emulate=False):
         return ring_lg[j], ring_dr[j]
 
     ran = np.zeros(8, np.int64)
+    alg3_iters = {"n": 0}     # device-loop iterations issued (Alg. 3 mode, native)
 
     if args.pool_exec == "native":
         sp.native(list(zip(ring_lg, ring_dr)), V=V, logit_dtype=ring_lg[0].dtype,
@@ -644,6 +646,18 @@ def run_pool(args, rank, world, device, emulate=False):
         sp.moved.zero_()
         epochs = batches = 0
         ran[:] = 0
+        if args.pool_exec == "native" and events is None and args.pool_mode == "alg3":
+            # Alg. 3 as printed on the device: chunks of plan -> batch 0 -> re-plan iterations
+            # with no host sync inside a chunk (specdec_pool_alg3); drained-pool iterations
+            # at the end of the last chunk are no-ops
+            sp.alg3_exec.zero_() if getattr(sp, "alg3_exec", None) is not None else None
+            alg3_iters["n"] = 0
+            while sp.has_active():
+                sp.alg3_native(ALG3_CHUNK)
+                alg3_iters["n"] += ALG3_CHUNK
+            ex = sp.alg3_exec.cpu().numpy()
+            ran[0], ran[1], ran[2], ran[3] = ex[0], ex[1], ex[2], ex[3]
+            return int(ex[0]), int(ex[0])
         if args.pool_exec == "native" and events is None:
             # the per-batch launch loop in C++ (csrc/pool_exec.cu)
             while True:
@@ -772,7 +786,8 @@ def run_pool(args, rank, world, device, emulate=False):
         "clocks": clocks.summary(), "status": status,
         # libspecdec launches in the timed drain: K4 per plan (the epochs + the final empty
         # plan), K1 with the fused write-back per batch, gather + scatter per fallback batch
-        "gpu_launches": (epochs + 1) + (1 if sp.fused else 2) * int(cnt[0])
+        # (Alg. 3 device loop: K4 + gate + gather + verify + scatter per issued iteration)
+        "gpu_launches": 5 * alg3_iters["n"] if alg3_iters["n"] else (epochs + 1) + (1 if sp.fused else 2) * int(cnt[0])
         + 2 * (int(cnt[0]) if sp.dense_consumer else int(cnt[0]) - int(cnt[1])),
         "e2e": None,
         "e2e_note": "pool: the per-batch logits come from the model's forward on the device (the "

@@ -48,6 +48,7 @@ _SIGS = {
                                 _I64, _P, _P], _INT),
     "specdec_pool_epoch": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P], _INT),
     "specdec_eqspec_round": ([_P, _INT, _P, _P, _P], _INT),
+    "specdec_pool_alg3": ([_P, _I32, _P, _P, _P], _INT),
     "specdec_eqspec_round_host": ([_P, _P, _INT, _INT, _P, _P, _P, _P], _INT),
     "specdec_pool_verify": ([_P, _INT, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _P,
                              _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P], _INT),
@@ -156,6 +157,12 @@ def specdec_pool_epoch(desc: PoolDesc, max_batches=0, stream=None, forward=None)
                                      *[ctypes.byref(o) for o in out], _stream(stream)),
            "specdec_pool_epoch")
     return tuple(o.value for o in out)
+
+
+def specdec_pool_alg3(desc: PoolDesc, iterations, scratch, exec_counters=None, stream=None):
+    """`iterations` Alg. 3 iterations (plan, batch 0, re-plan) with no host synchronisation."""
+    _check(load().specdec_pool_alg3(ctypes.byref(desc), iterations, _ptr(scratch), _ptr(exec_counters),
+                                    _stream(stream)), "specdec_pool_alg3")
 
 
 class SpecdecError(RuntimeError):

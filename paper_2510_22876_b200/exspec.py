@@ -279,5 +279,15 @@ class SequencePool:
         self.verify_calls += r[0]
         return r
 
+    def alg3_native(self, iterations, stream=None):
+        """`iterations` iterations of Alg. 3 as printed (plan, batch 0, re-plan) in one C call
+        with no host synchronisation (specdec_pool_alg3; after `native`).  Executed-batch
+        counters accumulate in self.alg3_exec [batches, same-length, their members,
+        fallback members]."""
+        if getattr(self, "_alg3_scratch", None) is None:
+            self._alg3_scratch = torch.zeros(4 * self.B, dtype=torch.int32, device=self.device)
+            self.alg3_exec = torch.zeros(4, dtype=torch.int64, device=self.device)
+        _abi.specdec_pool_alg3(self._desc, iterations, self._alg3_scratch, self.alg3_exec, stream)
+
     def has_active(self) -> bool:
         return bool(self.active.any().item())
