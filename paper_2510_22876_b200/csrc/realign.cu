@@ -2,26 +2,26 @@
 // PAPER.md:447) and the EXSpec pool gather / write-back scatter (Alg. 3, PAPER.md:492,
 // 505) as one row-mapped KV move.
 //
-// A slab is one (plane, row, KV head): `cnt` contiguous KV rows of D elements.  Each slab
-// is cut into segments of ~kSegBytes -- the work units -- so every CTA gets the same number
-// of bytes however few rows move (a B=2 batch moves one row) and the tail is one segment,
-// not one slab.  One single-warp CTA streams its units through a ring of shared-memory
-// stages with TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP): a bulk load completes an
-// mbarrier transaction, the same elected lane bulk-stores the chunk to its destination,
-// loads run STAGES-1 chunks ahead of stores, and the chunk stream is continuous across a
-// CTA's units.
+// A slab is one (plane, row, KV head): `cnt` contiguous KV rows of D elements.  The work
+// units are whole slabs in place, and segments of ~kSegBytes between distinct buffers (or
+// in place with SPECDEC_SEGMENTED, below).  One single-warp CTA streams its units through
+// a ring of shared-memory stages with TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP): a
+// bulk load completes an mbarrier transaction, the same elected lane bulk-stores the chunk
+// to its destination, loads run STAGES-1 chunks ahead of stores, and the chunk stream is
+// continuous across a CTA's units.  Units go to CTAs by a rotated static order, or with
+// SPECDEC_DYNAMIC from a ticket counter in the caller's workspace (dyn_done below).
 //
 // In place (the EqSpec realign) a segment is walked in the hazard-free direction -- right
 // shifts (dst > src) top-down, left shifts bottom-up -- so a chunk's store only hits bytes
 // of its own segment that were already loaded.  The only cross-segment hazard is at
 // segment boundaries: a segment's stores overwrite the first |shift| rows of its neighbour
 // (right shift: the upper neighbour's bottom rows; left: the lower neighbour's top rows).
-// A small first kernel (realign_save_kernel) copies exactly those boundary rows of every
-// segment into a workspace slot before the main kernel starts; the owning segment then
-// takes them from its slot (as its last chunk), never from the live buffer.  Segments thus
-// need no ordering at all.  Without a workspace, or for shifts wider than a slot, a slab
-// is one segment (the PR-1 behaviour).  Rows whose source and destination coincide
-// (Delta = 0) are skipped: in place they cost zero bytes.
+// With SPECDEC_SEGMENTED a small first kernel (realign_save_kernel) copies exactly those
+// boundary rows of every segment into a workspace slot before the main kernel starts; the
+// owning segment then takes them from its slot (as its last chunk), never from the live
+// buffer.  Segments thus need no ordering at all (measured slower than whole slabs, so off
+// by default).  For shifts wider than a slot a slab stays one segment.  Rows whose source
+// and destination coincide (Delta = 0) are skipped: in place they cost zero bytes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
