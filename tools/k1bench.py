@@ -5,8 +5,8 @@ graph, per-launch time from CUDA events.
 
 SPECDEC_K1_EXP=1 times the argmax phase alone (no grid-wide arrival / epilogue), =2 an empty
 kernel on the same grid (the launch floor), =3 the loads and per-thread max only (no CTA
-reduction), =4 up to the CTA maximum (no pass 2), =5 up to pass 2 (no merge) -- results
-invalid, for splitting the latency.
+reduction), =4 up to the CTA maximum (no pass 2), =5 up to pass 2 (no merge), =6 the
+grid-wide arrival without the epilogue -- results invalid, for splitting the latency.
 """
 from __future__ import annotations
 
