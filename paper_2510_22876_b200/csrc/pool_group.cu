@@ -1,7 +1,8 @@
 // pool_group.cu -- K4: EXSpec GetBatch over a sliding window (Alg. 3, PAPER.md:488-494,
 // 508; §3.2; readings R11-R14).
 //
-// One CTA of 1024 threads plans the whole window on device:
+// One CTA (up to 1024 threads: half the window rounded up to a power of two, >= 64) plans
+// the whole window on device:
 //   1. RefillWindow: stable compaction of d_order by d_active (block scan), first W ids;
 //   2. the length histogram: a block-wide bitonic sort of the (length, window position)
 //      keys puts every group contiguous and in window order, so a member's group is a
@@ -13,6 +14,8 @@
 // Every step is a deterministic function of the inputs, so the plan is bit-identical to
 // the oracle's (tests/test_gpu_pool.py).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "host_util.h"
@@ -301,7 +304,12 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
         if (e != cudaSuccess) return record_cuda_error(e);
         attr_done = true;
     }
-    return launch_k(pool_group_kernel, dim3(1), dim3(kPoolThreads), smem,
+    // threads: enough for the bitonic sorts (n <= 2 * threads, n = the window rounded up to
+    // a power of two) and no more -- a block barrier costs more with more warps
+    int w2 = 1;
+    while (w2 < W) w2 <<= 1;
+    const int threads = std::min(kPoolThreads, std::max(64, w2 / 2));
+    return launch_k(pool_group_kernel, dim3(1), dim3(threads), smem,
                     reinterpret_cast<cudaStream_t>(stream), d_len, d_active, d_order, N, W, B,
                     min_group, d_window, d_window_size, d_batch_of, d_slot_of, d_members, d_mlen,
                     d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches, d_counters);
