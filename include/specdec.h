@@ -273,8 +273,8 @@ int specdec_pool_writeback(const int32_t *d_members, int64_t B, int64_t k,
  * specdec_pool_verify -- one EXSpec batch's Alg. 1 BatchVerify with
  * the Alg. 3 Phase 4 write-back fused into its epilogue: exactly
  * specdec_verify(n = d_mlen, active = d_mactive, budget = NULL, no plan outputs) followed
- * by specdec_pool_writeback(d_members, ...), in one launch (the pool's per-batch path is
- * latency-bound: one launch and one dependent kernel fewer per batch).
+ * by specdec_pool_writeback(d_members, ...), with the write-back inside K1's epilogue (the
+ * pool's per-batch path is latency-bound: one dependent kernel fewer per batch).
  * Arguments as in those two calls; d_mlen / d_mactive / d_members are one batch's rows of
  * specdec_pool_group's outputs.  Errors: as specdec_verify (logits / shape / workspace)
  * and specdec_pool_writeback (pool pointers, cap_tok, max_new); SPECDEC_ST_CAPACITY if a

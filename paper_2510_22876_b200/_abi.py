@@ -22,6 +22,9 @@ OVERLAP_PREV = 2
 DYNAMIC = 4
 SEGMENTED = 8
 DTYPE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
+# kernels one specdec_verify / specdec_pool_verify launches: the argmax grid and the
+# one-CTA epilogue behind it (SPECDEC_K1_SPLIT=0: one kernel, last-CTA epilogue)
+K1_KERNELS = 1 if os.environ.get("SPECDEC_K1_SPLIT", "1") == "0" else 2
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -266,11 +266,13 @@ class EqSpecBatch:
 
     @property
     def kernels_per_round(self) -> int:
-        """libspecdec kernels one round launches (K1, K3, K2 per cache, + save kernels)."""
+        """libspecdec kernels one round launches (K1 = argmax grid + epilogue, K3, K2 per
+        cache, + save kernels)."""
+        k13 = _abi.K1_KERNELS + 1
         if self.B == 1 and self.anchor is None and self.kv_mode == "inplace":
-            return 2
+            return k13
         per_cache = 2 if self.segment and self.kv_mode == "inplace" else 1
-        return 2 + per_cache * (2 if self.dkv is not None else 1)
+        return k13 + per_cache * (2 if self.dkv is not None else 1)
 
     # ----------------------------------------------------------------- native round driver
     def round_desc(self, logits):

@@ -33,10 +33,12 @@ def test_option_validation():
 
 
 def test_kernels_per_round():
-    assert EqSpecBatch(1, 4, 64, 1, 1, 8, "bf16", "cpu").kernels_per_round == 2        # B=1: no K2
-    assert EqSpecBatch(1, 4, 64, 1, 1, 8, "bf16", "cpu", kv_mode="pingpong").kernels_per_round == 3
-    assert EqSpecBatch(4, 4, 64, 1, 1, 8, "bf16", "cpu").kernels_per_round == 3
-    assert EqSpecBatch(4, 4, 64, 1, 1, 8, "bf16", "cpu", draft=(1, 1, 8)).kernels_per_round == 4
+    from paper_2510_22876_b200 import _abi
+    k1 = _abi.K1_KERNELS                   # the argmax grid + the epilogue kernel (default 2)
+    assert EqSpecBatch(1, 4, 64, 1, 1, 8, "bf16", "cpu").kernels_per_round == k1 + 1     # B=1: no K2
+    assert EqSpecBatch(1, 4, 64, 1, 1, 8, "bf16", "cpu", kv_mode="pingpong").kernels_per_round == k1 + 2
+    assert EqSpecBatch(4, 4, 64, 1, 1, 8, "bf16", "cpu").kernels_per_round == k1 + 2
+    assert EqSpecBatch(4, 4, 64, 1, 1, 8, "bf16", "cpu", draft=(1, 1, 8)).kernels_per_round == k1 + 3
 
 
 def test_result_sets_per_parity():
