@@ -50,13 +50,13 @@ def test_fuzz_episode(cuda, i):
 
 @pytest.mark.parametrize("i", range(N_CASES))
 def test_fuzz_episode_native_drivers(cuda, i):
-    """The same episodes through the native round driver (even i) and the host-buffer
-    driver (odd i; packed inputs every fourth), with the KV mode drawn too (ping-pong when
-    not anchored)."""
+    """The same episodes through the native round driver, the host-buffer driver (separate
+    or packed inputs) and graph replay of the captured round, in turn, with the KV mode
+    drawn too (ping-pong when not anchored)."""
     c = draw_case(i)
     rng = np.random.default_rng(20_000 + i)
     kv_mode = "pingpong" if (c["anchor_slack"] == 0 and not c["zero_pads"] and rng.random() < 0.4) else "inplace"
     _run_rounds(cuda, c["shape"], c["B"], c["rounds"], c["pattern"], seed=c["seed"],
                 max_new=c["max_new"], eos_id=c["eos_id"], zero_pads=c["zero_pads"],
                 anchor_slack=c["anchor_slack"], kv_mode=kv_mode,
-                drive=("native", "host", "native", "host_packed")[i % 4])
+                drive=("native", "host", "graph", "host_packed")[i % 4])

@@ -29,8 +29,9 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
                      max_new=max_new, eos_id=eos_id, pad_id=W.PAD_ID, anchor_slack=anchor_slack,
                      kv_mode=kv_mode)
     bt.load(tokens, lengths, bits_to_torch(kv_bits, shape.kv_dtype, cuda))
-    bt.native_round = drive == "native"
+    bt.native_round = drive in ("native", "graph")
     host = drive in ("host", "host_packed")
+    graph_io = None
     h_emit = torch.zeros(B, dtype=torch.int32).pin_memory() if host else None
     base_o = anchor_slack
     bases = []
@@ -61,6 +62,14 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
         elif drive == "host_packed":  # logits + drafts in one pinned buffer: one copy
             hl, hd = pack_host_inputs(lg.cpu(), torch.from_numpy(rt.draft))
             bt.step_host(hl, hd, h_emit, V=V, zero_pads=zero_pads)
+        elif drive == "graph":        # the captured round (PDL edges inside the graph) replayed
+            if graph_io is None:
+                graph_io = (torch.empty_like(lg), torch.empty_like(draft))
+                bt.zero_pads = zero_pads
+                bt.capture([graph_io], V=V)
+            graph_io[0].copy_(lg)
+            graph_io[1].copy_(draft)
+            bt.replay(0)
         else:
             bt.step(lg, draft, V=V, zero_pads=zero_pads)
         # oracle
@@ -417,3 +426,53 @@ def test_rounds_native_driver_anchored(cuda, drive):
     assert nat["bases"] == py["bases"] and nat["moved"] == py["moved"]
     _run_rounds(cuda, SMALL16, 6, 14, "alpha", seed=2, max_new=33, anchor_slack=32, drive=drive)
     _run_rounds(cuda, SMALL, 1, 6, "alpha", anchor_slack=16, drive=drive)
+
+
+@pytest.mark.parametrize("shape,B,pattern,kw", [(SMALL, 8, "alpha", {}), (SMALL16, 5, "alternating", {"kv_mode": "pingpong"}),
+                                               (SMALL, 6, "alpha", {"anchor_slack": 64}),
+                                               (W.SHAPES["toy"], 2, "alpha", {"max_new": 24, "eos_id": 7}),
+                                               (SMALL, 1, "all_k", {})])
+def test_rounds_graph_replay(cuda, shape, B, pattern, kw):
+    """Rounds replayed from the captured CUDA graphs (the bench's value path: programmatic
+    edges between K1's grid, its epilogue kernel, K3 and K2; K2 starting under K3; dynamic
+    K2 tickets reset across replays) against the oracle, round by round."""
+    _run_rounds(cuda, shape, B, 10, pattern, drive="graph", **kw)
+
+
+def test_multi_round_graph_equals_direct(cuda):
+    """A graph holding 6 consecutive rounds (distinct input buffers, parities alternating),
+    replayed twice, leaves exactly the state of 12 directly launched rounds -- tokens,
+    lengths, pads, masks, positions, results and every KV byte."""
+    sh = SMALL
+    B, k, V = 8, sh.k, sh.V
+    cap = W.derive_cap(sh.with_(B=B), 14)
+    lengths = W.gen_lengths(sh, 4, B)
+    tokens = W.left_padded_tokens(lengths, cap, 4, V)
+    kv_bits = W.gen_kv_bits_np(4, sh.n_planes * B * sh.H * cap * sh.D).reshape(sh.n_planes, B, sh.H, cap, sh.D)
+    ins = [(padded_logits(W.gen_logits_np(4, r, B, k, V, sh.logit_dtype), sh.logit_dtype, cuda),
+            torch.from_numpy(W.gen_round_truth(4, r, B, k, V, "alpha").draft).to(cuda)) for r in range(6)]
+    bts = []
+    for _ in range(2):
+        bt = EqSpecBatch(B, k, cap, sh.layers, sh.H, sh.D, sh.kv_dtype, cuda, max_new=40, pad_id=W.PAD_ID)
+        bt.load(tokens, lengths, bits_to_torch(kv_bits, sh.kv_dtype, cuda))
+        bt.V = V
+        bts.append(bt)
+    direct, graphed = bts
+    for r in range(12):
+        direct.step(*ins[r % 6], V=V)
+    s = torch.cuda.Stream(cuda)
+    s.wait_stream(torch.cuda.current_stream(cuda))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+        for r in range(6):
+            graphed.launch_round(*ins[r], stream=s)
+            graphed.cur = 1 - graphed.cur
+    torch.cuda.current_stream(cuda).wait_stream(s)
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    assert direct.cur == graphed.cur
+    for name in ("tok", "n", "pad", "mask", "pos", "active", "budget", "gen", "out_buf", "_accept", "_emit",
+                 "_bonus", "_finished", "kept", "plan_L", "status"):
+        assert torch.equal(getattr(direct, name), getattr(graphed, name)), name
+    assert torch.equal(direct.kv.view(torch.int16), graphed.kv.view(torch.int16))
