@@ -30,6 +30,7 @@ def _run_rounds(cuda, shape: W.Shape, B, rounds, pattern, seed=0, max_new=0, eos
                      kv_mode=kv_mode)
     bt.load(tokens, lengths, bits_to_torch(kv_bits, shape.kv_dtype, cuda))
     bt.native_round = drive in ("native", "graph")
+    bt.fork = drive == "fork"                 # K3 on a side stream under K2 (Python path)
     host = drive in ("host", "host_packed")
     graph_io = None
     h_emit = torch.zeros(B, dtype=torch.int32).pin_memory() if host else None
@@ -402,7 +403,7 @@ def test_full_size_sampled(cuda, name):
     assert int(bt.status.item()) == 0
 
 
-@pytest.mark.parametrize("drive", ["native", "host", "host_packed"])
+@pytest.mark.parametrize("drive", ["native", "host", "host_packed", "fork"])
 @pytest.mark.parametrize("pattern", ["alpha", "alternating", "all_k"])
 def test_rounds_native_driver(cuda, drive, pattern):
     """specdec_eqspec_round (one C call per round) and specdec_eqspec_round_host (H2D +
