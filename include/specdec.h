@@ -466,9 +466,10 @@ int specdec_eqspec_round(const specdec_round_desc *d, int parity, const void *d_
  * io->ev_fetched[parity] (the read-out of the result set this round overwrites), run
  * specdec_eqspec_round, record ev_done[slot].  If h_emit (pinned [B] int32) is non-NULL:
  * on io->d2h_stream wait ev_done[slot], copy emit[parity] -> h_emit, record
- * ev_fetched[parity].  If the drafts directly follow the logits in memory on both sides
- * (h_draft == h_logits + logits bytes, and the same for the slot's staging), the inputs go
- * in one copy instead of two.  Nothing synchronises the host: successive calls with the slot
+ * ev_fetched[parity].  If the caller sets io->inputs_packed (the drafts directly follow
+ * the logits in ONE pinned allocation) and the slot's staging is laid out the same way,
+ * the inputs go in one copy instead of two.  (Adjacency alone is not enough: two separate
+ * pinned allocations can be adjacent, and one copy may not span both.)  Nothing synchronises the host: successive calls with the slot
  * cycling through n_slots and the parity alternating overlap the copies of the next
  * rounds with this one.  With n_slots = 3 the copy of round r starts when round r-3 is
  * done, two rounds ahead of its use, which absorbs the occasional slow H2D (measured at
@@ -487,6 +488,8 @@ typedef struct specdec_host_io {
     specdec_stream_t copy_stream, d2h_stream;
     void *ev_ready[SPECDEC_HOST_SLOTS], *ev_done[SPECDEC_HOST_SLOTS];
     void *ev_fetched[2];       /* per result parity */
+    int32_t inputs_packed;     /* per call: 1 = h_draft directly follows h_logits in the SAME
+                                * pinned allocation (one copy); 0 = two copies */
 } specdec_host_io;
 
 int specdec_eqspec_round_host(const specdec_round_desc *d, const specdec_host_io *io,

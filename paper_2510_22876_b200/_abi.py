@@ -116,7 +116,8 @@ _PS = _P * HOST_SLOTS
 class HostIO(ctypes.Structure):
     """Mirror of `specdec_host_io` (include/specdec.h)."""
     _fields_ = [("n_slots", _I32), ("d_logits", _PS), ("d_draft", _PS), ("copy_stream", _P),
-                ("d2h_stream", _P), ("ev_ready", _PS), ("ev_done", _PS), ("ev_fetched", _P2)]
+                ("d2h_stream", _P), ("ev_ready", _PS), ("ev_done", _PS), ("ev_fetched", _P2),
+                ("inputs_packed", _I32)]
 
 
 def specdec_eqspec_round(desc: RoundDesc, parity, logits, draft, stream=None):
@@ -142,6 +143,9 @@ def specdec_eqspec_round_host(desc: RoundDesc, io: HostIO, parity, slot, h_logit
                 raise SpecdecError("pinned host tensor expected")
             _PINNED_OK.add(key)
         ptrs.append(key[0])
+    # one copy only when the drafts follow the logits inside one allocation (same storage)
+    io.inputs_packed = int(h_logits.untyped_storage().data_ptr() == h_draft.untyped_storage().data_ptr()
+                           and ptrs[1] == ptrs[0] + h_logits.numel() * h_logits.element_size())
     _check(load().specdec_eqspec_round_host(ctypes.byref(desc), ctypes.byref(io), parity, slot,
                                             ptrs[0], ptrs[1], ptrs[2], _stream(stream)),
            "specdec_eqspec_round_host")

@@ -71,7 +71,8 @@ extern "C" int specdec_eqspec_round_host(const specdec_round_desc *d, const spec
     const size_t dr_bytes = static_cast<size_t>(d->B * d->k) * sizeof(int64_t);
     cudaError_t e = cudaStreamWaitEvent(cp, ev(io->ev_done[slot]), 0);
     // one DMA when the drafts directly follow the logits on both sides (packed buffers)
-    const bool packed = reinterpret_cast<const char *>(h_draft) == static_cast<const char *>(h_logits) + lg_bytes &&
+    const bool packed = io->inputs_packed &&
+                        reinterpret_cast<const char *>(h_draft) == static_cast<const char *>(h_logits) + lg_bytes &&
                         reinterpret_cast<const char *>(io->d_draft[slot]) ==
                             static_cast<const char *>(io->d_logits[slot]) + lg_bytes;
     if (e == cudaSuccess)

@@ -48,7 +48,9 @@ def test_fuzz_episode(cuda, i):
                 anchor_slack=c["anchor_slack"])
 
 
-@pytest.mark.parametrize("i", range(N_CASES))
+# 3029: separate pinned logits / drafts that the caching host allocator placed back to back
+# -- a single copy spanning both allocations failed (inputs_packed is now explicit)
+@pytest.mark.parametrize("i", sorted(set(range(N_CASES)) | {3029}))
 def test_fuzz_episode_native_drivers(cuda, i):
     """The same episodes through the native round driver, the host-buffer driver (separate
     or packed inputs) and graph replay of the captured round, in turn, with the KV mode
