@@ -477,3 +477,30 @@ def test_multi_round_graph_equals_direct(cuda):
                  "_bonus", "_finished", "kept", "plan_L", "status"):
         assert torch.equal(getattr(direct, name), getattr(graphed, name)), name
     assert torch.equal(direct.kv.view(torch.int16), graphed.kv.view(torch.int16))
+
+
+K2_FUZZ = int(__import__("os").environ.get("SPECDEC_K2_FUZZ_CASES", "16"))
+
+
+@pytest.mark.parametrize("i", range(K2_FUZZ))
+def test_realign_fuzz(cuda, i):
+    """K2 alone on seeded random geometry: rows, planes, heads, head_dim, dtype, capacity,
+    arbitrary shifts of either sign (not only |delta| <= k), Delta = 0 rows, empty rows, and
+    random flag sets (ZERO_PADS, SEGMENTED, DYNAMIC, count_bound) -- every defined KV entry
+    and zeroed pad against the oracle."""
+    r = np.random.default_rng(40_000 + i)
+    B = int(r.integers(1, 13))
+    D, dtype = [(8, "bf16"), (16, "fp16"), (64, "bf16"), (128, "bf16"), (4, "fp32"), (72, "fp16")][int(r.integers(0, 6))]
+    planes, H = int(r.integers(1, 5)), int(r.integers(1, 4))
+    kept = r.integers(0, 300, B)
+    kept[r.random(B) < 0.15] = 0
+    pad_old = r.integers(0, 60, B)
+    shift = r.integers(-40, 41, B)
+    shift[r.random(B) < 0.2] = 0
+    pad_new = np.maximum(pad_old + shift, 0)
+    zero = bool(r.random() < 0.3)
+    seg = bool(r.random() < 0.3)
+    dyn = bool(r.random() < 0.5)
+    bound = int(kept.max()) if (r.random() < 0.2 and kept.max() * D * (4 if dtype == "fp32" else 2) <= 4096) else 0
+    _realign_case(cuda, pad_old.tolist(), pad_new.tolist(), kept.tolist(), D=D, H=H, planes=planes, dtype=dtype,
+                  zero=zero, seg=seg, bound=bound, dyn=dyn)
