@@ -89,7 +89,11 @@ def batch_verify(logit_bits, dtype, draft, n, pad, active, eos_id=-1, budget=Non
     Returns a dict of numpy arrays."""
     draft = np.asarray(draft)
     B, k = draft.shape
-    pred, nan_seen = argmax_rows(logit_bits, dtype)
+    pred, _ = argmax_rows(logit_bits, dtype)
+    # R4 status: a NaN among the logits of the rows verified this round (a row that is not
+    # active is not read at all)
+    live = np.asarray(active).astype(bool)
+    nan_seen = bool(np.isnan(widen(logit_bits[live], dtype)).any()) if live.any() else False
     accept = np.zeros(B, np.int32)
     bonus = np.full(B, pad_id, np.int64)
     emit = np.zeros(B, np.int32)
