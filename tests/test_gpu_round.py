@@ -504,3 +504,60 @@ def test_realign_fuzz(cuda, i):
     bound = int(kept.max()) if (r.random() < 0.2 and kept.max() * D * (4 if dtype == "fp32" else 2) <= 4096) else 0
     _realign_case(cuda, pad_old.tolist(), pad_new.tolist(), kept.tolist(), D=D, H=H, planes=planes, dtype=dtype,
                   zero=zero, seg=seg, bound=bound, dyn=dyn)
+
+
+K3_FUZZ = int(__import__("os").environ.get("SPECDEC_K3_FUZZ_CASES", "12"))
+
+
+@pytest.mark.parametrize("i", range(K3_FUZZ))
+def test_repad_fuzz(cuda, i):
+    """K3 alone, in place (one CTA walks each row in the hazard-free direction) and out of
+    place (column gather), on seeded random plans from the oracle's verify (ragged
+    lengths, every accept pattern, EOS / budget finishes, inactive rows, output buffers):
+    tokens', masks, positions, outputs and counts bit-exact against the oracle."""
+    r = np.random.default_rng(70_000 + i)
+    B, k = int(r.integers(1, 13)), int(r.integers(1, 9))
+    V = 97
+    n = r.integers(1, 120, B).astype(np.int32)
+    L = int(n.max())
+    pad = (L - n).astype(np.int32)
+    cap = L + 3 * (k + 1) + int(r.integers(0, 20))
+    tokens = np.full((B, cap), W.PAD_ID, np.int64)
+    for b in range(B):
+        tokens[b, pad[b]:L] = r.integers(1, V, n[b])
+    pattern = W.ACCEPT_PATTERNS[int(r.integers(0, len(W.ACCEPT_PATTERNS)))]
+    rt = W.gen_round_truth(80 + i, 0, B, k, V, pattern)
+    bits = W.gen_logits_np(80 + i, 0, B, k, V, "fp32")
+    act = (r.random(B) < 0.85).astype(np.uint8)
+    eos = int(r.integers(0, V)) if r.random() < 0.3 else -1
+    budget = r.integers(0, 10, B).astype(np.int64) if r.random() < 0.4 else None
+    v = OV.batch_verify(bits, "fp32", rt.draft, n, pad, act, eos, budget, W.PAD_ID)
+    tok_o, mask_o, pos_o = OA.repad_tokens(tokens, cap, k, pad, L, v, W.PAD_ID)
+    max_new = 64
+    gen0 = r.integers(0, 20, B).astype(np.int32)
+    t32 = lambda x: torch.as_tensor(np.asarray(x, np.int32), device=cuda)
+    t64 = lambda x: torch.as_tensor(np.asarray(x, np.int64), device=cuda)
+    for inplace in (True, False):
+        tin = t64(tokens)
+        tout = tin if inplace else torch.full_like(tin, -7)
+        mask = torch.full((B, cap + k), -7, dtype=torch.int64, device=cuda)
+        pos = torch.full_like(mask, -7)
+        out_buf = torch.zeros((B, max_new), dtype=torch.int64, device=cuda)
+        gen = t32(gen0)
+        st = torch.zeros(1, dtype=torch.int32, device=cuda)
+        _abi.specdec_rebuild_pos_mask(tin, tout, k, t32(n), t32(pad), t64(rt.draft), t32(v["accept"]),
+                                      t64(v["bonus"]), t32(v["emit"]), torch.as_tensor(v["finished"], device=cuda),
+                                      t32([v["L_new"]]), t32(v["pad_new"]), mask, pos, pad_id=W.PAD_ID,
+                                      out_buf=out_buf, gen=gen, status=st)
+        torch.cuda.synchronize()
+        Ln = v["L_new"]
+        assert int(st.item()) == 0, inplace
+        if Ln > 0:
+            assert np.array_equal(tout[:, :Ln].cpu().numpy(), tok_o[:, :Ln]), inplace
+            assert np.array_equal(mask[:, :Ln + k].cpu().numpy(), mask_o), inplace
+            assert np.array_equal(pos[:, :Ln + k].cpu().numpy(), pos_o), inplace
+        g = gen.cpu().numpy()
+        assert np.array_equal(g, gen0 + v["emit"]), inplace
+        ob = out_buf.cpu().numpy()
+        for b in range(B):
+            assert list(ob[b, gen0[b]:g[b]]) == v["E"][b], (inplace, b)
