@@ -68,28 +68,56 @@ struct PoolSmem {
 };
 
 // Ascending bitonic sort of key[0, n) (n a power of two <= 2 * blockDim.x, padded with ~0).
-// Keys are unique, so the result is unique whatever the thread schedule.  Thread p owns
-// compare-exchange pair p; for j <= 32 the pairs of warp w all lie in key[64w, 64w + 64),
-// so two consecutive such substeps need only a warp barrier -- a block barrier is paid
-// around every substep with j >= 64 (none for n <= 64).
+// Keys are unique (or equal padding), so the result is unique whatever the thread
+// schedule.  Register resident: thread t < P = n / 2 holds elements t and t + P.  A substep with j < 32 pairs lanes of one warp (shuffle), j == P pairs the
+// thread's own two elements, and only 32 <= j < P goes through shared memory (two block
+// barriers) -- 14 of the 55 substeps at n = 1024.  (The former all-shared-memory version,
+// with an integer division per pair, took 11.5 us at n = 1024; profiles/r01/k4bench.txt.)
+__device__ __forceinline__ unsigned long long keep(unsigned long long x, unsigned long long y, bool lo) {
+    return lo ? (x < y ? x : y) : (x > y ? x : y);
+}
+
 __device__ void block_bitonic_sort(unsigned long long *key, int n) {
-    const int p = threadIdx.x;
+    const int tid = threadIdx.x;
+    const int P = n >> 1;
+    const bool on = tid < P;
+    const bool wact = tid < ((P + 31) & ~31);  // whole warps for the shuffles (P < 32: warp 0)
+    unsigned long long x0 = on ? key[tid] : 0ull, x1 = on ? key[tid + P] : 0ull;
+    const int i0 = tid, i1 = tid + P;
     for (int k = 2; k <= n; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-            if (p < (n >> 1)) {
-                const int i = 2 * j * (p / j) + (p % j), l = i + j;
-                const unsigned long long a = key[i], b = key[l];
-                const bool up = (i & k) == 0;
-                if ((a > b) == up) {
-                    key[i] = b;
-                    key[l] = a;
+            if (j == P) {  // only at k == n: every pair ascending, i0 the lower
+                if (on) {
+                    const unsigned long long lo = x0 < x1 ? x0 : x1, hi = x0 < x1 ? x1 : x0;
+                    x0 = lo;
+                    x1 = hi;
+                }
+            } else if (j >= 32) {
+                __syncthreads();  // the previous exchange's reads are done
+                if (on) {
+                    key[i0] = x0;
+                    key[i1] = x1;
+                }
+                __syncthreads();
+                if (on) {
+                    const unsigned long long y0 = key[i0 ^ j], y1 = key[i1 ^ j];
+                    x0 = keep(x0, y0, ((i0 & j) == 0) == ((i0 & k) == 0));
+                    x1 = keep(x1, y1, ((i1 & j) == 0) == ((i1 & k) == 0));
+                }
+            } else if (wact) {  // j < min(P, 32): lane ^ j < P for every lane < P
+                const unsigned long long y0 = __shfl_xor_sync(0xFFFFFFFFu, x0, j);
+                const unsigned long long y1 = __shfl_xor_sync(0xFFFFFFFFu, x1, j);
+                if (on) {
+                    x0 = keep(x0, y0, ((i0 & j) == 0) == ((i0 & k) == 0));
+                    x1 = keep(x1, y1, ((i1 & j) == 0) == ((i1 & k) == 0));
                 }
             }
-            // a block barrier when this or the next substep crosses warps (j >= 64);
-            // jn = the next substep's j (k: the next stage's first)
-            const int jn = j > 1 ? j >> 1 : k;
-            if ((j >= 64 || jn >= 64) && (j > 1 || k < n)) __syncthreads(); else __syncwarp();
         }
+    }
+    __syncthreads();
+    if (on) {
+        key[i0] = x0;
+        key[i1] = x1;
     }
     __syncthreads();
 }
@@ -98,7 +126,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     const int32_t *len, const uint8_t *active, const int32_t *order, int32_t N, int32_t W,
     int32_t B, int32_t min_group, int32_t *window, int32_t *window_size, int32_t *batch_of,
     int32_t *slot_of, int32_t *members, int32_t *mlen, int32_t *mpad, uint8_t *mactive,
-    int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters) {
+    int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters, int exp) {
     pdl_wait();
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -129,6 +157,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     }
     const int Wn = min(filled, W);
     __syncthreads();
+    if (exp == 1) return;  // timing probe only (SPECDEC_K4_EXP): up to RefillWindow
     // ---- 2. length histogram: sort (length, window position), groups = equal-length runs
     int n2 = 1;
     while (n2 < Wn) n2 <<= 1;
@@ -138,6 +167,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
                            : ~0ull;
     __syncthreads();
     block_bitonic_sort(sm.key, n2);
+    if (exp == 2) return;  // probe: + the member sort
     int n_groups = 0;
     for (int base = 0; base < Wn; base += T) {  // group id = number of run heads before
         const int i = base + tid;
@@ -184,6 +214,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
             : ~0ull;
     __syncthreads();
     block_bitonic_sort(sm.key, g2);
+    if (exp == 3) return;  // probe: + groups and the group sort
     int run = 0;
     for (int base = 0; base < n_groups; base += T) {  // gbase: exclusive scan of nsb in that order
         const int q = base + tid;
@@ -220,6 +251,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
         n_left += tot;
     }
     const int nb_total = tot_same + (n_left + B - 1) / B;
+    if (exp == 4) return;  // probe: + member placement scans
     for (int b = tid; b < nb_total; b += T) {
         sm.bmax[b] = 0;
         sm.bmin[b] = 0x7FFFFFFF;
@@ -298,6 +330,7 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
         return SPECDEC_ERR_ARG;
     if (reinterpret_cast<uintptr_t>(d_counters) & 7u) return SPECDEC_ERR_ARG;
     static bool attr_done = false;
+    static const int exp = getenv("SPECDEC_K4_EXP") ? atoi(getenv("SPECDEC_K4_EXP")) : 0;
     const int smem = static_cast<int>(sizeof(PoolSmem));
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(pool_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -312,5 +345,5 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
     return launch_k(pool_group_kernel, dim3(1), dim3(threads), smem,
                     reinterpret_cast<cudaStream_t>(stream), d_len, d_active, d_order, N, W, B,
                     min_group, d_window, d_window_size, d_batch_of, d_slot_of, d_members, d_mlen,
-                    d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches, d_counters);
+                    d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches, d_counters, exp);
 }
