@@ -73,22 +73,26 @@ struct PoolSmem {
 // thread's own two elements, and only 32 <= j < P goes through shared memory (two block
 // barriers) -- 14 of the 55 substeps at n = 1024.  (The former all-shared-memory version,
 // with an integer division per pair, took 11.5 us at n = 1024; profiles/r01/k4bench.txt.)
-__device__ __forceinline__ unsigned long long keep(unsigned long long x, unsigned long long y, bool lo) {
+// 32-bit keys (the common case, see the callers) halve the shuffles and compares of the
+// dependent chain each substep is.
+template <typename K>
+__device__ __forceinline__ K keep(K x, K y, bool lo) {
     return lo ? (x < y ? x : y) : (x > y ? x : y);
 }
 
-__device__ void block_bitonic_sort(unsigned long long *key, int n) {
+template <typename K>
+__device__ void block_bitonic_sort(K *key, int n) {
     const int tid = threadIdx.x;
     const int P = n >> 1;
     const bool on = tid < P;
     const bool wact = tid < ((P + 31) & ~31);  // whole warps for the shuffles (P < 32: warp 0)
-    unsigned long long x0 = on ? key[tid] : 0ull, x1 = on ? key[tid + P] : 0ull;
+    K x0 = on ? key[tid] : K(0), x1 = on ? key[tid + P] : K(0);
     const int i0 = tid, i1 = tid + P;
     for (int k = 2; k <= n; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             if (j == P) {  // only at k == n: every pair ascending, i0 the lower
                 if (on) {
-                    const unsigned long long lo = x0 < x1 ? x0 : x1, hi = x0 < x1 ? x1 : x0;
+                    const K lo = x0 < x1 ? x0 : x1, hi = x0 < x1 ? x1 : x0;
                     x0 = lo;
                     x1 = hi;
                 }
@@ -100,13 +104,13 @@ __device__ void block_bitonic_sort(unsigned long long *key, int n) {
                 }
                 __syncthreads();
                 if (on) {
-                    const unsigned long long y0 = key[i0 ^ j], y1 = key[i1 ^ j];
+                    const K y0 = key[i0 ^ j], y1 = key[i1 ^ j];
                     x0 = keep(x0, y0, ((i0 & j) == 0) == ((i0 & k) == 0));
                     x1 = keep(x1, y1, ((i1 & j) == 0) == ((i1 & k) == 0));
                 }
             } else if (wact) {  // j < min(P, 32): lane ^ j < P for every lane < P
-                const unsigned long long y0 = __shfl_xor_sync(0xFFFFFFFFu, x0, j);
-                const unsigned long long y1 = __shfl_xor_sync(0xFFFFFFFFu, x1, j);
+                const K y0 = __shfl_xor_sync(0xFFFFFFFFu, x0, j);
+                const K y1 = __shfl_xor_sync(0xFFFFFFFFu, x1, j);
                 if (on) {
                     x0 = keep(x0, y0, ((i0 & j) == 0) == ((i0 & k) == 0));
                     x1 = keep(x1, y1, ((i1 & j) == 0) == ((i1 & k) == 0));
@@ -158,21 +162,39 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     const int Wn = min(filled, W);
     __syncthreads();
     if (exp == 1) return;  // timing probe only (SPECDEC_K4_EXP): up to RefillWindow
-    // ---- 2. length histogram: sort (length, window position), groups = equal-length runs
+    // ---- 2. length histogram: sort (length, window position), groups = equal-length runs.
+    // Keys are 32-bit, (length << 11) | position, when every window length is in [0, 2^20)
+    // (position < W <= 2048), else 64-bit (length << 32) | position.
     int n2 = 1;
     while (n2 < Wn) n2 <<= 1;
-    for (int i = tid; i < n2; i += T)
-        sm.key[i] = i < Wn ? (static_cast<unsigned long long>(static_cast<uint32_t>(sm.wlen[i])) << 32) |
-                                 static_cast<uint32_t>(i)
-                           : ~0ull;
-    __syncthreads();
-    block_bitonic_sort(sm.key, n2);
+    int big = 0;
+    for (int i = tid; i < Wn; i += T) big |= (sm.wlen[i] < 0 || sm.wlen[i] >= (1 << 20)) ? 1 : 0;
+    const bool wide = __syncthreads_or(big) != 0;
+    uint32_t *key32 = reinterpret_cast<uint32_t *>(sm.key);
+    if (wide) {
+        for (int i = tid; i < n2; i += T)
+            sm.key[i] = i < Wn ? (static_cast<unsigned long long>(static_cast<uint32_t>(sm.wlen[i])) << 32) |
+                                     static_cast<uint32_t>(i)
+                               : ~0ull;
+        __syncthreads();
+        block_bitonic_sort(sm.key, n2);
+    } else {
+        for (int i = tid; i < n2; i += T)
+            key32[i] = i < Wn ? (static_cast<uint32_t>(sm.wlen[i]) << 11) | static_cast<uint32_t>(i) : ~0u;
+        __syncthreads();
+        block_bitonic_sort(key32, n2);
+    }
+    // the i-th sorted member's length class and window position
+    auto klen = [&](int i) -> uint32_t { return wide ? static_cast<uint32_t>(sm.key[i] >> 32) : key32[i] >> 11; };
+    auto kpos = [&](int i) -> int {
+        return wide ? static_cast<int>(sm.key[i] & 0xFFFFFFFFull) : static_cast<int>(key32[i] & 0x7FFu);
+    };
     if (exp == 2) return;  // probe: + the member sort
     int n_groups = 0;
     for (int base = 0; base < Wn; base += T) {  // group id = number of run heads before
         const int i = base + tid;
         int head = 0;
-        if (i < Wn) head = (i == 0 || (sm.key[i] >> 32) != (sm.key[i - 1] >> 32)) ? 1 : 0;
+        if (i < Wn) head = (i == 0 || klen(i) != klen(i - 1)) ? 1 : 0;
         int tot;
         const int g = n_groups + block_exclusive_scan(head, sm.warp, tot);
         if (head) sm.gstart[g] = i;
@@ -187,7 +209,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
             const int mid = (lo + hi + 1) >> 1;
             if (sm.gstart[mid] <= i) lo = mid; else hi = mid - 1;
         }
-        const int w = static_cast<int>(sm.key[i] & 0xFFFFFFFFull);
+        const int w = kpos(i);
         sm.grp[w] = lo;
         sm.rank[w] = i - sm.gstart[lo];
     }
@@ -207,18 +229,19 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     __syncthreads();
     int g2 = 1;
     while (g2 < n_groups) g2 <<= 1;
-    for (int g = tid; g < g2; g += T)   // key: (-count, length) ascending; group id in the low bits
-        sm.key[g] = g < n_groups
-            ? (static_cast<unsigned long long>(kPoolMaxW - (sm.gstart[g + 1] - sm.gstart[g])) << 32) |
-                  static_cast<unsigned long long>(g)  // ids ascend with the length: (-count, length)
-            : ~0ull;
+    // key: (-count, length) ascending, 32-bit: (2048 - count) << 11 | group id (ids ascend
+    // with the length; count in [1, 2048], id < 2048)
+    for (int g = tid; g < g2; g += T)
+        key32[g] = g < n_groups
+            ? (static_cast<uint32_t>(kPoolMaxW - (sm.gstart[g + 1] - sm.gstart[g])) << 11) | static_cast<uint32_t>(g)
+            : ~0u;
     __syncthreads();
-    block_bitonic_sort(sm.key, g2);
+    block_bitonic_sort(key32, g2);
     if (exp == 3) return;  // probe: + groups and the group sort
     int run = 0;
     for (int base = 0; base < n_groups; base += T) {  // gbase: exclusive scan of nsb in that order
         const int q = base + tid;
-        const int g = q < n_groups ? static_cast<int>(sm.key[q] & 0xFFFFFFFFull) : 0;
+        const int g = q < n_groups ? static_cast<int>(key32[q] & 0x7FFu) : 0;
         const int v = q < n_groups ? sm.nsb[g] : 0;
         int tot;
         const int before = run + block_exclusive_scan(v, sm.warp, tot);
