@@ -73,15 +73,14 @@ struct PoolSmem {
 // thread's own two elements, and only 32 <= j < P goes through shared memory (two block
 // barriers) -- 14 of the 55 substeps at n = 1024.  (The former all-shared-memory version,
 // with an integer division per pair, took 11.5 us at n = 1024; profiles/r01/k4bench.txt.)
-// 32-bit keys (the common case, see the callers) halve the shuffles and compares of the
-// dependent chain each substep is.
+// Generic (64-bit keys: window lengths >= 2^20 only).
 template <typename K>
 __device__ __forceinline__ K keep(K x, K y, bool lo) {
     return lo ? (x < y ? x : y) : (x > y ? x : y);
 }
 
 template <typename K>
-__device__ void block_bitonic_sort(K *key, int n) {
+__device__ void block_bitonic_sort_generic(K *key, int n) {
     const int tid = threadIdx.x;
     const int P = n >> 1;
     const bool on = tid < P;
@@ -124,6 +123,90 @@ __device__ void block_bitonic_sort(K *key, int n) {
         key[i1] = x1;
     }
     __syncthreads();
+}
+
+// The 32-bit keys' sort, unrolled for a fixed n = 2^LOGN: thread t < n / E holds the E
+// consecutive elements t*E .. t*E + E - 1, so substeps with j < E are register
+// compare-exchanges, E <= j < 32 E warp shuffles (lane ^ j / E) and only larger j go
+// through shared memory; every direction and partner is a compile-time constant or a
+// bit test on t.
+template <int LOGN>
+__device__ void block_bitonic_sort_fixed(uint32_t *key) {
+    constexpr int n = 1 << LOGN;
+    constexpr int E = n >= 128 ? 4 : 2;
+    constexpr int NT = n / E > 0 ? n / E : 1;
+    const int t = threadIdx.x;
+    const bool on = t < NT;
+    const bool wact = t < ((NT + 31) & ~31);
+    uint32_t x[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) x[r] = (on && t * E + r < n) ? key[t * E + r] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 2; k <= n; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < E) {
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    if ((r & j) == 0) {
+                        const bool up = ((t * E + r) & k) == 0;
+                        const uint32_t a = x[r], b = x[r | j];
+                        const uint32_t lo = min(a, b), hi = max(a, b);
+                        x[r] = up ? lo : hi;
+                        x[r | j] = up ? hi : lo;
+                    }
+                }
+            } else if (j < 32 * E) {
+                if (wact) {
+#pragma unroll
+                    for (int r = 0; r < E; ++r) {
+                        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x[r], j / E);
+                        const int i = t * E + r;
+                        x[r] = (((i & j) == 0) == ((i & k) == 0)) ? min(x[r], y) : max(x[r], y);
+                    }
+                }
+            } else {
+                __syncthreads();  // the previous exchange's reads are done
+                if (on) {
+#pragma unroll
+                    for (int r = 0; r < E; ++r) key[t * E + r] = x[r];
+                }
+                __syncthreads();
+                if (on) {
+#pragma unroll
+                    for (int r = 0; r < E; ++r) {
+                        const int i = t * E + r;
+                        const uint32_t y = key[i ^ j];
+                        x[r] = (((i & j) == 0) == ((i & k) == 0)) ? min(x[r], y) : max(x[r], y);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (on) {
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+            if (t * E + r < n) key[t * E + r] = x[r];
+    }
+    __syncthreads();
+}
+
+__device__ void block_bitonic_sort(uint32_t *key, int n) {
+    switch (n) {
+        case 1: break;
+        case 2: block_bitonic_sort_fixed<1>(key); break;
+        case 4: block_bitonic_sort_fixed<2>(key); break;
+        case 8: block_bitonic_sort_fixed<3>(key); break;
+        case 16: block_bitonic_sort_fixed<4>(key); break;
+        case 32: block_bitonic_sort_fixed<5>(key); break;
+        case 64: block_bitonic_sort_fixed<6>(key); break;
+        case 128: block_bitonic_sort_fixed<7>(key); break;
+        case 256: block_bitonic_sort_fixed<8>(key); break;
+        case 512: block_bitonic_sort_fixed<9>(key); break;
+        case 1024: block_bitonic_sort_fixed<10>(key); break;
+        default: block_bitonic_sort_fixed<11>(key); break;
+    }
 }
 
 __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
@@ -177,7 +260,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
                                      static_cast<uint32_t>(i)
                                : ~0ull;
         __syncthreads();
-        block_bitonic_sort(sm.key, n2);
+        block_bitonic_sort_generic(sm.key, n2);
     } else {
         for (int i = tid; i < n2; i += T)
             key32[i] = i < Wn ? (static_cast<uint32_t>(sm.wlen[i]) << 11) | static_cast<uint32_t>(i) : ~0u;
