@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "host_util.h"
+#include "pool_gate.h"
 #include "specdec.h"
 
 using namespace specdec;
@@ -227,40 +228,10 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
 // ----------------------------------------------------------------------------- Alg. 3 loop
 // Alg. 3 as printed: GetBatch -> verify -> write-back -> RefillWindow,
 // one batch per iteration, each iteration re-planning the window -- here without any host
-// synchronisation: a tiny gate kernel reads batch 0's header on the device and gates the
-// gather / scatter (row map -1 = skip) and the verify (no active row) of a same-length or
-// empty plan, so `iterations` iterations are enqueued back to back.  Iterations after the
+// synchronisation: K4's tail (the gate, pool_gate.h) writes batch 0 as row maps that gate
+// the gather / scatter (row map -1 = skip) and the verify (no active row) of a same-length
+// or empty plan, so `iterations` iterations are enqueued back to back.  Iterations after the
 // pool drains are no-ops.
-namespace specdec {
-__global__ void alg3_gate_kernel(const int32_t *n_batches, const uint8_t *bkind, const int32_t *members0,
-                                 const uint8_t *mactive0, const int32_t *bsize, const int32_t *blen,
-                                 int dense, int B, int32_t *g_members, int32_t *g_kv, int32_t *g_scol,
-                                 uint8_t *g_active, unsigned long long *exec) {
-    pdl_wait();
-    pdl_launch_dependents();
-    const int j = threadIdx.x;
-    const bool valid = *n_batches > 0;
-    const bool same = valid && bkind[0] != 0;
-    const bool moves = valid && (!same || dense);  // the batch goes through the staging
-    if (j < B) {
-        const int32_t m = members0[j];
-        g_members[j] = valid ? m : -1;
-        g_active[j] = valid ? mactive0[j] : 0;
-        g_kv[j] = moves ? m : -1;
-        g_scol[j] = blen[0] - 1;
-    }
-    if (j == 0 && exec && valid) {  // executed batches, same-length ones, their members, fallback members
-        atomicAdd(exec, 1ull);
-        if (same) {
-            atomicAdd(exec + 1, 1ull);
-            atomicAdd(exec + 2, static_cast<unsigned long long>(bsize[0]));
-        } else {
-            atomicAdd(exec + 3, static_cast<unsigned long long>(bsize[0]));
-        }
-    }
-}
-}  // namespace specdec
-
 extern "C" int specdec_pool_alg3(const specdec_pool_desc *d, int32_t iterations, int32_t *d_scratch,
                                  unsigned long long *d_exec_counters, specdec_stream_t stream) {
     if (!d || !d_scratch || d->W < 1 || d->B < 1 || d->B > 1024 || iterations < 0) return SPECDEC_ERR_ARG;
@@ -273,18 +244,18 @@ extern "C" int specdec_pool_alg3(const specdec_pool_desc *d, int32_t iterations,
     const int64_t s_plane = B * hcd, s_row = hcd, s_head = d->cap * d->D;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const uint32_t gflags = d->gather_ws ? SPECDEC_DYNAMIC : 0u;
+    Alg3Gate gate;
+    gate.members = g_members;
+    gate.kv = g_kv;
+    gate.scol = g_scol;
+    gate.active = g_active;
+    gate.exec = d_exec_counters;
+    gate.dense = d->dense_consumer ? 1 : 0;
     for (int32_t it = 0; it < iterations; ++it) {
-        int rc = specdec_pool_group(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
-                                    d->window_size, d->batch_of, d->slot_of, d->members, d->mlen,
-                                    d->mpad, d->mactive, d->bsize, d->bkind, d->blen, d->n_batches,
-                                    d->counters, stream);
-        if (rc) return rc;
-        rc = launch_k(alg3_gate_kernel, dim3(1), dim3(((B + 31) / 32) * 32), 0, s,
-                      static_cast<const int32_t *>(d->n_batches), static_cast<const uint8_t *>(d->bkind),
-                      static_cast<const int32_t *>(d->members), static_cast<const uint8_t *>(d->mactive),
-                      static_cast<const int32_t *>(d->bsize), static_cast<const int32_t *>(d->blen),
-                      d->dense_consumer ? 1 : 0, static_cast<int>(B), g_members, g_kv, g_scol, g_active,
-                      d_exec_counters);
+        int rc = pool_group_launch(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
+                                   d->window_size, d->batch_of, d->slot_of, d->members, d->mlen, d->mpad,
+                                   d->mactive, d->bsize, d->bkind, d->blen, d->n_batches, d->counters, gate,
+                                   stream);
         if (rc) return rc;
         // fallback batch 0: pool slots [0, len-1) -> staging, right-aligned (rows -1: skipped)
         rc = specdec_realign_kv(d->kv, d->staging, d->kv_dtype, d->n_planes, B, d->H, d->D, p_plane, p_row,

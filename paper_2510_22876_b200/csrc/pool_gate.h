@@ -1,0 +1,30 @@
+// pool_gate.h -- internal (not part of the C ABI): K4 with the Alg. 3 device loop's gate
+// fused into its tail (pool_group.cu, used by specdec_pool_alg3 in pool_exec.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "specdec.h"
+
+namespace specdec {
+
+// Batch 0 of the plan as the row maps of the iteration's gather / verify / scatter:
+// members (or -1), active flags, the KV rows to move (-1 unless batch 0 goes through the
+// staging) and the scatter column (width - 1); exec counts executed batches, same-length
+// ones, their members and fallback members.  members == nullptr: no gate.
+struct Alg3Gate {
+    int32_t *members = nullptr, *kv = nullptr, *scol = nullptr;
+    uint8_t *active = nullptr;
+    unsigned long long *exec = nullptr;
+    int dense = 0;
+};
+
+int pool_group_launch(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order, int32_t N,
+                      int32_t W, int32_t B, int32_t min_group, int32_t *d_window, int32_t *d_window_size,
+                      int32_t *d_batch_of, int32_t *d_slot_of, int32_t *d_members, int32_t *d_mlen,
+                      int32_t *d_mpad, uint8_t *d_mactive, int32_t *d_bsize, uint8_t *d_bkind,
+                      int32_t *d_blen, int32_t *d_n_batches, int64_t *d_counters, const Alg3Gate &gate,
+                      specdec_stream_t stream);
+
+}  // namespace specdec

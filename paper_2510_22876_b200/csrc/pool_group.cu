@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "host_util.h"
+#include "pool_gate.h"
 
 namespace specdec {
 
@@ -213,7 +214,8 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     const int32_t *len, const uint8_t *active, const int32_t *order, int32_t N, int32_t W,
     int32_t B, int32_t min_group, int32_t *window, int32_t *window_size, int32_t *batch_of,
     int32_t *slot_of, int32_t *members, int32_t *mlen, int32_t *mpad, uint8_t *mactive,
-    int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters, int exp) {
+    int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters, Alg3Gate gate,
+    int exp) {
     pdl_wait();
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -414,6 +416,31 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
         atomicAdd(reinterpret_cast<unsigned long long *>(counters + 5), static_cast<unsigned long long>(Wn));
         atomicAdd(reinterpret_cast<unsigned long long *>(counters + 6), static_cast<unsigned long long>(n_groups));
     }
+    if (gate.members) {
+        // Alg. 3 device loop: batch 0 as the row maps of this iteration's gather / verify /
+        // scatter (one launch fewer than a separate gate kernel).  The barrier makes this
+        // block's stores of batch 0's members / mactive visible to every thread.
+        __syncthreads();
+        const bool valid = nb_total > 0;
+        const bool same = valid && sm.bmax[0] == sm.bmin[0];
+        const bool moves = valid && (!same || gate.dense);  // batch 0 goes through the staging
+        for (int j = tid; j < B; j += T) {
+            const int32_t m = valid ? members[j] : -1;
+            gate.members[j] = m;
+            gate.active[j] = valid ? mactive[j] : 0;
+            gate.kv[j] = moves ? m : -1;
+            gate.scol[j] = (valid ? sm.bmax[0] : 0) - 1;
+        }
+        if (tid == 0 && gate.exec && valid) {
+            atomicAdd(gate.exec, 1ull);
+            if (same) {
+                atomicAdd(gate.exec + 1, 1ull);
+                atomicAdd(gate.exec + 2, static_cast<unsigned long long>(sm.bcnt[0]));
+            } else {
+                atomicAdd(gate.exec + 3, static_cast<unsigned long long>(sm.bcnt[0]));
+            }
+        }
+    }
 }
 
 }  // namespace specdec
@@ -428,6 +455,17 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
                                   int32_t *d_bsize, uint8_t *d_bkind, int32_t *d_blen,
                                   int32_t *d_n_batches, int64_t *d_counters,
                                   specdec_stream_t stream) {
+    return pool_group_launch(d_len, d_active, d_order, N, W, B, min_group, d_window, d_window_size, d_batch_of,
+                             d_slot_of, d_members, d_mlen, d_mpad, d_mactive, d_bsize, d_bkind, d_blen,
+                             d_n_batches, d_counters, Alg3Gate{}, stream);
+}
+
+int specdec::pool_group_launch(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order, int32_t N,
+                               int32_t W, int32_t B, int32_t min_group, int32_t *d_window,
+                               int32_t *d_window_size, int32_t *d_batch_of, int32_t *d_slot_of,
+                               int32_t *d_members, int32_t *d_mlen, int32_t *d_mpad, uint8_t *d_mactive,
+                               int32_t *d_bsize, uint8_t *d_bkind, int32_t *d_blen, int32_t *d_n_batches,
+                               int64_t *d_counters, const Alg3Gate &gate, specdec_stream_t stream) {
     if (N < 1 || W < 1 || W > kPoolMaxW || B < 1 || B > W) return SPECDEC_ERR_SHAPE;
     if (min_group < 1) return SPECDEC_ERR_ARG;
     if (!d_len || !d_active || !d_order || !d_window || !d_window_size || !d_batch_of ||
@@ -451,5 +489,5 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
     return launch_k(pool_group_kernel, dim3(1), dim3(threads), smem,
                     reinterpret_cast<cudaStream_t>(stream), d_len, d_active, d_order, N, W, B,
                     min_group, d_window, d_window_size, d_batch_of, d_slot_of, d_members, d_mlen,
-                    d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches, d_counters, exp);
+                    d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches, d_counters, gate, exp);
 }
