@@ -500,9 +500,9 @@ int specdec_eqspec_round_host(const specdec_round_desc *d, const specdec_host_io
 /* specdec_pool_alg3 -- `iterations` iterations of Alg. 3 as printed:
  * specdec_pool_group over the window, then batch 0 of the plan only (gather if it is a
  * fallback batch, specdec_pool_verify with the write-back, scatter), then re-plan -- all
- * enqueued on `stream` with NO host synchronisation: a one-CTA gate kernel reads batch 0's
- * header on the device and hands the gather / verify / scatter gated member rows (-1 or
- * inactive for the parts that must not run).  Iterations after the pool drains are no-ops;
+ * enqueued on `stream` with NO host synchronisation: the plan kernel's tail writes batch
+ * 0 as gated member rows for the gather / verify / scatter (-1 or inactive for the parts
+ * that must not run).  Iterations after the pool drains are no-ops;
  * the caller checks `active` between calls.  Inputs come from the descriptor's ring (one
  * slot per iteration); the staging is `staging`; `gather_ws` as in specdec_pool_epoch.
  * d_scratch: device int32 [4 * B] (caller-owned, contents don't-care).
