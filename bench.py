@@ -38,7 +38,7 @@ METRIC = "verify+realign rounds/s (B=8,k=5); KV-realign HBM GB/s vs ~8 TB/s peak
 RING = 16
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
@@ -89,7 +89,7 @@ def parse():
                     choices=["graph-block", "graph-fork", "graph-serial", "direct-fork", "direct-serial"],
                     help="value region: CUDA graphs of one episode of rounds (block), one graph per "
                          "round, or direct launches; K3 forked under K2 or serial")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def peaks():
@@ -256,6 +256,28 @@ class RoundBench:
             bt.anchor.fill_(bt.anchor_slack)
         bt.cur = 0
 
+    def capture_block(self, episode_len, hook=None):
+        """One CUDA graph per episode: the episode's state reset (3 device copies) and its
+        `episode_len` rounds (ring slot r % RING, parity alternating; an even count, so the
+        graph ends at the parity it starts from).  `hook(r, stream)`, if given, is captured
+        after round r (tests: snapshots of the per-round results); the bench passes none."""
+        import torch
+        bt = self.bt
+        self.reset()
+        cs = torch.cuda.Stream(self.dev)
+        cs.wait_stream(self.stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cs), torch.cuda.graph(g, stream=cs):
+            self.reset_fast()
+            for r in range(episode_len):
+                bt.launch_round(self.logits[r % RING], self.drafts[r % RING], stream=cs)
+                if hook is not None:
+                    hook(r, cs)
+                bt.cur = 1 - bt.cur
+        self.stream.wait_stream(cs)
+        torch.cuda.synchronize()
+        return g
+
     def episode(self, r, episode_len):
         if episode_len and r and r % episode_len == 0:
             self.reset_fast()
@@ -326,17 +348,7 @@ def run_ours(args, rank, world, device):
     block = None
     blk = args.episode
     if args.round_mode == "graph-block" and blk and blk % RING == 0 and blk % 2 == 0:
-        rb.reset()
-        cs = torch.cuda.Stream(device)
-        cs.wait_stream(rb.stream)
-        block = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(cs), torch.cuda.graph(block, stream=cs):
-            rb.reset_fast()
-            for r in range(blk):
-                bt.launch_round(rb.logits[r % RING], rb.drafts[r % RING], stream=cs)
-                bt.cur = 1 - bt.cur
-        rb.stream.wait_stream(cs)
-        torch.cuda.synchronize()
+        block = rb.capture_block(blk)
 
     def one_round(r):
         if use_graph:

@@ -57,6 +57,7 @@ typedef struct CUstream_st *specdec_stream_t; /* == cudaStream_t */
 #define SPECDEC_OVERLAP_PREV 2u /* start under the previous kernel on the stream (see below) */
 #define SPECDEC_DYNAMIC 4u      /* dynamic work tickets from the workspace header (see below) */
 #define SPECDEC_SEGMENTED 8u    /* in place: cut slabs into segments (workspace slots) */
+#define SPECDEC_DYNAMIC_FORCE 16u /* with SPECDEC_DYNAMIC: tickets even for few units per CTA */
 
 /* ------------------------------------------------------------------------------ misc */
 int specdec_version(void);                /* ABI version (major*100 + minor) */
@@ -161,6 +162,9 @@ int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_tokens_out, 
  *   and every plane (layer x {K,V}) and KV head h:
  *       dst[plane, drow, h, dcol + c, :] = src[plane, srow, h, scol + c, :]   c < cnt_r
  *
+ *   and no other byte of dst is written (except the SPECDEC_ZERO_PADS columns): in place,
+ *   every column outside a row's destination range keeps its value.
+ *
  * EqSpec in place: kv_dst == kv_src, src_col = pad_old, dst_col = pad_new, count = kept.
  * Rows whose source and destination coincide move nothing.  Each (plane, row, head)
  * slab is streamed by one CTA in the hazard-free direction through a TMA bulk-copy
@@ -185,15 +189,20 @@ int specdec_rebuild_pos_mask(const int64_t *d_tokens_in, int64_t *d_tokens_out, 
  *   off.
  *   SPECDEC_DYNAMIC: the streaming CTAs take work units from a ticket counter in the
  *   workspace header instead of a static assignment, so CTAs that stream faster take more
- *   units (measured +1 % at Qwen3 B=8, +1.2 % Vicuna).  Needs d_ws.
+ *   units (measured +1 % at Qwen3 B=8, +1.2 % Vicuna).  Needs d_ws.  With fewer than ~8
+ *   units per CTA the static assignment is as balanced and avoids the ticket round trips,
+ *   so the library then ignores SPECDEC_DYNAMIC unless SPECDEC_DYNAMIC_FORCE is also set
+ *   (tests use it to exercise the ticket path on small problems).
  *   SPECDEC_SEGMENTED (in place): every slab is cut into ~128 KB segments that any CTA can
  *   stream independently: the rows a segment's neighbour overwrites (|dcol - scol| rows,
  *   <= 4 KB) are first copied to a workspace slot by a small kernel on the same stream.
  *   Without it a slab is one unit in place (correct; less balanced when few rows move).
  *   Needs d_ws.  Distinct buffers are always segmented (no slots needed).
  * d_ws / ws_bytes: device workspace (16-B aligned) for SPECDEC_DYNAMIC / SPECDEC_SEGMENTED:
- *   a 128-byte header -- the dynamic-schedule counters, which must be ZERO before the first
- *   call and are left zero by every call -- then the segment slots.  Size: 128 bytes for
+ *   a 128-byte header -- the dynamic-schedule counters (uint32 words 0-1), which must be
+ *   ZERO before the first call and are left zero by every call; words 2-3 are diagnostics
+ *   that only accumulate (dynamic launches completed, work units streamed by ticket) and
+ *   are never read by the library -- then the segment slots.  Size: 128 bytes for
  *   SPECDEC_DYNAMIC alone, specdec_realign_workspace_size(dtype, n_planes, n_rows, H, D,
  *   cap_src) with SPECDEC_SEGMENTED.  Calls that share a workspace must not run
  *   concurrently (stream-ordered calls are fine).  NULL: static assignment, no segments.

@@ -105,8 +105,13 @@ def copy_rows(src, dst, count, src_col=None, dst_col=None, src_row=None, dst_row
     """Generic row-mapped KV move (a3/a5): for every batch row i with count_i > 0 and
     mapped rows >= 0: dst[dst_row_i][:, :, dst_col_i + c] = src[src_row_i][:, :, src_col_i + c]
     for c < count_i.  src/dst are logical [rows][planes][H][cap][D] views.
-    dst is modified in place; the definition is out-of-place (src is read first)."""
-    src = np.array(src, copy=True)
+    dst is modified in place; no other byte of dst changes.  The definition is
+    out-of-place: every source is read before it is overwritten.  Without row maps row i
+    writes only row i, so reading each row's source block before writing it is enough
+    (also when dst is src: the in-place realign); with row maps and aliasing buffers the
+    whole source is copied first."""
+    if (src_row is not None or dst_row is not None) and np.shares_memory(src, dst):
+        src = np.array(src, copy=True)
     for i in range(len(count)):
         c = int(count[i])
         sr = i if src_row is None else int(src_row[i])
@@ -115,8 +120,20 @@ def copy_rows(src, dst, count, src_col=None, dst_col=None, src_row=None, dst_row
             continue
         sc = 0 if src_col is None else int(src_col[i])
         dc = 0 if dst_col is None else int(dst_col[i])
-        dst[dr, :, :, dc:dc + c, :] = src[sr, :, :, sc:sc + c, :]
+        block = np.array(src[sr, :, :, sc:sc + c, :], copy=True)
+        dst[dr, :, :, dc:dc + c, :] = block
     return dst
+
+
+def realign_kv_inplace(kv, pad_old, pad_new, kept):
+    """Realign in the in-place form K2's contract states (specdec.h): for
+    every row i, plane and head, KV[.., i, h, p'_i + c, :] <- KV[.., i, h, p_i + c, :] for
+    c < kept_i (the row's source read before it is written), and NO other byte changes --
+    so the whole buffer, stale columns included, is defined and comparable.
+    kv [planes, B, H, cap, D] is modified in place and returned."""
+    rows = np.moveaxis(kv, 1, 0)                 # view [B, planes, H, cap, D]
+    copy_rows(rows, rows, kept, src_col=pad_old, dst_col=pad_new)
+    return kv
 
 
 def anchor_plan(pad_old, pad_new, kept, finished, accept, L_old, L_new, base, cap_phys, k):
@@ -126,7 +143,9 @@ def anchor_plan(pad_old, pad_new, kept, finished, accept, L_old, L_new, base, ca
     move: logical column c lives at physical base + c.  Per round the new origin
     base' = base + d is chosen among d = 0 and the shifts that leave one accept class in
     place, d = (a + 1) - (L' - L), minimising the KV rows that must move (ties: d = 0,
-    then larger d), subject to 0 <= base' and base' + L' + k <= cap_phys.
+    then larger d), subject to 0 <= base' and base' + L' + k <= cap_phys.  If no candidate
+    is feasible (the origin sits too high for the grown width), the feasible shift closest
+    to 0 is taken (every kept row moves; none exists only if L' + k > cap_phys).
     Returns (base', physical old columns, physical new columns)."""
     pad_old = np.asarray(pad_old, np.int64)
     pad_new = np.asarray(pad_new, np.int64)
@@ -143,6 +162,10 @@ def anchor_plan(pad_old, pad_new, kept, finished, accept, L_old, L_new, base, ca
                            if alive[i] and kept[i] > 0 and d + pad_new[i] != pad_old[i]))
             if best_cost is None or cost < best_cost:
                 best_d, best_cost = d, cost
+        if best_cost is None:
+            lo, hi = -base, cap_phys - L_new - k - base
+            if lo <= hi:
+                best_d = min(max(0, lo), hi)
     base_new = base + best_d
     return base_new, (base + pad_old).astype(np.int32), (base_new + pad_new).astype(np.int32)
 

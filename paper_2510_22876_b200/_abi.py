@@ -21,6 +21,7 @@ ZERO_PADS = 1
 OVERLAP_PREV = 2
 DYNAMIC = 4
 SEGMENTED = 8
+DYNAMIC_FORCE = 16
 DTYPE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
 # kernels one specdec_verify / specdec_pool_verify launches: the argmax grid and the
 # one-CTA epilogue behind it (SPECDEC_K1_SPLIT=0: one kernel, last-CTA epilogue)
@@ -122,6 +123,7 @@ class HostIO(ctypes.Structure):
 
 def specdec_eqspec_round(desc: RoundDesc, parity, logits, draft, stream=None):
     """One EqSpec round (K1 -> K3 -> K2) in the native driver."""
+    _check_logits(logits)
     _check(load().specdec_eqspec_round(ctypes.byref(desc), parity, _ptr(logits), _ptr(draft),
                                        _stream(stream)), "specdec_eqspec_round")
 
@@ -228,11 +230,22 @@ def specdec_verify_workspace_size(B: int, k: int) -> int:
     return load().specdec_verify_workspace_size(B, k)
 
 
+def _check_logits(logits):
+    """The kernels read row (i, j) at (i * (k+1) + j) * row_stride with unit element stride:
+    a view whose batch stride is not (k+1) * row_stride (e.g. logits[:, -(k+1):] of a
+    [B, T, V] forward output) would be read wrongly, so it is refused."""
+    if logits.dim() != 3 or logits.stride(2) != 1 or logits.stride(0) != logits.shape[1] * logits.stride(1):
+        raise SpecdecError(f"logits must be [B, k+1, row_stride] with batch stride (k+1)*row_stride and "
+                           f"unit last stride (got shape {tuple(logits.shape)}, strides {logits.stride()}); "
+                           "pass .contiguous()")
+
+
 def specdec_verify(logits, draft, n, active, accept, bonus, emit, finished, plan_L, n_new,
                    pad_new, kept, ws, *, V=None, eos_id=-1, pad_id=0, budget=None, pred=None,
                    kept_draft=None, anchor=None, anchor_cap=0, phys_old=None, phys_new=None,
                    status=None, stream=None):
     """logits [B, k+1, row_stride] (fp32/fp16/bf16); see include/specdec.h."""
+    _check_logits(logits)
     B, K1, rs = logits.shape
     _check(load().specdec_verify(
         _ptr(logits), DTYPE[logits.dtype], B, K1 - 1, rs if V is None else V, logits.stride(1),
@@ -280,6 +293,7 @@ def specdec_pool_verify(logits, draft, members, mlen, mactive, accept, bonus, em
                         pool_len, pool_gen, pool_active, ws, *, V=None, eos_id=-1, pad_id=0,
                         max_new, pool_tokens=None, out_buf=None, status=None, stream=None):
     """K1 + the pool write-back in one launch (include/specdec.h)."""
+    _check_logits(logits)
     B, K1, _ = logits.shape
     _check(load().specdec_pool_verify(
         _ptr(logits), DTYPE[logits.dtype], B, K1 - 1, V or logits.shape[2], logits.stride(1),

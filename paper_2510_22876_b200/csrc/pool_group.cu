@@ -303,10 +303,14 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     for (int g = tid; g < n_groups; g += T) {
         const int c = sm.gstart[g + 1] - sm.gstart[g];
         int nb = 0, m = 0;
-        if (c >= mg) {
-            const int full = c / B, rem = c % B;
+        // batches of min(B, remaining) while remaining >= mg (R11), in closed form
+        if (c >= mg && mg <= B) {
+            const int full = c / B, rem = c % B;  // every full batch starts with >= B >= mg left
             nb = full + (rem >= mg ? 1 : 0);
             m = full * B + (rem >= mg ? rem : 0);
+        } else if (c >= mg) {                     // mg > B: only full batches, while >= mg left
+            nb = (c - mg) / B + 1;
+            m = nb * B;
         }
         sm.nsb[g] = nb;
         sm.matched[g] = m;

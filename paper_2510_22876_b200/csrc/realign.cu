@@ -37,8 +37,8 @@ constexpr int kZeroBytes = 2048;
 constexpr int64_t kSegBytes = 128 * 1024;     // target bytes per work unit
 constexpr int64_t kSlotBytes = 4096;          // boundary slot: |shift| * row bytes <= this
 static int g_ctas_per_sm = 0;                 // tuning override (SPECDEC_REALIGN_CTAS)
-static int64_t g_grid_cap = 0;
-constexpr int64_t kWsHeader = 128;            // workspace header: the dynamic-schedule counters                // tuning override (SPECDEC_REALIGN_GRID): max CTAs
+static int64_t g_grid_cap = 0;                // tuning override (SPECDEC_REALIGN_GRID): max CTAs
+constexpr int64_t kWsHeader = 128;            // workspace header: the dynamic-schedule counters
 static int64_t g_seg_bytes = kSegBytes;       // tuning override (SPECDEC_REALIGN_SEG, >= default)
 
 __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -313,6 +313,9 @@ __global__ void __launch_bounds__(32 * kSmallWarps) realign_small_kernel(Realign
 #pragma unroll
         for (int q = 0; q < kSmallVec; ++q)  // plain (coherent) loads: in place, dst aliases src
             if (lane + q * 32 < nv) v[q] = reinterpret_cast<const uint4 *>(src)[lane + q * 32];
+        // in place a lane's stores can hit another lane's source vectors: every lane's loads
+        // complete before any lane stores (independent thread scheduling gives no such order)
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < kSmallVec; ++q)
             if (lane + q * 32 < nv) reinterpret_cast<uint4 *>(dst)[lane + q * 32] = v[q];
@@ -376,11 +379,16 @@ __device__ __forceinline__ void iter_unit(const RealignParams &p, const RealignS
 // CTAs that stream faster take more units and all finish within about one unit of each
 // other.  Each CTA reports once when done; the last one leaves both counters zero for
 // the next call, so a workspace is reusable by stream-ordered calls.
-__device__ __forceinline__ void dyn_done(const RealignParams &p) {
+// Diagnostics in the same header (never read by the schedule): sched[2] counts completed
+// dynamic launches, sched[3] the work units streamed by ticket -- tests use them to prove
+// that the ticket path ran.
+__device__ __forceinline__ void dyn_done(const RealignParams &p, unsigned int units_done) {
     if (!p.sched) return;
+    if (units_done) atomicAdd(p.sched + 3, units_done);
     if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
         atomicExch(p.sched, 0u);
         atomicExch(p.sched + 1, 0u);
+        atomicAdd(p.sched + 2, 1u);
     }
 }
 
@@ -397,7 +405,7 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
     fence_proxy_async_smem();  // zero buffer (generic writes) visible to the bulk engine
     __syncwarp();
     if (lane != 0) return;
-    if (sm.t.n_mv == 0) { dyn_done(p); return; }
+    if (sm.t.n_mv == 0) { dyn_done(p, 0u); return; }
 
     const uint64_t pol = p.policy_mode == 0 ? policy_evict_first() : policy_evict_normal();
     ChunkIter it;
@@ -411,9 +419,10 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
     } else {
         it.u = unit_of_round(0, blockIdx.x, it.stride);
     }
-    if (it.u >= it.n_units) { dyn_done(p); return; }
+    if (it.u >= it.n_units) { dyn_done(p, 0u); return; }
     iter_unit<STAGES, CHUNK>(p, sm, it);
     unsigned long long moved = 0;
+    unsigned int units_done = 1;
 
     auto issue = [&](int stage) {
         const Unit &un = it.un;
@@ -457,7 +466,10 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
             } else {
                 it.u = unit_of_round(++it.round, blockIdx.x, it.stride);
             }
-            if (it.u < it.n_units) iter_unit<STAGES, CHUNK>(p, sm, it);
+            if (it.u < it.n_units) {
+                iter_unit<STAGES, CHUNK>(p, sm, it);
+                ++units_done;
+            }
         }
     };
     auto more = [&]() { return it.u < it.n_units; };
@@ -492,7 +504,7 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
     }
     bulk_wait_all<0>();
     if (p.moved && moved) atomicAdd(p.moved, moved);
-    dyn_done(p);
+    dyn_done(p, units_done);
 }
 
 template <int STAGES, int CHUNK>
@@ -547,7 +559,8 @@ int launch_realign(const RealignParams &p, int64_t max_units, cudaStream_t s) {
     // dynamic tickets pay an L2 round trip before the first unit and at exit: with fewer
     // than ~8 units per CTA the static rotation is as balanced and faster (measured: toy
     // rounds 12.2 vs 10.6 us, Qwen3 B=2 -0.6 %; B >= 4 and GLM/Vicuna gain 0.4-1.2 %)
-    if (max_units < 8 * grid) pm.sched = nullptr;
+    // (SPECDEC_DYNAMIC_FORCE keeps the tickets regardless: tests and diagnosis)
+    if (max_units < 8 * grid && !(p.flags & SPECDEC_DYNAMIC_FORCE)) pm.sched = nullptr;
     // One streaming CTA per SM is enforced through shared memory, not left to the CTA
     // scheduler: launched early under PDL, a persistent grid could otherwise double up on
     // the SMs that are free first (measured -5..7 % before this).
@@ -603,8 +616,10 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     if (!d_kv_src || !d_kv_dst || !d_count) return SPECDEC_ERR_ARG;
     if (n_planes < 1 || n_rows < 1 || H < 1 || D < 1 || cap_src < 1 || cap_dst < 1) return SPECDEC_ERR_SHAPE;
     if (n_rows > kRealignMaxRows) return SPECDEC_ERR_SHAPE;
-    if (flags & ~(SPECDEC_ZERO_PADS | SPECDEC_OVERLAP_PREV | SPECDEC_DYNAMIC | SPECDEC_SEGMENTED))
+    if (flags & ~(SPECDEC_ZERO_PADS | SPECDEC_OVERLAP_PREV | SPECDEC_DYNAMIC | SPECDEC_SEGMENTED |
+                  SPECDEC_DYNAMIC_FORCE))
         return SPECDEC_ERR_ARG;
+    if ((flags & SPECDEC_DYNAMIC_FORCE) && !(flags & SPECDEC_DYNAMIC)) return SPECDEC_ERR_ARG;
     const int64_t rb = D * es;
     if (rb % 16 != 0 || !aligned16(d_kv_src) || !aligned16(d_kv_dst)) return SPECDEC_ERR_ARG;
     const int64_t st[6] = {src_s_plane, src_s_row, src_s_head, dst_s_plane, dst_s_row, dst_s_head};

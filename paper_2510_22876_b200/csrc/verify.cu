@@ -202,6 +202,12 @@ __device__ void verify_epilogue(const VerifyParams &p, int32_t pre_sq) {
                 const unsigned long long c = total - s_w[a];
                 if (c < best_cost) { best_cost = c; best = d; }
             }
+            if (best_cost == ~0ull) {
+                // no candidate fits (the origin sits too high for the grown width): the
+                // feasible shift closest to 0 -- every kept row moves, the bound holds
+                const int64_t lo = -base, hi = p.anchor_cap - Lnew - k - base;
+                if (lo <= hi) best = min(max(static_cast<int64_t>(0), lo), hi);
+            }
         }
         s_base[0] = static_cast<int>(base);
         s_base[1] = static_cast<int>(base + best);

@@ -130,11 +130,15 @@ class SequencePool:
                                 self.bkind, self.blen, self.n_batches, self.counters, stream=stream)
         W = self.W
         hdr = self._pinned
-        hdr[0:1].copy_(self.n_batches, non_blocking=True)
-        hdr[1:1 + W].copy_(self.bkind.to(torch.int32), non_blocking=True)
-        hdr[1 + W:1 + 2 * W].copy_(self.blen, non_blocking=True)
-        hdr[1 + 2 * W:1 + 3 * W].copy_(self.bsize, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
+        # the copies are ordered after K4 on the stream it ran on, and that stream is the one
+        # synchronised (a non-current `stream` gets no implicit order with torch's stream)
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        with torch.cuda.stream(s):
+            hdr[0:1].copy_(self.n_batches, non_blocking=True)
+            hdr[1:1 + W].copy_(self.bkind.to(torch.int32), non_blocking=True)
+            hdr[1 + W:1 + 2 * W].copy_(self.blen, non_blocking=True)
+            hdr[1 + 2 * W:1 + 3 * W].copy_(self.bsize, non_blocking=True)
+        s.synchronize()
         nb = int(hdr[0])
         h = hdr.numpy()
         return nb, h[1:1 + nb].copy(), h[1 + W:1 + W + nb].copy(), h[1 + 2 * W:1 + 2 * W + nb].copy()

@@ -200,19 +200,28 @@ def _realign_case(cuda, pad_old, pad_new, kept, D=128, H=3, planes=2, cap=None, 
         ws = torch.full((_abi.specdec_realign_workspace_size(kv.dtype, planes, B, H, D, cap),), 0xAB,
                         dtype=torch.uint8, device=cuda)          # slot contents are don't-care
         flags |= _abi.SEGMENTED
-    if dyn:   # DYNAMIC: work tickets from the (zeroed) 128-byte header
+    if dyn:   # DYNAMIC (+ FORCE: tickets even below 8 units per CTA) from the zeroed header
         if ws is None:
             ws = torch.zeros(128, dtype=torch.uint8, device=cuda)
         ws[:128] = 0
-        flags |= _abi.DYNAMIC
+        flags |= _abi.DYNAMIC | _abi.DYNAMIC_FORCE
     _abi.specdec_realign_kv(kv, kv, t32(kept), n_planes=planes, n_rows=B, H=H, D=D,
                             src_strides=s[:3], dst_strides=s[:3], cap_src=cap, cap_dst=cap, ws=ws,
                             src_col=t32(pad_old), dst_col=t32(pad_new),
                             flags=flags, moved_bytes=moved, status=st,
                             count_bound=bound)
     torch.cuda.synchronize()
+    rb = D * (4 if dtype == "fp32" else 2)
+    small = bound > 0 and bound * rb <= 4096          # warp-per-slab kernel: no schedule
     if dyn:
-        assert not ws[:128].any(), "the schedule counters are left zero"
+        hdr = ws[:16].view(torch.int32).cpu().numpy()
+        assert hdr[0] == 0 and hdr[1] == 0, "the schedule counters are left zero"
+        if not small:
+            # the ticket path ran: one completed dynamic launch, >= one ticket per moving slab
+            moving = sum(1 for i in range(B) if kept[i] > 0 and pad_old[i] != pad_new[i]
+                         and max(pad_old[i], pad_new[i]) + kept[i] <= cap and (bound == 0 or kept[i] <= bound))
+            assert hdr[2] == 1, hdr
+            assert hdr[3] >= planes * H * moving, (hdr, moving)
     g = torch_to_bits(kv)
     o, defined = OA.realign_kv(bits, pad_old, pad_new, kept)
     for i in range(B):

@@ -140,6 +140,35 @@ def test_copy_rows_gather_scatter():
     assert dst[0, :, :, :5].sum() == 0
 
 
+def test_realign_kv_inplace_tracks_token_identity():
+    """In-place Realign (the K2 contract): brute force over shifts of both signs, Delta = 0,
+    empty rows and overlapping source / destination ranges.  Every entry is tagged with its
+    (row, column, plane, head, d) identity; afterwards column p'_i + c holds the entry that
+    was at p_i + c, and every other column still holds its own (closed form, no formula of
+    the oracle restated)."""
+    rng = np.random.default_rng(12)
+    for _ in range(300):
+        B, P, H, D = int(rng.integers(1, 5)), int(rng.integers(1, 3)), int(rng.integers(1, 3)), 2
+        cap = int(rng.integers(8, 40))
+        kept = rng.integers(0, cap // 2, B)
+        po = np.array([int(rng.integers(0, cap - kept[i] + 1)) for i in range(B)])
+        pn = np.array([int(rng.integers(0, cap - kept[i] + 1)) if rng.random() < 0.8 else po[i] for i in range(B)])
+        tag = np.zeros((P, B, H, cap, D), np.int64)
+        pl, b, h, c, d = np.indices(tag.shape)
+        tag[:] = (((pl * 8 + b) * 8 + h) * 64 + c) * 4 + d
+        kv = A.realign_kv_inplace(tag.copy(), po, pn, kept)
+        for i in range(B):
+            for col in range(cap):
+                want = col
+                if pn[i] <= col < pn[i] + kept[i]:
+                    want = col - pn[i] + po[i]
+                assert np.array_equal(kv[:, i, :, col], tag[:, i, :, want]), (i, col)
+        # the defined region agrees with the fresh-rectangle form
+        ref, defined = A.realign_kv(tag, po, pn, kept)
+        assert np.array_equal(kv[:, :, :][np.broadcast_to(defined[None, :, None, :, None], kv.shape)],
+                              ref[np.broadcast_to(defined[None, :, None, :, None], ref.shape)])
+
+
 # --------------------------------------------------------------------------- toy-LM equivalence
 PROMPTS_SEED = 0
 
@@ -273,8 +302,11 @@ def test_anchor_plan_is_the_brute_force_minimum():
         plan = V.repad_plan(n, a, fin)
         L, Ln = int(n.max()), plan["L_new"]
         pad_old = L - n
-        base = int(rng.integers(0, 12))
-        cap_phys = base + Ln + k + int(rng.integers(0, 12))
+        # capacity room above L'+k, and an origin anywhere up to 3 columns past the highest
+        # one that keeps d = 0 feasible (then only a moving shift -- or the fallback -- fits)
+        room = int(rng.integers(0, 12))
+        cap_phys = Ln + k + room
+        base = int(rng.integers(0, room + 4))
         b2, col_old, col_new = A.anchor_plan(pad_old, plan["pad_new"], plan["kept"], fin, a, L, Ln,
                                              base, cap_phys, k)
         d = b2 - base
@@ -282,9 +314,26 @@ def test_anchor_plan_is_the_brute_force_minimum():
         feas = [x for x in range(-base, cap_phys - base - Ln - k + 1)] if Ln else [0]
         best = min(_cost(x, pad_old, plan["pad_new"], plan["kept"], alive) for x in feas)
         assert _cost(d, pad_old, plan["pad_new"], plan["kept"], alive) == best
-        assert best <= _cost(0, pad_old, plan["pad_new"], plan["kept"], alive)
+        if 0 in feas:
+            assert best <= _cost(0, pad_old, plan["pad_new"], plan["kept"], alive)
         assert 0 <= b2 and (Ln == 0 or b2 + Ln + k <= cap_phys)
         assert list(col_old) == list(base + pad_old) and list(col_new) == list(b2 + plan["pad_new"])
+
+
+def test_anchor_plan_fallback_when_no_candidate_fits():
+    """base' + L + k == cap, then L grows by one with a = 0 for the longest row:
+    d = 0 and every class shift d = a + 1 - (L' - L) >= 0 overflow the physical buffer; the
+    origin must drop to the highest feasible one (every kept row moves) instead of staying."""
+    k, cap_phys, base = 2, 20, 5
+    n, a = np.array([13, 10]), np.array([0, 2])
+    fin = np.zeros(2, np.uint8)
+    plan = V.repad_plan(n, a, fin)
+    L, Ln = 13, plan["L_new"]
+    assert Ln == 14 and base + L + k == cap_phys
+    b2, co, cn = A.anchor_plan(L - n, plan["pad_new"], plan["kept"], fin, a, L, Ln, base, cap_phys, k)
+    assert b2 == 4 and b2 + Ln + k == cap_phys
+    assert list(co) == [5, 8] and list(cn) == [4, 5]
+    assert np.all(cn + plan["kept"] <= cap_phys)
 
 
 def test_anchor_moves_only_the_logical_origin():

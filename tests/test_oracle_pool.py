@@ -23,6 +23,13 @@ def test_form_batch_spec_examples():
     assert all(p["kind"])
 
 
+def test_form_batch_min_group_above_B():
+    """R11 with min_group > B (hand-worked): length 7 has 4 members -> one batch of B=2
+    (4 >= 3), then 2 < 3 remain; leftovers 2, 3, 4 in window order -> [2,3] (mixed), [4]."""
+    p = form_batches([7, 7, 7, 5, 7], [1] * 5, [0, 1, 2, 3, 4], W=5, B=2, min_group=3)
+    assert p["batches"] == [[0, 1], [2, 3], [4]] and p["kind"] == [1, 0, 1]
+
+
 def test_admission_and_window():
     order = admission_order([5, 2, 9, 2], sort_by_length=True)
     assert list(order) == [1, 3, 0, 2]          # ascending prompt length, ties by id
