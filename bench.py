@@ -800,8 +800,8 @@ def run_pool(args, rank, world, device, emulate=False):
         # libspecdec launches in the timed drain: K4 per plan (the epochs + the final empty
         # plan), K1 with the fused write-back per batch, gather + scatter per fallback batch
         # (Alg. 3 device loop: K4 + gate + gather + verify + scatter per issued iteration)
-        "gpu_launches": (3 + _abi.K1_KERNELS) * alg3_iters["n"] if alg3_iters["n"] else (epochs + 1)
-        + (_abi.K1_KERNELS if sp.fused else _abi.K1_KERNELS + 1) * int(cnt[0])
+        "gpu_launches": (3 + _abi.specdec_verify_kernels(True)) * alg3_iters["n"] if alg3_iters["n"] else (epochs + 1)
+        + (_abi.specdec_verify_kernels(True) if sp.fused else _abi.specdec_verify_kernels(False) + 1) * int(cnt[0])
         + 2 * (int(cnt[0]) if sp.dense_consumer else int(cnt[0]) - int(cnt[1])),
         "e2e": None,
         "e2e_note": "pool: the per-batch logits come from the model's forward on the device (the "

@@ -63,6 +63,13 @@ typedef struct CUstream_st *specdec_stream_t; /* == cudaStream_t */
 int specdec_version(void);                /* ABI version (major*100 + minor) */
 const char *specdec_last_cuda_error(void); /* message for the last SPECDEC_ERR_CUDA (thread-local) */
 
+/* Kernels one specdec_verify (pool = 0) or specdec_pool_verify (pool = 1) call launches:
+ * 2 for specdec_verify (the argmax grid, then a one-CTA epilogue kernel that builds the
+ * plan), 1 for specdec_pool_verify (each batch row's epilogue runs in the last CTA of that
+ * row; the pool has no cross-row plan) -- the measured best of each; SPECDEC_K1_SPLIT=E[,P]
+ * overrides (0 grid arrival, 1 epilogue kernel, 2 per-row arrival). */
+int specdec_verify_kernels(int pool);
+
 /* Bytes of the device workspace specdec_verify needs for (B, k).  The workspace must be
  * zero-filled ONCE when allocated; every completed specdec_verify leaves it zeroed again
  * (self-cleaning), so it can be reused by consecutive calls on one stream. */

@@ -23,9 +23,6 @@ DYNAMIC = 4
 SEGMENTED = 8
 DYNAMIC_FORCE = 16
 DTYPE = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2}
-# kernels one specdec_verify / specdec_pool_verify launches: the argmax grid and the
-# one-CTA epilogue behind it (SPECDEC_K1_SPLIT=0: one kernel, last-CTA epilogue)
-K1_KERNELS = 1 if os.environ.get("SPECDEC_K1_SPLIT", "1") == "0" else 2
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -37,6 +34,7 @@ _SIGS = {
     "specdec_version": ([], _INT),
     "specdec_last_cuda_error": ([], ctypes.c_char_p),
     "specdec_verify_workspace_size": ([_I64, _I64], ctypes.c_size_t),
+    "specdec_verify_kernels": ([_INT], _INT),
     "specdec_verify": ([_P, _INT, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
                         _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P,
                         ctypes.c_size_t, _P], _INT),
@@ -224,6 +222,11 @@ def _check(rc: int, name: str):
 
 def version() -> int:
     return load().specdec_version()
+
+
+def specdec_verify_kernels(pool: bool = False) -> int:
+    """Kernels one specdec_verify (or specdec_pool_verify) call launches."""
+    return load().specdec_verify_kernels(1 if pool else 0)
 
 
 def specdec_verify_workspace_size(B: int, k: int) -> int:

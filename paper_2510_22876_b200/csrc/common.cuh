@@ -22,6 +22,12 @@ __device__ __forceinline__ uint32_t key16(uint32_t bits, uint32_t exp_all_ones) 
     const uint32_t k = (bits & 0x8000u) ? (0x8000u - mag) : (0x8000u + mag);
     return mag > exp_all_ones ? 0xFFFFFFFFu : k;
 }
+// the same order in 16 bits (NaN -> 0xFFFF, above +inf's 0xFF80 / 0xFC00)
+__device__ __forceinline__ uint32_t key16s(uint32_t bits, uint32_t exp_all_ones) {
+    const uint32_t mag = bits & 0x7FFFu;
+    const uint32_t k = (bits & 0x8000u) ? (0x8000u - mag) : (0x8000u + mag);
+    return mag > exp_all_ones ? 0xFFFFu : k;
+}
 __device__ __forceinline__ uint32_t key32(uint32_t bits) {
     const uint32_t mag = bits & 0x7FFFFFFFu;
     const uint32_t k = (bits & 0x80000000u) ? (0x80000000u - mag) : (0x80000000u + mag);

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "common.cuh"
 #include "host_util.h"
@@ -28,6 +29,8 @@ namespace specdec {
 constexpr int kVerifyThreads = 256;
 constexpr int kMaxK = 31;  // k + 1 <= 32: one lane per slot in the epilogue
 constexpr int kEpiCache = 1024;  // rows whose n' the epilogue keeps in shared memory
+// default completion modes (VerifyParams::split), measured: tools/k1bench.py
+constexpr int kSplitEqSpec = 1, kSplitPool = 2;
 
 struct VerifyParams {
     const void *logits;
@@ -52,10 +55,13 @@ struct VerifyParams {
     uint8_t *wb_active;
     int64_t *wb_tokens, wb_cap_tok, *wb_out_buf, wb_max_new;
     int exp;                  // SPECDEC_K1_EXP timing experiments (0 = normal)
-    int split;                // epilogue in its own kernel behind the grid (no arrival)
+    int split;                // completion: 0 grid arrival, 1 epilogue kernel, 2 row arrival
     uint32_t *status;
     unsigned long long *ws_keys;  // [B*(k+1)]
-    unsigned int *ws_counter;      // [1]
+    unsigned int *ws_counter;      // [1] grid / row-finish arrivals
+    int32_t *ws_lmax;              // [1] split 2: max n' over the still-active rows
+    unsigned int *ws_rowcnt;       // [B] split 2: CTA arrivals per batch row
+    unsigned long long *ws_w;      // [k+1] split 2 + f3: kept rows per accept class
 };
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
@@ -68,10 +74,146 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
 }
 
 // ----------------------------------------------------------------------------- epilogue
-// pre_sq: the pool sequence of this warp's first row (pool mode), loaded before the
-// arrival so that the row's pool length / generated count loads issue together with the
-// key loads instead of one dependent round trip later.
-__device__ void verify_epilogue(const VerifyParams &p, int32_t pre_sq) {
+// The epilogue of one batch row, warp-wide (lane j < k+1 holds slot j's key).  RowPre is
+// everything it reads besides the keys -- loaded before the arrival so that no load of
+// it sits on the critical path after the last CTA of the row arrives.
+struct RowPre {
+    uint8_t act;
+    int32_t n, bud, sq, len0, gen0;  // sq: pool sequence of the row (pool mode), else -1
+    int64_t d;                       // lane t < k: draft[i][t]
+};
+
+__device__ __forceinline__ RowPre load_pre(const VerifyParams &p, int64_t i, int lane) {
+    RowPre r;
+    r.act = p.active[i];
+    r.n = p.n[i];
+    r.d = lane < p.k ? p.draft[i * p.k + lane] : -1;
+    r.bud = p.budget ? p.budget[i] : 0;
+    r.sq = p.wb_members ? p.wb_members[i] : -1;
+    r.len0 = r.sq >= 0 ? p.wb_len[r.sq] : 0;
+    r.gen0 = r.sq >= 0 ? p.wb_gen[r.sq] : 0;
+    return r;
+}
+
+struct RowOut {
+    int a, nn, kp;
+    bool fin;
+};
+
+// Alg. 1 lines 3-9 for row i: first mismatch by warp ballot (R1: all k
+// match -> a = k), bonus = pred[a] (R2), E = D[:a] ++ [b] cut after the first EOS and to the
+// budget (R10), the row's plan entries (n', kept; R6 / R9), and in pool mode the Phase 4
+// write-back.  Writes every per-row output and self-cleans the row's keys.
+__device__ __forceinline__ RowOut row_epilogue(const VerifyParams &p, int64_t i, const RowPre &r,
+                                               unsigned long long key) {
+    const int lane = threadIdx.x & 31;
+    const int k = static_cast<int>(p.k);
+    const int K1 = k + 1;
+    const bool act = r.act != 0;
+    int a = 0, m = 0, nn = 1, kp = 0;
+    int64_t b = p.pad_id;
+    bool fin = true;
+    const int64_t pr = (act && lane < K1) ? static_cast<int64_t>(unpack_idx(key)) : -1;
+    if (p.pred && lane < K1) p.pred[i * K1 + lane] = pr;
+    int64_t tok = -1;
+    if (act) {
+        // first mismatch; R1: all k match -> a = k
+        const unsigned mism = __ballot_sync(0xFFFFFFFFu, lane < k && pr != r.d);
+        a = mism ? __ffs(mism) - 1 : k;
+        b = __shfl_sync(0xFFFFFFFFu, pr, a);  // bonus = pred at the first mismatch (R2)
+        // E = D[:a] ++ [b]: lane t < a holds D[t], lane a holds b; cut after the first EOS
+        tok = lane < a ? r.d : b;
+        m = a + 1;
+        fin = false;
+        if (p.eos_id >= 0) {
+            const unsigned e = __ballot_sync(0xFFFFFFFFu, lane <= a && tok == p.eos_id);
+            if (e) { m = __ffs(e); fin = true; }
+        }
+        if (p.budget) {  // then to the remaining budget (R10)
+            const int bud = max(r.bud, 0);
+            if (m >= bud) { m = bud; fin = true; }
+            if (lane == 0) p.budget[i] = bud - m;  // in/out
+        }
+        if (!fin) {
+            nn = r.n + a + 1;  // accepted + bonus
+            kp = r.n + a;      // the bonus has no KV yet
+        }
+    }
+    if (lane < K1) p.ws_keys[i * K1 + lane] = 0ull;  // self-clean
+    if (r.sq >= 0) {
+        // Alg. 3 Phase 4, as specdec_pool_writeback: E cut to the
+        // sequence's remaining budget, appended to its pool tokens / output, len and gen
+        // advanced, deactivated when finished
+        const int32_t len = r.len0, g = r.gen0;
+        const int32_t em = min(m, static_cast<int32_t>(max(static_cast<int64_t>(0), p.wb_max_new - g)));
+        const bool fin2 = fin || g + em >= p.wb_max_new;
+        if (p.wb_tokens && len + em > p.wb_cap_tok) {
+            if (lane == 0 && p.status) atomicOr(p.status, SPECDEC_ST_CAPACITY);
+        } else {
+            if (lane < em) {
+                if (p.wb_tokens) p.wb_tokens[static_cast<int64_t>(r.sq) * p.wb_cap_tok + len + lane] = tok;
+                if (p.wb_out_buf) p.wb_out_buf[static_cast<int64_t>(r.sq) * p.wb_max_new + g + lane] = tok;
+            }
+            if (lane == 0) {
+                p.wb_len[r.sq] = len + em;
+                p.wb_gen[r.sq] = g + em;
+                if (fin2) p.wb_active[r.sq] = 0;
+            }
+        }
+    }
+    if (lane == 0) {
+        p.accept[i] = a;
+        p.bonus[i] = b;
+        p.emit[i] = m;
+        p.finished[i] = fin ? 1 : 0;
+        p.active[i] = fin ? 0 : 1;  // in/out: rows still active after this round
+        if (p.n_new) p.n_new[i] = nn;
+        if (p.kept) p.kept[i] = kp;
+        // f1: a draft model that cached its own k forwards (pending token, d_1..d_{k-1})
+        // keeps n + min(a, k-1) entries: d_k never had a draft KV entry
+        if (p.kept_draft) p.kept_draft[i] = kp ? r.n + min(a, k - 1) : 0;
+    }
+    return RowOut{a, nn, kp, fin};
+}
+
+// f3 (lane 0): move the physical origin to the shift d that leaves the heaviest accept class
+// in place (rows with a = d + (L' - L) - 1 do not move); candidates d = 0 first, then larger
+// d; feasible iff 0 <= base + d and base + d + L' + k <= anchor_cap; if none is, the
+// feasible shift closest to 0.  w[a] = kept rows of accept class a.  Returns base'.
+__device__ __forceinline__ int64_t anchor_choose(const VerifyParams &p, const unsigned long long *w,
+                                                 int Lnew, int Lold) {
+    const int k = static_cast<int>(p.k);
+    const int64_t base = *p.anchor;
+    unsigned long long total = 0;
+    for (int a = 0; a <= k; ++a) total += w[a];
+    auto saved = [&](int64_t d) -> unsigned long long {
+        const int64_t a = d + (Lnew - Lold) - 1;
+        return (a >= 0 && a <= k) ? w[a] : 0ull;
+    };
+    auto feasible = [&](int64_t d) { return base + d >= 0 && base + d + Lnew + k <= p.anchor_cap; };
+    int64_t best = 0;
+    unsigned long long best_cost = ~0ull;
+    if (Lnew > 0) {
+        if (feasible(0)) best_cost = total - saved(0);
+        for (int a = k; a >= 0; --a) {  // larger d first
+            const int64_t d = (a + 1) - (Lnew - Lold);
+            if (d == 0 || !feasible(d)) continue;
+            const unsigned long long c = total - w[a];
+            if (c < best_cost) { best_cost = c; best = d; }
+        }
+        if (best_cost == ~0ull) {
+            // no candidate fits (the origin sits too high for the grown width): the
+            // feasible shift closest to 0 -- every kept row moves, the bound holds
+            const int64_t lo = -base, hi = p.anchor_cap - Lnew - k - base;
+            if (lo <= hi) best = min(max(static_cast<int64_t>(0), lo), hi);
+        }
+    }
+    return base + best;
+}
+
+// All rows in one CTA (the epilogue kernel behind the argmax grid, or the last CTA of the
+// grid-wide arrival): one warp per row, then the BatchRepad plan (L', p', f3 origin).
+__device__ void verify_epilogue(const VerifyParams &p) {
     __shared__ int s_red[kVerifyThreads / kWarp];
     __shared__ int s_nmax[kVerifyThreads / kWarp];
     __shared__ unsigned long long s_w[kMaxK + 1];  // f3: kept rows per accept class
@@ -79,89 +221,20 @@ __device__ void verify_epilogue(const VerifyParams &p, int32_t pre_sq) {
     __shared__ int32_t s_nn[kEpiCache];  // n' of the first rows (no global re-read below)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
-    const int k = static_cast<int>(p.k);
-    const int K1 = k + 1;
+    const int K1 = static_cast<int>(p.k) + 1;
     if (threadIdx.x <= kMaxK) s_w[threadIdx.x] = 0ull;
     __syncthreads();
     int local_max = 0, local_nmax = 0;
     for (int64_t i = warp; i < p.B; i += nwarps) {
         // every load of the row first, independent of each other: one memory round trip
-        const uint8_t act_b = p.active[i];
-        const int32_t n_i = p.n[i];
         const unsigned long long key = lane < K1 ? __ldcg(p.ws_keys + i * K1 + lane) : 0ull;
-        const int64_t d = lane < k ? p.draft[i * k + lane] : -1;
-        const int32_t bud_i = p.budget ? p.budget[i] : 0;
-        const int32_t sq = p.wb_members ? (i == warp ? pre_sq : p.wb_members[i]) : -1;
-        const int32_t wb_len0 = sq >= 0 ? p.wb_len[sq] : 0, wb_gen0 = sq >= 0 ? p.wb_gen[sq] : 0;
-        const bool act = act_b != 0;
-        local_nmax = max(local_nmax, n_i);  // old width L = max n (R6 held last round)
-        int a = 0, m = 0, nn = 1, kp = 0;
-        int64_t b = p.pad_id;
-        bool fin = true;
-        const int64_t pr = (act && lane < K1) ? static_cast<int64_t>(unpack_idx(key)) : -1;
-        if (p.pred && lane < K1) p.pred[i * K1 + lane] = pr;
-        int64_t tok = -1;
-        if (act) {
-            // first mismatch; R1: all k match -> a = k
-            const unsigned mism = __ballot_sync(0xFFFFFFFFu, lane < k && pr != d);
-            a = mism ? __ffs(mism) - 1 : k;
-            b = __shfl_sync(0xFFFFFFFFu, pr, a);  // bonus = pred at the first mismatch (R2)
-            // E = D[:a] ++ [b]: lane t < a holds D[t], lane a holds b; cut after the first EOS
-            tok = lane < a ? d : b;
-            m = a + 1;
-            fin = false;
-            if (p.eos_id >= 0) {
-                const unsigned e = __ballot_sync(0xFFFFFFFFu, lane <= a && tok == p.eos_id);
-                if (e) { m = __ffs(e); fin = true; }
-            }
-            if (p.budget) {  // then to the remaining budget (R10)
-                const int bud = max(bud_i, 0);
-                if (m >= bud) { m = bud; fin = true; }
-                if (lane == 0) p.budget[i] = bud - m;  // in/out
-            }
-            if (!fin) {
-                nn = n_i + a + 1;  // accepted + bonus
-                kp = n_i + a;      // the bonus has no KV yet
-                local_max = max(local_max, nn);
-            }
-        }
-        if (lane < K1) p.ws_keys[i * K1 + lane] = 0ull;  // self-clean
-        if (p.wb_members) {
-            // Alg. 3 Phase 4, as specdec_pool_writeback: E cut to the
-            // sequence's remaining budget, appended to its pool tokens / output, len and gen
-            // advanced, deactivated when finished
-            if (sq >= 0) {
-                const int32_t len = wb_len0, g = wb_gen0;
-                const int32_t em = min(m, static_cast<int32_t>(max(static_cast<int64_t>(0), p.wb_max_new - g)));
-                const bool fin2 = fin || g + em >= p.wb_max_new;
-                if (p.wb_tokens && len + em > p.wb_cap_tok) {
-                    if (lane == 0 && p.status) atomicOr(p.status, SPECDEC_ST_CAPACITY);
-                } else {
-                    if (lane < em) {
-                        if (p.wb_tokens) p.wb_tokens[static_cast<int64_t>(sq) * p.wb_cap_tok + len + lane] = tok;
-                        if (p.wb_out_buf) p.wb_out_buf[static_cast<int64_t>(sq) * p.wb_max_new + g + lane] = tok;
-                    }
-                    if (lane == 0) {
-                        p.wb_len[sq] = len + em;
-                        p.wb_gen[sq] = g + em;
-                        if (fin2) p.wb_active[sq] = 0;
-                    }
-                }
-            }
-        }
+        const RowPre r = load_pre(p, i, lane);
+        local_nmax = max(local_nmax, r.n);  // old width L = max n (R6 held last round)
+        const RowOut o = row_epilogue(p, i, r, key);
+        if (!o.fin) local_max = max(local_max, o.nn);
         if (lane == 0) {
-            p.accept[i] = a;
-            p.bonus[i] = b;
-            p.emit[i] = m;
-            p.finished[i] = fin ? 1 : 0;
-            p.active[i] = fin ? 0 : 1;  // in/out: rows still active after this round
-            if (p.n_new) p.n_new[i] = nn;
-            if (i < kEpiCache) s_nn[i] = nn;
-            if (p.kept) p.kept[i] = kp;
-            // f1: a draft model that cached its own k forwards (pending token, d_1..d_{k-1})
-            // keeps n + min(a, k-1) entries: d_k never had a draft KV entry
-            if (p.kept_draft) p.kept_draft[i] = kp ? n_i + min(a, k - 1) : 0;
-            if (p.anchor && kp) atomicAdd(&s_w[a], static_cast<unsigned long long>(kp));
+            if (i < kEpiCache) s_nn[i] = o.nn;
+            if (p.anchor && o.kp) atomicAdd(&s_w[o.a], static_cast<unsigned long long>(o.kp));
         }
     }
     // L' = max n' over still-active rows (R6 minimal padding)
@@ -181,37 +254,9 @@ __device__ void verify_epilogue(const VerifyParams &p, int32_t pre_sq) {
         Lold = max(Lold, s_nmax[w]);
     }
     if (p.anchor && threadIdx.x == 0) {
-        // f3: move the physical origin to the shift d that leaves the heaviest accept class
-        // in place (rows with a = d + (L' - L) - 1 do not move); candidates d = 0 first,
-        // then larger d; feasible iff 0 <= base + d and base + d + L' + k <= anchor_cap.
-        const int64_t base = *p.anchor;
-        unsigned long long total = 0;
-        for (int a = 0; a <= k; ++a) total += s_w[a];
-        auto saved = [&](int64_t d) -> unsigned long long {
-            const int64_t a = d + (Lnew - Lold) - 1;
-            return (a >= 0 && a <= k) ? s_w[a] : 0ull;
-        };
-        auto feasible = [&](int64_t d) { return base + d >= 0 && base + d + Lnew + k <= p.anchor_cap; };
-        int64_t best = 0;
-        unsigned long long best_cost = ~0ull;
-        if (Lnew > 0) {
-            if (feasible(0)) best_cost = total - saved(0);
-            for (int a = k; a >= 0; --a) {  // larger d first
-                const int64_t d = (a + 1) - (Lnew - Lold);
-                if (d == 0 || !feasible(d)) continue;
-                const unsigned long long c = total - s_w[a];
-                if (c < best_cost) { best_cost = c; best = d; }
-            }
-            if (best_cost == ~0ull) {
-                // no candidate fits (the origin sits too high for the grown width): the
-                // feasible shift closest to 0 -- every kept row moves, the bound holds
-                const int64_t lo = -base, hi = p.anchor_cap - Lnew - k - base;
-                if (lo <= hi) best = min(max(static_cast<int64_t>(0), lo), hi);
-            }
-        }
-        s_base[0] = static_cast<int>(base);
-        s_base[1] = static_cast<int>(base + best);
-        *p.anchor = static_cast<int32_t>(base + best);
+        s_base[0] = *p.anchor;
+        s_base[1] = static_cast<int>(anchor_choose(p, s_w, Lnew, Lold));
+        *p.anchor = s_base[1];
     }
     if (p.anchor) __syncthreads();
     for (int64_t i = threadIdx.x; i < p.B && p.pad_new; i += blockDim.x) {
@@ -233,18 +278,12 @@ __device__ void verify_epilogue(const VerifyParams &p, int32_t pre_sq) {
 __global__ void __launch_bounds__(kVerifyThreads) verify_epilogue_kernel(VerifyParams p) {
     pdl_wait();
     pdl_launch_dependents();
-    const int w = static_cast<int>(threadIdx.x >> 5);
-    const int32_t pre_sq = (p.wb_members && w < p.B) ? p.wb_members[w] : -1;
-    verify_epilogue(p, pre_sq);
+    verify_epilogue(p);
 }
 
-// Arrival on the grid-wide counter; the last CTA runs the epilogue.
+// split == 0: arrival on the grid-wide counter; the last CTA runs the epilogue.
 __device__ __forceinline__ void arrive_and_maybe_finish(const VerifyParams &p, int *s_last) {
-    if (p.exp == 1 || p.split) return;  // split: the epilogue kernel follows (EXP=1: probe)
-    // pool mode: every warp loads its first row's pool sequence now (not written by this
-    // grid), under the arrival round trip; only the last CTA uses it
-    const int32_t w = static_cast<int32_t>(threadIdx.x >> 5);
-    const int32_t pre_sq = (p.wb_members && w < p.B) ? p.wb_members[w] : -1;
+    if (p.exp == 1 || p.split == 1) return;  // split: the epilogue kernel follows (EXP=1: probe)
     if (threadIdx.x == 0) {
         // acq_rel: releases this CTA's key atomicMax (same thread, cta_merge) and, in the
         // last CTA, acquires every other CTA's -- no separate sequentially-consistent fences
@@ -260,7 +299,81 @@ __device__ __forceinline__ void arrive_and_maybe_finish(const VerifyParams &p, i
         for (int64_t x = threadIdx.x; x < p.B * (p.k + 1); x += blockDim.x) p.ws_keys[x] = 0ull;
         return;
     }
-    verify_epilogue(p, pre_sq);
+    verify_epilogue(p);
+}
+
+// The plan after every row's epilogue (warp-wide, run by the last row to finish):
+// L' = max n' over still-active rows (accumulated in ws_lmax), p'_i = L' - n'_i, the f3
+// origin from the accept-class weights in ws_w, plan_L.  Self-cleans the plan words.
+__device__ void plan_finalize_warp(const VerifyParams &p) {
+    __shared__ unsigned long long s_w[kMaxK + 1];
+    __shared__ int s_base[2];
+    const int lane = threadIdx.x & 31;
+    const int K1 = static_cast<int>(p.k) + 1;
+    __syncwarp();
+    const int Lnew = __ldcg(p.ws_lmax);
+    int Lold = 0;
+    for (int64_t t = lane; t < p.B; t += 32) Lold = max(Lold, __ldcg(p.n + t));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Lold = max(Lold, __shfl_xor_sync(0xFFFFFFFFu, Lold, o));
+    if (p.anchor) {
+        if (lane < K1) {
+            s_w[lane] = __ldcg(p.ws_w + lane);
+            p.ws_w[lane] = 0ull;  // self-clean
+        }
+        __syncwarp();
+        if (lane == 0) {
+            s_base[0] = *p.anchor;
+            s_base[1] = static_cast<int>(anchor_choose(p, s_w, Lnew, Lold));
+            *p.anchor = s_base[1];
+        }
+        __syncwarp();
+    }
+    for (int64_t t = lane; t < p.B; t += 32) {
+        const int32_t pn = Lnew > 0 ? Lnew - __ldcg(p.n_new + t) : 0;
+        p.pad_new[t] = pn;
+        if (p.anchor) {
+            p.phys_old[t] = s_base[0] + (Lold - __ldcg(p.n + t));
+            p.phys_new[t] = s_base[1] + pn;
+        }
+    }
+    if (lane == 0) {
+        *p.plan_L = Lnew;
+        *p.ws_lmax = 0;        // self-clean
+        *p.ws_counter = 0u;
+    }
+}
+
+// split == 2: arrival on the batch row's counter ((k+1) x chunks CTAs per row).  The last
+// CTA of row i runs that row's epilogue at once (warp 0, with the row inputs prefetched
+// before the arrival); in pool mode that is all.  With a plan to build, the row then
+// arrives on the grid counter (one arrival per batch row) and the last row writes p', L'.
+__device__ __forceinline__ void row_arrive_and_finish(const VerifyParams &p, int64_t i, const RowPre *s_pre,
+                                                      int *s_last) {
+    const int K1 = static_cast<int>(p.k) + 1;
+    if (threadIdx.x == 0) {
+        const unsigned int total = static_cast<unsigned int>(K1) * gridDim.x;
+        unsigned int prev;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.ws_rowcnt + i) : "memory");
+        *s_last = (prev == total - 1);
+    }
+    __syncthreads();
+    if (!*s_last || threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const unsigned long long key = lane < K1 ? __ldcg(p.ws_keys + i * K1 + lane) : 0ull;
+    const RowOut o = row_epilogue(p, i, s_pre[lane], key);
+    unsigned last = 0;
+    if (lane == 0) {
+        p.ws_rowcnt[i] = 0u;  // self-clean
+        if (p.plan_L) {
+            if (!o.fin) atomicMax(p.ws_lmax, o.nn);
+            if (p.anchor && o.kp) atomicAdd(p.ws_w + o.a, static_cast<unsigned long long>(o.kp));
+            unsigned int prev;
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(p.ws_counter) : "memory");
+            last = prev == static_cast<unsigned int>(p.B) - 1;
+        }
+    }
+    if (__shfl_sync(0xFFFFFFFFu, last, 0)) plan_finalize_warp(p);
 }
 
 __device__ __forceinline__ void cta_merge(const VerifyParams &p, int64_t row, unsigned long long best,
@@ -279,6 +392,13 @@ __device__ __forceinline__ void cta_merge(const VerifyParams &p, int64_t row, un
     }
 }
 
+// After the CTA's merge: the configured completion (epilogue kernel / grid arrival / row
+// arrival).  s_pre (shared) holds warp 0's row inputs when p.split == 2.
+__device__ __forceinline__ void finish_cta(const VerifyParams &p, int64_t i, const RowPre *s_pre, int *s_last) {
+    if (p.split == 2) row_arrive_and_finish(p, i, s_pre, s_last);
+    else arrive_and_maybe_finish(p, s_last);
+}
+
 // ----------------------------------------------------------------------------- fp32 (toy)
 // Per-element keys, strict '>' over ascending indices within a thread.
 __global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams p) {
@@ -286,10 +406,13 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams
     pdl_launch_dependents();
     __shared__ unsigned long long s_red[kVerifyThreads / kWarp];
     __shared__ int s_last;
+    __shared__ RowPre s_pre[kWarp];
     const int tid = threadIdx.x;
     const int64_t row = blockIdx.y;
     const int64_t i = row / (p.k + 1);
-    if (p.active[i]) {
+    if (p.split == 2 && tid < kWarp) s_pre[tid] = load_pre(p, i, tid);
+    const bool act = p.active[i] != 0;
+    {
         const char *rowp = static_cast<const char *>(p.logits) + row * p.row_stride * 4;
         const int64_t v0 = static_cast<int64_t>(blockIdx.x) * p.chunk;
         const int64_t v1 = min(p.V, v0 + p.chunk);
@@ -308,9 +431,9 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams
             const uint32_t kk = key32(reinterpret_cast<const uint32_t *>(rowp)[v]);
             if (kk > bk || (kk == bk && static_cast<uint32_t>(v) < bi)) { bk = kk; bi = static_cast<uint32_t>(v); }
         }
-        cta_merge(p, row, bk ? pack_key(bk, bi) : 0ull, s_red);
+        if (act) cta_merge(p, row, bk ? pack_key(bk, bi) : 0ull, s_red);
     }
-    arrive_and_maybe_finish(p, &s_last);
+    finish_cta(p, i, s_pre, &s_last);
 }
 
 // ----------------------------------------------------------------------------- fp16 / bf16
@@ -338,6 +461,9 @@ struct H16 {
         else
             return __heq2_mask(*reinterpret_cast<__half2 *>(&a), *reinterpret_cast<__half2 *>(&b));
     }
+    __device__ static uint32_t vmax(const uint4 &v) { return max2(max2(v.x, v.y), max2(v.z, v.w)); }
+    // the maximum of the two halves, as 16 bits
+    __device__ static uint32_t fold(uint32_t m2) { return max2(m2, (m2 >> 16) | (m2 << 16)) & 0xFFFFu; }
     static constexpr uint32_t kExp = BF16 ? 0x7F80u : 0x7C00u;
     static constexpr uint32_t kNegInf2 = BF16 ? 0xFF80FF80u : 0xFC00FC00u;
 };
@@ -345,18 +471,21 @@ struct H16 {
 constexpr int kVPT = 8;  // 16-byte vectors per thread, all in flight, kept in registers
 
 template <bool BF16>
-__global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p) {
+__global__ void __launch_bounds__(kVerifyThreads, 4) verify_kernel16(VerifyParams p) {
     pdl_wait();                // the logits' producer (and the previous round) completed
     pdl_launch_dependents();
     if (p.exp == 2) return;    // timing experiment only: the launch floor of this grid
     using T = H16<BF16>;
-    __shared__ unsigned long long s_red[kVerifyThreads / kWarp];
-    __shared__ uint32_t s_m[kVerifyThreads / kWarp];
+    __shared__ uint32_t s_c[kVerifyThreads / kWarp];
     __shared__ int s_last;
+    __shared__ RowPre s_pre[kWarp];  // split 2: the row's epilogue inputs, per lane of warp 0
+    bool act = false;
     const int tid = threadIdx.x;
     const int64_t row = blockIdx.y;
     const int64_t i = row / (p.k + 1);
-    if (p.active[i]) {
+    {
+        // the loads are issued before anything else is read (an inactive row's logits are
+        // streamed too -- its CTAs just do not merge): no dependent load ahead of them
         const char *rowp = static_cast<const char *>(p.logits) + row * p.row_stride * 2;
         const int64_t v0 = static_cast<int64_t>(blockIdx.x) * p.chunk;
         const int64_t v1 = min(p.V, v0 + p.chunk);
@@ -370,105 +499,132 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel16(VerifyParams p
         for (int u = 0; u < kVPT; ++u)
             w[u] = u < mine ? ld_stream_v4(vp + u * kVerifyThreads)
                             : make_uint4(T::kNegInf2, T::kNegInf2, T::kNegInf2, T::kNegInf2);
+        if (p.split == 2 && tid < kWarp) s_pre[tid] = load_pre(p, i, tid);
+        act = p.active[i] != 0;
+        // pass 1: the thread's packed maximum (HMNMX2: one instruction per two logits,
+        // NaN-propagating)
         uint32_t m2 = T::kNegInf2;
 #pragma unroll
-        for (int u = 0; u < kVPT; ++u)
-            m2 = T::max2(T::max2(m2, T::max2(w[u].x, w[u].y)), T::max2(w[u].z, w[u].w));
+        for (int u = 0; u < kVPT; ++u) m2 = T::max2(m2, T::vmax(w[u]));
         const int64_t tail0 = max(vec_end * 8, v0);  // ragged tail (V % 8), scalar
         for (int64_t v = tail0 + tid; v < v1; v += kVerifyThreads) {
             const uint32_t x = reinterpret_cast<const uint16_t *>(rowp)[v];
             m2 = T::max2(m2, x | (x << 16));
         }
-        const uint32_t my_m = T::max2(m2, (m2 >> 16) | (m2 << 16)) & 0xFFFFu;
+        const uint32_t my_m = T::fold(m2);
         if (p.exp == 3) {  // timing experiment only: stream + per-thread max, no CTA reduction
             if (my_m == 0x7FFFu && p.status) atomicOr(p.status, 0x80000000u);
             return;
         }
-        uint32_t m = my_m;
+        // pass 2, per thread (no CTA maximum first): the first of its vectors whose maximum
+        // equals my_m, then the first element of that vector that does.  An ordinary
+        // maximum (not NaN, not +-0) matches by bits; the special ones by key (+0 == -0,
+        // NaN == NaN: the argmax equality of R4/R5).
+        const uint32_t kM = key16s(my_m, T::kExp);
+        const bool plain = (my_m & 0x7FFFu) != 0 && (my_m & 0x7FFFu) <= T::kExp;
+        int ustar = -1;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, m, o);
-            m = T::max2(m | (m << 16), y | (y << 16)) & 0xFFFFu;
+        for (int u = kVPT - 1; u >= 0; --u) {
+            const uint32_t fu = T::fold(T::vmax(w[u]));  // recomputed: registers stay <= 64
+            if (u < mine && (plain ? fu == my_m : key16s(fu, T::kExp) == kM)) ustar = u;
         }
-        if ((tid & 31) == 0) s_m[tid >> 5] = m;
-        __syncthreads();
-        m = s_m[0];
-#pragma unroll
-        for (int q = 1; q < kVerifyThreads / kWarp; ++q) m = T::max2(m | (m << 16), s_m[q] | (s_m[q] << 16)) & 0xFFFFu;
-        const uint32_t kM = key16(m, T::kExp);
-        if (p.exp == 4) {  // timing experiment only: stream + CTA maximum, no pass 2 / merge
-            if (kM == 0xFFFFFFFFu && p.status) atomicOr(p.status, 0x80000000u);
+        if (p.exp == 4) {  // timing experiment only: + the first matching vector
+            if (ustar == 100 && p.status) atomicOr(p.status, 0x80000000u);
             return;
         }
-        uint32_t first = 0xFFFFFFFFu;
-        if (key16(my_m, T::kExp) == kM) {
-            // pass 2 over the registers, without a serial scan: per vector u, one packed
-            // compare per word (0xFFFF per equal half) and two byte permutes give 8 flag
-            // bytes, byte j set iff half j of the vector equals M; the lowest u with a flag
-            // and its lowest flag byte are the first match (ascending u, then j = ascending
-            // index).  Every warp with a matching lane executes this, and with ties (common
-            // on bf16's coarse grid) that is most warps: it must be short.  An ordinary M
-            // (not NaN, not +-0) matches by value == by bits; the special cases by key.
-            const bool plain = (m & 0x7FFFu) != 0 && (m & 0x7FFFu) <= T::kExp;
-            int code = -1;  // 8 u + j of the first match
+        // CTA-local packed candidate: (key << 16) | (0xFFFF - index in the chunk) -- the
+        // unsigned max is "largest key, then lowest index" (chunk <= 16384 logits)
+        uint32_t cand = 0u;
+        if (ustar >= 0) {
+            uint4 x = w[0];
+#pragma unroll
+            for (int u = 1; u < kVPT; ++u)
+                if (u == ustar) x = w[u];
+            int j;
             if (plain) {
-                const uint32_t mm = m | (m << 16);
-#pragma unroll
-                for (int u = kVPT - 1; u >= 0; --u) {
-                    const uint32_t r0 = T::eq2(w[u].x, mm), r1 = T::eq2(w[u].y, mm);
-                    const uint32_t r2 = T::eq2(w[u].z, mm), r3 = T::eq2(w[u].w, mm);
-                    const uint32_t lo = __byte_perm(r0, r1, 0x6420), hi = __byte_perm(r2, r3, 0x6420);
-                    if (u < mine && (lo | hi))
-                        code = 8 * u + (lo ? (__ffs(lo) - 1) >> 3 : 4 + ((__ffs(hi) - 1) >> 3));
-                }
+                // one packed compare per word (0xFFFF per equal half), two byte permutes: 8
+                // flag bytes, byte j set iff half j equals M; the lowest flag is the first
+                const uint32_t mm = my_m | (my_m << 16);
+                const uint32_t lo = __byte_perm(T::eq2(x.x, mm), T::eq2(x.y, mm), 0x6420);
+                const uint32_t hi = __byte_perm(T::eq2(x.z, mm), T::eq2(x.w, mm), 0x6420);
+                j = lo ? (__ffs(lo) - 1) >> 3 : 4 + ((__ffs(hi) - 1) >> 3);
             } else {
+                const uint32_t e[4] = {x.x, x.y, x.z, x.w};
+                j = 7;
 #pragma unroll
-                for (int u = kVPT - 1; u >= 0; --u) {
-                    const uint32_t e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-                    int j = -1;
-#pragma unroll
-                    for (int q = 3; q >= 0; --q) {
-                        if (key16(e[q] >> 16, T::kExp) == kM) j = 2 * q + 1;
-                        if (key16(e[q] & 0xFFFFu, T::kExp) == kM) j = 2 * q;
-                    }
-                    if (u < mine && j >= 0) code = 8 * u + j;
+                for (int q = 3; q >= 0; --q) {
+                    if (key16s(e[q] >> 16, T::kExp) == kM) j = 2 * q + 1;
+                    if (key16s(e[q] & 0xFFFFu, T::kExp) == kM) j = 2 * q;
                 }
             }
-            if (code >= 0)
-                first = static_cast<uint32_t>((vec0 + tid + (code >> 3) * kVerifyThreads) * 8 + (code & 7));
-            for (int64_t v = tail0 + tid; v < v1 && first == 0xFFFFFFFFu; v += kVerifyThreads)
-                if (key16(reinterpret_cast<const uint16_t *>(rowp)[v], T::kExp) == kM) first = static_cast<uint32_t>(v);
+            const int64_t e = (vec0 + tid + static_cast<int64_t>(ustar) * kVerifyThreads) * 8 + j;
+            cand = (kM << 16) | (0xFFFFu - static_cast<uint32_t>(e - v0));
+        } else {
+            for (int64_t v = tail0 + tid; v < v1; v += kVerifyThreads)
+                if (key16s(reinterpret_cast<const uint16_t *>(rowp)[v], T::kExp) == kM) {
+                    cand = (kM << 16) | (0xFFFFu - static_cast<uint32_t>(v - v0));
+                    break;
+                }
         }
         if (p.exp == 5) {  // timing experiment only: up to pass 2, no merge
-            if (first == 0xFFFFFFFEu && p.status) atomicOr(p.status, 0x80000000u);
+            if (cand == 1u && p.status) atomicOr(p.status, 0x80000000u);
             return;
         }
-        // every thread holding M contributes (key(M), ~first); the max picks the lowest index
-        cta_merge(p, row, first != 0xFFFFFFFFu ? pack_key(kM, first) : 0ull, s_red);
+        // CTA maximum of the candidates (redux.sync), then one 64-bit atomicMax per CTA
+        cand = __reduce_max_sync(0xFFFFFFFFu, cand);
+        if ((tid & 31) == 0) s_c[tid >> 5] = cand;
+        __syncthreads();
+        if (tid < kWarp) {
+            cand = __reduce_max_sync(0xFFFFFFFFu, tid < kVerifyThreads / kWarp ? s_c[tid] : 0u);
+            if (tid == 0 && act && cand) {
+                const uint32_t key = cand >> 16;
+                atomicMax(p.ws_keys + row, pack_key(key, static_cast<uint32_t>(v0 + (0xFFFFu - (cand & 0xFFFFu)))));
+                if (key == 0xFFFFu && p.status) atomicOr(p.status, SPECDEC_ST_NAN);
+            }
+        }
     }
-    arrive_and_maybe_finish(p, &s_last);
+    finish_cta(p, i, s_pre, &s_last);
 }
 
 }  // namespace specdec
 
 using namespace specdec;
 
+// Workspace: keys [B*(k+1)] u64 | grid counter u32, max n' i32, 8 pad | row counters [B]
+// u32 (padded to 8) | accept-class weights [k+1] u64.
+static size_t ws_rowcnt_off(int64_t B, int64_t k) { return static_cast<size_t>(B * (k + 1)) * 8 + 16; }
+static size_t ws_w_off(int64_t B, int64_t k) { return ws_rowcnt_off(B, k) + static_cast<size_t>((B * 4 + 7) / 8 * 8); }
+
 extern "C" size_t specdec_verify_workspace_size(int64_t B, int64_t k) {
     if (B < 1 || k < 1) return 0;
-    return static_cast<size_t>(B * (k + 1)) * sizeof(unsigned long long) + 16;
+    return ws_w_off(B, k) + static_cast<size_t>(k + 1) * 8;
 }
 
 namespace specdec {
 
+static void set_ws(VerifyParams &p, void *d_ws) {
+    char *w = static_cast<char *>(d_ws);
+    p.ws_keys = reinterpret_cast<unsigned long long *>(w);
+    p.ws_counter = reinterpret_cast<unsigned int *>(w + p.B * (p.k + 1) * 8);
+    p.ws_lmax = reinterpret_cast<int32_t *>(w + p.B * (p.k + 1) * 8 + 4);
+    p.ws_rowcnt = reinterpret_cast<unsigned int *>(w + ws_rowcnt_off(p.B, p.k));
+    p.ws_w = reinterpret_cast<unsigned long long *>(w + ws_w_off(p.B, p.k));
+}
+
 // Common host path of specdec_verify / specdec_pool_verify: shape checks done by the
 // callers, p filled except the launch geometry.
 static int launch_verify(VerifyParams &p, int dtype, int es, specdec_stream_t stream) {
-    static int exp = -1, cta_mult = 4, vpt = 0, split = 1;
+    static int exp = -1, cta_mult = 4, vpt = 0, split_eq = kSplitEqSpec, split_pool = kSplitPool;
     if (exp < 0) {
         const char *e = getenv("SPECDEC_K1_EXP");
         exp = e ? atoi(e) : 0;
-        const char *sp = getenv("SPECDEC_K1_SPLIT");  // 0: last-CTA arrival epilogue
-        split = sp ? atoi(sp) : 1;
+        // completion mode override "E[,P]" (EqSpec verify, pool verify): 0 grid-wide
+        // arrival, 1 epilogue kernel, 2 per-row arrival
+        if (const char *sp = getenv("SPECDEC_K1_SPLIT")) {
+            split_eq = atoi(sp);
+            const char *c2 = strchr(sp, ',');
+            split_pool = c2 ? atoi(c2 + 1) : split_eq;
+        }
         const char *c = getenv("SPECDEC_K1_CTAS");  // tuning override: target CTAs per SM
         if (c && atoi(c) > 0) cta_mult = atoi(c);
         const char *v = getenv("SPECDEC_K1_VPT");   // tuning override: 16-B vectors per thread
@@ -503,8 +659,8 @@ static int launch_verify(VerifyParams &p, int dtype, int es, specdec_stream_t st
     const int64_t n_chunks = (V + chunk - 1) / chunk;
     dim3 grid(static_cast<unsigned>(n_chunks), static_cast<unsigned>(rows));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    p.split = (split && exp == 0) ? 1 : 0;  // the probes measure the arrival design
-    if (p.split) {
+    p.split = exp ? 0 : (p.wb_members ? split_pool : split_eq);  // the probes: grid arrival
+    if (p.split == 1) {
         int rc;
         switch (dtype) {
             case SPECDEC_F32: rc = launch_k(verify_kernel_f32, grid, dim3(kVerifyThreads), 0, s, p); break;
@@ -520,6 +676,24 @@ static int launch_verify(VerifyParams &p, int dtype, int es, specdec_stream_t st
         default: return launch_k(verify_kernel16<true>, grid, dim3(kVerifyThreads), 0, s, p);
     }
 }
+
+}  // namespace specdec
+
+extern "C" int specdec_verify_kernels(int pool) {
+    static int split_eq = -1, split_pool = -1;
+    if (split_eq < 0) {
+        split_eq = kSplitEqSpec;
+        split_pool = kSplitPool;
+        if (const char *sp = getenv("SPECDEC_K1_SPLIT")) {
+            split_eq = atoi(sp);
+            const char *c2 = strchr(sp, ',');
+            split_pool = c2 ? atoi(c2 + 1) : split_eq;
+        }
+    }
+    return (pool ? split_pool : split_eq) == 1 ? 2 : 1;
+}
+
+namespace specdec {
 
 // shape / pointer checks shared by both entry points
 static int check_verify(const void *d_logits, int es, int64_t B, int64_t k, int64_t V,
@@ -564,8 +738,7 @@ extern "C" int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_
     p.kept_draft = d_kept_draft;
     p.anchor = d_anchor; p.anchor_cap = anchor_cap; p.phys_old = d_phys_old; p.phys_new = d_phys_new;
     p.status = d_status;
-    p.ws_keys = static_cast<unsigned long long *>(d_ws);
-    p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
+    set_ws(p, d_ws);
     return launch_verify(p, dtype, es, stream);
 }
 
@@ -595,7 +768,6 @@ extern "C" int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, i
     p.wb_members = d_members; p.wb_len = d_pool_len; p.wb_gen = d_pool_gen; p.wb_active = d_pool_active;
     p.wb_tokens = d_pool_tokens; p.wb_cap_tok = cap_tok; p.wb_out_buf = d_out_buf; p.wb_max_new = max_new;
     p.status = d_status;
-    p.ws_keys = static_cast<unsigned long long *>(d_ws);
-    p.ws_counter = reinterpret_cast<unsigned int *>(static_cast<char *>(d_ws) + B * (k + 1) * 8);
+    set_ws(p, d_ws);
     return launch_verify(p, dtype, es, stream);
 }

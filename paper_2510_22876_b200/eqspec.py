@@ -268,7 +268,7 @@ class EqSpecBatch:
     def kernels_per_round(self) -> int:
         """libspecdec kernels one round launches (K1 = argmax grid + epilogue, K3, K2 per
         cache, + save kernels)."""
-        k13 = _abi.K1_KERNELS + 1
+        k13 = _abi.specdec_verify_kernels(False) + 1
         if self.B == 1 and self.anchor is None and self.kv_mode == "inplace":
             return k13
         per_cache = 2 if self.segment and self.kv_mode == "inplace" else 1

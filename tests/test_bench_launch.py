@@ -80,6 +80,6 @@ def test_default_line_has_the_contract_keys():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 14_000_000 and e["d2h_bytes_per_step"] > 0
     from paper_2510_22876_b200 import _abi
-    assert d["gpu_launches"] == (2 + _abi.K1_KERNELS) * 6      # K1 (argmax + epilogue), K3, K2
+    assert d["gpu_launches"] == (2 + _abi.specdec_verify_kernels(False)) * 6      # K1, K3, K2
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["bytes_moved_check"]["value_region"] == d["bytes_moved_check"]["kernel_region"]

@@ -1,5 +1,7 @@
 """Host-side driver logic of EqSpecBatch / SequencePool that needs no GPU: buffer modes,
 parity bookkeeping, option validation, launch counts (CPU tensors; no kernel is called)."""
+import os
+
 import pytest
 import torch
 
@@ -34,7 +36,8 @@ def test_option_validation():
 
 def test_kernels_per_round():
     from paper_2510_22876_b200 import _abi
-    k1 = _abi.K1_KERNELS                   # the argmax grid + the epilogue kernel (default 2)
+    k1 = _abi.specdec_verify_kernels(False)     # argmax grid + epilogue kernel (default): 2
+    assert k1 == (1 if os.environ.get("SPECDEC_K1_SPLIT", "1").split(",")[0] in ("0", "2") else 2)
     assert EqSpecBatch(1, 4, 64, 1, 1, 8, "bf16", "cpu").kernels_per_round == k1 + 1     # B=1: no K2
     assert EqSpecBatch(1, 4, 64, 1, 1, 8, "bf16", "cpu", kv_mode="pingpong").kernels_per_round == k1 + 2
     assert EqSpecBatch(4, 4, 64, 1, 1, 8, "bf16", "cpu").kernels_per_round == k1 + 2

@@ -30,7 +30,9 @@ def main():
     ap.add_argument("--k", type=int, default=5)
     ap.add_argument("--V", type=int, default=151936)
     ap.add_argument("--n", type=int, default=50)
-    ap.add_argument("--ring", type=int, default=8, help="logits buffers (16 at Qwen3 B=8 > L2)")
+    ap.add_argument("--ring", type=int, default=16, help="logits buffers (16 at Qwen3 B=8 > L2)")
+    ap.add_argument("--pool", action="store_true",
+                    help="specdec_pool_verify (the pool's K1 with the fused write-back) instead")
     a = ap.parse_args()
     dev = torch.device("cuda")
     B, k, V = a.B, a.k, a.V
@@ -43,9 +45,23 @@ def main():
     plan = [torch.zeros(1, dtype=i32, device=dev)] + [torch.zeros(B, dtype=i32, device=dev) for _ in range(3)]
     ws = torch.zeros((_abi.specdec_verify_workspace_size(B, k) + 7) // 8, dtype=i64, device=dev)
 
+    # pool mode: B member rows of a pool of 4B sequences with room for every launch's tokens
+    N, max_new = 4 * B, 1 << 20
+    members = torch.arange(B, dtype=i32, device=dev)
+    p_len = torch.full((N,), 100, dtype=i32, device=dev)
+    p_gen = torch.zeros(N, dtype=i32, device=dev)
+    p_act = torch.ones(N, dtype=u8, device=dev)
+
+    def call(lg, stream=None):
+        if a.pool:
+            _abi.specdec_pool_verify(lg, draft, members, n, act, *out, p_len, p_gen, p_act, ws, max_new=max_new,
+                                     stream=stream)
+        else:
+            _abi.specdec_verify(lg, draft, n, act, *out, plan[0], plan[1], plan[2], plan[3], ws, stream=stream)
+
     def one(j):
         act.fill_(1)
-        _abi.specdec_verify(ring[j % len(ring)], draft, n, act, *out, plan[0], plan[1], plan[2], plan[3], ws)
+        call(ring[j % len(ring)])
     for j in range(3):
         one(j)
     torch.cuda.synchronize()
@@ -54,8 +70,7 @@ def main():
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
         for j in range(a.n):
-            _abi.specdec_verify(ring[j % len(ring)], draft, n, act, *out, plan[0], plan[1], plan[2], plan[3], ws,
-                                stream=s)
+            call(ring[j % len(ring)], stream=s)
     torch.cuda.current_stream().wait_stream(s)
     g.replay()
     torch.cuda.synchronize()
@@ -70,6 +85,7 @@ def main():
     mb = B * (k + 1) * V * 2 / 1e6
     print(json.dumps({"B": B, "k": k, "V": V, "us_per_launch": round(best, 2), "logits_MB": round(mb, 2),
                       "GBps": round(mb * 1e3 / best, 1), "ring_MB": round(mb * len(ring), 1), "exp": os.environ.get("SPECDEC_K1_EXP", "0"),
+                      "split": os.environ.get("SPECDEC_K1_SPLIT", "default"), "pool": a.pool,
                       "pdl": os.environ.get("SPECDEC_PDL", "1")}))
 
 
