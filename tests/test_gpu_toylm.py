@@ -59,7 +59,7 @@ def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, dr
     stale = None
     first = True
     rounds = 0
-    for _ in range(64):
+    for _ in range(128):
         if not bt.active.any().item():
             break
         act = bt.active.cpu().numpy()
@@ -106,6 +106,22 @@ def _eqspec_gpu(cuda, T, prompts, k, max_new, eos, noise, cap=64, fault=None, dr
                     if c >= L - 1:
                         logits[i, c - L + 1] = lg.astype(np.float32)
         kv_view.copy_(_to_dev(cache, cuda))
+        if fault == "rollback_min":
+            # rollback: every row is cut to the batch-minimum accept
+            # length -- the drafts of longer-accepting rows are made to mismatch at that
+            # slot, so K1 accepts min(a) everywhere and the bonus is the target's token there
+            pred = logits.argmax(axis=2)
+            acc = [next((j for j in range(k) if pred[i, j] != draft[i, j]), k) for i in range(B)]
+            m = min(acc[i] for i in range(B) if act[i])
+            for i in range(B):
+                if act[i] and acc[i] > m:
+                    draft[i, m] = (pred[i, m] + 1) % V
+        if fault == "skip_unpad" and not first:
+            # DSD: "merely repads ... without ever unpadding": the old pads
+            # are kept as content, so every active row's content is the whole width L
+            a = bt.active.bool()
+            bt.n[bt.cur].copy_(torch.where(a, torch.full_like(bt.n[bt.cur], L), bt.n[bt.cur]))
+            bt.pad[bt.cur].copy_(torch.where(a, torch.zeros_like(bt.pad[bt.cur]), bt.pad[bt.cur]))
         bt.step(torch.from_numpy(logits).to(cuda), torch.from_numpy(draft).to(cuda), V=V)
         first = False
         rounds += 1
@@ -153,17 +169,35 @@ def test_draft_kv_realign_on_gpu(cuda, B, noise):
     assert len(log) >= rounds and all(c == r for c, r in log)
 
 
-@pytest.mark.parametrize("fault", ["skip_kv_realign", "bonus_from_draft", "stale_position_ids"])
-def test_fault_modes_break_equivalence(cuda, fault):
-    """f4: each §2 failure class, injected at its
-    seam of the GPU path, must be caught by the equivalence check (exact match < 1)."""
+CORRUPTING = ("skip_kv_realign", "bonus_from_draft", "stale_position_ids", "skip_unpad")
+
+
+@pytest.mark.parametrize("seed,B,noise", [(44, 4, 0.35), (45, 6, 0.3), (46, 8, 0.25)])
+def test_fault_modes_scored(cuda, seed, B, noise):
+    """f4: each §2 failure class injected at
+    its seam of the GPU path, scored with exact / partial match (oracle.metrics,
+    PAPER.md:658) against per-sequence greedy decoding:
+      * control: exact 1.0;
+      * skip_kv_realign, bonus_from_draft (DSD i), stale_position_ids (BSP), skip_unpad (DSD
+        "merely repads ... without ever unpadding"): exact < 1 -- every fault is caught;
+      * rollback_min (rows cut to the batch-minimum accept length): exact 1.0 with strictly
+        more rounds -- correct but wasteful;
+      * signature separation: bonus_from_draft fails at the first rejection (lowest partial
+        match), the stale-position and unrealigned-KV faults decay gradually (higher)."""
+    from oracle.metrics import score_equivalence
     T = ToyLM(V, LAYERS, H, D, seed=7)
-    prompts = _prompts(4, seed=44)
-    ref = [T.greedy_generate(p, 16, -1, 64) for p in prompts]
-    out, _, _ = _eqspec_gpu(cuda, T, prompts, 4, 16, -1, 0.35)
-    assert out == ref                              # control
-    bad, _, _ = _eqspec_gpu(cuda, T, prompts, 4, 16, -1, 0.35, fault=fault)
-    assert bad != ref
+    k, max_new, cap = 4, 16 if B == 4 else 24, 192
+    prompts = _prompts(B, seed=seed)
+    ref = [T.greedy_generate(p, max_new, -1, cap) for p in prompts]
+    runs = {}
+    for f in (None,) + CORRUPTING + ("rollback_min",):
+        out, rounds, _ = _eqspec_gpu(cuda, T, prompts, k, max_new, -1, noise, cap=cap, fault=f)
+        runs[f] = score_equivalence(out, ref) + (rounds,)
+    assert runs[None][:2] == (1.0, 1.0), runs
+    for f in CORRUPTING:
+        assert runs[f][0] < 1.0, (f, runs)
+    assert runs["rollback_min"][:2] == (1.0, 1.0) and runs["rollback_min"][2] > runs[None][2], runs
+    assert runs["bonus_from_draft"][1] < min(runs["stale_position_ids"][1], runs["skip_kv_realign"][1]), runs
 
 
 @pytest.mark.parametrize("N,Wn,B,mg,alg3,dense", [(10, 6, 3, 2, False, False), (8, 8, 4, 4, False, False),
