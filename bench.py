@@ -484,39 +484,65 @@ def run_e2e(rb, args, world):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_round_sample(sh, args, plane_sample=2, rounds=2, seed=0):
-    """Time the CPU oracle (never tuned) on the same workload: full verify over the
-    logits tail, full repad, realign over `plane_sample` of the 2*layers KV planes
-    (extrapolated linearly -- the realign is per-plane independent).  Returns rounds/s."""
+def oracle_round_sample(sh, args, rounds=2, seed=0, threads=1):
+    """Time the CPU oracle (never tuned) on the same workload: whole rounds -- Alg. 1 over
+    the full logits tail, the token repad, and Realign over EVERY plane of the KV (no
+    extrapolation) -- on `threads` host threads.  threads == 1 runs the serial oracle
+    functions; threads > 1 the thread-parallel driver (oracle/driver.py: the same
+    functions on independent batch rows and (plane, row) slab groups).  Input generation
+    is outside the timed region.  Returns (rounds/s, per-part seconds per round)."""
     from oracle import align as OA
+    from oracle import driver as OD
     from oracle import verify as OV
     B, k = sh.B, sh.k
     cap = W.derive_cap(sh, rounds + 2)
     lengths = W.gen_lengths(sh, seed, B)
     tokens = W.left_padded_tokens(lengths, cap, seed, sh.V)
-    P = min(plane_sample, sh.n_planes)
-    shp = (P, B, sh.H, cap, sh.D)
+    shp = (sh.n_planes, B, sh.H, cap, sh.D)
     kv = W.gen_kv_bits_np(seed, int(np.prod(shp))).reshape(shp)
     n = lengths.astype(np.int32)
     L = int(n.max())
     pad = (L - n).astype(np.int32)
     act = np.ones(B, np.uint8)
+    ins = [(W.gen_logits_np(seed, r, B, k, sh.V, sh.logit_dtype),
+            W.gen_round_truth(seed, r, B, k, sh.V, args.pattern, alpha=args.alpha)) for r in range(rounds)]
     tv = tr = tk = 0.0
-    for r in range(rounds):
-        bits = W.gen_logits_np(seed, r, B, k, sh.V, sh.logit_dtype)
-        rt = W.gen_round_truth(seed, r, B, k, sh.V, args.pattern, alpha=args.alpha)
-        a = time.perf_counter()
-        v = OV.batch_verify(bits, sh.logit_dtype, rt.draft, n, pad, act)
-        b = time.perf_counter()
-        tokens, _, _ = OA.repad_tokens(tokens, cap, k, pad, L, v)
-        c = time.perf_counter()
-        kv, _ = OA.realign_kv(kv, pad, v["pad_new"], v["kept"])
-        d = time.perf_counter()
-        tv, tr, tk = tv + b - a, tr + c - b, tk + d - c
-        n, pad, L = v["n_new"], v["pad_new"], v["L_new"]
-    per_round = (tv + tr + tk * sh.n_planes / P) / rounds
-    return 1.0 / per_round, dict(verify_s=tv / rounds, repad_s=tr / rounds,
-                                 realign_sample_s=tk / rounds, planes=P)
+    with OD.make_pool(threads) as pool:
+        for bits, rt in ins:
+            a = time.perf_counter()
+            if threads > 1:
+                v = OD.batch_verify_parallel(pool, bits, sh.logit_dtype, rt.draft, n, pad, act)
+            else:
+                v = OV.batch_verify(bits, sh.logit_dtype, rt.draft, n, pad, act)
+            b = time.perf_counter()
+            tokens, _, _ = OA.repad_tokens(tokens, cap, k, pad, L, v)
+            c = time.perf_counter()
+            if threads > 1:
+                OD.realign_parallel(pool, kv, pad, v["pad_new"], v["kept"])
+            else:
+                OA.realign_kv_inplace(kv, pad, v["pad_new"], v["kept"])
+            d = time.perf_counter()
+            tv, tr, tk = tv + b - a, tr + c - b, tk + d - c
+            n, pad, L = v["n_new"], v["pad_new"], v["L_new"]
+    per_round = (tv + tr + tk) / rounds
+    return 1.0 / per_round, dict(verify_s=tv / rounds, repad_s=tr / rounds, realign_s=tk / rounds,
+                                 planes=sh.n_planes, rounds=rounds, threads=threads)
+
+
+def round_cpu_baseline(sh, args, rounds=2):
+    """cpu_baseline of the round line: the oracle on `nproc` host threads (value) and on one
+    thread, both over whole rounds of the bench workload."""
+    from oracle import driver as OD
+    nthr = OD.host_threads()
+    rps_n, parts_n = oracle_round_sample(sh, args, rounds=rounds, threads=nthr)
+    rps_1, parts_1 = oracle_round_sample(sh, args, rounds=rounds, threads=1)
+    return {"value": rps_n, "unit": "rounds/s", "cores": nthr, "kind": "oracle",
+            "sample": (f"{rounds} whole oracle rounds of the {sh.name} workload (verify over the full "
+                       f"logits tail, repad, realign over all {sh.n_planes} KV planes; no extrapolation), "
+                       f"thread-parallel driver over batch rows and (plane, row) slabs on {nthr} threads "
+                       f"(oracle/driver.py); numpy on {cpu_info()}"),
+            "nproc": nthr, "cpu_model": cpu_info(), "parts_s": parts_n,
+            "single_thread": {"value": rps_1, "cores": 1, "parts_s": parts_1}}
 
 
 def cpu_info():
@@ -543,14 +569,16 @@ def pool_workload(args):
     return lens, order
 
 
-def oracle_pool_sample(args, verify_samples=2):
+def oracle_pool_sample(args, verify_samples=2, threads=1):
     """The CPU oracle on the pool workload, as a bounded sample: the oracle's own GetBatch
     plan (oracle.pool.form_batches, timed in full) drives the whole drain with the planted
     accept lengths; the per-batch Alg. 1 verify (oracle.verify.batch_verify over the full
-    B x (k+1) x V logits) and the KV gather / scatter copy rate (oracle.align.copy_rows on
-    2 of the 72 planes of one member) are timed on samples and extrapolated to the drain's
-    batch count and algorithmic KV bytes.  Returns (sequences/s, parts)."""
+    B x (k+1) x V logits) and the KV gather copy rate (oracle.align.copy_rows of one whole
+    member, all 72 planes) are timed on samples and extrapolated to the drain's batch count
+    and algorithmic KV bytes.  threads > 1: the thread-parallel driver (oracle/driver.py:
+    batch rows / planes on separate threads).  Returns (sequences/s, parts)."""
     from oracle import align as OA
+    from oracle import driver as OD
     from oracle import pool as OP
     from oracle import verify as OV
     sh = W.SHAPES["qwen3"]
@@ -583,24 +611,47 @@ def oracle_pool_sample(args, verify_samples=2):
             n_batches += 1
     # per-batch verify, timed on samples of the same logits
     t_ver = []
+    pool = OD.make_pool(threads)
     for r in range(verify_samples):
         bits = W.gen_logits_np(args.seed, r, B, k, V, sh.logit_dtype)
         n = np.full(B, 300, np.int32)
         t0 = time.perf_counter()
-        OV.batch_verify(bits, sh.logit_dtype, truth[r].draft, n, np.zeros(B, np.int32), np.ones(B, np.uint8))
+        if threads > 1:
+            OD.batch_verify_parallel(pool, bits, sh.logit_dtype, truth[r].draft, n, np.zeros(B, np.int32),
+                                     np.ones(B, np.uint8))
+        else:
+            OV.batch_verify(bits, sh.logit_dtype, truth[r].draft, n, np.zeros(B, np.int32), np.ones(B, np.uint8))
         t_ver.append(time.perf_counter() - t0)
-    # KV copy rate of the oracle's gather (2 planes of one 300-token member)
-    P, cap = 2, 320
+    # KV copy rate of the oracle's gather: one whole 300-token member, every plane, into a
+    # right-aligned staging row (per plane on its own thread when threads > 1)
+    P, cap = sh.n_planes, 320
     src = W.gen_kv_bits_np(args.seed, 1 * P * sh.H * cap * sh.D).reshape(1, P, sh.H, cap, sh.D)
     dst = np.zeros((1, P, sh.H, cap, sh.D), np.uint16)
+
+    def gather_plane(p):
+        OA.copy_rows(src[:, p:p + 1], dst[:, p:p + 1], count=np.array([299]), src_row=np.array([0]),
+                     dst_col=np.array([1]))
     t0 = time.perf_counter()
-    OA.copy_rows(src, dst, count=np.array([299]), src_row=np.array([0]), dst_col=np.array([1]))
+    if threads > 1:
+        list(pool.map(gather_plane, range(P)))
+    else:
+        OA.copy_rows(src, dst, count=np.array([299]), src_row=np.array([0]), dst_col=np.array([1]))
     t_cp = time.perf_counter() - t0
+    pool.shutdown()
     kv_rate = 2 * 299 * P * sh.H * sh.D * 2 / max(t_cp, 1e-9)   # bytes read + written per s
     t_total = t_plan + n_batches * float(np.mean(t_ver)) + kv_bytes / kv_rate
     parts = {"plan_s": t_plan, "verify_s_per_batch": float(np.mean(t_ver)), "batches": n_batches,
-             "kv_bytes": kv_bytes, "kv_copy_GBps": kv_rate / 1e9, "total_s": t_total}
+             "kv_bytes": kv_bytes, "kv_copy_GBps": kv_rate / 1e9, "total_s": t_total, "threads": threads}
     return N / t_total, parts
+
+
+def pool_sample_text(args, parts, threads):
+    return (f"the oracle's GetBatch plan over the whole {args.pool_n}-sequence drain ({parts['batches']} "
+            f"batches, timed in full); per-batch oracle verify timed on 2 batches and the KV gather of one "
+            f"whole member (all 72 planes), extrapolated to the drain's batches and "
+            f"{parts['kv_bytes'] / 1e9:.0f} GB; numpy, "
+            + (f"thread-parallel driver on {threads} threads" if threads > 1 else "single thread")
+            + f", on {cpu_info()}")
 
 
 SLEEP_CYCLES = 200_000     # ~0.1 ms at 1.965 GHz: longer than Python's enqueue of one batch
@@ -816,13 +867,13 @@ def pool_cpu_baseline(args):
     oracle_pool_sample), for the pool line's cpu_baseline."""
     if args.no_cpu_baseline:
         return None
-    sps, parts = oracle_pool_sample(args)
-    return {"value": sps, "unit": "sequences/s", "cores": 1, "kind": "oracle",
-            "sample": (f"the oracle's GetBatch plan over the whole {args.pool_n}-sequence drain "
-                       f"({parts['batches']} batches, timed in full); per-batch oracle verify timed on 2 "
-                       f"batches and KV copies on 2 of 72 planes of one member, extrapolated to the drain's "
-                       f"batches and {parts['kv_bytes'] / 1e9:.0f} GB; numpy single-threaded on {cpu_info()}"),
-            "parts": parts}
+    from oracle import driver as OD
+    nthr = OD.host_threads()
+    sps, parts = oracle_pool_sample(args, threads=nthr)
+    sps1, parts1 = oracle_pool_sample(args, threads=1)
+    return {"value": sps, "unit": "sequences/s", "cores": nthr, "kind": "oracle",
+            "sample": pool_sample_text(args, parts, nthr), "nproc": nthr, "cpu_model": cpu_info(),
+            "parts": parts, "single_thread": {"value": sps1, "cores": 1, "parts": parts1}}
 
 
 def run_pool_emulated(args, device):
@@ -862,38 +913,37 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle as it stands, rank 0 only."""
     if rank != 0:
         return None
+    from oracle import driver as OD
+    nthr = OD.host_threads()
     if args.config == "pool":
         t0 = time.perf_counter()
-        sps, parts = oracle_pool_sample(args)
+        sps, parts = oracle_pool_sample(args, threads=nthr)
         wall = time.perf_counter() - t0
-        sample = (f"the oracle's GetBatch plan over the whole {args.pool_n}-sequence drain "
-                  f"({parts['batches']} batches, timed in full); per-batch oracle verify timed on 2 "
-                  f"batches and KV copies on 2 of 72 planes of one member, extrapolated to the "
-                  f"drain's batches and {parts['kv_bytes'] / 1e9:.0f} GB; numpy single-threaded on {cpu_info()}")
+        sample = pool_sample_text(args, parts, nthr)
         return {"impl": "reference", "metric": "EXSpec pool sequences/s (Qwen3-8B shape, N=%d, B=8, k=5)"
                 % args.pool_n, "value": sps, "unit": "sequences/s", "n_gpus": world, "steps": 1,
                 "warmup": 0, "ms_per_step": parts["total_s"] * 1e3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": f"EXSpec pool drain: {args.pool_n} seqs, prompt {args.pool_lengths}"},
-                "cpu_baseline": {"value": sps, "unit": "sequences/s", "cores": 1, "kind": "oracle",
-                                 "sample": sample, "parts": parts, "wall_s": wall},
+                "cpu_baseline": {"value": sps, "unit": "sequences/s", "cores": nthr, "kind": "oracle",
+                                 "sample": sample, "nproc": nthr, "cpu_model": cpu_info(), "parts": parts,
+                                 "wall_s": wall},
                 "e2e": {"value": sps, "unit": "sequences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     sh = shape_for(args)
-    for _ in range(max(0, min(args.warmup, 1))):
-        oracle_round_sample(sh, args, rounds=1)
-    n = max(1, min(args.steps, 3))
+    n = max(2, min(args.steps, 3))
     t0 = time.perf_counter()
-    rps, parts = oracle_round_sample(sh, args, rounds=n)
+    rps, parts = oracle_round_sample(sh, args, rounds=n, threads=nthr)
     wall = time.perf_counter() - t0
-    sample = (f"{n} oracle rounds of the {sh.name} workload; verify + repad in full, realign on "
-              f"{parts['planes']} of {sh.n_planes} KV planes extrapolated x{sh.n_planes / parts['planes']:.0f}; "
-              f"numpy single-threaded on {cpu_info()}")
+    sample = (f"{n} whole oracle rounds of the {sh.name} workload (verify over the full logits tail, repad, "
+              f"realign over all {sh.n_planes} KV planes; no extrapolation), thread-parallel driver on {nthr} "
+              f"threads (oracle/driver.py); numpy on {cpu_info()}")
     return {"impl": "reference", "metric": METRIC, "value": rps, "unit": "rounds/s",
             "n_gpus": world, "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 / rps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": sh.kv_dtype,
             "data": "synthetic", "config": {"workload": workload_name(sh, args)},
-            "cpu_baseline": {"value": rps, "unit": "rounds/s", "cores": 1, "kind": "oracle",
-                             "sample": sample, "parts_s": parts, "wall_s": wall},
+            "cpu_baseline": {"value": rps, "unit": "rounds/s", "cores": nthr, "kind": "oracle",
+                             "sample": sample, "nproc": nthr, "cpu_model": cpu_info(), "parts_s": parts,
+                             "wall_s": wall},
             "e2e": {"value": rps, "unit": "rounds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -945,11 +995,7 @@ def main():
         traffic, traffic_note = ncu_traffic(f"{sh.name}_B{sh.B}" + ("_pingpong" if args.kv_mode == "pingpong" else ""))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            rps, parts = oracle_round_sample(sh, args, rounds=2)
-            cpu = {"value": rps, "unit": "rounds/s", "cores": 1, "kind": "oracle",
-                   "sample": (f"2 oracle rounds, verify+repad in full, realign on {parts['planes']} of "
-                              f"{sh.n_planes} planes extrapolated; numpy 1 thread; {cpu_info()}"),
-                   "parts_s": parts}
+            cpu = round_cpu_baseline(sh, args, rounds=2)
         out = {
             "metric": METRIC, "value": value, "unit": "rounds/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"] / args.steps,
