@@ -75,6 +75,8 @@ def parse(argv=None):
     ap.add_argument("--ctx", type=int, default=0, help="override the context: n ~ U[ctx-512, ctx]")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=1,
+                    help="repeat the timed region (value) this many times and report the median")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--episode", type=int, default=32,
@@ -373,22 +375,25 @@ def run_ours(args, rank, world, device):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- A: value (graphs)
+    # ---- A: value (graphs); --reps R: R timed repetitions, the median is reported
     rb.reset()
     run_rounds(args.warmup)
-    rb.reset()
-    moved0 = int(bt.moved.item())
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sync()
     clocks = ClockSampler(device.index if device.index is not None else 0)
+    reps = []
     with clocks:
-        t0.record(rb.stream)
-        run_rounds(args.steps)
-        t1.record(rb.stream)
-        torch.cuda.synchronize()
-    sync()
-    ms = t0.elapsed_time(t1)
-    moved_A = int(bt.moved.item()) - moved0
+        for _ in range(max(1, args.reps)):
+            rb.reset()
+            moved0 = int(bt.moved.item())
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            sync()
+            t0.record(rb.stream)
+            run_rounds(args.steps)
+            t1.record(rb.stream)
+            torch.cuda.synchronize()
+            sync()
+            reps.append(max_over_ranks(t0.elapsed_time(t1), device, world))
+            moved_A = int(bt.moved.item()) - moved0
+    ms = float(np.median(reps))
     width_end = int((bt.pad_cur + bt.n_cur).max().item())
     status = int(bt.status.item())
     # ---- B: per-kernel events (direct launches, same rounds)
@@ -410,7 +415,7 @@ def run_ours(args, rank, world, device):
     # ---- C: e2e
     e2e = None if args.no_e2e else run_e2e(rb, args, world)
     logits_bytes = sh.B * (sh.k + 1) * sh.V * (4 if sh.logit_dtype == "fp32" else 2)
-    return dict(sh=sh, ms=max_over_ranks(ms, device, world), moved=alg_B, copied=moved_B, moved_A=moved_A,
+    return dict(sh=sh, ms=ms, reps_ms=reps, moved=alg_B, copied=moved_B, moved_A=moved_A,
                 k1_ms=k1, k3_ms=k3,
                 kernels_per_round=bt.kernels_per_round,
                 k2_ms=k2, status=status | int(bt.status.item()), clocks=clocks.summary(), e2e=e2e,
@@ -775,16 +780,22 @@ def run_pool(args, rank, world, device, emulate=False):
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(device.index if device.index is not None else 0)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    reps = []
     with clocks:
-        t0.record()
-        epochs, batches = drain()
-        # the only collective: finished outputs + counters, once, at the end
-        counters = sp.counters.clone()
-        t1.record()
-        torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
+        for _ in range(max(1, args.reps)):       # --reps R: median of R timed drains
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            if world > 1 and not emulate:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0.record()
+            epochs, batches = drain()
+            # the only collective: finished outputs + counters, once, at the end
+            counters = sp.counters.clone()
+            t1.record()
+            torch.cuda.synchronize()
+            reps.append(t0.elapsed_time(t1))
+    ms = float(np.median(reps))
     moved = int(sp.moved.item())
     cnt = ran.copy()          # executed batches (see drain); K4's counters: planned ones
     cnt[5] = int(counters[0].item())
@@ -837,6 +848,7 @@ def run_pool(args, rank, world, device, emulate=False):
                  "fallback_members": int(cnt_all[3]), "planned_batches_K4": int(cnt_all[5]),
                  "mean_batch": (int(cnt_all[2]) + int(cnt_all[3])) / max(1, int(cnt_all[0])),
                  "kv_bytes_moved_rank0": moved, "gather_ms": gather_ms,
+                 "reps_drain_ms": reps if len(reps) > 1 else None,
                  # kernel time sums from a serial drain with events around every launch
                  # (rank 0): the overlapped executor's lower bound is max(K2, K1 same-length)
                  "serial_kernel_ms": {"K2_gather_scatter": k2_ms, "K1_same_length": k1_same_ms,
@@ -1033,6 +1045,8 @@ def main():
                                               f"per-round graphs)" if args.round_mode == "graph-block" else
                                               " (graph: one CUDA graph per (parity, ring slot), 3 kernels per replay)"),
             "bytes_moved_check": {"value_region": res["moved_A"], "kernel_region": res["copied"]},
+            "reps": {"n": len(res["reps_ms"]), "ms_per_step": [x / args.steps for x in res["reps_ms"]],
+                     "value": "median"} if len(res["reps_ms"]) > 1 else None,
             "status": res["status"],
             "cpu_baseline": cpu,
         }

@@ -1,7 +1,10 @@
 """SURVEY §8d bench matrix: runs bench.py over the cells and prints one summary line per
-cell (plus the raw JSON lines to --jsonl).
+cell (plus the raw JSON lines to --jsonl).  Every cell is first checked against the oracle
+on its first rounds / epoch (tests/test_gpu_bench_cells.py, one pytest run for all cells)
+and its verdict printed with its numbers; each cell's value is the median of --reps timed
+repetitions (default 5).
 
-    python tools/bench_matrix.py [--quick] [--jsonl out.jsonl]
+    python tools/bench_matrix.py [--quick] [--reps 5] [--no-oracle] [--jsonl out.jsonl]
 """
 from __future__ import annotations
 
@@ -10,6 +13,8 @@ import json
 import os
 import subprocess
 import sys
+import tempfile
+import xml.etree.ElementTree as ET
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -56,26 +61,45 @@ def summary(label, d):
             f"K1 {k['verify_K1'] * 1e3:5.1f} K3 {k['repad_K3'] * 1e3:5.1f} K2 {k['realign_K2'] * 1e3:7.1f} us")
 
 
+def oracle_verdicts(quick):
+    """Run the per-cell oracle checks once; returns {cell label: "pass" | "FAIL" | "skip"}."""
+    xml = os.path.join(tempfile.mkdtemp(), "cells.xml")
+    sel = ["-k", "test_round_cell"] if quick else []
+    subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_bench_cells.py"), "-q",
+                    "-m", "gpu", f"--junitxml={xml}"] + sel, cwd=ROOT, capture_output=True, text=True, timeout=3600)
+    res = {}
+    for tc in ET.parse(xml).getroot().iter("testcase"):
+        name = tc.get("name")
+        label = name[name.index("[") + 1:-1] if "[" in name else name
+        bad = tc.find("failure") is not None or tc.find("error") is not None
+        res[label] = "FAIL" if bad else ("skip" if tc.find("skipped") is not None else "pass")
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="round cells only")
+    ap.add_argument("--reps", type=int, default=5, help="timed repetitions per cell (median reported)")
+    ap.add_argument("--no-oracle", action="store_true", help="skip the per-cell oracle checks")
     ap.add_argument("--jsonl", default="")
     a = ap.parse_args()
     cells = [(lbl, ROUND + args) for lbl, args in CELLS]
     if not a.quick:
         cells += [(lbl, ["--no-cpu-baseline"] + args) for lbl, args in POOL]
+    verdict = {} if a.no_oracle else oracle_verdicts(a.quick)
     out = open(a.jsonl, "w") if a.jsonl else None
     for lbl, args in cells:
-        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, capture_output=True,
-                           text=True, timeout=900)
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--reps", str(a.reps)] + args,
+                           capture_output=True, text=True, timeout=1800)
         lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
         if r.returncode or not lines:
             print(f"{lbl:26s} FAILED rc={r.returncode} {r.stderr.strip().splitlines()[-1:]}", flush=True)
             continue
         d = json.loads(lines[-1])
+        d["oracle_check"] = verdict.get(lbl, "not run")
         if out:
             out.write(json.dumps({"cell": lbl, **d}) + "\n")
-        print(summary(lbl, d), flush=True)
+        print(f"{summary(lbl, d)}  oracle {d['oracle_check']}", flush=True)
 
 
 if __name__ == "__main__":
