@@ -52,9 +52,10 @@ def parse(argv=None):
     ap.add_argument("--shard", default="balanced", choices=["band", "strided", "balanced"],
                     help="pool sharding over ranks: equal-count bands, strided, or bands of "
                          "equal estimated cost (prompt length + max_new per sequence)")
-    ap.add_argument("--pool-consumer", default="zero-copy", choices=["zero-copy", "dense"],
+    ap.add_argument("--pool-consumer", default="zero-copy", choices=["zero-copy", "dense", "slot"],
                     help="pool: same-length batches run on the pool slots (zero-copy) or are "
-                         "gathered into a dense staging rectangle too (PAPER.md:537)")
+                         "gathered into a dense staging rectangle too (PAPER.md:537); slot: a "
+                         "slot-indexed consumer, no batch moves KV (SURVEY 8f f3)")
     ap.add_argument("--pool-exec", default="native", choices=["native", "python"],
                     help="pool: per-batch launch loop in C++ (specdec_pool_epoch) or Python")
     ap.add_argument("--pool-staging", type=int, default=2,
@@ -597,6 +598,7 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
     n_batches = 0
     kv_bytes = 0
     dense = args.pool_consumer == "dense"
+    slot = args.pool_consumer == "slot"
     while act.any():
         t0 = time.perf_counter()
         plan = OP.form_batches(o_len, act, order, Wn, B, args.min_group)
@@ -607,7 +609,7 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
             acc = truth[n_batches % RING].accept
             for j, s in enumerate(mem):
                 e = min(int(acc[j]) + 1, args.max_new - int(gen[s]))
-                if dense or not plan["kind"][b]:
+                if dense or (not plan["kind"][b] and not slot):
                     kv_bytes += 2 * (int(o_len[s]) - 1) * sh.bpt + 2 * (int(acc[j]) + 1) * sh.bpt
                 o_len[s] += e
                 gen[s] += e
@@ -689,7 +691,7 @@ def run_pool(args, rank, world, device, emulate=False):
     Wn = min(args.pool_W or n_loc, 2048, n_loc)
     sp = SequencePool(n_loc, cap, sh.layers, sh.H, sh.D, k, W=Wn, B=min(B, Wn),
                       min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False,
-                      dense_consumer=args.pool_consumer == "dense",
+                      consumer=args.pool_consumer,
                       n_staging=args.pool_staging if args.pool_exec == "native" else 1)
     local_lens = lens[mine]
     local_order = np.arange(n_loc)            # `mine` is already in admission order
@@ -755,7 +757,7 @@ def run_pool(args, rank, world, device, emulate=False):
                 ran[2] += int(sizes[b]) if kinds[b] else 0
                 lg, d = inputs(b)
                 if events is not None:
-                    fb = not kinds[b] or sp.dense_consumer
+                    fb = sp.moves_kv(kinds[b])
                     e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                     # keep the GPU busy while Python enqueues this batch, so that the event
                     # intervals hold kernel time only, not host launch gaps
@@ -829,6 +831,21 @@ def run_pool(args, rank, world, device, emulate=False):
     peak, peak_src = peaks()
     achieved = moved2 / (k2_ms / 1e3) / 1e9 if k2_ms else 0.0
     rate_same = cnt_all[1] / max(1, cnt_all[0])
+    roof = {"bound": "hbm", "kernel": "specdec_realign_kv gather+scatter (fallback batches)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            # launches differ in size (one per fallback batch): no single per-launch
+            # figure; the note gives the ncu traffic of one representative gather
+            "traffic_note": ncu_traffic("pool_gather")[1], "peak_source": peak_src}
+    if sp.consumer == "slot":
+        # no KV moves: the dominant kernel is the verify (logits of every member row)
+        lg_bytes = (int(cnt[2]) + int(cnt[3])) * (k + 1) * V * 2
+        k1_ms = k1_same_ms + k1_fb_ms
+        ach = lg_bytes / (k1_ms / 1e3) / 1e9 if k1_ms else 0.0
+        roof = {"bound": "hbm", "kernel": "specdec_pool_verify (K1 + write-back), every batch",
+                "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                "note": "latency-bound launches of mean batch size "
+                        f"{(int(cnt[2]) + int(cnt[3])) / max(1, int(cnt[0])):.2f}; event-timed one by one",
+                "peak_source": peak_src}
     return {
         "metric": "EXSpec pool sequences/s (Qwen3-8B shape, N=%d, B=%d, k=%d)" % (N, sp.B, k),
         "value": N / (ms / 1e3), "unit": "sequences/s", "n_gpus": world, "steps": epochs,
@@ -853,19 +870,14 @@ def run_pool(args, rank, world, device, emulate=False):
                  # (rank 0): the overlapped executor's lower bound is max(K2, K1 same-length)
                  "serial_kernel_ms": {"K2_gather_scatter": k2_ms, "K1_same_length": k1_same_ms,
                                       "K1_fallback": k1_fb_ms, "drain_ms": ms}},
-        "roofline": {"bound": "hbm", "kernel": "specdec_realign_kv gather+scatter (fallback batches)",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     # launches differ in size (one per fallback batch): no single per-launch
-                     # figure; the note gives the ncu traffic of one representative gather
-                     "traffic_note": ncu_traffic("pool_gather")[1], "peak_source": peak_src},
+        "roofline": roof,
         "clocks": clocks.summary(), "status": status,
         # libspecdec launches in the timed drain: K4 per plan (the epochs + the final empty
         # plan), K1 with the fused write-back per batch, gather + scatter per fallback batch
         # (Alg. 3 device loop: K4 + gate + gather + verify + scatter per issued iteration)
         "gpu_launches": (3 + _abi.specdec_verify_kernels(True)) * alg3_iters["n"] if alg3_iters["n"] else (epochs + 1)
         + (_abi.specdec_verify_kernels(True) if sp.fused else _abi.specdec_verify_kernels(False) + 1) * int(cnt[0])
-        + 2 * (int(cnt[0]) if sp.dense_consumer else int(cnt[0]) - int(cnt[1])),
+        + 2 * (int(cnt[0]) if sp.dense_consumer else 0 if sp.consumer == "slot" else int(cnt[0]) - int(cnt[1])),
         "e2e": None,
         "e2e_note": "pool: the per-batch logits come from the model's forward on the device (the "
                     "executor's forward callback); the host-buffer end-to-end path is the default "

@@ -328,8 +328,8 @@ int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, int64_t k, i
  * the members of the fallback batches run.  All device buffers are caller-owned
  * (paper_2510_22876_b200/exspec.py allocates them); host_header is pinned, 1 + 3W int32.
  */
-typedef void (*specdec_forward_fn)(void *ctx, int32_t batch, int32_t same_length, int32_t width,
-                                   const void **logits, const int64_t **draft);
+typedef void (*specdec_forward_fn)(void *ctx, int32_t batch, int32_t same_length /* KV in the pool slots */,
+                                   int32_t width, const void **logits, const int64_t **draft);
 
 typedef struct specdec_pool_desc {
     /* pool state */
@@ -371,9 +371,17 @@ typedef struct specdec_pool_desc {
     const int64_t *const *draft_ring;
     int32_t ring_n;
     int32_t *ring_pos; /* host, advanced per batch */
-    /* 1: gather / scatter every batch, same-length ones too -- a consumer that needs a
-     * dense rectangle ("concatenate directly"); 0: same-length batches run
-     * zero-copy on the pool slots (forward kind = 1) */
+    /* The consumer of a batch's KV (the model's verify forward):
+     * 0: a dense right-aligned rectangle -- mixed-length batches are gathered into the
+     *    staging (realigned) and scattered back; same-length batches run zero-copy on the
+     *    pool slots (lazy realignment);
+     * 1: a dense rectangle for every batch, same-length ones too ("concatenate directly",
+     *    PAPER.md:537);
+     * 2: slot-indexed (e.g. a variable-length attention reading each member's KV rows
+     *    [0, len-1) in its own slot and appending at column len-1): no batch moves KV
+     *    ("slot-indexed zero-copy consumer").
+     * The forward callback's `same_length` argument is 1 when the batch's KV is in the pool
+     * slots, 0 when it is in the staging. */
     int32_t dense_consumer;
     /* Overlapped fallback gathers (n_staging >= 2; 0 or 1 = off, the serial loop above).
      * The batches of one epoch have disjoint members and are planned from one window

@@ -80,7 +80,8 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     std::vector<int32_t> fbs;
     seq.reserve(run);
     for (int32_t b = 0; b < run; ++b)
-        if (kinds[b] == 0 || d->dense_consumer) fb_rank[b] = static_cast<int32_t>(fbs.size()), fbs.push_back(b);
+        if ((kinds[b] == 0 && d->dense_consumer != 2) || d->dense_consumer == 1)
+            fb_rank[b] = static_cast<int32_t>(fbs.size()), fbs.push_back(b);
     if (!overlap) {
         for (int32_t b = 0; b < run; ++b) seq.push_back(b);
     } else {
@@ -250,7 +251,7 @@ extern "C" int specdec_pool_alg3(const specdec_pool_desc *d, int32_t iterations,
     gate.scol = g_scol;
     gate.active = g_active;
     gate.exec = d_exec_counters;
-    gate.dense = d->dense_consumer ? 1 : 0;
+    gate.dense = d->dense_consumer;
     for (int32_t it = 0; it < iterations; ++it) {
         int rc = pool_group_launch(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
                                    d->window_size, d->batch_of, d->slot_of, d->members, d->mlen, d->mpad,

@@ -17,7 +17,7 @@ struct Alg3Gate {
     int32_t *members = nullptr, *kv = nullptr, *scol = nullptr;
     uint8_t *active = nullptr;
     unsigned long long *exec = nullptr;
-    int dense = 0;
+    int dense = 0;  // specdec_pool_desc::dense_consumer
 };
 
 int pool_group_launch(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order, int32_t N,

@@ -427,7 +427,9 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
         __syncthreads();
         const bool valid = nb_total > 0;
         const bool same = valid && sm.bmax[0] == sm.bmin[0];
-        const bool moves = valid && (!same || gate.dense);  // batch 0 goes through the staging
+        // batch 0 goes through the staging: a mixed batch (dense rectangle consumer) or every
+        // batch (dense = 1); never with the slot-indexed consumer (dense = 2)
+        const bool moves = valid && gate.dense != 2 && (!same || gate.dense == 1);
         for (int j = tid; j < B; j += T) {
             const int32_t m = valid ? members[j] : -1;
             gate.members[j] = m;

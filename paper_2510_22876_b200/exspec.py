@@ -29,7 +29,7 @@ from .eqspec import TORCH_DT
 class SequencePool:
     def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
                  max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True,
-                 dense_consumer=False, n_staging=1):
+                 dense_consumer=False, n_staging=1, consumer=None):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         if B > W:
@@ -39,8 +39,14 @@ class SequencePool:
         self.W, self.B, self.min_group = W, B, min_group
         self.max_new, self.eos_id, self.pad_id = max_new, eos_id, pad_id
         self.device = dev
-        # gather / scatter same-length batches too (a dense-rectangle consumer)
-        self.dense_consumer = bool(dense_consumer)
+        # the consumer of a batch's KV (specdec_pool_desc::dense_consumer): "zero-copy"
+        # (mixed batches gathered into the staging, same-length ones on the pool slots),
+        # "dense" (every batch gathered) or "slot" (a slot-indexed consumer:
+        # no batch moves KV)
+        self.consumer = consumer or ("dense" if dense_consumer else "zero-copy")
+        if self.consumer not in ("zero-copy", "dense", "slot"):
+            raise ValueError(f"consumer {self.consumer!r}")
+        self.dense_consumer = self.consumer == "dense"
         # verify + write-back in one launch (specdec_pool_verify); False: the two calls
         self.fused = True
         self.cap_tok = cap_tok or cap
@@ -192,8 +198,12 @@ class SequencePool:
                                  status=self.status, stream=stream)
         self.verify_calls += 1
 
+    def moves_kv(self, kind) -> bool:
+        """Does a batch of this kind go through the staging (gather / scatter)?"""
+        return self.consumer == "dense" or (not kind and self.consumer == "zero-copy")
+
     def run_batch(self, b, kind, blen, logits, draft, forward=None, V=None, stream=None):
-        fallback = not kind or self.dense_consumer
+        fallback = self.moves_kv(kind)
         if fallback:
             self.gather(b, stream)
         if forward is not None:
@@ -253,7 +263,7 @@ class SequencePool:
         d.draft_ring = ctypes.cast(self._dr_ptrs, ctypes.c_void_p)
         d.ring_n = len(ring)
         d.ring_pos = ctypes.addressof(self._ring_pos)
-        d.dense_consumer = 1 if self.dense_consumer else 0
+        d.dense_consumer = {"zero-copy": 0, "dense": 1, "slot": 2}[self.consumer]
         # the gathers take K2 work tickets (SPECDEC_DYNAMIC) from a zeroed 128-byte header
         self._gather_ws = torch.zeros(128, dtype=torch.uint8, device=self.device)
         d.gather_ws = self._gather_ws.data_ptr()

@@ -200,12 +200,16 @@ def test_fault_modes_scored(cuda, seed, B, noise):
     assert runs["bonus_from_draft"][1] < min(runs["stale_position_ids"][1], runs["skip_kv_realign"][1]), runs
 
 
-@pytest.mark.parametrize("N,Wn,B,mg,alg3,dense", [(10, 6, 3, 2, False, False), (8, 8, 4, 4, False, False),
-                                                   (7, 7, 1, 2, False, False), (9, 6, 3, 2, True, False),
-                                                   (10, 6, 3, 2, False, True)])
-def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3, dense):
+@pytest.mark.parametrize("N,Wn,B,mg,alg3,consumer", [(10, 6, 3, 2, False, "zero-copy"), (8, 8, 4, 4, False, "zero-copy"),
+                                                      (7, 7, 1, 2, False, "zero-copy"), (9, 6, 3, 2, True, "zero-copy"),
+                                                      (10, 6, 3, 2, False, "dense"), (10, 6, 3, 2, False, "slot"),
+                                                      (12, 12, 4, 2, False, "slot")])
+def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3, consumer):
     """EXSpec on the GPU path; alg3=True runs Alg. 3 as printed (batch 0, then re-plan);
-    dense=True gathers / scatters same-length batches too (a dense-rectangle consumer)."""
+    consumer "dense" gathers / scatters same-length batches too (a dense-rectangle
+    consumer), "slot" moves no KV at all: every member's forward reads its own slot at its
+    own width (a slot-indexed consumer)."""
+    dense = consumer == "dense"
     T = ToyLM(V, LAYERS, H, D, seed=7)
     k, max_new = 3, 12
     prompts = _prompts(N, seed=N + B)
@@ -221,7 +225,7 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3, dense):
         for c, t in enumerate(p[:-1]):                    # prefill all but the pending token
             T.token_forward(t, c, c, kv[s], ones)
     sp = SequencePool(N, cap, LAYERS, H, D, k, W=Wn, B=B, min_group=mg, max_new=max_new, eos_id=1,
-                      device=cuda, dense_consumer=dense)
+                      device=cuda, consumer=consumer)
     sp.load(lens, tokens, order, _to_dev(kv, cuda))
     sp.fused = not dense          # the dense case also covers the unfused verify + write-back
     kinds_seen = set()
@@ -232,7 +236,7 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3, dense):
         for b in range(1 if alg3 else nb):
             mem = sp.members[b].cpu().numpy()
             Lb = int(blens[b])
-            fallback = not kinds[b] or dense
+            fallback = sp.moves_kv(kinds[b])
             kinds_seen.add(int(kinds[b]))
             if fallback:
                 sp.gather(b)
@@ -246,18 +250,19 @@ def test_exspec_pool_on_gpu_equals_greedy(cuda, N, Wn, B, mg, alg3, dense):
                 if s < 0:
                     continue
                 n = int(plen[s])
-                p = Lb - n
+                Lr = Lb if fallback or kinds[b] else n     # slot consumer: the member's own width
+                p = Lr - n
                 content = list(ptok[s, :n])
                 draft[j] = T.propose(content, k, 0.3)
-                mask, pos = mask_pos_row(p, Lb + k)
+                mask, pos = mask_pos_row(p, Lr + k)
                 if fallback:
                     row = src[:, j]                        # right-aligned staging row
                 else:
                     row = pool_kv[s]                       # zero-copy: the pool slot itself
-                for c in range(Lb - 1, Lb + k):
-                    t = content[-1] if c == Lb - 1 else int(draft[j, c - Lb])
+                for c in range(Lr - 1, Lr + k):
+                    t = content[-1] if c == Lr - 1 else int(draft[j, c - Lr])
                     lg = T.token_forward(t, int(pos[c]), c, row, mask)
-                    logits[j, c - Lb + 1] = lg.astype(np.float32)
+                    logits[j, c - Lr + 1] = lg.astype(np.float32)
             if fallback:
                 sp.staging.copy_(_to_dev(src, cuda))
             else:

@@ -64,9 +64,19 @@ def test_pool_dense_consumer_flag():
     seen = []
     sp.run_batch(0, 1, 5, None, None, forward=lambda pool, b, zero_copy, blen: seen.append(zero_copy))
     assert calls == [("g", 0), ("vw",), ("s", 0)] and seen == [False]
-    sp.dense_consumer = False
+    sp.consumer = "zero-copy"
     calls.clear()
     seen.clear()
     sp.run_batch(0, 1, 5, None, None, forward=lambda pool, b, zero_copy, blen: seen.append(zero_copy))
     assert calls == [("vw",)] and seen == [True]
+    calls.clear()
+    sp.run_batch(0, 0, 5, None, None)                  # a mixed-length batch is gathered
+    assert calls == [("g", 0), ("vw",), ("s", 0)]
+    sp.consumer = "slot"                               # slot-indexed consumer: never
+    calls.clear()
+    seen.clear()
+    sp.run_batch(0, 0, 5, None, None, forward=lambda pool, b, zero_copy, blen: seen.append(zero_copy))
+    assert calls == [("vw",)] and seen == [True]
     assert torch.equal(sp.order, torch.arange(6, dtype=torch.int32))
+    with pytest.raises(ValueError):
+        SequencePool(6, 16, 1, 1, 8, 3, W=4, B=2, device="cpu", consumer="paged")

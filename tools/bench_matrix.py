@@ -37,6 +37,7 @@ POOL = (
     + [("P N1024 min_group 8", ["--config", "pool", "--min-group", "8"]),
        ("P N1024 alg3", ["--config", "pool", "--pool-mode", "alg3"]),
        ("P N1024 dense consumer", ["--config", "pool", "--pool-consumer", "dense"]),
+       ("P N1024 slot consumer", ["--config", "pool", "--pool-consumer", "slot"]),
        ("P N1024 serial executor", ["--config", "pool", "--pool-staging", "1"]),
        ("P N1024 emul x8 count bands", ["--config", "pool", "--emulate-ranks", "8", "--shard", "band"])]
     + [(f"P N1024 emulated x{g}", ["--config", "pool", "--emulate-ranks", str(g)]) for g in (2, 4, 8)]
