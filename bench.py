@@ -230,6 +230,8 @@ class RoundBench:
         # ping-pong: the method's (algorithmic) KV bytes are those of the rows that shift;
         # K2 also copies the Delta = 0 rows (counted by the device `moved` counter)
         self.alg_rows = torch.zeros(1, dtype=torch.int64, device=device)
+        # kept KV rows of every round (region B): the moved share = moved / all kept bytes
+        self.kept_rows = torch.zeros(1, dtype=torch.int64, device=device)
         if draft is not None:
             self.bt.dkv.copy_(W.gen_kv_torch(args.seed + 1, self.bt.dkv.shape, self.bt.dkv.dtype, device))
         self.bt.load(self.tokens, self.lengths)
@@ -303,6 +305,7 @@ class RoundBench:
         bt.realign()
         if ev is not None:
             ev[3].record(self.stream)
+            self.kept_rows += bt.kept.long().sum()
             if bt.kv_mode == "pingpong":
                 c = bt.cur
                 self.alg_rows += (bt.kept.long() * (bt.pad[c] != bt.pad[1 - c])).sum()
@@ -400,6 +403,7 @@ def run_ours(args, rank, world, device):
     # ---- B: per-kernel events (direct launches, same rounds)
     rb.reset()
     moved0 = int(bt.moved.item())
+    rb.kept_rows.zero_()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     sync()
     for r in range(args.steps):
@@ -416,7 +420,8 @@ def run_ours(args, rank, world, device):
     # ---- C: e2e
     e2e = None if args.no_e2e else run_e2e(rb, args, world)
     logits_bytes = sh.B * (sh.k + 1) * sh.V * (4 if sh.logit_dtype == "fp32" else 2)
-    return dict(sh=sh, ms=ms, reps_ms=reps, moved=alg_B, copied=moved_B, moved_A=moved_A,
+    kept_bytes = 2 * int(rb.kept_rows.item()) * sh.bpt
+    return dict(sh=sh, ms=ms, reps_ms=reps, moved=alg_B, copied=moved_B, moved_A=moved_A, kept_bytes=kept_bytes,
                 k1_ms=k1, k3_ms=k3,
                 kernels_per_round=bt.kernels_per_round,
                 k2_ms=k2, status=status | int(bt.status.item()), clocks=clocks.summary(), e2e=e2e,
@@ -808,8 +813,10 @@ def run_pool(args, rank, world, device, emulate=False):
         # one rank's shard drained alone on this GPU (no collectives): see run_pool_emulated
         assert int((gen_loc == args.max_new).sum()) == n_loc, "every sequence reaches max_new (EOS off)"
         return {"rank": rank, "ms": ms, "seqs": n_loc, "epochs": epochs, "batches": int(cnt[0]),
-                "same_length_batches": int(cnt[1]), "kv_bytes": moved, "status": status,
-                "clocks": clocks.summary()}
+                "same_length_batches": int(cnt[1]), "fallback_batches": int(cnt[0]) - int(cnt[1]),
+                "fallback_members": int(cnt[3]), "kv_bytes": moved, "status": status,
+                "prompt_len_range": [int(local_lens.min()), int(local_lens.max())],
+                "prompt_tokens": int(local_lens.sum()), "clocks": clocks.summary()}
     if world > 1:
         ms = max_over_ranks(ms, device, world)
         g0 = time.perf_counter()
@@ -926,6 +933,12 @@ def run_pool_emulated(args, device):
                      "per_rank_ms": [p["ms"] for p in per], "per_rank_seqs": [p["seqs"] for p in per],
                      "per_rank_batches": [p["batches"] for p in per],
                      "per_rank_kv_GB": [p["kv_bytes"] / 1e9 for p in per],
+                     "per_rank_fallback_batches": [p["fallback_batches"] for p in per],
+                     "per_rank_fallback_members": [p["fallback_members"] for p in per],
+                     "per_rank_same_length_batches": [p["same_length_batches"] for p in per],
+                     "per_rank_prompt_len_range": [p["prompt_len_range"] for p in per],
+                     "total_kv_GB": sum(p["kv_bytes"] for p in per) / 1e9,
+                     "total_batches": sum(p["batches"] for p in per),
                      "imbalance_max_over_mean": mx / (sum(p["ms"] for p in per) / G),
                      "note": "prediction: job time = slowest shard; the end-of-run all-gather (~2 MB over "
                              "NVLink) is not included"},
@@ -1057,6 +1070,11 @@ def main():
                                               f"per-round graphs)" if args.round_mode == "graph-block" else
                                               " (graph: one CUDA graph per (parity, ring slot), 3 kernels per replay)"),
             "bytes_moved_check": {"value_region": res["moved_A"], "kernel_region": res["copied"]},
+            # share of the kept KV bytes that K2 had to move (rows with a shift; f3 moves the
+            # physical origin to shrink it), over the kernel-timing region's rounds
+            "moved_share": {"value": res["moved"] / res["kept_bytes"] if res["kept_bytes"] else 0.0,
+                            "moved_bytes": res["moved"], "all_kept_bytes": res["kept_bytes"],
+                            "episode": args.episode},
             "reps": {"n": len(res["reps_ms"]), "ms_per_step": [x / args.steps for x in res["reps_ms"]],
                      "value": "median"} if len(res["reps_ms"]) > 1 else None,
             "status": res["status"],
