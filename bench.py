@@ -600,7 +600,7 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
     o_len, gen, act = lens.astype(np.int64), np.zeros(N, np.int64), np.ones(N, np.uint8)
     truth = [W.gen_round_truth(args.seed, r, B, k, V, args.pattern, alpha=args.alpha) for r in range(RING)]
     t_plan = 0.0
-    n_batches = 0
+    n_batches = n_same = same_members = fb_members = 0
     kv_bytes = 0
     dense = args.pool_consumer == "dense"
     slot = args.pool_consumer == "slot"
@@ -611,6 +611,11 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
         nb = 1 if args.pool_mode == "alg3" else len(plan["batches"])
         for b in range(nb):
             mem = plan["batches"][b]
+            if plan["kind"][b]:
+                n_same += 1
+                same_members += len(mem)
+            else:
+                fb_members += len(mem)
             acc = truth[n_batches % RING].accept
             for j, s in enumerate(mem):
                 e = min(int(acc[j]) + 1, args.max_new - int(gen[s]))
@@ -653,7 +658,8 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
     kv_rate = 2 * 299 * P * sh.H * sh.D * 2 / max(t_cp, 1e-9)   # bytes read + written per s
     t_total = t_plan + n_batches * float(np.mean(t_ver)) + kv_bytes / kv_rate
     parts = {"plan_s": t_plan, "verify_s_per_batch": float(np.mean(t_ver)), "batches": n_batches,
-             "kv_bytes": kv_bytes, "kv_copy_GBps": kv_rate / 1e9, "total_s": t_total, "threads": threads}
+             "same_length_batches": n_same, "same_length_members": same_members,
+             "fallback_members": fb_members, "kv_bytes": kv_bytes, "kv_copy_GBps": kv_rate / 1e9, "total_s": t_total, "threads": threads}
     return N / t_total, parts
 
 
@@ -718,7 +724,9 @@ def run_pool(args, rank, world, device, emulate=False):
                   est_gather_GBps=args.pool_est[0], est_verify_us=args.pool_est[1])
 
     def drain(events=None):
+        # every drain is the same workload: the pool state and the input ring restart
         sp.load(local_lens, order=local_order)
+        ctr["i"] = 0
         sp.moved.zero_()
         epochs = batches = 0
         ran[:] = 0
@@ -810,13 +818,23 @@ def run_pool(args, rank, world, device, emulate=False):
     out_loc = sp.out_buf.cpu().numpy()
     gen_loc = sp.gen.cpu().numpy()
     if emulate:
-        # one rank's shard drained alone on this GPU (no collectives): see run_pool_emulated
+        # one rank's shard drained alone on this GPU (no collectives): see run_pool_emulated.
+        # A second, serial drain with events around every launch splits the shard's time
+        # into its two streams (fallback KV moves, verifies)
         assert int((gen_loc == args.max_new).sum()) == n_loc, "every sequence reaches max_new (EOS off)"
+        evs = []
+        drain(evs)
+        torch.cuda.synchronize()
         return {"rank": rank, "ms": ms, "seqs": n_loc, "epochs": epochs, "batches": int(cnt[0]),
                 "same_length_batches": int(cnt[1]), "fallback_batches": int(cnt[0]) - int(cnt[1]),
-                "fallback_members": int(cnt[3]), "kv_bytes": moved, "status": status,
+                "same_length_members": int(cnt[2]), "fallback_members": int(cnt[3]), "kv_bytes": moved,
+                "status": status, "window": Wn,
                 "prompt_len_range": [int(local_lens.min()), int(local_lens.max())],
-                "prompt_tokens": int(local_lens.sum()), "clocks": clocks.summary()}
+                "prompt_tokens": int(local_lens.sum()), "clocks": clocks.summary(),
+                "serial_ms": {"K2_gather_scatter": sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3])
+                                                       for fb, e in evs if fb),
+                              "K1_same_length": sum(e[1].elapsed_time(e[2]) for fb, e in evs if not fb),
+                              "K1_fallback": sum(e[1].elapsed_time(e[2]) for fb, e in evs if fb)}}
     if world > 1:
         ms = max_over_ranks(ms, device, world)
         g0 = time.perf_counter()
@@ -853,6 +871,17 @@ def run_pool(args, rank, world, device, emulate=False):
                 "note": "latency-bound launches of mean batch size "
                         f"{(int(cnt[2]) + int(cnt[3])) / max(1, int(cnt[0])):.2f}; event-timed one by one",
                 "peak_source": peak_src}
+    cb = pool_cpu_baseline(args) if (world == 1 and rank == 0) else None
+    check = None
+    if cb is not None:
+        # the oracle's plan-driven drain (the cpu_baseline's own simulation) against the
+        # counters of the timed GPU drain: the whole drain, not a sample
+        o = cb["parts"]
+        ours = {"batches": int(cnt_all[0]), "same_length_batches": int(cnt_all[1]),
+                "same_length_members": int(cnt_all[2]), "fallback_members": int(cnt_all[3]),
+                "kv_bytes": moved}
+        ref = {key: int(o[key]) for key in ours}
+        check = {"match": ours == ref, "ours": ours, "oracle": ref}
     return {
         "metric": "EXSpec pool sequences/s (Qwen3-8B shape, N=%d, B=%d, k=%d)" % (N, sp.B, k),
         "value": N / (ms / 1e3), "unit": "sequences/s", "n_gpus": world, "steps": epochs,
@@ -889,7 +918,8 @@ def run_pool(args, rank, world, device, emulate=False):
         "e2e_note": "pool: the per-batch logits come from the model's forward on the device (the "
                     "executor's forward callback); the host-buffer end-to-end path is the default "
                     "(EqSpec round) line's e2e",
-        "cpu_baseline": pool_cpu_baseline(args) if (world == 1 and rank == 0) else None,
+        "cpu_baseline": cb,
+        "oracle_drain_check": check,
     }
 
 
@@ -937,6 +967,9 @@ def run_pool_emulated(args, device):
                      "per_rank_fallback_members": [p["fallback_members"] for p in per],
                      "per_rank_same_length_batches": [p["same_length_batches"] for p in per],
                      "per_rank_prompt_len_range": [p["prompt_len_range"] for p in per],
+                     "per_rank_window": [p["window"] for p in per],
+                     "per_rank_same_length_members": [p["same_length_members"] for p in per],
+                     "per_rank_serial_ms": [p["serial_ms"] for p in per],
                      "total_kv_GB": sum(p["kv_bytes"] for p in per) / 1e9,
                      "total_batches": sum(p["batches"] for p in per),
                      "imbalance_max_over_mean": mx / (sum(p["ms"] for p in per) / G),

@@ -126,6 +126,25 @@ int specdec_verify(const void *d_logits, int dtype, int64_t B, int64_t k, int64_
                    int32_t *d_phys_old, int32_t *d_phys_new, uint32_t *d_status, void *d_ws,
                    size_t ws_bytes, specdec_stream_t stream);
 
+/* ------------------------------------------------------------------------------ a2 (init)
+ * specdec_batch_init -- Alg. 2 line 1, S <- Tokenize(P) with "batch left padding"
+ * (PAPER.md:334): the batch state an EqSpec loop starts from.
+ *
+ *   L = max_i n_i (R6: the minimal width; every row is active at admission),
+ *   pad_i = L - n_i (content right-aligned at width L),
+ *   d_active[i] = 1, d_budget[i] = max_new.
+ *
+ * d_n [B] int32 content lengths (>= 1; a row with n_i < 1 sets SPECDEC_ST_CAPACITY and
+ *   gets pad_i = L).  Outputs: d_pad [B] int32; d_L [1] int32, d_active [B] uint8 and
+ *   d_budget [B] int32 are each optional (NULL: not written).  One CTA; no host sync.
+ * The caller places the prompt tokens right-aligned in its [B][cap_tok] token buffer
+ * (specdec_rebuild_pos_mask derives masks / positions from pad each round).
+ * Errors: SPECDEC_ERR_ARG for NULL d_n / d_pad; SPECDEC_ERR_SHAPE for B < 1.
+ */
+int specdec_batch_init(const int32_t *d_n, int64_t B, int32_t *d_pad, int32_t *d_L,
+                       uint8_t *d_active, int32_t *d_budget, int32_t max_new,
+                       uint32_t *d_status, specdec_stream_t stream);
+
 /* ------------------------------------------------------------------------------ a2
  * specdec_rebuild_pos_mask -- Alg. 2 Phase 3 unpad-append-repad and
  * the padding-agnostic positions / masks of §3.1, from specdec_verify's

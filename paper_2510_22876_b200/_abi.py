@@ -38,6 +38,7 @@ _SIGS = {
     "specdec_verify": ([_P, _INT, _I64, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
                         _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P,
                         ctypes.c_size_t, _P], _INT),
+    "specdec_batch_init": ([_P, _I64, _P, _P, _P, _P, _I32, _P, _P], _INT),
     "specdec_rebuild_pos_mask": ([_P, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P,
                                   _P, _P, _P, _P, _I64, _P, _P, _I64, _P, _P], _INT),
     "specdec_realign_workspace_size": ([_INT, _I64, _I64, _I64, _I64, _I64], ctypes.c_size_t),
@@ -257,6 +258,12 @@ def specdec_verify(logits, draft, n, active, accept, bonus, emit, finished, plan
         _ptr(pad_new), _ptr(kept), _ptr(kept_draft), _ptr(anchor), anchor_cap, _ptr(phys_old),
         _ptr(phys_new), _ptr(status), _ptr(ws), ws.numel() * ws.element_size(),
         _stream(stream)), "specdec_verify")
+
+
+def specdec_batch_init(n, pad, *, L=None, active=None, budget=None, max_new=0, status=None,
+                       stream=None):
+    _check(load().specdec_batch_init(_ptr(n), n.shape[0], _ptr(pad), _ptr(L), _ptr(active), _ptr(budget),
+                                     max_new, _ptr(status), _stream(stream)), "specdec_batch_init")
 
 
 def specdec_rebuild_pos_mask(tokens_in, tokens_out, k, n_old, pad_old, draft, accept, bonus,

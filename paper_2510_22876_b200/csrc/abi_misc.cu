@@ -41,6 +41,6 @@ bool pdl_enabled() {
 
 }  // namespace specdec
 
-extern "C" int specdec_version(void) { return 120; }  // 1.20: K1 per-row completion, DYNAMIC_FORCE
+extern "C" int specdec_version(void) { return 121; }  // 1.21: specdec_batch_init
 
 extern "C" const char *specdec_last_cuda_error(void) { return specdec::g_last_error.c_str(); }

@@ -258,3 +258,39 @@ extern "C" int specdec_pool_writeback(const int32_t *d_members, int64_t B, int64
                     d_bonus, d_emit, d_finished, d_pool_len, d_pool_gen, d_pool_active,
                     d_pool_tokens, cap_tok, d_out_buf, max_new, d_status);
 }
+
+// ----------------------------------------------------------------------------- batch init
+// Alg. 2 line 1: the left-padded batch state -- L = max n (R6), pad = L - n.
+__global__ void __launch_bounds__(1024) batch_init_kernel(const int32_t *n, int64_t B, int32_t *pad,
+                                                          int32_t *L_out, uint8_t *active,
+                                                          int32_t *budget, int32_t max_new,
+                                                          uint32_t *status) {
+    pdl_wait();
+    pdl_launch_dependents();
+    __shared__ int s_max[32];
+    int m = 0;
+    for (int64_t i = threadIdx.x; i < B; i += blockDim.x) m = max(m, n[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
+    __syncthreads();
+    int L = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) L = max(L, s_max[w]);
+    for (int64_t i = threadIdx.x; i < B; i += blockDim.x) {
+        const int32_t ni = n[i];
+        if (ni < 1 && status) atomicOr(status, SPECDEC_ST_CAPACITY);
+        pad[i] = ni >= 1 ? L - ni : L;
+        if (active) active[i] = 1;
+        if (budget) budget[i] = max_new;
+    }
+    if (threadIdx.x == 0 && L_out) *L_out = L;
+}
+
+extern "C" int specdec_batch_init(const int32_t *d_n, int64_t B, int32_t *d_pad, int32_t *d_L,
+                                  uint8_t *d_active, int32_t *d_budget, int32_t max_new,
+                                  uint32_t *d_status, specdec_stream_t stream) {
+    if (!d_n || !d_pad) return SPECDEC_ERR_ARG;
+    if (B < 1) return SPECDEC_ERR_SHAPE;
+    return launch_k(batch_init_kernel, dim3(1), dim3(1024), 0, reinterpret_cast<cudaStream_t>(stream), d_n, B,
+                    d_pad, d_L, d_active, d_budget, max_new, d_status);
+}

@@ -141,14 +141,13 @@ class EqSpecBatch:
         """tokens [B, cap] left-padded at width L = max(lengths); kv [planes, B, H, cap, D]
         (logical columns; placed at the origin when anchored)."""
         lengths = torch.as_tensor(np.asarray(lengths), dtype=torch.int32)
-        L = int(lengths.max())
         self.cur = 0
         self.tok[0].copy_(torch.as_tensor(tokens))
         self.n[0].copy_(lengths)
-        self.pad[0].copy_(L - lengths)
-        self.active.fill_(1)
-        if self.budget is not None:
-            self.budget.fill_(self.max_new)
+        # Alg. 2 line 1, the batch left padding (PAPER.md:334): pad = max n - n, every row
+        # active, the budget full -- on the device
+        _abi.specdec_batch_init(self.n[0], self.pad[0], active=self.active, budget=self.budget,
+                                max_new=self.max_new or 0, status=self.status)
         self.gen.zero_()
         if self.kept_draft is not None:
             self.kept_draft.zero_()     # no draft KV yet: the drafter prefills in round 1

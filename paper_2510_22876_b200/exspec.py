@@ -115,6 +115,8 @@ class SequencePool:
             self.kv.copy_(kv)
         self.counters.zero_()
         self.verify_calls = 0
+        if getattr(self, "_ring_pos", None) is not None:
+            self._ring_pos.value = 0      # the native executor's input ring restarts too
 
     @property
     def kv_strides(self):

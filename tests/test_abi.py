@@ -34,7 +34,7 @@ def test_header_symbols_exported(lib):
 
 
 def test_version_and_workspace(lib):
-    assert _abi.version() == 120
+    assert _abi.version() == 121
     # keys [B(k+1)] u64 | counter, max n', pad | row counters [B] u32 | class weights [k+1] u64
     assert _abi.specdec_verify_workspace_size(8, 5) == 8 * 6 * 8 + 16 + 32 + 6 * 8
     assert _abi.specdec_verify_workspace_size(3, 2) == 3 * 3 * 8 + 16 + 16 + 3 * 8
@@ -141,7 +141,7 @@ int main(void) {
     subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
                     "-L", libdir, "-l:libspecdec.so", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
-    assert out == ["120", str(_abi.ERR_ARG), str(8 * 6 * 8 + 16 + 32 + 6 * 8)]
+    assert out == ["121", str(_abi.ERR_ARG), str(8 * 6 * 8 + 16 + 32 + 6 * 8)]
 
 
 def test_host_validation_drivers_and_flags(lib):

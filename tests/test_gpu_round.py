@@ -570,3 +570,27 @@ def test_repad_fuzz(cuda, i):
         ob = out_buf.cpu().numpy()
         for b in range(B):
             assert list(ob[b, gen0[b]:g[b]]) == v["E"][b], (inplace, b)
+
+
+@pytest.mark.parametrize("B", [1, 2, 8, 37, 1500])
+def test_batch_init_matches_oracle_left_padding(cuda, B):
+    """specdec_batch_init (Alg. 2 line 1) == oracle.align.build_batch's pads
+    and width on seeded ragged lengths (B up to 1500: several strides of the one CTA)."""
+    rng = np.random.default_rng(B)
+    lens = rng.integers(1, 3000, size=B).astype(np.int32)
+    _, pad_o, L_o = OA.build_batch([[5] * int(n) for n in lens], int(lens.max()) + 1)
+    n = torch.from_numpy(lens).to(cuda)
+    pad = torch.full((B,), -7, dtype=torch.int32, device=cuda)
+    L = torch.zeros(1, dtype=torch.int32, device=cuda)
+    act = torch.zeros(B, dtype=torch.uint8, device=cuda)
+    bud = torch.zeros(B, dtype=torch.int32, device=cuda)
+    st = torch.zeros(1, dtype=torch.int32, device=cuda)
+    _abi.specdec_batch_init(n, pad, L=L, active=act, budget=bud, max_new=77, status=st)
+    torch.cuda.synchronize()
+    assert np.array_equal(pad.cpu().numpy(), pad_o) and int(L.item()) == L_o
+    assert bool((act == 1).all()) and bool((bud == 77).all()) and int(st.item()) == 0
+    # a row with n < 1 is flagged (SPECDEC_ST_CAPACITY), its pad is L
+    n[0] = 0
+    _abi.specdec_batch_init(n, pad, status=st)
+    torch.cuda.synchronize()
+    assert int(st.item()) & _abi.ST_CAPACITY and int(pad[0].item()) == int(n.max().item())
