@@ -58,6 +58,8 @@ def parse(argv=None):
                          "slot-indexed consumer, no batch moves KV (SURVEY 8f f3)")
     ap.add_argument("--pool-exec", default="native", choices=["native", "python"],
                     help="pool: per-batch launch loop in C++ (specdec_pool_epoch) or Python")
+    ap.add_argument("--pool-verify-group", type=int, default=8,
+                    help="pool (native executor): same-length batches verified per launch (1 = per batch)")
     ap.add_argument("--pool-staging", type=int, default=2,
                     help="pool, native executor: staging buffers; >= 2 overlaps the fallback "
                          "gathers (copy stream) with the same-length batches, 1 = serial")
@@ -702,7 +704,7 @@ def run_pool(args, rank, world, device, emulate=False):
     Wn = min(args.pool_W or n_loc, 2048, n_loc)
     sp = SequencePool(n_loc, cap, sh.layers, sh.H, sh.D, k, W=Wn, B=min(B, Wn),
                       min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False,
-                      consumer=args.pool_consumer,
+                      consumer=args.pool_consumer, verify_group=args.pool_verify_group,
                       n_staging=args.pool_staging if args.pool_exec == "native" else 1)
     local_lens = lens[mine]
     local_order = np.arange(n_loc)            # `mine` is already in admission order
@@ -743,7 +745,8 @@ def run_pool(args, rank, world, device, emulate=False):
             ran[0], ran[1], ran[2], ran[3] = ex[0], ex[1], ex[2], ex[3]
             return int(ex[0]), int(ex[0])
         if args.pool_exec == "native" and events is None:
-            # the per-batch launch loop in C++ (csrc/pool_exec.cu)
+            # the per-batch launch loop in C++ (csrc/pool_exec.cu), which counts its launches
+            sp._launches.value = 0
             while True:
                 r_run, r_same, m_same, m_fb = sp.epoch_native(1 if args.pool_mode == "alg3" else 0)
                 if r_run == 0:
@@ -893,7 +896,10 @@ def run_pool(args, rank, world, device, emulate=False):
                                f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}, {args.pool_consumer} consumer, "
                                f"{args.pool_exec} launch loop"
                                + (f", fallback gathers overlapped ({sp.n_staging} staging buffers)"
-                                  if args.pool_exec == "native" and sp.n_staging >= 2 else ""),
+                                  if args.pool_exec == "native" and sp.n_staging >= 2 else "")
+                               + (f", up to {sp.verify_group} same-length batches per verify launch"
+                                  if args.pool_exec == "native" and args.pool_mode == "epoch" and sp.verify_group > 1
+                                  else ""),
                    "cap": cap, "pool_kv_GB_per_rank": sp.kv.numel() * 2 / 1e9,
                    "parallelism": f"pool sharded x{world}", "step": "one epoch (K4 plan + its batches)"},
         "pool": {"epochs": epochs, "batch_verifications": int(cnt_all[0]),
@@ -911,7 +917,8 @@ def run_pool(args, rank, world, device, emulate=False):
         # libspecdec launches in the timed drain: K4 per plan (the epochs + the final empty
         # plan), K1 with the fused write-back per batch, gather + scatter per fallback batch
         # (Alg. 3 device loop: K4 + gate + gather + verify + scatter per issued iteration)
-        "gpu_launches": (3 + _abi.specdec_verify_kernels(True)) * alg3_iters["n"] if alg3_iters["n"] else (epochs + 1)
+        "gpu_launches": (3 + _abi.specdec_verify_kernels(True)) * alg3_iters["n"] if alg3_iters["n"]
+        else int(sp._launches.value) if args.pool_exec == "native" else (epochs + 1)
         + (_abi.specdec_verify_kernels(True) if sp.fused else _abi.specdec_verify_kernels(False) + 1) * int(cnt[0])
         + 2 * (int(cnt[0]) if sp.dense_consumer else 0 if sp.consumer == "slot" else int(cnt[0]) - int(cnt[1])),
         "e2e": None,

@@ -324,6 +324,29 @@ int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, int64_t k, i
                         int64_t *d_out_buf, int64_t max_new, uint32_t *d_status, void *d_ws,
                         size_t ws_bytes, specdec_stream_t stream);
 
+/* specdec_pool_verify_group -- specdec_pool_verify over n_batches (1..16) batches of one
+ * epoch plan in ONE launch (reading R21: the batches of one plan have disjoint members and
+ * are planned from one window state, so verifying them together changes no result; the
+ * executor calls each batch's forward first).  Batch g: logits h_logits[g] [h_rows[g]][k+1]
+ * [row_stride] and drafts h_draft[g] [h_rows[g]][k] (device pointers held in HOST arrays),
+ * member rows d_members / d_mlen / d_mactive [h_offset[g] .. h_offset[g] + h_rows[g]) (the
+ * plan arrays, e.g. offset = plan batch index x B).  Per-row outputs d_accept, d_bonus,
+ * d_emit, d_finished are flat over the R = sum h_rows rows in group order; d_ws holds
+ * specdec_verify_workspace_size(R, k) bytes.  Everything else as specdec_pool_verify.
+ * Errors: SPECDEC_ERR_ARG for n_batches outside [1, 16] or a NULL / misaligned pointer;
+ * SPECDEC_ERR_SHAPE for h_rows[g] < 1 or the shape errors of specdec_pool_verify.
+ */
+int specdec_pool_verify_group(int32_t n_batches, const void *const *h_logits,
+                              const int64_t *const *h_draft, const int32_t *h_offset,
+                              const int32_t *h_rows, int dtype, int64_t k, int64_t V,
+                              int64_t row_stride, const int32_t *d_members, const int32_t *d_mlen,
+                              uint8_t *d_mactive, int64_t eos_id, int64_t pad_id,
+                              int32_t *d_accept, int64_t *d_bonus, int32_t *d_emit,
+                              uint8_t *d_finished, int32_t *d_pool_len, int32_t *d_pool_gen,
+                              uint8_t *d_pool_active, int64_t *d_pool_tokens, int64_t cap_tok,
+                              int64_t *d_out_buf, int64_t max_new, uint32_t *d_status, void *d_ws,
+                              size_t ws_bytes, specdec_stream_t stream);
+
 /* ------------------------------------------------------------------------------ a4 + a5
  * specdec_pool_epoch -- native EXSpec epoch executor (Alg. 3): the
  * host-side launch loop of one epoch in C++ instead of one Python call per kernel.
@@ -432,6 +455,14 @@ typedef struct specdec_pool_desc {
     /* optional >= 128-byte zeroed workspace: the fallback gathers take SPECDEC_DYNAMIC
      * work tickets from it (they run one after another on one stream); NULL = static */
     void *gather_ws;
+    /* same-length batches verified per launch (specdec_pool_verify_group, <= 16); <= 1:
+     * one specdec_pool_verify per batch.  Runs of same-length batches in the processing
+     * order are grouped; forward() is called for every batch of a group before the group's
+     * verify, so the buffers it returns must stay valid until then.  Needs `ws` of
+     * specdec_verify_workspace_size(verify_group * B, k) bytes (else no grouping) and
+     * accept / bonus / emit / finished of verify_group * B entries. */
+    int32_t verify_group;
+    int64_t *host_launches;    /* host, nullable: += the libspecdec kernels the call launched */
 } specdec_pool_desc;
 
 int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,

@@ -53,6 +53,9 @@ _SIGS = {
     "specdec_eqspec_round": ([_P, _INT, _P, _P, _P], _INT),
     "specdec_pool_alg3": ([_P, _I32, _P, _P, _P], _INT),
     "specdec_eqspec_round_host": ([_P, _P, _INT, _INT, _P, _P, _P, _P], _INT),
+    "specdec_pool_verify_group": ([_I32, _P, _P, _P, _P, _INT, _I64, _I64, _I64, _P, _P, _P, _I64, _I64,
+                                   _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, ctypes.c_size_t,
+                                   _P], _INT),
     "specdec_pool_verify": ([_P, _INT, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _P,
                              _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, ctypes.c_size_t, _P], _INT),
 }
@@ -82,6 +85,7 @@ class PoolDesc(ctypes.Structure):
         ("cur_staging", _P), ("accept_ring", _P),
         ("est_gather_GBps", ctypes.c_double), ("est_verify_us", ctypes.c_double),
         ("gather_ws", _P),
+        ("verify_group", _I32), ("host_launches", _P),
     ]
 
 
@@ -312,6 +316,29 @@ def specdec_pool_verify(logits, draft, members, mlen, mactive, accept, bonus, em
         _ptr(pool_active), _ptr(pool_tokens), 0 if pool_tokens is None else pool_tokens.shape[1],
         _ptr(out_buf), max_new, _ptr(status), _ptr(ws), ws.numel() * ws.element_size(),
         _stream(stream)), "specdec_pool_verify")
+
+
+def specdec_pool_verify_group(logits_list, draft_list, offsets, rows, members, mlen, mactive, accept, bonus,
+                              emit, finished, pool_len, pool_gen, pool_active, ws, *, V=None, eos_id=-1,
+                              pad_id=0, max_new, pool_tokens=None, out_buf=None, status=None, stream=None):
+    """specdec_pool_verify over len(logits_list) batches in one launch (include/specdec.h):
+    batch g's logits [rows[g]][k+1][V'] and drafts, its member rows at offsets[g] of the
+    plan arrays; per-row outputs flat over sum(rows)."""
+    G = len(logits_list)
+    for lg, r in zip(logits_list, rows):
+        _check_logits(lg)
+        if lg.shape[0] < r or lg.stride(1) != logits_list[0].stride(1) or lg.dtype != logits_list[0].dtype:
+            raise ValueError("grouped logits: rows, row stride and dtype must agree")
+    K1 = logits_list[0].shape[1]
+    arr = lambda ts: (ctypes.c_void_p * G)(*[t.data_ptr() for t in ts])
+    i32 = lambda xs: (ctypes.c_int32 * G)(*[int(x) for x in xs])
+    _check(load().specdec_pool_verify_group(
+        G, arr(logits_list), arr(draft_list), i32(offsets), i32(rows), DTYPE[logits_list[0].dtype], K1 - 1,
+        V or logits_list[0].shape[2], logits_list[0].stride(1), _ptr(members), _ptr(mlen), _ptr(mactive),
+        eos_id, pad_id, _ptr(accept), _ptr(bonus), _ptr(emit), _ptr(finished), _ptr(pool_len), _ptr(pool_gen),
+        _ptr(pool_active), _ptr(pool_tokens), 0 if pool_tokens is None else pool_tokens.shape[1],
+        _ptr(out_buf), max_new, _ptr(status), _ptr(ws), ws.numel() * ws.element_size(),
+        _stream(stream)), "specdec_pool_verify_group")
 
 
 def specdec_pool_group(length, active, order, W, B, min_group, window, window_size, batch_of,

@@ -76,6 +76,11 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     // gathers fallback f the main stream keeps verifying same-length batches.
     const int32_t NS = d->n_staging >= 2 ? d->n_staging : 0;
     const bool overlap = NS > 0 && run > 1;
+    // same-length batches per verify launch (specdec_pool_verify_group), if the workspace
+    // holds the grouped rows
+    int32_t G = std::min<int32_t>(std::max<int32_t>(d->verify_group, 1), 16);
+    while (G > 1 && specdec_verify_workspace_size(static_cast<int64_t>(G) * B, d->k) > d->ws_bytes) --G;
+    int64_t launches = 1;  // K4
     std::vector<int32_t> seq, fb_rank(run, -1);
     std::vector<int32_t> fbs;
     seq.reserve(run);
@@ -114,8 +119,8 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
                 if (nx < nf) g_end[nx] = std::max(g_end[nx - 1], s_end[fi]) + tv + gather_us(fbs[nx]);
                 seq.push_back(fbs[fi++]);
             } else {
-                t += tv;
-                seq.push_back(sames[si++]);
+                t += tv;  // one (grouped) verify
+                for (int32_t q = 0; q < G && si < ns; ++q) seq.push_back(sames[si++]);
             }
         }
     }
@@ -141,14 +146,40 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     if (overlap) {
         for (int32_t f = 0; f < NS && f < static_cast<int32_t>(fbs.size()); ++f) {
             if ((rc = gather(fbs[f], cs))) return rc;
+            ++launches;
             if ((e = cudaEventRecord(ev(f % NS), cs)) != cudaSuccess) return record_cuda_error(e);
         }
     }
+    const int kv1 = specdec_verify_kernels(1);
+    // a group of same-length batches: each batch's inputs (forward or ring), one launch
+    const void *g_lg[16];
+    const int64_t *g_dr[16];
+    int32_t g_off[16], g_rows[16];
+    int32_t ng = 0;
+    auto flush_group = [&]() -> int {
+        if (!ng) return SPECDEC_OK;
+        const int r = ng == 1
+            ? specdec_pool_verify(g_lg[0], d->logit_dtype, g_rows[0], d->k, d->V, d->logit_stride, g_dr[0],
+                                  d->members + g_off[0], d->mlen + g_off[0], d->mactive + g_off[0], d->eos_id,
+                                  d->pad_id, d->accept, d->bonus, d->emit, d->finished, d->len, d->gen,
+                                  d->active, d->tokens, d->cap_tok, d->out_buf, d->max_new, d->status, d->ws,
+                                  d->ws_bytes, stream)
+            : specdec_pool_verify_group(ng, g_lg, g_dr, g_off, g_rows, d->logit_dtype, d->k, d->V,
+                                        d->logit_stride, d->members, d->mlen, d->mactive, d->eos_id,
+                                        d->pad_id, d->accept, d->bonus, d->emit, d->finished, d->len,
+                                        d->gen, d->active, d->tokens, d->cap_tok, d->out_buf, d->max_new,
+                                        d->status, d->ws, d->ws_bytes, stream);
+        launches += kv1;
+        ng = 0;
+        return r;
+    };
     const int32_t ring_base = d->ring_pos ? *d->ring_pos : 0;
     int32_t ran = 0, same = 0, msame = 0, mfb = 0;
-    for (const int32_t b : seq) {
+    for (size_t qi = 0; qi < seq.size(); ++qi) {
+        const int32_t b = seq[qi];
         const bool same_len = kinds[b] != 0;
         const bool fallback = fb_rank[b] >= 0;  // moves KV through the staging
+        if (fallback && (rc = flush_group())) return rc;
         int32_t *members = d->members + static_cast<int64_t>(b) * B;
         int32_t *mlen = d->mlen + static_cast<int64_t>(b) * B;
         uint8_t *mact = d->mactive + static_cast<int64_t>(b) * B;
@@ -158,6 +189,8 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
                 if (e != cudaSuccess) return record_cuda_error(e);
             } else if ((rc = gather(b, s))) {
                 return rc;
+            } else {
+                ++launches;
             }
         }
         const void *logits;
@@ -175,11 +208,24 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         // scatter on the copy stream after later batches have reused d->accept
         const int32_t slot = fallback && overlap ? fb_rank[b] % NS : -1;
         int32_t *acc = slot >= 0 ? d->accept_ring + static_cast<int64_t>(slot) * B : d->accept;
-        rc = specdec_pool_verify(logits, d->logit_dtype, rows(b), d->k, d->V, d->logit_stride, draft, members,
-                                 mlen, mact, d->eos_id, d->pad_id, acc, d->bonus, d->emit,
-                                 d->finished, d->len, d->gen, d->active, d->tokens, d->cap_tok,
-                                 d->out_buf, d->max_new, d->status, d->ws, d->ws_bytes, stream);
-        if (rc) return rc;
+        if (!fallback) {
+            // joins the open group; launched when the group is full, at the next fallback
+            // batch, or at the end of the run of same-length batches
+            g_lg[ng] = logits;
+            g_dr[ng] = draft;
+            g_off[ng] = static_cast<int32_t>(static_cast<int64_t>(b) * B);
+            g_rows[ng] = rows(b);
+            ++ng;
+            const bool next_same = qi + 1 < seq.size() && fb_rank[seq[qi + 1]] < 0;
+            if ((ng == G || !next_same) && (rc = flush_group())) return rc;
+        } else {
+            rc = specdec_pool_verify(logits, d->logit_dtype, rows(b), d->k, d->V, d->logit_stride, draft, members,
+                                     mlen, mact, d->eos_id, d->pad_id, acc, d->bonus, d->emit,
+                                     d->finished, d->len, d->gen, d->active, d->tokens, d->cap_tok,
+                                     d->out_buf, d->max_new, d->status, d->ws, d->ws_bytes, stream);
+            if (rc) return rc;
+            launches += kv1;
+        }
         if (fallback) {
             // scatter of the a+1 new KV rows back to the pool: on `stream` (serial) or on the
             // copy stream after this verify (overlap), where stream order also keeps the
@@ -198,9 +244,11 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
                                     nullptr, members, 0, nullptr, 0, d->moved, d->status,
                                     reinterpret_cast<specdec_stream_t>(on));
             if (rc) return rc;
+            ++launches;
             const int32_t nxt = fb_rank[b] + NS;  // the gather that reuses this staging buffer
             if (overlap && nxt < static_cast<int32_t>(fbs.size())) {
                 if ((rc = gather(fbs[nxt], cs))) return rc;
+                ++launches;
                 if ((e = cudaEventRecord(ev(nxt % NS), cs)) != cudaSuccess) return record_cuda_error(e);
             }
         }
@@ -218,7 +266,9 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         if ((e = cudaEventRecord(ev(0), cs)) != cudaSuccess || (e = cudaStreamWaitEvent(s, ev(0), 0)) != cudaSuccess)
             return record_cuda_error(e);
     }
+    if ((rc = flush_group())) return rc;
     if (!forward && d->ring_pos) *d->ring_pos = ring_base + run;
+    if (d->host_launches) *d->host_launches += launches;
     if (h_ran) *h_ran = ran;
     if (h_same) *h_same = same;
     if (h_members_same) *h_members_same = msame;

@@ -31,6 +31,7 @@ constexpr int kMaxK = 31;  // k + 1 <= 32: one lane per slot in the epilogue
 constexpr int kEpiCache = 1024;  // rows whose n' the epilogue keeps in shared memory
 // default completion modes (VerifyParams::split), measured: tools/k1bench.py
 constexpr int kSplitEqSpec = 1, kSplitPool = 2;
+constexpr int kMaxGroup = 16;  // specdec_pool_verify_group: batches per launch
 
 struct VerifyParams {
     const void *logits;
@@ -62,7 +63,34 @@ struct VerifyParams {
     int32_t *ws_lmax;              // [1] split 2: max n' over the still-active rows
     unsigned int *ws_rowcnt;       // [B] split 2: CTA arrivals per batch row
     unsigned long long *ws_w;      // [k+1] split 2 + f3: kept rows per accept class
+    // grouped pool verify (specdec_pool_verify_group): the flat batch rows
+    // [g_row0[g], g_row0[g+1]) are batch g of the group -- its own logits and drafts, its
+    // member / length / active entries at g_off[g] + (row - g_row0[g]) of the plan arrays
+    int ngroup;                    // 0: one batch (flat row = member row)
+    int32_t g_row0[kMaxGroup + 1];
+    int32_t g_off[kMaxGroup];
+    const void *g_logits[kMaxGroup];
+    const int64_t *g_draft[kMaxGroup];
 };
+
+__device__ __forceinline__ int group_of(const VerifyParams &p, int64_t i) {
+    int g = 0;
+    while (g + 1 < p.ngroup && p.g_row0[g + 1] <= i) ++g;
+    return g;
+}
+// the plan-array index (members / lengths / active) of flat batch row i
+__device__ __forceinline__ int64_t src_row(const VerifyParams &p, int64_t i) {
+    if (!p.ngroup) return i;
+    const int g = group_of(p, i);
+    return p.g_off[g] + (i - p.g_row0[g]);
+}
+// logits row (i, j) = flat logits row `row` = i * (k+1) + j
+__device__ __forceinline__ const char *logits_row(const VerifyParams &p, int64_t row, int es) {
+    if (!p.ngroup) return static_cast<const char *>(p.logits) + row * p.row_stride * es;
+    const int64_t K1 = p.k + 1, i = row / K1;
+    const int g = group_of(p, i);
+    return static_cast<const char *>(p.g_logits[g]) + ((i - p.g_row0[g]) * K1 + row % K1) * p.row_stride * es;
+}
 
 __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
 #pragma unroll
@@ -81,15 +109,25 @@ struct RowPre {
     uint8_t act;
     int32_t n, bud, sq, len0, gen0;  // sq: pool sequence of the row (pool mode), else -1
     int64_t d;                       // lane t < k: draft[i][t]
+    int64_t src;                     // the row's index in the plan arrays (src_row)
 };
 
 __device__ __forceinline__ RowPre load_pre(const VerifyParams &p, int64_t i, int lane) {
     RowPre r;
-    r.act = p.active[i];
-    r.n = p.n[i];
-    r.d = lane < p.k ? p.draft[i * p.k + lane] : -1;
+    int64_t di = i;
+    const int64_t *draft = p.draft;
+    r.src = i;
+    if (p.ngroup) {
+        const int g = group_of(p, i);
+        di = i - p.g_row0[g];
+        draft = p.g_draft[g];
+        r.src = p.g_off[g] + di;
+    }
+    r.act = p.active[r.src];
+    r.n = p.n[r.src];
+    r.d = lane < p.k ? draft[di * p.k + lane] : -1;
     r.bud = p.budget ? p.budget[i] : 0;
-    r.sq = p.wb_members ? p.wb_members[i] : -1;
+    r.sq = p.wb_members ? p.wb_members[r.src] : -1;
     r.len0 = r.sq >= 0 ? p.wb_len[r.sq] : 0;
     r.gen0 = r.sq >= 0 ? p.wb_gen[r.sq] : 0;
     return r;
@@ -166,7 +204,7 @@ __device__ __forceinline__ RowOut row_epilogue(const VerifyParams &p, int64_t i,
         p.bonus[i] = b;
         p.emit[i] = m;
         p.finished[i] = fin ? 1 : 0;
-        p.active[i] = fin ? 0 : 1;  // in/out: rows still active after this round
+        p.active[r.src] = fin ? 0 : 1;  // in/out: rows still active after this round
         if (p.n_new) p.n_new[i] = nn;
         if (p.kept) p.kept[i] = kp;
         // f1: a draft model that cached its own k forwards (pending token, d_1..d_{k-1})
@@ -411,9 +449,9 @@ __global__ void __launch_bounds__(kVerifyThreads) verify_kernel_f32(VerifyParams
     const int64_t row = blockIdx.y;
     const int64_t i = row / (p.k + 1);
     if (p.split == 2 && tid < kWarp) s_pre[tid] = load_pre(p, i, tid);
-    const bool act = p.active[i] != 0;
+    const bool act = p.active[src_row(p, i)] != 0;
     {
-        const char *rowp = static_cast<const char *>(p.logits) + row * p.row_stride * 4;
+        const char *rowp = logits_row(p, row, 4);
         const int64_t v0 = static_cast<int64_t>(blockIdx.x) * p.chunk;
         const int64_t v1 = min(p.V, v0 + p.chunk);
         const int64_t vec_end = v1 / 4;
@@ -486,7 +524,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 4) verify_kernel16(VerifyParam
     {
         // the loads are issued before anything else is read (an inactive row's logits are
         // streamed too -- its CTAs just do not merge): no dependent load ahead of them
-        const char *rowp = static_cast<const char *>(p.logits) + row * p.row_stride * 2;
+        const char *rowp = logits_row(p, row, 2);
         const int64_t v0 = static_cast<int64_t>(blockIdx.x) * p.chunk;
         const int64_t v1 = min(p.V, v0 + p.chunk);
         const int64_t vec0 = v0 / 8, vec_end = v1 / 8;
@@ -500,7 +538,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 4) verify_kernel16(VerifyParam
             w[u] = u < mine ? ld_stream_v4(vp + u * kVerifyThreads)
                             : make_uint4(T::kNegInf2, T::kNegInf2, T::kNegInf2, T::kNegInf2);
         if (p.split == 2 && tid < kWarp) s_pre[tid] = load_pre(p, i, tid);
-        act = p.active[i] != 0;
+        act = p.active[src_row(p, i)] != 0;
         // pass 1: the thread's packed maximum (HMNMX2: one instruction per two logits,
         // NaN-propagating)
         uint32_t m2 = T::kNegInf2;
@@ -768,6 +806,57 @@ extern "C" int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, i
     p.wb_members = d_members; p.wb_len = d_pool_len; p.wb_gen = d_pool_gen; p.wb_active = d_pool_active;
     p.wb_tokens = d_pool_tokens; p.wb_cap_tok = cap_tok; p.wb_out_buf = d_out_buf; p.wb_max_new = max_new;
     p.status = d_status;
+    set_ws(p, d_ws);
+    return launch_verify(p, dtype, es, stream);
+}
+
+extern "C" int specdec_pool_verify_group(int32_t n_batches, const void *const *h_logits,
+                                         const int64_t *const *h_draft, const int32_t *h_offset,
+                                         const int32_t *h_rows, int dtype, int64_t k, int64_t V,
+                                         int64_t row_stride, const int32_t *d_members,
+                                         const int32_t *d_mlen, uint8_t *d_mactive, int64_t eos_id,
+                                         int64_t pad_id, int32_t *d_accept, int64_t *d_bonus,
+                                         int32_t *d_emit, uint8_t *d_finished, int32_t *d_pool_len,
+                                         int32_t *d_pool_gen, uint8_t *d_pool_active,
+                                         int64_t *d_pool_tokens, int64_t cap_tok, int64_t *d_out_buf,
+                                         int64_t max_new, uint32_t *d_status, void *d_ws,
+                                         size_t ws_bytes, specdec_stream_t stream) {
+    if (n_batches < 1 || n_batches > kMaxGroup || !h_logits || !h_draft || !h_offset || !h_rows)
+        return SPECDEC_ERR_ARG;
+    const int es = dtype_size(dtype);
+    int64_t R = 0;
+    for (int32_t g = 0; g < n_batches; ++g) {
+        if (h_rows[g] < 1 || h_offset[g] < 0) return SPECDEC_ERR_SHAPE;
+        if (!h_logits[g] || !h_draft[g] || !aligned16(h_logits[g])) return SPECDEC_ERR_ARG;
+        R += h_rows[g];
+    }
+    // the shape checks of one launch over R flat rows (logits pointer: the first batch's)
+    const int rc = check_verify(h_logits[0], es, R, k, V, row_stride, d_ws, ws_bytes);
+    if (rc) return rc;
+    if (!d_members || !d_mlen || !d_mactive || !d_accept || !d_bonus || !d_emit || !d_finished ||
+        !d_pool_len || !d_pool_gen || !d_pool_active)
+        return SPECDEC_ERR_ARG;
+    if (d_pool_tokens && cap_tok < 1) return SPECDEC_ERR_SHAPE;
+    if (max_new < 1) return SPECDEC_ERR_SHAPE;
+    VerifyParams p{};
+    p.logits = h_logits[0];
+    p.B = R; p.k = k; p.V = V; p.row_stride = row_stride;
+    p.draft = h_draft[0]; p.n = d_mlen; p.active = d_mactive;
+    p.eos_id = eos_id; p.pad_id = pad_id;
+    p.accept = d_accept; p.bonus = d_bonus; p.emit = d_emit; p.finished = d_finished;
+    p.wb_members = d_members; p.wb_len = d_pool_len; p.wb_gen = d_pool_gen; p.wb_active = d_pool_active;
+    p.wb_tokens = d_pool_tokens; p.wb_cap_tok = cap_tok; p.wb_out_buf = d_out_buf; p.wb_max_new = max_new;
+    p.status = d_status;
+    p.ngroup = n_batches;
+    int32_t r0 = 0;
+    for (int32_t g = 0; g < n_batches; ++g) {
+        p.g_row0[g] = r0;
+        p.g_off[g] = h_offset[g];
+        p.g_logits[g] = h_logits[g];
+        p.g_draft[g] = h_draft[g];
+        r0 += h_rows[g];
+    }
+    p.g_row0[n_batches] = r0;
     set_ws(p, d_ws);
     return launch_verify(p, dtype, es, stream);
 }

@@ -29,7 +29,7 @@ from .eqspec import TORCH_DT
 class SequencePool:
     def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
                  max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True,
-                 dense_consumer=False, n_staging=1, consumer=None):
+                 dense_consumer=False, n_staging=1, consumer=None, verify_group=8):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         if B > W:
@@ -82,16 +82,19 @@ class SequencePool:
         self.blen = self._hdr_dev[1 + W:1 + 2 * W]
         self.bsize = self._hdr_dev[1 + 2 * W:1 + 3 * W]
         self.counters = torch.zeros(8, dtype=i64, device=dev)
-        # per-batch verify scratch
-        self.accept = torch.zeros(B, dtype=i32, device=dev)
-        self.bonus = torch.zeros(B, dtype=i64, device=dev)
-        self.emit = torch.zeros(B, dtype=i32, device=dev)
-        self.finished = torch.zeros(B, dtype=u8, device=dev)
+        # per-batch verify scratch; the native executor verifies up to `verify_group`
+        # same-length batches per launch (specdec_pool_verify_group): rows for all of them
+        self.verify_group = max(1, min(int(verify_group), 16))
+        GB = self.verify_group * B
+        self.accept = torch.zeros(GB, dtype=i32, device=dev)
+        self.bonus = torch.zeros(GB, dtype=i64, device=dev)
+        self.emit = torch.zeros(GB, dtype=i32, device=dev)
+        self.finished = torch.zeros(GB, dtype=u8, device=dev)
         self.n_new = torch.zeros(B, dtype=i32, device=dev)
         self.pad_new = torch.zeros(B, dtype=i32, device=dev)
         self.kept = torch.zeros(B, dtype=i32, device=dev)
         self.plan_L = torch.zeros(1, dtype=i32, device=dev)
-        ws = _abi.specdec_verify_workspace_size(B, k)
+        ws = _abi.specdec_verify_workspace_size(GB, k)
         self.ws = torch.zeros((ws + 7) // 8, dtype=i64, device=dev)
         self.status = torch.zeros(1, dtype=i32, device=dev)
         self.moved = torch.zeros(1, dtype=i64, device=dev)
@@ -269,6 +272,9 @@ class SequencePool:
         # the gathers take K2 work tickets (SPECDEC_DYNAMIC) from a zeroed 128-byte header
         self._gather_ws = torch.zeros(128, dtype=torch.uint8, device=self.device)
         d.gather_ws = self._gather_ws.data_ptr()
+        d.verify_group = self.verify_group
+        self._launches = ctypes.c_int64(0)      # libspecdec kernels the executor launched
+        d.host_launches = ctypes.addressof(self._launches)
         if self.n_staging >= 2:
             ns = self.n_staging
             self._copy_stream = torch.cuda.Stream(self.device)
