@@ -407,12 +407,20 @@ def run_ours(args, rank, world, device):
     moved0 = int(bt.moved.item())
     rb.kept_rows.zero_()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    # the moved-bytes counter after every round (a device copy on the launching stream,
+    # outside the event intervals): per-launch K2 bytes for the per-launch rate spread
+    snap = torch.zeros(args.steps + 1, dtype=torch.int64, device=device)
     sync()
+    with torch.cuda.stream(rb.stream):
+        snap[0].copy_(bt.moved[0])
     for r in range(args.steps):
         rb.episode(r, args.episode)
         rb.step(r, evs[r])
+        with torch.cuda.stream(rb.stream):
+            snap[r + 1].copy_(bt.moved[0])
     sync()
     moved_B = int(bt.moved.item()) - moved0
+    per_launch = np.diff(snap.cpu().numpy())
     # algorithmic K2 bytes of region B: in place = the device counter (only shifting rows
     # move); ping-pong = the shifting rows' bytes, although every kept row is copied
     alg_B = moved_B if bt.kv_mode == "inplace" else int(rb.alg_rows.item()) * 2 * sh.bpt
@@ -423,11 +431,34 @@ def run_ours(args, rank, world, device):
     e2e = None if args.no_e2e else run_e2e(rb, args, world)
     logits_bytes = sh.B * (sh.k + 1) * sh.V * (4 if sh.logit_dtype == "fp32" else 2)
     kept_bytes = 2 * int(rb.kept_rows.item()) * sh.bpt
+    k2_each = np.array([e[2].elapsed_time(e[3]) for e in evs])
     return dict(sh=sh, ms=ms, reps_ms=reps, moved=alg_B, copied=moved_B, moved_A=moved_A, kept_bytes=kept_bytes,
+                k2_launches=(per_launch, k2_each),
                 k1_ms=k1, k3_ms=k3,
                 kernels_per_round=bt.kernels_per_round,
                 k2_ms=k2, status=status | int(bt.status.item()), clocks=clocks.summary(), e2e=e2e,
                 end_width=width_end, logits_bytes=logits_bytes)
+
+
+def k2_spread(nbytes, ms, peak):
+    """Per-launch K2 rates over the kernel-timing region: how the launch-level rate depends on
+    the bytes a launch moves (small launches: the fixed launch / first-load / last-store cost
+    weighs more), and the time share of launches that move nothing."""
+    nbytes, ms = np.asarray(nbytes, np.float64), np.asarray(ms, np.float64)
+    mv = nbytes > 0
+    if not mv.any():
+        return None
+    rate = nbytes[mv] / (ms[mv] / 1e3) / 1e9
+    q = lambda x: [float(v) for v in np.percentile(x, [0, 25, 50, 75, 100])]
+    # least squares t = t0 + bytes / R over the moving launches: t0 = fixed cost per launch,
+    # R = the streaming rate once the stream is full
+    A = np.stack([np.ones(mv.sum()), nbytes[mv]], 1)
+    (t0, inv), *_ = np.linalg.lstsq(A, ms[mv] / 1e3, rcond=None)
+    return {"launches": int(len(ms)), "zero_byte_launches": int((~mv).sum()),
+            "zero_byte_time_share": float(ms[~mv].sum() / ms.sum()) if ms.sum() else 0.0,
+            "MB_quartiles": [x / 1e6 for x in q(nbytes[mv])], "GBps_quartiles": q(rate),
+            "fit_fixed_us": float(t0 * 1e6), "fit_stream_GBps": float(1 / inv / 1e9) if inv > 0 else None,
+            "fit_stream_frac": float(1 / inv / 1e9 / peak) if inv > 0 else None}
 
 
 def round_bandwidth(res, sh, args, peak):
@@ -1110,6 +1141,7 @@ def main():
                                               f"per-round graphs)" if args.round_mode == "graph-block" else
                                               " (graph: one CUDA graph per (parity, ring slot), 3 kernels per replay)"),
             "bytes_moved_check": {"value_region": res["moved_A"], "kernel_region": res["copied"]},
+            "k2_per_launch": k2_spread(*res["k2_launches"], peak),
             # share of the kept KV bytes that K2 had to move (rows with a shift; f3 moves the
             # physical origin to shrink it), over the kernel-timing region's rounds
             "moved_share": {"value": res["moved"] / res["kept_bytes"] if res["kept_bytes"] else 0.0,
