@@ -1100,7 +1100,8 @@ def main():
         bytes_per_launch = res["moved"] / args.steps
         # (B=1 moves no KV: K2 is not launched and the roofline line reports 0 bytes)
         achieved = bytes_per_launch / (k2_launch_ms / 1e3) / 1e9 if k2_launch_ms > 1e-6 else 0.0
-        traffic, traffic_note = ncu_traffic(f"{sh.name}_B{sh.B}" + ("_pingpong" if args.kv_mode == "pingpong" else ""))
+        traffic, traffic_note = ncu_traffic(f"{sh.name}_B{sh.B}" + (f"_ctx{args.ctx}" if args.ctx else "")
+                                            + ("_pingpong" if args.kv_mode == "pingpong" else ""))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = round_cpu_baseline(sh, args, rounds=2)
