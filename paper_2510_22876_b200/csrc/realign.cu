@@ -658,7 +658,7 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     static int cfg = -1, pol = 0;
     if (cfg < 0) {
         const char *e = getenv("SPECDEC_REALIGN_CFG");
-        cfg = e ? atoi(e) : 0;
+        cfg = e ? atoi(e) : 3;  // 3 = automatic (below)
         const char *q = getenv("SPECDEC_REALIGN_POLICY");
         pol = q ? atoi(q) : 0;
         const char *c = getenv("SPECDEC_REALIGN_CTAS");
@@ -679,9 +679,13 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     const int64_t units_launch = count_bound > 0
         ? std::min(units, max_units_bound(n_planes, n_rows, H, rb, std::min<int64_t>(cap_src, count_bound)))
         : units;
-    switch (cfg) {
+    // ring shape: 6 x 32 KB in flight per SM from 4 batch rows up (Qwen3 B=8 0.975 -> 0.988
+    // of the copy peak, Vicuna 1.000 -> 1.013, ctx 512 0.802 -> 0.839), 3 x 32 KB below
+    // (B=2: 0.856 vs 0.838) -- profiles/r02/k2_small_moves.txt
+    const int shape = cfg == 3 ? (n_rows >= 4 ? 2 : 0) : cfg;
+    switch (shape) {
         case 1: return launch_realign<4, 16384>(p, units_launch, s);
         case 2: return launch_realign<6, 32768>(p, units_launch, s);
-        default: return launch_realign<3, 32768>(p, units_launch, s);  // measured best
+        default: return launch_realign<3, 32768>(p, units_launch, s);
     }
 }
