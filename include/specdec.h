@@ -282,6 +282,28 @@ int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active, const int3
                        int32_t *d_blen, int32_t *d_n_batches, int64_t *d_counters,
                        specdec_stream_t stream);
 
+/* specdec_pool_getbatch -- Alg. 3's GetBatch(Window, B) as printed (ONE batch
+ * per iteration): batch 0 of the specdec_pool_group plan, without planning the others.
+ * Batch 0 is the first batch of the heaviest length group -- the largest count, ties to
+ * the smaller length -- when that count reaches min_group (>= 1 when B == 1): its first
+ * min(B, count) members in window order; otherwise the first min(B, |window|) members of
+ * the window.  Same arguments as specdec_pool_group; outputs: d_window, d_window_size;
+ * batch 0's row of d_members / d_mlen / d_mpad / d_mactive (B entries); d_bsize[0],
+ * d_bkind[0], d_blen[0]; d_n_batches = 1 (0 for an empty window); d_batch_of / d_slot_of
+ * = 0 / slot for batch 0's members, -1 for every other sequence; d_counters += the
+ * counters of that one batch (window size and distinct lengths as specdec_pool_group).
+ * Other batch rows are not written.  A window whose lengths span more than 8192 values
+ * is planned in full (then batches >= 1 are written too).  specdec_pool_alg3 plans with
+ * this call.
+ */
+int specdec_pool_getbatch(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order,
+                          int32_t N, int32_t W, int32_t B, int32_t min_group, int32_t *d_window,
+                          int32_t *d_window_size, int32_t *d_batch_of, int32_t *d_slot_of,
+                          int32_t *d_members, int32_t *d_mlen, int32_t *d_mpad,
+                          uint8_t *d_mactive, int32_t *d_bsize, uint8_t *d_bkind,
+                          int32_t *d_blen, int32_t *d_n_batches, int64_t *d_counters,
+                          specdec_stream_t stream);
+
 /* ------------------------------------------------------------------------------ a5
  * specdec_pool_writeback -- Alg. 3 Phase 4: the pool-mode half of
  * the repad step.  For every batch slot r with d_members[r] = s >= 0:
@@ -572,7 +594,8 @@ int specdec_eqspec_round_host(const specdec_round_desc *d, const specdec_host_io
                               specdec_stream_t stream);
 
 /* specdec_pool_alg3 -- `iterations` iterations of Alg. 3 as printed:
- * specdec_pool_group over the window, then batch 0 of the plan only (gather if it is a
+ * specdec_pool_getbatch over the window (batch 0 of the plan only; d->counters accumulate
+ * that batch's counters), then that batch (gather if it is a
  * fallback batch, specdec_pool_verify with the write-back, scatter), then re-plan -- all
  * enqueued on `stream` with NO host synchronisation: the plan kernel's tail writes batch
  * 0 as gated member rows for the gather / verify / scatter (-1 or inactive for the parts

@@ -303,10 +303,11 @@ extern "C" int specdec_pool_alg3(const specdec_pool_desc *d, int32_t iterations,
     gate.exec = d_exec_counters;
     gate.dense = d->dense_consumer;
     for (int32_t it = 0; it < iterations; ++it) {
+        // Alg. 3's GetBatch: batch 0 of the window plan only (specdec_pool_getbatch)
         int rc = pool_group_launch(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
                                    d->window_size, d->batch_of, d->slot_of, d->members, d->mlen, d->mpad,
                                    d->mactive, d->bsize, d->bkind, d->blen, d->n_batches, d->counters, gate,
-                                   stream);
+                                   stream, true);
         if (rc) return rc;
         // fallback batch 0: pool slots [0, len-1) -> staging, right-aligned (rows -1: skipped)
         rc = specdec_realign_kv(d->kv, d->staging, d->kv_dtype, d->n_planes, B, d->H, d->D, p_plane, p_row,

@@ -25,6 +25,6 @@ int pool_group_launch(const int32_t *d_len, const uint8_t *d_active, const int32
                       int32_t *d_batch_of, int32_t *d_slot_of, int32_t *d_members, int32_t *d_mlen,
                       int32_t *d_mpad, uint8_t *d_mactive, int32_t *d_bsize, uint8_t *d_bkind,
                       int32_t *d_blen, int32_t *d_n_batches, int64_t *d_counters, const Alg3Gate &gate,
-                      specdec_stream_t stream);
+                      specdec_stream_t stream, bool one_batch = false);
 
 }  // namespace specdec

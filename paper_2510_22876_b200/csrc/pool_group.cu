@@ -61,12 +61,19 @@ struct PoolSmem {
     int gstart[kPoolMaxW + 1];  // group -> first position in the sorted member order
     int nsb[kPoolMaxW];     // group -> number of same-length batches
     int matched[kPoolMaxW]; // group -> members placed in same-length batches
-    int gbase[kPoolMaxW];   // group -> first batch index
-    int bmax[kPoolMaxW];    // per batch: max length
-    int bmin[kPoolMaxW];    // per batch: min length
-    int bcnt[kPoolMaxW];    // per batch: member count
+    union {
+        struct {
+            int gbase[kPoolMaxW];   // group -> first batch index
+            int bmax[kPoolMaxW];    // per batch: max length
+            int bmin[kPoolMaxW];    // per batch: min length
+            int bcnt[kPoolMaxW];    // per batch: member count
+        };
+        int hist[4 * kPoolMaxW];    // GetBatch (batch 0 only): window length histogram
+    };
     int warp[32];
+    int red[4];
 };
+constexpr int kHistBins = 4 * kPoolMaxW;  // length range the one-batch GetBatch histograms directly
 
 // Ascending bitonic sort of key[0, n) (n a power of two <= 2 * blockDim.x, padded with ~0).
 // Keys are unique (or equal padding), so the result is unique whatever the thread
@@ -210,24 +217,11 @@ __device__ void block_bitonic_sort(uint32_t *key, int n) {
     }
 }
 
-__global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
-    const int32_t *len, const uint8_t *active, const int32_t *order, int32_t N, int32_t W,
-    int32_t B, int32_t min_group, int32_t *window, int32_t *window_size, int32_t *batch_of,
-    int32_t *slot_of, int32_t *members, int32_t *mlen, int32_t *mpad, uint8_t *mactive,
-    int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters, Alg3Gate gate,
-    int exp) {
-    pdl_wait();
-    pdl_launch_dependents();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    PoolSmem &sm = *reinterpret_cast<PoolSmem *>(smem_raw);
-    const int tid = threadIdx.x;
-    const int T = blockDim.x;
-
-    for (int s = tid; s < N; s += T) {
-        batch_of[s] = -1;
-        slot_of[s] = -1;
-    }
-    // ---- 1. RefillWindow: first W active ids in admission order
+// ---- RefillWindow: the first W active ids in admission order, into
+// sm.wid / sm.wlen; returns the window size.
+__device__ int refill_window(PoolSmem &sm, const int32_t *len, const uint8_t *active, const int32_t *order,
+                             int32_t N, int32_t W) {
+    const int tid = threadIdx.x, T = blockDim.x;
     int filled = 0;
     for (int base = 0; base < N && filled < W; base += T) {
         const int t = base + tid;
@@ -244,8 +238,17 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
         }
         filled += tot;
     }
-    const int Wn = min(filled, W);
     __syncthreads();
+    return min(filled, W);
+}
+
+// The whole-window plan (steps 2-4 above) after RefillWindow, plus the Alg. 3 gate.
+__device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, int32_t *window,
+                          int32_t *window_size, int32_t *batch_of, int32_t *slot_of, int32_t *members,
+                          int32_t *mlen, int32_t *mpad, uint8_t *mactive, int32_t *bsize, uint8_t *bkind,
+                          int32_t *blen, int32_t *n_batches, int64_t *counters, const Alg3Gate &gate, int exp) {
+    const int tid = threadIdx.x;
+    const int T = blockDim.x;
     if (exp == 1) return;  // timing probe only (SPECDEC_K4_EXP): up to RefillWindow
     // ---- 2. length histogram: sort (length, window position), groups = equal-length runs.
     // Keys are 32-bit, (length << 11) | position, when every window length is in [0, 2^20)
@@ -449,6 +452,185 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     }
 }
 
+__global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
+    const int32_t *len, const uint8_t *active, const int32_t *order, int32_t N, int32_t W,
+    int32_t B, int32_t min_group, int32_t *window, int32_t *window_size, int32_t *batch_of,
+    int32_t *slot_of, int32_t *members, int32_t *mlen, int32_t *mpad, uint8_t *mactive,
+    int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters, Alg3Gate gate,
+    int exp) {
+    pdl_wait();
+    pdl_launch_dependents();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PoolSmem &sm = *reinterpret_cast<PoolSmem *>(smem_raw);
+    for (int s = threadIdx.x; s < N; s += blockDim.x) {
+        batch_of[s] = -1;
+        slot_of[s] = -1;
+    }
+    const int Wn = refill_window(sm, len, active, order, N, W);
+    plan_full(sm, Wn, B, min_group, window, window_size, batch_of, slot_of, members, mlen, mpad, mactive, bsize,
+              bkind, blen, n_batches, counters, gate, exp);
+}
+
+// ---- Alg. 3's GetBatch as printed (one batch per iteration): batch 0 of the
+// window plan above, without planning the rest.  Batch 0 is the first batch of the
+// heaviest length group -- largest count, ties to the smaller length -- if its count
+// reaches min_group (R11), i.e. min(B, count) of its members in window order; else no
+// group qualifies and batch 0 is the first min(B, |window|) members of the window.  A
+// length histogram (shared-memory atomics; counts are order-independent) and one block
+// maximum find the group, one block scan in window order picks its members: no sort.
+// Windows whose lengths span more than kHistBins values take the full plan instead.
+__device__ __forceinline__ int block_reduce_max(int v, int *s_warp) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = __reduce_max_sync(0xFFFFFFFFu, v);
+    __syncthreads();
+    if (lane == 0) s_warp[wid] = v;
+    __syncthreads();
+    int m = s_warp[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = max(m, s_warp[w]);
+    return m;
+}
+__device__ __forceinline__ int block_reduce_sum(int v, int *s_warp) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = __reduce_add_sync(0xFFFFFFFFu, v);
+    __syncthreads();
+    if (lane == 0) s_warp[wid] = v;
+    __syncthreads();
+    int m = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m += s_warp[w];
+    return m;
+}
+
+__global__ void __launch_bounds__(kPoolThreads) pool_getbatch_kernel(
+    const int32_t *len, const uint8_t *active, const int32_t *order, int32_t N, int32_t W,
+    int32_t B, int32_t min_group, int32_t *window, int32_t *window_size, int32_t *batch_of,
+    int32_t *slot_of, int32_t *members, int32_t *mlen, int32_t *mpad, uint8_t *mactive,
+    int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters, Alg3Gate gate) {
+    pdl_wait();
+    pdl_launch_dependents();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PoolSmem &sm = *reinterpret_cast<PoolSmem *>(smem_raw);
+    const int tid = threadIdx.x, T = blockDim.x;
+    for (int s = tid; s < N; s += T) {
+        batch_of[s] = -1;
+        slot_of[s] = -1;
+    }
+    const int Wn = refill_window(sm, len, active, order, N, W);
+    // the window's length range (lengths are >= 1)
+    int lo = 0x7FFFFFFF, hi = 0;
+    for (int w = tid; w < Wn; w += T) {
+        lo = min(lo, sm.wlen[w]);
+        hi = max(hi, sm.wlen[w]);
+    }
+    const int Lmax = block_reduce_max(hi, sm.warp);
+    const int Lmin = -block_reduce_max(-lo, sm.warp);
+    if (Wn > 0 && (Lmin < 0 || static_cast<int64_t>(Lmax) - Lmin >= kHistBins)) {
+        plan_full(sm, Wn, B, min_group, window, window_size, batch_of, slot_of, members, mlen, mpad, mactive,
+                  bsize, bkind, blen, n_batches, counters, gate, 0);
+        return;
+    }
+    const int R = Wn > 0 ? Lmax - Lmin + 1 : 0;
+    for (int b = tid; b < R; b += T) sm.hist[b] = 0;
+    __syncthreads();
+    for (int w = tid; w < Wn; w += T) atomicAdd(&sm.hist[sm.wlen[w] - Lmin], 1);
+    __syncthreads();
+    // the heaviest group: (count, then the smaller length) as one packed maximum over the
+    // groups that reach min_group (>= 1 when B == 1)
+    const int mg = B == 1 ? 1 : min_group;
+    int best = 0, distinct = 0;
+    for (int b = tid; b < R; b += T) {
+        const int c = sm.hist[b];
+        distinct += c > 0;
+        if (c >= mg) best = max(best, (c << 13) | (kHistBins - 1 - b));  // c <= 2048: 25 bits
+    }
+    best = block_reduce_max(best, sm.warp);
+    distinct = block_reduce_sum(distinct, sm.warp);
+    const bool grouped = best > 0;
+    const int Lsel = grouped ? Lmin + (kHistBins - 1 - (best & (kHistBins - 1))) : 0;
+    const int take = grouped ? min(B, best >> 13) : min(B, Wn);
+    // batch 0's members in window order: the first `take` of the chosen length (or of the
+    // window); the scan stops once they are found
+    for (int x = tid; x < B; x += T) {
+        members[x] = -1;
+        mlen[x] = 0;
+        mpad[x] = 0;
+        mactive[x] = 0;
+    }
+    __syncthreads();
+    int found = 0;
+    for (int base = 0; base < Wn && found < take; base += T) {
+        const int w = base + tid;
+        const int f = (w < Wn && (!grouped || sm.wlen[w] == Lsel)) ? 1 : 0;
+        int tot;
+        const int r = found + block_exclusive_scan(f, sm.warp, tot);
+        if (f && r < take) {
+            sm.rank[r] = w;  // slot r <- window position w
+        }
+        found += tot;
+    }
+    __syncthreads();
+    // batch 0: width, kind (every member the same length), outputs
+    int bmx = 0, bmn = 0x7FFFFFFF;
+    for (int r = tid; r < take; r += T) {
+        const int l = sm.wlen[sm.rank[r]];
+        bmx = max(bmx, l);
+        bmn = min(bmn, l);
+    }
+    bmx = block_reduce_max(bmx, sm.warp);
+    bmn = -block_reduce_max(-bmn, sm.warp);
+    const bool same = take > 0 && bmx == bmn;
+    long long tok = 0;
+    for (int r = tid; r < take; r += T) {
+        const int w = sm.rank[r], s = sm.wid[w], l = sm.wlen[w];
+        members[r] = s;
+        mlen[r] = l;
+        mpad[r] = bmx - l;
+        mactive[r] = 1;
+        batch_of[s] = 0;
+        slot_of[s] = r;
+        tok += l;
+    }
+    for (int w = tid; w < Wn; w += T) window[w] = sm.wid[w];
+    if (tok && !same) atomicAdd(reinterpret_cast<unsigned long long *>(counters + 4), static_cast<unsigned long long>(tok));
+    if (tid == 0) {
+        *window_size = Wn;
+        *n_batches = take > 0 ? 1 : 0;
+        bsize[0] = take;
+        bkind[0] = static_cast<uint8_t>(same);
+        blen[0] = take > 0 ? bmx : 0;
+        // counters (accumulated) of the batch planned: batches, same-length batches, their
+        // members, fallback members, fallback tokens (above), window size, distinct lengths
+        if (take > 0) {
+            atomicAdd(reinterpret_cast<unsigned long long *>(counters + 0), 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long *>(counters + (same ? 1 : 3)),
+                      same ? 1ull : static_cast<unsigned long long>(take));
+            if (same) atomicAdd(reinterpret_cast<unsigned long long *>(counters + 2), static_cast<unsigned long long>(take));
+        }
+        atomicAdd(reinterpret_cast<unsigned long long *>(counters + 5), static_cast<unsigned long long>(Wn));
+        atomicAdd(reinterpret_cast<unsigned long long *>(counters + 6), static_cast<unsigned long long>(distinct));
+    }
+    if (gate.members) {
+        __syncthreads();  // batch 0's member / mactive stores visible to every thread
+        const bool valid = take > 0;
+        const bool moves = valid && gate.dense != 2 && (!same || gate.dense == 1);
+        for (int j = tid; j < B; j += T) {
+            const int32_t m = valid ? members[j] : -1;
+            gate.members[j] = m;
+            gate.active[j] = valid ? mactive[j] : 0;
+            gate.kv[j] = moves ? m : -1;
+            gate.scol[j] = (valid ? bmx : 0) - 1;
+        }
+        if (tid == 0 && gate.exec && valid) {
+            atomicAdd(gate.exec, 1ull);
+            if (same) {
+                atomicAdd(gate.exec + 1, 1ull);
+                atomicAdd(gate.exec + 2, static_cast<unsigned long long>(take));
+            } else {
+                atomicAdd(gate.exec + 3, static_cast<unsigned long long>(take));
+            }
+        }
+    }
+}
+
 }  // namespace specdec
 
 using namespace specdec;
@@ -466,12 +648,26 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
                              d_n_batches, d_counters, Alg3Gate{}, stream);
 }
 
+extern "C" int specdec_pool_getbatch(const int32_t *d_len, const uint8_t *d_active,
+                                     const int32_t *d_order, int32_t N, int32_t W, int32_t B,
+                                     int32_t min_group, int32_t *d_window, int32_t *d_window_size,
+                                     int32_t *d_batch_of, int32_t *d_slot_of, int32_t *d_members,
+                                     int32_t *d_mlen, int32_t *d_mpad, uint8_t *d_mactive,
+                                     int32_t *d_bsize, uint8_t *d_bkind, int32_t *d_blen,
+                                     int32_t *d_n_batches, int64_t *d_counters,
+                                     specdec_stream_t stream) {
+    return pool_group_launch(d_len, d_active, d_order, N, W, B, min_group, d_window, d_window_size, d_batch_of,
+                             d_slot_of, d_members, d_mlen, d_mpad, d_mactive, d_bsize, d_bkind, d_blen,
+                             d_n_batches, d_counters, Alg3Gate{}, stream, true);
+}
+
 int specdec::pool_group_launch(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order, int32_t N,
                                int32_t W, int32_t B, int32_t min_group, int32_t *d_window,
                                int32_t *d_window_size, int32_t *d_batch_of, int32_t *d_slot_of,
                                int32_t *d_members, int32_t *d_mlen, int32_t *d_mpad, uint8_t *d_mactive,
                                int32_t *d_bsize, uint8_t *d_bkind, int32_t *d_blen, int32_t *d_n_batches,
-                               int64_t *d_counters, const Alg3Gate &gate, specdec_stream_t stream) {
+                               int64_t *d_counters, const Alg3Gate &gate, specdec_stream_t stream,
+                               bool one_batch) {
     if (N < 1 || W < 1 || W > kPoolMaxW || B < 1 || B > W) return SPECDEC_ERR_SHAPE;
     if (min_group < 1) return SPECDEC_ERR_ARG;
     if (!d_len || !d_active || !d_order || !d_window || !d_window_size || !d_batch_of ||
@@ -484,6 +680,8 @@ int specdec::pool_group_launch(const int32_t *d_len, const uint8_t *d_active, co
     const int smem = static_cast<int>(sizeof(PoolSmem));
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(pool_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(pool_getbatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return record_cuda_error(e);
         attr_done = true;
     }
@@ -492,6 +690,11 @@ int specdec::pool_group_launch(const int32_t *d_len, const uint8_t *d_active, co
     int w2 = 1;
     while (w2 < W) w2 <<= 1;
     const int threads = std::min(kPoolThreads, std::max(64, w2 / 2));
+    if (one_batch)
+        return launch_k(pool_getbatch_kernel, dim3(1), dim3(threads), smem, reinterpret_cast<cudaStream_t>(stream),
+                        d_len, d_active, d_order, N, W, B, min_group, d_window, d_window_size, d_batch_of,
+                        d_slot_of, d_members, d_mlen, d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches,
+                        d_counters, gate);
     return launch_k(pool_group_kernel, dim3(1), dim3(threads), smem,
                     reinterpret_cast<cudaStream_t>(stream), d_len, d_active, d_order, N, W, B,
                     min_group, d_window, d_window_size, d_batch_of, d_slot_of, d_members, d_mlen,

@@ -124,3 +124,20 @@ def test_pool_group_brute_force(cuda):
                     _check_plan(g, OP.form_batches(lens, [1] * Wn, order, Wn, B, mg), lens, B)
                     cnt += 1
     assert cnt > 10_000
+
+
+def test_pool_getbatch_brute_force(cuda):
+    """Alg. 3's one-batch GetBatch on every window of W <= 6 sequences with lengths in
+    {1, 2, 3}, every B <= W and every min_group in 1..B+1: batch 0 == the oracle plan's."""
+    from tests.test_gpu_pool import _check_getbatch, _getbatch_gpu
+    cnt = 0
+    for Wn in range(1, 7):
+        for lens in itertools.product((1, 2, 3), repeat=Wn):
+            lens = list(lens)
+            order = list(range(Wn))
+            for B in range(1, Wn + 1):
+                for mg in range(1, B + 2):
+                    g = _getbatch_gpu(cuda, lens, [1] * Wn, order, Wn, B, mg)
+                    _check_getbatch(g, OP.form_batches(lens, [1] * Wn, order, Wn, B, mg), lens, B)
+                    cnt += 1
+    assert cnt > 10_000

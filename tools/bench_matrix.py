@@ -92,15 +92,16 @@ def main():
     # cell K4: the plan alone (tools/k4bench.py: 50 plans per CUDA graph, best of 5), W in
     # {32, 128, 1024} (+2048); its plans are checked bit-exact against the oracle by
     # tests/test_gpu_pool.py (random pools, the W=2048 window, the fuzz)
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "k4bench.py")], capture_output=True, text=True,
-                       timeout=600)
-    for ln in r.stdout.strip().splitlines():
-        if ln.startswith("{"):
-            d = json.loads(ln)
-            if out:
-                out.write(json.dumps({"cell": f"K4 W{d['W']} mg{d['min_group']}", **d}) + "\n")
-            print(f"{'K4 W%d min_group %d' % (d['W'], d['min_group']):26s} {d['us_per_plan']:8.2f} us per plan  "
-                  f"batches {d['n_batches']:4d}  (N={d['N']}, B={d['B']})", flush=True)
+    for extra, tag in (([], "K4"), (["--getbatch"], "K4 getbatch")):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "k4bench.py")] + extra, capture_output=True,
+                           text=True, timeout=600)
+        for ln in r.stdout.strip().splitlines():
+            if ln.startswith("{"):
+                d = json.loads(ln)
+                if out:
+                    out.write(json.dumps({"cell": f"{tag} W{d['W']} mg{d['min_group']}", **d}) + "\n")
+                print(f"{tag + ' W%d min_group %d' % (d['W'], d['min_group']):26s} {d['us_per_plan']:8.2f} us per "
+                      f"plan  batches {d['n_batches']:4d}  (N={d['N']}, B={d['B']})", flush=True)
     for lbl, args in cells:
         r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--reps", str(a.reps)] + args,
                            capture_output=True, text=True, timeout=1800)

@@ -1,4 +1,4 @@
-"""K4 (specdec_pool_group) latency: N back-to-back plans captured in one CUDA graph, µs per
+"""K4 (specdec_pool_group, or with --getbatch specdec_pool_getbatch) latency: N back-to-back plans captured in one CUDA graph, µs per
 plan from CUDA events, for pools of random lengths U[64, 512] (SURVEY §8d cell K4).
 
     python tools/k4bench.py [--N 1024] [--B 8] [--n 50]
@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--N", type=int, default=1024)
     ap.add_argument("--B", type=int, default=8)
     ap.add_argument("--n", type=int, default=50)
+    ap.add_argument("--getbatch", action="store_true",
+                    help="time specdec_pool_getbatch (Alg. 3's one-batch GetBatch) instead of the full plan")
     a = ap.parse_args()
     dev = torch.device("cuda")
     rng = np.random.default_rng(0)
@@ -37,8 +39,10 @@ def main():
             lens = rng.integers(64, 513, a.N)
             sp.load(lens, order=np.argsort(lens, kind="stable"))
 
+            fn = _abi.specdec_pool_getbatch if a.getbatch else _abi.specdec_pool_group
+
             def plan(stream=None):
-                _abi.specdec_pool_group(sp.len, sp.active, sp.order, sp.W, sp.B, sp.min_group,
+                fn(sp.len, sp.active, sp.order, sp.W, sp.B, sp.min_group,
                                         sp.window, sp.window_size, sp.batch_of, sp.slot_of,
                                         sp.members, sp.mlen, sp.mpad, sp.mactive, sp.bsize,
                                         sp.bkind, sp.blen, sp.n_batches, sp.counters, stream=stream)
@@ -61,7 +65,8 @@ def main():
                 e1.record()
                 torch.cuda.synchronize()
                 best = min(best, e0.elapsed_time(e1) / a.n * 1e3)
-            out.append({"N": a.N, "W": Wn, "B": a.B, "min_group": mg, "us_per_plan": round(best, 2),
+            out.append({"N": a.N, "W": Wn, "B": a.B, "min_group": mg, "getbatch": a.getbatch,
+                        "us_per_plan": round(best, 2),
                         "n_batches": int(sp.n_batches.item())})
     for o in out:
         print(json.dumps(o))
