@@ -58,6 +58,9 @@ def parse(argv=None):
                          "slot-indexed consumer, no batch moves KV (SURVEY 8f f3)")
     ap.add_argument("--pool-exec", default="native", choices=["native", "python"],
                     help="pool: per-batch launch loop in C++ (specdec_pool_epoch) or Python")
+    ap.add_argument("--alg3-graph", type=int, default=1,
+                    help="pool --pool-mode alg3: replay the device loop from a CUDA graph of 16 iterations (0: direct, "
+                         "2: the KV moves in conditional graph nodes)")
     ap.add_argument("--pool-verify-group", type=int, default=8,
                     help="pool (native executor): same-length batches verified per launch (1 = per batch)")
     ap.add_argument("--pool-staging", type=int, default=2,
@@ -355,8 +358,13 @@ def run_ours(args, rank, world, device):
     # replay call each.  Same kernels, same order, same bytes as the per-round graphs.
     block = None
     blk = args.episode
+    tails = {}
     if args.round_mode == "graph-block" and blk and blk % RING == 0 and blk % 2 == 0:
         block = rb.capture_block(blk)
+        # the rounds after the last whole episode (e.g. a 20-step run) replay a block graph
+        # of their own: the episode's reset + those rounds (captured here, outside timing)
+        for m in {args.steps % blk, args.warmup % blk} - {0}:
+            tails[m] = rb.capture_block(m)
 
     def one_round(r):
         if use_graph:
@@ -372,6 +380,10 @@ def run_ours(args, rank, world, device):
                 block.replay()           # reset + blk rounds; bt.cur is back where it started
                 bt._last = 1 - bt.cur
                 r += blk
+            if n - r in tails:           # reset + the remaining rounds (parities 0, 1, ...)
+                tails[n - r].replay()
+                bt.cur, bt._last = (n - r) % 2, (n - r - 1) % 2
+                r = n
         for q in range(r, n):
             rb.episode(q, args.episode)
             one_round(q)
@@ -769,8 +781,14 @@ def run_pool(args, rank, world, device, emulate=False):
             # at the end of the last chunk are no-ops
             sp.alg3_exec.zero_() if getattr(sp, "alg3_exec", None) is not None else None
             alg3_iters["n"] = 0
+            if args.alg3_graph and getattr(sp, "_alg3_gexec", None) is None:
+                sp.alg3_native(RING)     # the first drain: direct launches set the kernels' attributes
+                alg3_iters["n"] += RING
             while sp.has_active():
-                sp.alg3_native(ALG3_CHUNK)
+                if args.alg3_graph:      # a CUDA graph of RING iterations, replayed
+                    sp.alg3_graph(ALG3_CHUNK // RING, conditional=args.alg3_graph == 2)
+                else:
+                    sp.alg3_native(ALG3_CHUNK)
                 alg3_iters["n"] += ALG3_CHUNK
             ex = sp.alg3_exec.cpu().numpy()
             ran[0], ran[1], ran[2], ran[3] = ex[0], ex[1], ex[2], ex[3]
@@ -930,6 +948,10 @@ def run_pool(args, rank, world, device, emulate=False):
                                   if args.pool_exec == "native" and sp.n_staging >= 2 else "")
                                + (f", up to {sp.verify_group} same-length batches per verify launch"
                                   if args.pool_exec == "native" and args.pool_mode == "epoch" and sp.verify_group > 1
+                                  else "")
+                               + (", Alg. 3 device loop replayed from a CUDA graph of 16 iterations"
+                                  + (" with the KV moves in conditional nodes" if args.alg3_graph == 2 else "")
+                                  if args.pool_exec == "native" and args.pool_mode == "alg3" and args.alg3_graph
                                   else ""),
                    "cap": cap, "pool_kv_GB_per_rank": sp.kv.numel() * 2 / 1e9,
                    "parallelism": f"pool sharded x{world}", "step": "one epoch (K4 plan + its batches)"},
@@ -948,7 +970,7 @@ def run_pool(args, rank, world, device, emulate=False):
         # libspecdec launches in the timed drain: K4 per plan (the epochs + the final empty
         # plan), K1 with the fused write-back per batch, gather + scatter per fallback batch
         # (Alg. 3 device loop: K4 + gate + gather + verify + scatter per issued iteration)
-        "gpu_launches": (3 + _abi.specdec_verify_kernels(True)) * alg3_iters["n"] if alg3_iters["n"]
+        "gpu_launches": alg3_launches(sp, args, alg3_iters["n"], cnt) if alg3_iters["n"]
         else int(sp._launches.value) if args.pool_exec == "native" else (epochs + 1)
         + (_abi.specdec_verify_kernels(True) if sp.fused else _abi.specdec_verify_kernels(False) + 1) * int(cnt[0])
         + 2 * (int(cnt[0]) if sp.dense_consumer else 0 if sp.consumer == "slot" else int(cnt[0]) - int(cnt[1])),
@@ -959,6 +981,20 @@ def run_pool(args, rank, world, device, emulate=False):
         "cpu_baseline": cb,
         "oracle_drain_check": check,
     }
+
+
+def alg3_launches(sp, args, iters, cnt):
+    """libspecdec kernels of the timed Alg. 3 drain: GetBatch + verify per iteration; the
+    gather and scatter per iteration when launched as gated no-ops (direct loop), only for
+    the batches that move KV in the graph's conditional nodes (none with the slot consumer)."""
+    from paper_2510_22876_b200 import _abi
+    kv1 = _abi.specdec_verify_kernels(True)
+    if sp.consumer == "slot" and not os.environ.get("SPECDEC_ALG3_NOOP"):
+        return (1 + kv1) * iters
+    if args.alg3_graph != 2:
+        return (3 + kv1) * iters
+    moving = int(cnt[0]) if sp.consumer == "dense" else int(cnt[0]) - int(cnt[1])
+    return (1 + kv1) * iters + 2 * moving
 
 
 def pool_cpu_baseline(args):
@@ -1138,8 +1174,9 @@ def main():
             "e2e": res["e2e"],
             "gpu_launches": res["kernels_per_round"] * args.steps,
             "launch_mode": args.round_mode + (f" (one CUDA graph per {args.episode}-round episode: the "
-                                              f"episode's state reset + its rounds; remainder rounds from "
-                                              f"per-round graphs)" if args.round_mode == "graph-block" else
+                                              f"episode's state reset + its rounds; the rounds after the last "
+                                              f"whole episode from a block graph of their own)"
+                                              if args.round_mode == "graph-block" else
                                               " (graph: one CUDA graph per (parity, ring slot), 3 kernels per replay)"),
             "bytes_moved_check": {"value_region": res["moved_A"], "kernel_region": res["copied"]},
             "k2_per_launch": k2_spread(*res["k2_launches"], peak),

@@ -611,6 +611,31 @@ int specdec_eqspec_round_host(const specdec_round_desc *d, const specdec_host_io
 int specdec_pool_alg3(const specdec_pool_desc *d, int32_t iterations, int32_t *d_scratch,
                       unsigned long long *d_exec_counters, specdec_stream_t stream);
 
+/* specdec_pool_alg3_graph -- `iterations` iterations of specdec_pool_alg3's loop built as
+ * ONE CUDA graph (instantiated; *graph_exec receives the cudaGraphExec_t).
+ *   conditional = 0: the iterations exactly as specdec_pool_alg3 enqueues them (gated
+ *     no-op gathers / scatters included), captured with their PDL edges -- the host issues
+ *     one graph launch instead of 4 x iterations kernel launches;
+ *   conditional = 1: per iteration the GetBatch kernel, the gather in a conditional (IF)
+ *     node, the verify with the write-back, the scatter in an IF node; GetBatch sets the
+ *     conditions to "batch 0 moves KV" (cudaGraphSetConditional), so a same-length
+ *     iteration launches nothing for its KV moves -- but measured slower on B200 (the IF
+ *     nodes cost more than the no-op launches they remove, and break the PDL chain):
+ *     Alg. 3 pool 3162 (direct) -> 2225 seq/s; kept for the record.
+ * With the slot-indexed consumer (dense_consumer = 2) there are no KV launches at all.
+ * Input-ring slots are bound
+ * at build time: iteration i uses slot (ring_pos + i) % ring_n and *ring_pos advances by
+ * `iterations` -- build ring_n iterations and every launch continues the slot sequence.
+ * Launch with specdec_graph_launch (any stream), release with specdec_graph_destroy.  The
+ * descriptor's buffers and d_scratch / d_exec_counters must outlive the graph.  Results
+ * equal specdec_pool_alg3 (tests/test_gpu_pool.py).
+ * Errors: as specdec_pool_alg3; SPECDEC_ERR_CUDA if the graph cannot be built.
+ */
+int specdec_pool_alg3_graph(const specdec_pool_desc *d, int32_t iterations, int32_t *d_scratch,
+                            unsigned long long *d_exec_counters, int32_t conditional, void **graph_exec);
+int specdec_graph_launch(void *graph_exec, specdec_stream_t stream);
+int specdec_graph_destroy(void *graph_exec);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,9 @@ _SIGS = {
     "specdec_pool_epoch": ([_P, _P, _P, _I32, _P, _P, _P, _P, _P], _INT),
     "specdec_eqspec_round": ([_P, _INT, _P, _P, _P], _INT),
     "specdec_pool_alg3": ([_P, _I32, _P, _P, _P], _INT),
+    "specdec_pool_alg3_graph": ([_P, _I32, _P, _P, _I32, _P], _INT),
+    "specdec_graph_launch": ([_P, _P], _INT),
+    "specdec_graph_destroy": ([_P], _INT),
     "specdec_eqspec_round_host": ([_P, _P, _INT, _INT, _P, _P, _P, _P], _INT),
     "specdec_pool_verify_group": ([_I32, _P, _P, _P, _P, _INT, _I64, _I64, _I64, _P, _P, _P, _I64, _I64,
                                    _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _I64, _P, _P, ctypes.c_size_t,
@@ -171,6 +174,23 @@ def specdec_pool_epoch(desc: PoolDesc, max_batches=0, stream=None, forward=None)
                                      *[ctypes.byref(o) for o in out], _stream(stream)),
            "specdec_pool_epoch")
     return tuple(o.value for o in out)
+
+
+def specdec_pool_alg3_graph(desc: PoolDesc, iterations, scratch, exec_counters=None, conditional=False):
+    """The Alg. 3 loop of `iterations` iterations as one CUDA graph (conditional: KV moves in
+    IF nodes); returns the cudaGraphExec_t handle (an int) for specdec_graph_launch / _destroy."""
+    out = ctypes.c_void_p(0)
+    _check(load().specdec_pool_alg3_graph(ctypes.byref(desc), iterations, _ptr(scratch), _ptr(exec_counters),
+                                          int(conditional), ctypes.byref(out)), "specdec_pool_alg3_graph")
+    return out.value
+
+
+def specdec_graph_launch(graph_exec, stream=None):
+    _check(load().specdec_graph_launch(graph_exec, _stream(stream)), "specdec_graph_launch")
+
+
+def specdec_graph_destroy(graph_exec):
+    _check(load().specdec_graph_destroy(graph_exec), "specdec_graph_destroy")
 
 
 def specdec_pool_alg3(desc: PoolDesc, iterations, scratch, exec_counters=None, stream=None):

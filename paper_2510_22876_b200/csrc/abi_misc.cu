@@ -15,6 +15,14 @@ int record_cuda_error(cudaError_t e) {
     return SPECDEC_ERR_CUDA;
 }
 
+int annotate_error(int rc, const char *where) {
+    if (rc == SPECDEC_ERR_CUDA) g_last_error = std::string(where) + ": " + g_last_error;
+    return rc;
+}
+
+static thread_local int g_pdl_suppress = 0;
+void pdl_suppress(bool on) { g_pdl_suppress += on ? 1 : -1; }
+
 int device_sm_count() {
     static std::mutex mu;
     static int cache[64] = {0};
@@ -36,7 +44,7 @@ bool pdl_enabled() {
         const char *e = getenv("SPECDEC_PDL");
         on = e ? atoi(e) != 0 : 1;
     }
-    return on != 0;
+    return on != 0 && g_pdl_suppress == 0;
 }
 
 }  // namespace specdec

@@ -29,7 +29,9 @@ inline int check_launch() {
     return e == cudaSuccess ? SPECDEC_OK : record_cuda_error(e);
 }
 
-bool pdl_enabled();  // SPECDEC_PDL (default on)
+bool pdl_enabled();  // SPECDEC_PDL (default on), unless suppressed on this thread
+void pdl_suppress(bool on);             // nestable: launches on this thread without PDL
+int annotate_error(int rc, const char *where);  // prefixes the last CUDA error message
 
 // Launch with the programmatic-stream-serialization attribute (PDL) when enabled; the
 // kernels call pdl_wait() before reading anything a predecessor may write.

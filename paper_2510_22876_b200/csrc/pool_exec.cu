@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -152,9 +153,9 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     }
     const int kv1 = specdec_verify_kernels(1);
     // a group of same-length batches: each batch's inputs (forward or ring), one launch
-    const void *g_lg[16];
-    const int64_t *g_dr[16];
-    int32_t g_off[16], g_rows[16];
+    const void *g_lg[16] = {};
+    const int64_t *g_dr[16] = {};
+    int32_t g_off[16] = {}, g_rows[16] = {};
     int32_t ng = 0;
     auto flush_group = [&]() -> int {
         if (!ng) return SPECDEC_OK;
@@ -295,6 +296,11 @@ extern "C" int specdec_pool_alg3(const specdec_pool_desc *d, int32_t iterations,
     const int64_t s_plane = B * hcd, s_row = hcd, s_head = d->cap * d->D;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const uint32_t gflags = d->gather_ws ? SPECDEC_DYNAMIC : 0u;
+    // the slot-indexed consumer (dense_consumer == 2) never moves KV: its gather / scatter
+    // would be gated no-ops, so they are not launched (SPECDEC_ALG3_NOOP=1 launches them
+    // anyway: measures what a gated no-op costs)
+    static const int keep_noop = getenv("SPECDEC_ALG3_NOOP") ? atoi(getenv("SPECDEC_ALG3_NOOP")) : 0;
+    const bool moves_kv = d->dense_consumer != 2 || keep_noop;
     Alg3Gate gate;
     gate.members = g_members;
     gate.kv = g_kv;
@@ -310,7 +316,8 @@ extern "C" int specdec_pool_alg3(const specdec_pool_desc *d, int32_t iterations,
                                    stream, true);
         if (rc) return rc;
         // fallback batch 0: pool slots [0, len-1) -> staging, right-aligned (rows -1: skipped)
-        rc = specdec_realign_kv(d->kv, d->staging, d->kv_dtype, d->n_planes, B, d->H, d->D, p_plane, p_row,
+        if (moves_kv)
+            rc = specdec_realign_kv(d->kv, d->staging, d->kv_dtype, d->n_planes, B, d->H, d->D, p_plane, p_row,
                                 p_head, d->cap, s_plane, s_row, s_head, d->cap, nullptr, 0, d->mpad, 0,
                                 d->mlen, -1, 0, g_kv, nullptr, gflags, d->gather_ws, d->gather_ws ? 128 : 0,
                                 d->moved, d->status, stream);
@@ -323,11 +330,170 @@ extern "C" int specdec_pool_alg3(const specdec_pool_desc *d, int32_t iterations,
                                  d->ws_bytes, stream);
         if (rc) return rc;
         // the a+1 new KV rows back to the pool (rows -1: skipped)
-        rc = specdec_realign_kv(d->staging, d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D, s_plane, s_row,
+        if (moves_kv)
+            rc = specdec_realign_kv(d->staging, d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D, s_plane, s_row,
                                 s_head, d->cap, p_plane, p_row, p_head, d->cap, g_scol, 0, d->mlen, -1,
                                 d->accept, 1, static_cast<int32_t>(d->k + 1), nullptr, g_kv, 0, nullptr, 0,
                                 d->moved, d->status, stream);
         if (rc) return rc;
     }
     return SPECDEC_OK;
+}
+
+// ----------------------------------------------------------------------------- Alg. 3 graph
+// `iterations` iterations of the Alg. 3 device loop as ONE CUDA graph, with the KV moves in
+// conditional (IF) nodes: the GetBatch kernel sets the condition to "batch 0 moves KV"
+// (cudaGraphSetConditional), so a same-length iteration runs GetBatch and the verify only
+// -- no launch at all for its gather and scatter, where specdec_pool_alg3 launches them as
+// gated no-ops (~2.3 us each, measured).  The graph is built piece by piece: each run of
+// plain launches is stream-captured into it (cudaStreamBeginCaptureToGraph after the
+// current frontier), each IF node is added between captures and its body captured from a
+// second stream.
+using Frontier = std::vector<cudaGraphNode_t>;
+
+static int capture_segment(cudaStream_t s, cudaGraph_t graph, Frontier &deps,
+                           const std::function<int(specdec_stream_t)> &launch, const char *what) {
+    cudaError_t e = cudaStreamBeginCaptureToGraph(s, graph, deps.empty() ? nullptr : deps.data(), nullptr,
+                                                  deps.size(), cudaStreamCaptureModeRelaxed);
+    if (e != cudaSuccess) return annotate_error(record_cuda_error(e), what);
+    int rc = launch(reinterpret_cast<specdec_stream_t>(s));
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t *fr = nullptr;
+    size_t nfr = 0;
+    e = cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &fr, &nfr);
+    Frontier next(fr, fr + nfr);
+    cudaGraph_t out = nullptr;
+    const cudaError_t e2 = cudaStreamEndCapture(s, &out);
+    if (rc) return annotate_error(rc, what);
+    if (e != cudaSuccess) return annotate_error(record_cuda_error(e), what);
+    if (e2 != cudaSuccess) return annotate_error(record_cuda_error(e2), what);
+    deps = next;
+    return SPECDEC_OK;
+}
+
+static int add_if(cudaStream_t bs, cudaGraph_t graph, Frontier &deps, cudaGraphConditionalHandle h,
+                  const std::function<int(specdec_stream_t)> &launch, const char *what) {
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    cudaError_t e = cudaGraphAddNode(&node, graph, deps.empty() ? nullptr : deps.data(), deps.size(), &cp);
+    if (e != cudaSuccess) return annotate_error(record_cuda_error(e), what);
+    Frontier none;
+    const int rc = capture_segment(bs, cp.conditional.phGraph_out[0], none, launch, what);
+    if (rc) return rc;
+    deps.assign(1, node);
+    return SPECDEC_OK;
+}
+
+extern "C" int specdec_pool_alg3_graph(const specdec_pool_desc *d, int32_t iterations, int32_t *d_scratch,
+                                       unsigned long long *d_exec_counters, int32_t conditional,
+                                       void **graph_exec) {
+    if (!d || !d_scratch || !graph_exec || d->W < 1 || d->B < 1 || d->B > 1024 || iterations < 1)
+        return SPECDEC_ERR_ARG;
+    if (!d->logits_ring || !d->draft_ring || d->ring_n < 1 || !d->ring_pos) return SPECDEC_ERR_ARG;
+    *graph_exec = nullptr;
+    const int32_t W = d->W, B = d->B;
+    int32_t *g_members = d_scratch, *g_kv = d_scratch + B, *g_scol = d_scratch + 2 * B;
+    uint8_t *g_active = reinterpret_cast<uint8_t *>(d_scratch + 3 * B);
+    const int64_t hcd = d->H * d->cap * d->D;
+    const int64_t p_plane = hcd, p_row = d->n_planes * hcd, p_head = d->cap * d->D;
+    const int64_t s_plane = B * hcd, s_row = hcd, s_head = d->cap * d->D;
+    const uint32_t gflags = d->gather_ws ? SPECDEC_DYNAMIC : 0u;
+    const bool moves_kv = d->dense_consumer != 2;  // the slot-indexed consumer moves no KV
+    cudaStream_t s = nullptr, bs = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaGraphCreate(&graph, 0);
+    int rc = e == cudaSuccess ? SPECDEC_OK : annotate_error(record_cuda_error(e), "graph setup");
+    Alg3Gate gate;
+    gate.members = g_members;
+    gate.kv = g_kv;
+    gate.scol = g_scol;
+    gate.active = g_active;
+    gate.exec = d_exec_counters;
+    gate.dense = d->dense_consumer;
+    Frontier deps;
+    if (!conditional) {
+        // plain: the iterations exactly as specdec_pool_alg3 enqueues them (gated no-op KV
+        // launches included), captured as one segment with their PDL edges
+        if (!rc)
+            rc = capture_segment(s, graph, deps, [&](specdec_stream_t on) {
+                return specdec_pool_alg3(d, iterations, d_scratch, d_exec_counters, on);
+            }, "alg3 loop");
+        iterations = 0;
+    } else {
+        // no programmatic (PDL) edges: the kernels sit between conditional nodes
+        pdl_suppress(true);
+    }
+    for (int32_t it = 0; it < iterations && !rc; ++it) {
+        // one conditional handle per IF node (a handle belongs to a single node): the
+        // iteration's GetBatch sets both
+        cudaGraphConditionalHandle hg = 0, hs = 0;
+        if (moves_kv) {
+            e = cudaGraphConditionalHandleCreate(&hg, graph, 0, cudaGraphCondAssignDefault);
+            if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hs, graph, 0, cudaGraphCondAssignDefault);
+            if (e != cudaSuccess) {
+                rc = annotate_error(record_cuda_error(e), "conditional handles");
+                break;
+            }
+        }
+        gate.cond = hg;
+        gate.cond2 = hs;
+        rc = capture_segment(s, graph, deps, [&](specdec_stream_t on) {
+            return pool_group_launch(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
+                                     d->window_size, d->batch_of, d->slot_of, d->members, d->mlen, d->mpad,
+                                     d->mactive, d->bsize, d->bkind, d->blen, d->n_batches, d->counters, gate, on,
+                                     true);
+        }, "getbatch");
+        if (!rc && moves_kv)
+            rc = add_if(bs, graph, deps, hg, [&](specdec_stream_t on) {
+                return specdec_realign_kv(d->kv, d->staging, d->kv_dtype, d->n_planes, B, d->H, d->D, p_plane,
+                                          p_row, p_head, d->cap, s_plane, s_row, s_head, d->cap, nullptr, 0,
+                                          d->mpad, 0, d->mlen, -1, 0, g_kv, nullptr, gflags, d->gather_ws,
+                                          d->gather_ws ? 128 : 0, d->moved, d->status, on);
+            }, "gather");
+        if (rc) break;
+        const int32_t j = (*d->ring_pos)++ % d->ring_n;
+        rc = capture_segment(s, graph, deps, [&](specdec_stream_t on) {
+            return specdec_pool_verify(d->logits_ring[j], d->logit_dtype, B, d->k, d->V, d->logit_stride,
+                                       d->draft_ring[j], g_members, d->mlen, g_active, d->eos_id, d->pad_id,
+                                       d->accept, d->bonus, d->emit, d->finished, d->len, d->gen, d->active,
+                                       d->tokens, d->cap_tok, d->out_buf, d->max_new, d->status, d->ws,
+                                       d->ws_bytes, on);
+        }, "verify");
+        if (!rc && moves_kv)
+            rc = add_if(bs, graph, deps, hs, [&](specdec_stream_t on) {
+                return specdec_realign_kv(d->staging, d->kv, d->kv_dtype, d->n_planes, B, d->H, d->D, s_plane,
+                                          s_row, s_head, d->cap, p_plane, p_row, p_head, d->cap, g_scol, 0,
+                                          d->mlen, -1, d->accept, 1, static_cast<int32_t>(d->k + 1), nullptr,
+                                          g_kv, 0, nullptr, 0, d->moved, d->status, on);
+            }, "scatter");
+    }
+    if (conditional) pdl_suppress(false);
+    cudaGraphExec_t ex = nullptr;
+    if (!rc) {
+        e = cudaGraphInstantiate(&ex, graph, 0);
+        if (e != cudaSuccess) rc = annotate_error(record_cuda_error(e), "instantiate");
+    }
+    if (graph) cudaGraphDestroy(graph);
+    if (bs) cudaStreamDestroy(bs);
+    if (s) cudaStreamDestroy(s);
+    if (!rc) *graph_exec = ex;
+    return rc;
+}
+
+extern "C" int specdec_graph_launch(void *graph_exec, specdec_stream_t stream) {
+    if (!graph_exec) return SPECDEC_ERR_ARG;
+    const cudaError_t e = cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? SPECDEC_OK : record_cuda_error(e);
+}
+
+extern "C" int specdec_graph_destroy(void *graph_exec) {
+    if (!graph_exec) return SPECDEC_OK;
+    const cudaError_t e = cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(graph_exec));
+    return e == cudaSuccess ? SPECDEC_OK : record_cuda_error(e);
 }

@@ -18,6 +18,10 @@ struct Alg3Gate {
     uint8_t *active = nullptr;
     unsigned long long *exec = nullptr;
     int dense = 0;  // specdec_pool_desc::dense_consumer
+    // CUDA-graph conditional handles (cudaGraphConditionalHandle; one per conditional node)
+    // set to "batch 0 moves KV" for the gather / scatter IF nodes of specdec_pool_alg3_graph;
+    // 0 = none
+    unsigned long long cond = 0, cond2 = 0;
 };
 
 int pool_group_launch(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order, int32_t N,

@@ -433,6 +433,10 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
         // batch 0 goes through the staging: a mixed batch (dense rectangle consumer) or every
         // batch (dense = 1); never with the slot-indexed consumer (dense = 2)
         const bool moves = valid && gate.dense != 2 && (!same || gate.dense == 1);
+        if (gate.cond && tid == 0) {
+            cudaGraphSetConditional(gate.cond, moves ? 1u : 0u);
+            if (gate.cond2) cudaGraphSetConditional(gate.cond2, moves ? 1u : 0u);
+        }
         for (int j = tid; j < B; j += T) {
             const int32_t m = valid ? members[j] : -1;
             gate.members[j] = m;
@@ -612,6 +616,10 @@ __global__ void __launch_bounds__(kPoolThreads) pool_getbatch_kernel(
         __syncthreads();  // batch 0's member / mactive stores visible to every thread
         const bool valid = take > 0;
         const bool moves = valid && gate.dense != 2 && (!same || gate.dense == 1);
+        if (gate.cond && tid == 0) {
+            cudaGraphSetConditional(gate.cond, moves ? 1u : 0u);
+            if (gate.cond2) cudaGraphSetConditional(gate.cond2, moves ? 1u : 0u);
+        }
         for (int j = tid; j < B; j += T) {
             const int32_t m = valid ? members[j] : -1;
             gate.members[j] = m;

@@ -311,5 +311,26 @@ class SequencePool:
             self.alg3_exec = torch.zeros(4, dtype=torch.int64, device=self.device)
         _abi.specdec_pool_alg3(self._desc, iterations, self._alg3_scratch, self.alg3_exec, stream)
 
+    def alg3_graph(self, replays, stream=None, conditional=False):
+        """`replays` x ring_n iterations of the Alg. 3 device loop from ONE CUDA graph of ring_n
+        iterations built by the library (specdec_pool_alg3_graph: the loop's launches with
+        their PDL edges; `conditional`: the KV moves in IF nodes instead -- measured slower).
+        Call after `native` and one direct `alg3_native` call (which creates the scratch and
+        sets the kernels' attributes).  The graph binds the input-ring slots from the ring
+        position at build time; ring_n iterations leave it unchanged modulo ring_n, so every
+        replay continues the sequence the direct loop takes."""
+        if getattr(self, "_alg3_gexec", None) is None:
+            self._alg3_gexec = _abi.specdec_pool_alg3_graph(self._desc, len(self._ring), self._alg3_scratch,
+                                                            self.alg3_exec, conditional)
+        s = stream or torch.cuda.current_stream(self.device)
+        for _ in range(replays):
+            _abi.specdec_graph_launch(self._alg3_gexec, s)
+
+    def close(self):
+        """Release the Alg. 3 graph (if built)."""
+        if getattr(self, "_alg3_gexec", None):
+            _abi.specdec_graph_destroy(self._alg3_gexec)
+            self._alg3_gexec = None
+
     def has_active(self) -> bool:
         return bool(self.active.any().item())
