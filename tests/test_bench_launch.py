@@ -83,3 +83,21 @@ def test_default_line_has_the_contract_keys():
     assert d["gpu_launches"] == (2 + _abi.specdec_verify_kernels(False)) * 6      # K1, K3, K2
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["bytes_moved_check"]["value_region"] == d["bytes_moved_check"]["kernel_region"]
+    kp = d["k2_per_launch"]                    # per-launch K2 rates (region B's 6 launches)
+    assert kp["launches"] == 6 and kp["GBps_quartiles"][2] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["epoch", "alg3"])
+def test_pool_line_drain_matches_the_oracle(mode):
+    """The pool line's timed drain (native executor; Alg. 3: the graph-replayed device loop)
+    against the oracle's own plan-driven drain of the same workload (the cpu_baseline leg):
+    batches, same-length batches and members, fallback members and KV bytes, exactly."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "pool", "--pool-n", "192",
+                        "--max-new", "64", "--pool-mode", mode], capture_output=True, text=True, timeout=900,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    chk = d["oracle_drain_check"]
+    assert chk["match"], chk
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["gpu_launches"] > 0 and d["status"] == 0
