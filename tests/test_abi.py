@@ -83,6 +83,28 @@ def test_host_validation_without_gpu(lib):
     # rebuild: capacity statically impossible
     rc = L.specdec_rebuild_pos_mask(nz, nz, 2, 4, 5, 0, *([nz] * 11), 64, None, None, 0, None, None)
     assert rc == _abi.ERR_CAPACITY
+    # getbatch: B > W (same limits as pool_group)
+    rc = L.specdec_pool_getbatch(nz, nz, nz, 10, 4, 8, 2, *([nz] * 14))
+    assert rc == _abi.ERR_SHAPE
+    # batch init: NULL lengths / B < 1
+    assert L.specdec_batch_init(None, 4, nz, None, None, None, 0, None, None) == _abi.ERR_ARG
+    assert L.specdec_batch_init(nz, 0, nz, None, None, None, 0, None, None) == _abi.ERR_SHAPE
+    # grouped pool verify: 0 or more than 16 batches, a batch with no rows
+    P = ctypes.c_void_p * 17
+    I = ctypes.c_int32 * 17
+    ptrs, offs, rows = P(*([16] * 17)), I(*([0] * 17)), I(*([1] * 17))
+    for n in (0, 17):
+        rc = L.specdec_pool_verify_group(n, ptrs, ptrs, offs, rows, 2, 5, 100, 104, *([nz] * 3), -1, 0,
+                                         *([nz] * 7), None, 0, None, 16, None, nz, 1 << 20, None)
+        assert rc == _abi.ERR_ARG, n
+    rows[1] = 0
+    rc = L.specdec_pool_verify_group(2, ptrs, ptrs, offs, rows, 2, 5, 100, 104, *([nz] * 3), -1, 0,
+                                     *([nz] * 7), None, 0, None, 16, None, nz, 1 << 20, None)
+    assert rc == _abi.ERR_SHAPE
+    # the Alg. 3 graph: NULL descriptor; graph launch / destroy of NULL
+    assert L.specdec_pool_alg3_graph(None, 16, nz, None, 0, ctypes.byref(ctypes.c_void_p())) == _abi.ERR_ARG
+    assert L.specdec_graph_launch(None, None) == _abi.ERR_ARG
+    assert L.specdec_graph_destroy(None) == _abi.OK
 
 
 def test_missing_library_fails_loudly(tmp_path):
