@@ -61,6 +61,8 @@ def parse(argv=None):
     ap.add_argument("--alg3-graph", type=int, default=1,
                     help="pool --pool-mode alg3: replay the device loop from a CUDA graph of 16 iterations (0: direct, "
                          "2: the KV moves in conditional graph nodes)")
+    ap.add_argument("--pool-scatter-stream", type=int, default=0,
+                    help="pool (native, overlapped): the scatters on a third stream beside the gathers")
     ap.add_argument("--pool-verify-group", type=int, default=8,
                     help="pool (native executor): same-length batches verified per launch (1 = per batch)")
     ap.add_argument("--pool-staging", type=int, default=2,
@@ -748,6 +750,7 @@ def run_pool(args, rank, world, device, emulate=False):
     sp = SequencePool(n_loc, cap, sh.layers, sh.H, sh.D, k, W=Wn, B=min(B, Wn),
                       min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False,
                       consumer=args.pool_consumer, verify_group=args.pool_verify_group,
+                      scatter_stream=bool(args.pool_scatter_stream),
                       n_staging=args.pool_staging if args.pool_exec == "native" else 1)
     local_lens = lens[mine]
     local_order = np.arange(n_loc)            # `mine` is already in admission order

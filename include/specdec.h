@@ -485,6 +485,14 @@ typedef struct specdec_pool_desc {
      * accept / bonus / emit / finished of verify_group * B entries. */
     int32_t verify_group;
     int64_t *host_launches;    /* host, nullable: += the libspecdec kernels the call launched */
+    /* optional third stream for the scatters (n_staging >= 2): scatter f waits for its
+     * verify and runs beside the copy stream's gathers (epoch batches have disjoint members,
+     * so a scatter and another batch's gather touch disjoint pool rows and staging slots);
+     * the gather of f + n_staging waits for scatter f (scatter_events[f % n_staging]).
+     * NULL: the scatters run on copy_stream as above.  scatter_events: host array of
+     * n_staging cudaEvent_t (timing disabled). */
+    specdec_stream_t scatter_stream;
+    void *const *scatter_events;
 } specdec_pool_desc;
 
 int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,

@@ -91,6 +91,7 @@ class PoolDesc(ctypes.Structure):
         ("est_gather_GBps", ctypes.c_double), ("est_verify_us", ctypes.c_double),
         ("gather_ws", _P),
         ("verify_group", _I32), ("host_launches", _P),
+        ("scatter_stream", _P), ("scatter_events", _P),
     ]
 
 

@@ -37,7 +37,9 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         return SPECDEC_ERR_ARG;
     if (d->n_staging >= 2)
         for (int32_t i = 0; i < d->n_staging; ++i)
-            if (!d->staging_ring[i] || !d->events[i] || !d->events[d->n_staging + i]) return SPECDEC_ERR_ARG;
+            if (!d->staging_ring[i] || !d->events[i] || !d->events[d->n_staging + i] ||
+                (d->scatter_stream && (!d->scatter_events || !d->scatter_events[i])))
+                return SPECDEC_ERR_ARG;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int32_t W = d->W, B = d->B;
     int rc = specdec_pool_group(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
@@ -126,7 +128,10 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
         }
     }
     cudaStream_t cs = overlap ? reinterpret_cast<cudaStream_t>(d->copy_stream) : nullptr;
+    // scatters on their own stream beside the gathers (optional), else on the copy stream
+    cudaStream_t ss = overlap && d->scatter_stream ? reinterpret_cast<cudaStream_t>(d->scatter_stream) : cs;
     auto ev = [&](int i) { return reinterpret_cast<cudaEvent_t>(d->events[i]); };
+    auto sev = [&](int i) { return reinterpret_cast<cudaEvent_t>(d->scatter_events[i]); };
     auto stg = [&](int32_t b) -> void * {
         return overlap ? d->staging_ring[fb_rank[b] % NS] : d->staging;
     };
@@ -234,9 +239,9 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
             cudaStream_t on = stream ? reinterpret_cast<cudaStream_t>(stream) : nullptr;
             if (overlap) {
                 if ((e = cudaEventRecord(ev(NS + slot), s)) != cudaSuccess ||
-                    (e = cudaStreamWaitEvent(cs, ev(NS + slot), 0)) != cudaSuccess)
+                    (e = cudaStreamWaitEvent(ss, ev(NS + slot), 0)) != cudaSuccess)
                     return record_cuda_error(e);
-                on = cs;
+                on = ss;
             }
             rc = specdec_realign_kv(stg(b), d->kv, d->kv_dtype, d->n_planes, rows(b), d->H, d->D,
                                     s_plane, s_row, s_head, d->cap, p_plane, p_row, p_head, d->cap,
@@ -248,6 +253,11 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
             ++launches;
             const int32_t nxt = fb_rank[b] + NS;  // the gather that reuses this staging buffer
             if (overlap && nxt < static_cast<int32_t>(fbs.size())) {
+                if (ss != cs) {  // the scatter (its own stream) first frees the staging slot
+                    if ((e = cudaEventRecord(sev(slot), ss)) != cudaSuccess ||
+                        (e = cudaStreamWaitEvent(cs, sev(slot), 0)) != cudaSuccess)
+                        return record_cuda_error(e);
+                }
                 if ((rc = gather(fbs[nxt], cs))) return rc;
                 ++launches;
                 if ((e = cudaEventRecord(ev(nxt % NS), cs)) != cudaSuccess) return record_cuda_error(e);
@@ -263,8 +273,12 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     }
     if (overlap && !fbs.empty()) {
         // the epoch ends on `stream`: it waits for the copy stream's last scatter (events[0]
-        // is free again -- every wait on its earlier records has been enqueued)
+        // is free again -- every wait on its earlier records has been enqueued), and for the
+        // scatter stream's (scatter_events[0] likewise)
         if ((e = cudaEventRecord(ev(0), cs)) != cudaSuccess || (e = cudaStreamWaitEvent(s, ev(0), 0)) != cudaSuccess)
+            return record_cuda_error(e);
+        if (ss != cs && ((e = cudaEventRecord(sev(0), ss)) != cudaSuccess ||
+                         (e = cudaStreamWaitEvent(s, sev(0), 0)) != cudaSuccess))
             return record_cuda_error(e);
     }
     if ((rc = flush_group())) return rc;

@@ -29,7 +29,7 @@ from .eqspec import TORCH_DT
 class SequencePool:
     def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
                  max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True,
-                 dense_consumer=False, n_staging=1, consumer=None, verify_group=8):
+                 dense_consumer=False, n_staging=1, consumer=None, verify_group=8, scatter_stream=False):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         if B > W:
@@ -63,6 +63,7 @@ class SequencePool:
         # native executor only: n_staging >= 2 overlaps the fallback gathers (copy stream,
         # ring of staging buffers) with the same-length batches (specdec_pool_desc)
         self.n_staging = int(n_staging)
+        self.scatter_stream = bool(scatter_stream)   # native executor: scatters on a third stream
         self.staging_ring = [self.staging] + [alloc(self.staging.shape, dtype=self.staging.dtype, device=dev)
                                               for _ in range(max(self.n_staging, 1) - 1)]
         # plan (K4 outputs)
@@ -289,6 +290,15 @@ class SequencePool:
             d.events = ctypes.cast(self._ev_ptrs, ctypes.c_void_p)
             self._accept_ring = torch.zeros((ns, self.B), dtype=torch.int32, device=self.device)
             d.accept_ring = self._accept_ring.data_ptr()
+            if self.scatter_stream:
+                # the scatters on a third stream, beside the gathers
+                self._scatter_stream = torch.cuda.Stream(self.device)
+                self._sevents = [torch.cuda.Event(enable_timing=False) for _ in range(ns)]
+                for ev in self._sevents:
+                    ev.record(torch.cuda.current_stream(self.device))
+                self._sev_ptrs = (ctypes.c_void_p * ns)(*[ev.cuda_event for ev in self._sevents])
+                d.scatter_stream = self._scatter_stream.cuda_stream
+                d.scatter_events = ctypes.cast(self._sev_ptrs, ctypes.c_void_p)
             d.est_gather_GBps, d.est_verify_us = float(est_gather_GBps), float(est_verify_us)
         self._desc = d
         return d
