@@ -61,7 +61,7 @@ def parse(argv=None):
     ap.add_argument("--alg3-graph", type=int, default=1,
                     help="pool --pool-mode alg3: replay the device loop from a CUDA graph of 16 iterations (0: direct, "
                          "2: the KV moves in conditional graph nodes)")
-    ap.add_argument("--pool-scatter-stream", type=int, default=0,
+    ap.add_argument("--pool-scatter-stream", type=int, default=1,
                     help="pool (native, overlapped): the scatters on a third stream beside the gathers")
     ap.add_argument("--pool-verify-group", type=int, default=8,
                     help="pool (native executor): same-length batches verified per launch (1 = per batch)")
@@ -771,9 +771,13 @@ def run_pool(args, rank, world, device, emulate=False):
         sp.native(list(zip(ring_lg, ring_dr)), V=V, logit_dtype=ring_lg[0].dtype,
                   est_gather_GBps=args.pool_est[0], est_verify_us=args.pool_est[1])
 
-    def drain(events=None):
-        # every drain is the same workload: the pool state and the input ring restart
-        sp.load(local_lens, order=local_order)
+    def drain(events=None, admit=None):
+        # every drain is the same workload: the pool state and the input ring restart.
+        # admit(): the e2e drain's own admission from pinned host buffers instead
+        if admit is None:
+            sp.load(local_lens, order=local_order)
+        else:
+            admit()
         ctr["i"] = 0
         sp.moved.zero_()
         epochs = batches = 0
@@ -899,6 +903,51 @@ def run_pool(args, rank, world, device, emulate=False):
     else:
         gen_all, cnt_all, gather_ms = gen_loc, cnt, 0.0
     assert int((gen_all == args.max_new).sum()) == N, "every sequence reaches max_new (EOS off)"
+    # e2e: the same drain through the public API with its host I/O inside the timed region --
+    # the sequences admitted from pinned host buffers (prompt lengths, admission order,
+    # prompt tokens [N, cap_tok]) and every generated token read back (out_buf, gen); the
+    # per-batch logits are the model's, produced on the device (the executor's forward)
+    e2e = None
+    if not args.no_e2e:
+        g = torch.Generator().manual_seed(args.seed)
+        h_len = torch.as_tensor(local_lens, dtype=torch.int32).pin_memory()
+        h_ord = torch.as_tensor(local_order, dtype=torch.int32).pin_memory()
+        h_tok = torch.randint(2, V, (n_loc, sp.tokens.shape[1]), generator=g, dtype=torch.int64)
+        h_tok[torch.arange(sp.tokens.shape[1])[None, :] >= torch.as_tensor(local_lens)[:, None]] = 0
+        h_tok = h_tok.pin_memory()
+        h_out = torch.empty(sp.out_buf.shape, dtype=sp.out_buf.dtype).pin_memory()
+        h_gen = torch.empty(sp.gen.shape, dtype=sp.gen.dtype).pin_memory()
+
+        def admit():
+            sp.len.copy_(h_len, non_blocking=True)
+            sp.order.copy_(h_ord, non_blocking=True)
+            sp.tokens.copy_(h_tok, non_blocking=True)
+            sp.gen.zero_()
+            sp.active.fill_(1)
+            sp.counters.zero_()
+            sp.verify_calls = 0
+            if getattr(sp, "_ring_pos", None) is not None:
+                sp._ring_pos.value = 0
+        ms_e = []
+        for _ in range(max(1, args.reps)):
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            t0.record()
+            drain(admit=admit)
+            h_out.copy_(sp.out_buf, non_blocking=True)
+            h_gen.copy_(sp.gen, non_blocking=True)
+            t1.record()
+            torch.cuda.synchronize()
+            ms_e.append(t0.elapsed_time(t1))
+        assert int((h_gen == args.max_new).sum()) == n_loc, "e2e: every sequence reaches max_new"
+        bi = h_len.numel() * 4 + h_ord.numel() * 4 + h_tok.numel() * 8
+        bo = h_out.numel() * 8 + h_gen.numel() * 4
+        e2e_ms = max_over_ranks(float(np.median(ms_e)), device, world) if world > 1 else float(np.median(ms_e))
+        e2e = {"value": N / (e2e_ms / 1e3), "unit": "sequences/s", "h2d_bytes_per_step": bi,
+               "d2h_bytes_per_step": bo,
+               "note": "one drain per step: prompt lengths, order and tokens copied in from pinned host memory, "
+                       "the generated tokens of every sequence read back, inside the timed region"}
     # second drain with events around the fallback batches' KV moves (roofline of K2)
     evs = []
     if rank == 0:
@@ -947,7 +996,8 @@ def run_pool(args, rank, world, device, emulate=False):
                                f"{args.max_new}, W={Wn}/rank, B={sp.B}, min_group={args.min_group}, "
                                f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}, {args.pool_consumer} consumer, "
                                f"{args.pool_exec} launch loop"
-                               + (f", fallback gathers overlapped ({sp.n_staging} staging buffers)"
+                               + (f", fallback gathers overlapped ({sp.n_staging} staging buffers"
+                                  + (", scatters on a third stream" if sp.scatter_stream else "") + ")"
                                   if args.pool_exec == "native" and sp.n_staging >= 2 else "")
                                + (f", up to {sp.verify_group} same-length batches per verify launch"
                                   if args.pool_exec == "native" and args.pool_mode == "epoch" and sp.verify_group > 1
@@ -977,10 +1027,7 @@ def run_pool(args, rank, world, device, emulate=False):
         else int(sp._launches.value) if args.pool_exec == "native" else (epochs + 1)
         + (_abi.specdec_verify_kernels(True) if sp.fused else _abi.specdec_verify_kernels(False) + 1) * int(cnt[0])
         + 2 * (int(cnt[0]) if sp.dense_consumer else 0 if sp.consumer == "slot" else int(cnt[0]) - int(cnt[1])),
-        "e2e": None,
-        "e2e_note": "pool: the per-batch logits come from the model's forward on the device (the "
-                    "executor's forward callback); the host-buffer end-to-end path is the default "
-                    "(EqSpec round) line's e2e",
+        "e2e": e2e,
         "cpu_baseline": cb,
         "oracle_drain_check": check,
     }
