@@ -12,7 +12,7 @@ import numpy as np
 
 from .align import (anchor_plan, build_batch, copy_rows, mask_pos_row, realign_kv, repad_tokens,
                     unpad)
-from .pool import admission_order, form_batches
+from .pool import admission_order, form_batches, form_batches_deferred
 from .toy_lm import ToyLM, greedy_fp32
 from .verify import batch_verify
 
@@ -132,9 +132,11 @@ def eqspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, ca
 
 
 def exspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, cap, W, B,
-                  min_group=2, sort_by_length=True, noise=0.0, pad_id=0, sequential=False):
+                  min_group=2, sort_by_length=True, noise=0.0, pad_id=0, sequential=False,
+                  patience=0):
     """Alg. 3 over a SequencePool.  Each epoch plans the whole window (K4 semantics);
-    with sequential=True only batch 0 runs per iteration (Alg. 3's one-batch GetBatch).
+    with sequential=True only batch 0 runs per iteration (Alg. 3's one-batch GetBatch);
+    patience > 0: the epoch plan defers leftovers (form_batches_deferred, reading R27).
     Returns (outputs, stats)."""
     N = len(prompts)
     lens = np.array([len(p) for p in prompts], np.int32)
@@ -149,8 +151,12 @@ def exspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, ca
         for c, t in enumerate(seqs[s][:-1]):
             target.token_forward(t, c, c, pool_kv[s], ones)
     stats = dict(verify_calls=0, batches=0, same_length=0, realigned_members=0)
+    wait = np.zeros(N, np.int64)
     while active.any():
-        plan = form_batches(lens, active, order, W, B, min_group)
+        if patience > 0:
+            plan = form_batches_deferred(lens, active, order, W, B, min_group, wait, patience)
+        else:
+            plan = form_batches(lens, active, order, W, B, min_group)
         todo = plan["batches"][:1] if sequential else plan["batches"]
         kinds = plan["kind"][:1] if sequential else plan["kind"]
         for members, kind in zip(todo, kinds):

@@ -106,3 +106,17 @@ def test_golden_pool_plans():
         assert r["batches"] == c["batches"], c["note"]
         assert r["kind"] == c["kind"] and r["blen"] == c["blen"], c["note"]
         assert r["counters"].tolist() == c["counters"], c["note"]
+
+
+def test_golden_pool_deferred():
+    """Deferred fallback (R27): hand-worked plans and wait updates (tests/golden/pool_deferred.json)."""
+    for c in load("pool_deferred.json")["cases"]:
+        wait = np.array(c["wait"], np.int64)
+        r = P.form_batches_deferred(np.array(c["lens"]), np.array(c["active"]), np.array(c["order"]),
+                                    c["W"], c["B"], c["min_group"], wait, c["patience"])
+        assert r["window"] == c["window"], c["note"]
+        assert r["batches"] == c["batches"], c["note"]
+        assert r["kind"] == c["kind"] and r["blen"] == c["blen"], c["note"]
+        assert r["deferred"] == c["deferred"], c["note"]
+        assert r["counters"].tolist() == c["counters"], c["note"]
+        assert wait.tolist() == c["wait_after"], c["note"]

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from oracle.loops import exspec_decode
-from oracle.pool import admission_order, form_batches, refill_window
+from oracle.pool import admission_order, form_batches, form_batches_deferred, refill_window
 from oracle.toy_lm import ToyLM
 
 
@@ -37,9 +37,10 @@ def test_admission_and_window():
     assert refill_window([1, 0, 1, 1], order, 2) == [3, 0]
 
 
-def _reference_plan(lens, window, B, mg):
+def _reference_groups(lens, window, B, mg):
     """Independent formulation: sort the window by the library sort on the key
-    (-group count, length, window position); walk it cutting batches."""
+    (-group count, length, window position); walk it cutting batches.  Returns the
+    same-length batches and the leftovers in window order."""
     cnt = {l: sum(1 for s in window if lens[s] == l) for l in {lens[s] for s in window}}
     pos = {s: t for t, s in enumerate(window)}
     srt = sorted(window, key=lambda s: (-cnt[lens[s]], lens[s], pos[s]))
@@ -50,7 +51,11 @@ def _reference_plan(lens, window, B, mg):
         while full and len(full[-1]) < (1 if B == 1 else mg):
             left += full.pop()
         same += full
-    left = sorted(left, key=lambda s: pos[s])
+    return same, sorted(left, key=lambda s: pos[s])
+
+
+def _reference_plan(lens, window, B, mg):
+    same, left = _reference_groups(lens, window, B, mg)
     return same + [left[i:i + B] for i in range(0, len(left), B)]
 
 
@@ -123,3 +128,89 @@ def test_exspec_uniform_lengths_all_same_length():
     prompts = [list(map(int, rng.integers(2, 32, size=6))) for _ in range(4)]
     out, st = exspec_decode(T, T, prompts, 3, 8, -1, 64, W=4, B=2, min_group=2)
     assert st["same_length"] == st["batches"] and st["realigned_members"] == 0
+
+
+def test_deferred_patience_zero_is_form_batches():
+    """R27 with patience 0 (or an all-stale pool) is R11's plan exactly."""
+    rng = np.random.default_rng(11)
+    for _ in range(300):
+        N = int(rng.integers(1, 40))
+        lens = rng.integers(1, 6, N).tolist()
+        active = (rng.random(N) < 0.8).astype(int).tolist()
+        order = rng.permutation(N).tolist()
+        W = int(rng.integers(1, N + 1))
+        B = int(rng.integers(1, 9))
+        mg = int(rng.integers(1, B + 1))
+        p = form_batches(lens, active, order, W, B, mg)
+        for patience, w0 in ((0, 0), (3, 3), (2, 7)):
+            wait = np.full(N, w0, np.int64)
+            q = form_batches_deferred(lens, active, order, W, B, mg, wait, patience)
+            assert q["batches"] == p["batches"] and q["kind"] == p["kind"] and q["deferred"] == []
+            assert (q["counters"] == p["counters"]).all()
+            assert all(wait[s] == 0 for s in p["window"])
+
+
+def test_deferred_brute_force_properties():
+    """Every window of W <= 6 with lengths in {1,2,3}, waits in {0,1,2}, patience 1 and 2:
+    planned + deferred partition the window; the group batches are R11's; a leftover is
+    deferred iff some group batch exists and its wait is below the patience; the fallback
+    batches chunk the rest in window order; the waits update as stated."""
+    for W in range(1, 7):
+        for lens in itertools.product([1, 2, 3], repeat=W):
+            rng = np.random.default_rng(hash(lens) & 0xFFFF)
+            for B, mg in [(1, 2), (2, 2), (3, 2), (4, 4), (8, 2)]:
+                w0 = rng.integers(0, 3, W)
+                for patience in (1, 2):
+                    wait = w0.copy()
+                    q = form_batches_deferred(list(lens), [1] * W, list(range(W)), W, B, mg, wait, patience)
+                    planned = [s for b in q["batches"] for s in b]
+                    assert sorted(planned + q["deferred"]) == list(range(W))
+                    groups, left = _reference_groups(list(lens), list(range(W)), B, mg)
+                    assert q["batches"][:len(groups)] == groups
+                    if groups:
+                        assert q["deferred"] == [s for s in left if w0[s] < patience]
+                        run = [s for s in left if w0[s] >= patience]
+                    else:
+                        assert q["deferred"] == []
+                        run = left
+                    assert q["batches"][len(groups):] == [run[t:t + B] for t in range(0, len(run), B)]
+                    for s in range(W):
+                        assert wait[s] == (w0[s] + 1 if s in q["deferred"] else 0)
+                    assert len(q["batches"]) >= 1                      # every epoch makes progress
+
+
+def test_deferred_drain_bounds_waits_and_finishes():
+    """A drain under R27 (planted accepts) ends, and no member is deferred more than
+    `patience` epochs in a row."""
+    rng = np.random.default_rng(4)
+    for patience in (1, 2, 4):
+        N, B = 48, 4
+        lens = rng.integers(5, 30, N).astype(np.int64)
+        gen = np.zeros(N, np.int64)
+        act = np.ones(N, np.uint8)
+        wait = np.zeros(N, np.int64)
+        epochs = 0
+        while act.any():
+            q = form_batches_deferred(lens, act, list(range(N)), N, B, 2, wait, patience)
+            assert q["batches"] and wait.max() <= patience
+            for b in q["batches"]:
+                for s in b:
+                    e = min(int(rng.integers(1, 5)), 24 - int(gen[s]))
+                    lens[s] += e
+                    gen[s] += e
+                    if gen[s] >= 24:
+                        act[s] = 0
+            epochs += 1
+            assert epochs < 10_000
+
+
+@pytest.mark.parametrize("patience,W,B", [(1, 6, 2), (2, 6, 3), (3, 4, 2)])
+def test_exspec_deferred_equals_autoregressive_greedy(patience, W, B):
+    """Deferring a sequence changes when it is verified, never what it emits (R27)."""
+    T = ToyLM(seed=7)
+    rng = np.random.default_rng(patience * 10 + W)
+    prompts = [list(map(int, rng.integers(2, 32, size=int(l)))) for l in rng.integers(1, 12, 7)]
+    ref = [T.greedy_generate(p, 14, 1, 64) for p in prompts]
+    out, st = exspec_decode(T, T, prompts, 4, 14, 1, 64, W=W, B=B, min_group=2, noise=0.3,
+                            patience=patience)
+    assert out == ref
