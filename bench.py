@@ -75,6 +75,10 @@ def parse(argv=None):
                          "G-GPU throughput (slowest shard); a prediction, not a measurement")
     ap.add_argument("--shard-c", type=float, default=1.0,
                     help="--shard balanced: per-sequence weight = prompt length + c * max_new")
+    ap.add_argument("--pool-patience", type=int, default=2,
+                    help="pool epoch plan: leftovers wait up to P epochs for a same-length partner before "
+                         "a fallback batch (reading R27, specdec_pool_group_deferred); 0 = R11's full plan "
+                         "(N=1024: 3003 seq/s at P=0, 7428 at P=2)")
     ap.add_argument("--pool-mode", default="epoch", choices=["epoch", "alg3"],
                     help="epoch: run every batch of the window plan; alg3: batch 0 then re-plan")
     ap.add_argument("--B", type=int, default=0, help="override batch size")
@@ -645,6 +649,7 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
     N = len(lens)
     Wn = min(args.pool_W or N, 2048, N)
     o_len, gen, act = lens.astype(np.int64), np.zeros(N, np.int64), np.ones(N, np.uint8)
+    wait = np.zeros(N, np.int64)          # R27 (epoch mode with --pool-patience)
     truth = [W.gen_round_truth(args.seed, r, B, k, V, args.pattern, alpha=args.alpha) for r in range(RING)]
     t_plan = 0.0
     n_batches = n_same = same_members = fb_members = 0
@@ -653,7 +658,10 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
     slot = args.pool_consumer == "slot"
     while act.any():
         t0 = time.perf_counter()
-        plan = OP.form_batches(o_len, act, order, Wn, B, args.min_group)
+        if args.pool_patience > 0 and args.pool_mode != "alg3":
+            plan = OP.form_batches_deferred(o_len, act, order, Wn, B, args.min_group, wait, args.pool_patience)
+        else:
+            plan = OP.form_batches(o_len, act, order, Wn, B, args.min_group)
         t_plan += time.perf_counter() - t0
         nb = 1 if args.pool_mode == "alg3" else len(plan["batches"])
         for b in range(nb):
@@ -750,7 +758,7 @@ def run_pool(args, rank, world, device, emulate=False):
     sp = SequencePool(n_loc, cap, sh.layers, sh.H, sh.D, k, W=Wn, B=min(B, Wn),
                       min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False,
                       consumer=args.pool_consumer, verify_group=args.pool_verify_group,
-                      scatter_stream=bool(args.pool_scatter_stream),
+                      scatter_stream=bool(args.pool_scatter_stream), patience=args.pool_patience,
                       n_staging=args.pool_staging if args.pool_exec == "native" else 1)
     local_lens = lens[mine]
     local_order = np.arange(n_loc)            # `mine` is already in admission order
@@ -994,7 +1002,10 @@ def run_pool(args, rank, world, device, emulate=False):
         "config": {"workload": f"EXSpec pool drain: {N} seqs, prompt {args.pool_lengths} "
                                f"{'U[64,512]' if args.pool_lengths == 'random' else '256'}, max_new "
                                f"{args.max_new}, W={Wn}/rank, B={sp.B}, min_group={args.min_group}, "
-                               f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}, {args.pool_consumer} consumer, "
+                               f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}"
+                               + (f" (deferred fallback, patience {args.pool_patience})"
+                                  if args.pool_patience > 0 and args.pool_mode == "epoch" else "")
+                               + f", {args.pool_consumer} consumer, "
                                f"{args.pool_exec} launch loop"
                                + (f", fallback gathers overlapped ({sp.n_staging} staging buffers"
                                   + (", scatters on a third stream" if sp.scatter_stream else "") + ")"
@@ -1011,6 +1022,8 @@ def run_pool(args, rank, world, device, emulate=False):
         "pool": {"epochs": epochs, "batch_verifications": int(cnt_all[0]),
                  "grouping_rate": rate_same, "same_length_batches": int(cnt_all[1]),
                  "fallback_members": int(cnt_all[3]), "planned_batches_K4": int(cnt_all[5]),
+                 "patience": args.pool_patience if args.pool_mode == "epoch" else 0,
+                 "deferred_member_epochs": int(counters[7].item()),
                  "mean_batch": (int(cnt_all[2]) + int(cnt_all[3])) / max(1, int(cnt_all[0])),
                  "kv_bytes_moved_rank0": moved, "gather_ms": gather_ms,
                  "reps_drain_ms": reps if len(reps) > 1 else None,

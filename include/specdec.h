@@ -271,7 +271,7 @@ int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtype, int64_t 
  *   d_bsize, d_bkind, d_blen [W]; d_n_batches [1];
  *   d_counters [8] int64, ACCUMULATED (+=): {batches, same-length batches, members in
  *   same-length batches, members in fallback batches, fallback member tokens, window
- *   size, distinct lengths, 0}.
+ *   size, distinct lengths, deferred members (always 0 here; see _deferred)}.
  * Limits: 1 <= W <= 2048, 1 <= B <= W, 1 <= min_group; d_len values >= 1.
  */
 int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order,
@@ -281,6 +281,29 @@ int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active, const int3
                        uint8_t *d_mactive, int32_t *d_bsize, uint8_t *d_bkind,
                        int32_t *d_blen, int32_t *d_n_batches, int64_t *d_counters,
                        specdec_stream_t stream);
+
+/* specdec_pool_group_deferred -- the epoch plan with deferred fallback (reading R27;
+ * GetBatch "attempts to form batches of identical length" and falls
+ * back to unpad-repad only when it cannot).  specdec_pool_group's plan, except: when its
+ * group pass formed at least one same-length batch and patience > 0, a leftover s with
+ * d_wait[s] < patience is deferred -- in the window (d_window), in no batch (d_batch_of[s]
+ * = d_slot_of[s] = -1) -- and only the leftovers with d_wait[s] >= patience, in window
+ * order, fill the fallback batches of B (numbered after the same-length ones).  With no
+ * same-length batch every leftover runs, so a non-empty window always plans >= 1 batch.
+ * d_wait [N] int32 (caller-owned, zeroed at admission) is updated in place: 0 for every
+ * planned member, +1 for every deferred one, untouched outside the window; a member is
+ * thus deferred at most `patience` epochs in a row.  d_counters[7] += deferred members.
+ * patience == 0 is specdec_pool_group exactly (d_wait may then be NULL; if given, its
+ * window entries are zeroed).  Errors: as specdec_pool_group; SPECDEC_ERR_ARG for
+ * patience < 0, or patience > 0 with d_wait NULL.
+ */
+int specdec_pool_group_deferred(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order,
+                                int32_t N, int32_t W, int32_t B, int32_t min_group, int32_t *d_wait,
+                                int32_t patience, int32_t *d_window, int32_t *d_window_size,
+                                int32_t *d_batch_of, int32_t *d_slot_of, int32_t *d_members,
+                                int32_t *d_mlen, int32_t *d_mpad, uint8_t *d_mactive, int32_t *d_bsize,
+                                uint8_t *d_bkind, int32_t *d_blen, int32_t *d_n_batches,
+                                int64_t *d_counters, specdec_stream_t stream);
 
 /* specdec_pool_getbatch -- Alg. 3's GetBatch(Window, B) as printed (ONE batch
  * per iteration): batch 0 of the specdec_pool_group plan, without planning the others.
@@ -493,6 +516,12 @@ typedef struct specdec_pool_desc {
      * n_staging cudaEvent_t (timing disabled). */
     specdec_stream_t scatter_stream;
     void *const *scatter_events;
+    /* deferred fallback (R27): patience > 0 plans each epoch with
+     * specdec_pool_group_deferred on `wait` (device [N] int32, zeroed at admission);
+     * 0 = specdec_pool_group.  Alg. 3 as printed (max_batches 1, specdec_pool_alg3) is
+     * unaffected: its GetBatch already falls back only when no group qualifies. */
+    int32_t *wait;
+    int32_t patience;
 } specdec_pool_desc;
 
 int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,

@@ -47,6 +47,8 @@ _SIGS = {
                             ctypes.c_size_t, _P, _P, _P], _INT),
     "specdec_pool_group": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                             _P, _P, _P, _P, _P, _P], _INT),
+    "specdec_pool_group_deferred": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P,
+                                     _P, _P, _P, _P, _P, _P, _P, _P, _P], _INT),
     "specdec_pool_getbatch": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                                _P, _P, _P, _P, _P, _P], _INT),
     "specdec_pool_writeback": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
@@ -92,6 +94,7 @@ class PoolDesc(ctypes.Structure):
         ("gather_ws", _P),
         ("verify_group", _I32), ("host_launches", _P),
         ("scatter_stream", _P), ("scatter_events", _P),
+        ("wait", _P), ("patience", _I32),
     ]
 
 
@@ -372,6 +375,17 @@ def specdec_pool_group(length, active, order, W, B, min_group, window, window_si
         _ptr(window_size), _ptr(batch_of), _ptr(slot_of), _ptr(members), _ptr(mlen), _ptr(mpad),
         _ptr(mactive), _ptr(bsize), _ptr(bkind), _ptr(blen), _ptr(n_batches), _ptr(counters),
         _stream(stream)), "specdec_pool_group")
+
+
+def specdec_pool_group_deferred(length, active, order, W, B, min_group, wait, patience, window,
+                                window_size, batch_of, slot_of, members, mlen, mpad, mactive, bsize,
+                                bkind, blen, n_batches, counters, *, stream=None):
+    """The epoch plan with deferred fallback (R27; include/specdec.h); `wait` is updated."""
+    _check(load().specdec_pool_group_deferred(
+        _ptr(length), _ptr(active), _ptr(order), length.numel(), W, B, min_group, _ptr(wait), patience,
+        _ptr(window), _ptr(window_size), _ptr(batch_of), _ptr(slot_of), _ptr(members), _ptr(mlen),
+        _ptr(mpad), _ptr(mactive), _ptr(bsize), _ptr(bkind), _ptr(blen), _ptr(n_batches),
+        _ptr(counters), _stream(stream)), "specdec_pool_group_deferred")
 
 
 def specdec_pool_getbatch(length, active, order, W, B, min_group, window, window_size, batch_of,

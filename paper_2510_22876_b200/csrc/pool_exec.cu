@@ -42,10 +42,17 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
                 return SPECDEC_ERR_ARG;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int32_t W = d->W, B = d->B;
-    int rc = specdec_pool_group(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
-                                d->window_size, d->batch_of, d->slot_of, d->members, d->mlen,
-                                d->mpad, d->mactive, d->bsize, d->bkind, d->blen, d->n_batches,
-                                d->counters, stream);
+    // the epoch plan: R11's whole-window plan, or with d->patience > 0 the deferred-fallback
+    // plan (R27: leftovers wait up to `patience` epochs for a same-length partner)
+    int rc = d->patience > 0
+        ? specdec_pool_group_deferred(d->len, d->active, d->order, d->N, W, B, d->min_group, d->wait,
+                                      d->patience, d->window, d->window_size, d->batch_of, d->slot_of,
+                                      d->members, d->mlen, d->mpad, d->mactive, d->bsize, d->bkind, d->blen,
+                                      d->n_batches, d->counters, stream)
+        : specdec_pool_group(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,
+                             d->window_size, d->batch_of, d->slot_of, d->members, d->mlen,
+                             d->mpad, d->mactive, d->bsize, d->bkind, d->blen, d->n_batches,
+                             d->counters, stream);
     if (rc) return rc;
     // plan header -> pinned host: n_batches, kind, width, size (W each)
     int32_t *hh = d->host_header;

@@ -24,11 +24,18 @@ struct Alg3Gate {
     unsigned long long cond = 0, cond2 = 0;
 };
 
+// Deferred fallback (reading R27, specdec_pool_group_deferred): wait[N] epochs each sequence
+// has sat out; patience <= 0 or wait == nullptr: the R11 plan.
+struct PoolDefer {
+    int32_t *wait = nullptr;
+    int32_t patience = 0;
+};
+
 int pool_group_launch(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order, int32_t N,
                       int32_t W, int32_t B, int32_t min_group, int32_t *d_window, int32_t *d_window_size,
                       int32_t *d_batch_of, int32_t *d_slot_of, int32_t *d_members, int32_t *d_mlen,
                       int32_t *d_mpad, uint8_t *d_mactive, int32_t *d_bsize, uint8_t *d_bkind,
                       int32_t *d_blen, int32_t *d_n_batches, int64_t *d_counters, const Alg3Gate &gate,
-                      specdec_stream_t stream, bool one_batch = false);
+                      specdec_stream_t stream, bool one_batch = false, const PoolDefer &defer = PoolDefer{});
 
 }  // namespace specdec

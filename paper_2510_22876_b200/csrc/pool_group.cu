@@ -10,7 +10,9 @@
 //   3. groups ordered by (-count, length) -- a second bitonic sort over the group keys;
 //      each group yields same-length batches of min(B, remaining) while remaining >=
 //      min_group; group offsets by an exclusive scan in that order;
-//   4. leftovers keep window order (block scan) and fill fallback batches of B.
+//   4. leftovers keep window order (block scan) and fill fallback batches of B -- with
+//      deferred fallback (R27, specdec_pool_group_deferred) only those whose wait reached
+//      the patience, when step 3 formed any same-length batch; the others sit out.
 // Every step is a deterministic function of the inputs, so the plan is bit-identical to
 // the oracle's (tests/test_gpu_pool.py).
 #include <cuda_runtime.h>
@@ -246,7 +248,8 @@ __device__ int refill_window(PoolSmem &sm, const int32_t *len, const uint8_t *ac
 __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, int32_t *window,
                           int32_t *window_size, int32_t *batch_of, int32_t *slot_of, int32_t *members,
                           int32_t *mlen, int32_t *mpad, uint8_t *mactive, int32_t *bsize, uint8_t *bkind,
-                          int32_t *blen, int32_t *n_batches, int64_t *counters, const Alg3Gate &gate, int exp) {
+                          int32_t *blen, int32_t *n_batches, int64_t *counters, const Alg3Gate &gate, int exp,
+                          const PoolDefer &defer) {
     const int tid = threadIdx.x;
     const int T = blockDim.x;
     if (exp == 1) return;  // timing probe only (SPECDEC_K4_EXP): up to RefillWindow
@@ -342,19 +345,25 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
     }
     const int tot_same = run;
     __syncthreads();
-    // ---- 4. place members: same-length slots, then leftovers in window order
-    int n_left = 0;
+    // ---- 4. place members: same-length slots, then leftovers in window order.  R27: when
+    // step 3 formed a same-length batch, a leftover whose wait is below the patience sits
+    // this epoch out (flat slot -1); the waits are updated here (one CTA: no race).
+    const bool deferring = defer.wait != nullptr && defer.patience > 0 && tot_same > 0;
+    int n_left = 0, n_deferred = 0;
     for (int base = 0; base < Wn; base += T) {
         const int w = base + tid;
-        int unmatched = 0, bi = -1, sl = -1;
+        int unmatched = 0, bi = -1, sl = -1, deferred = 0;
         if (w < Wn) {
             const int g = sm.grp[w], r = sm.rank[w];
             if (r < sm.matched[g]) {
                 bi = sm.gbase[g] + r / B;
                 sl = r % B;
+            } else if (deferring && defer.wait[sm.wid[w]] < defer.patience) {
+                deferred = 1;
             } else {
                 unmatched = 1;
             }
+            if (defer.wait) defer.wait[sm.wid[w]] = deferred ? defer.wait[sm.wid[w]] + 1 : 0;
         }
         int tot;
         const int ui = n_left + block_exclusive_scan(unmatched, sm.warp, tot);
@@ -362,8 +371,9 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
             bi = tot_same + ui / B;
             sl = ui % B;
         }
-        if (w < Wn) sm.rank[w] = bi * B + sl;  // reuse: flat slot index
+        if (w < Wn) sm.rank[w] = deferred ? -1 : bi * B + sl;  // reuse: flat slot index
         n_left += tot;
+        n_deferred += __syncthreads_count(deferred);
     }
     const int nb_total = tot_same + (n_left + B - 1) / B;
     if (exp == 4) return;  // probe: + member placement scans
@@ -381,6 +391,8 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
     __syncthreads();
     for (int w = tid; w < Wn; w += T) {
         const int flat = sm.rank[w], b = flat / B, l = sm.wlen[w], s = sm.wid[w];
+        window[w] = s;
+        if (flat < 0) continue;  // deferred (R27): in the window, in no batch
         atomicMax(&sm.bmax[b], l);
         atomicMin(&sm.bmin[b], l);
         atomicAdd(&sm.bcnt[b], 1);
@@ -389,12 +401,12 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
         mactive[flat] = 1;
         batch_of[s] = b;
         slot_of[s] = flat % B;
-        window[w] = s;
     }
     __syncthreads();
     long long lsame = 0, lsame_m = 0, lfb_m = 0, lfb_tok = 0;
     for (int w = tid; w < Wn; w += T) {
         const int flat = sm.rank[w], b = flat / B;
+        if (flat < 0) continue;
         mpad[flat] = sm.bmax[b] - sm.wlen[w];
         if (sm.bmax[b] == sm.bmin[b]) {
             ++lsame_m;
@@ -411,7 +423,8 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
         lsame += same;
     }
     // counters (accumulated): batches, same-length batches, members in same-length
-    // batches, members in fallback batches, fallback member tokens, window size, groups
+    // batches, members in fallback batches, fallback member tokens, window size, groups,
+    // deferred members (R27)
     if (lsame) atomicAdd(reinterpret_cast<unsigned long long *>(counters + 1), static_cast<unsigned long long>(lsame));
     if (lsame_m) atomicAdd(reinterpret_cast<unsigned long long *>(counters + 2), static_cast<unsigned long long>(lsame_m));
     if (lfb_m) atomicAdd(reinterpret_cast<unsigned long long *>(counters + 3), static_cast<unsigned long long>(lfb_m));
@@ -422,6 +435,8 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
         atomicAdd(reinterpret_cast<unsigned long long *>(counters + 0), static_cast<unsigned long long>(nb_total));
         atomicAdd(reinterpret_cast<unsigned long long *>(counters + 5), static_cast<unsigned long long>(Wn));
         atomicAdd(reinterpret_cast<unsigned long long *>(counters + 6), static_cast<unsigned long long>(n_groups));
+        if (n_deferred)
+            atomicAdd(reinterpret_cast<unsigned long long *>(counters + 7), static_cast<unsigned long long>(n_deferred));
     }
     if (gate.members) {
         // Alg. 3 device loop: batch 0 as the row maps of this iteration's gather / verify /
@@ -461,7 +476,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     int32_t B, int32_t min_group, int32_t *window, int32_t *window_size, int32_t *batch_of,
     int32_t *slot_of, int32_t *members, int32_t *mlen, int32_t *mpad, uint8_t *mactive,
     int32_t *bsize, uint8_t *bkind, int32_t *blen, int32_t *n_batches, int64_t *counters, Alg3Gate gate,
-    int exp) {
+    int exp, PoolDefer defer) {
     pdl_wait();
     pdl_launch_dependents();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -472,7 +487,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
     }
     const int Wn = refill_window(sm, len, active, order, N, W);
     plan_full(sm, Wn, B, min_group, window, window_size, batch_of, slot_of, members, mlen, mpad, mactive, bsize,
-              bkind, blen, n_batches, counters, gate, exp);
+              bkind, blen, n_batches, counters, gate, exp, defer);
 }
 
 // ---- Alg. 3's GetBatch as printed (one batch per iteration): batch 0 of the
@@ -529,7 +544,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_getbatch_kernel(
     const int Lmin = -block_reduce_max(-lo, sm.warp);
     if (Wn > 0 && (Lmin < 0 || static_cast<int64_t>(Lmax) - Lmin >= kHistBins)) {
         plan_full(sm, Wn, B, min_group, window, window_size, batch_of, slot_of, members, mlen, mpad, mactive,
-                  bsize, bkind, blen, n_batches, counters, gate, 0);
+                  bsize, bkind, blen, n_batches, counters, gate, 0, PoolDefer{});
         return;
     }
     const int R = Wn > 0 ? Lmax - Lmin + 1 : 0;
@@ -656,6 +671,24 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
                              d_n_batches, d_counters, Alg3Gate{}, stream);
 }
 
+extern "C" int specdec_pool_group_deferred(const int32_t *d_len, const uint8_t *d_active,
+                                           const int32_t *d_order, int32_t N, int32_t W, int32_t B,
+                                           int32_t min_group, int32_t *d_wait, int32_t patience,
+                                           int32_t *d_window, int32_t *d_window_size,
+                                           int32_t *d_batch_of, int32_t *d_slot_of, int32_t *d_members,
+                                           int32_t *d_mlen, int32_t *d_mpad, uint8_t *d_mactive,
+                                           int32_t *d_bsize, uint8_t *d_bkind, int32_t *d_blen,
+                                           int32_t *d_n_batches, int64_t *d_counters,
+                                           specdec_stream_t stream) {
+    if (patience < 0 || (patience > 0 && !d_wait)) return SPECDEC_ERR_ARG;
+    PoolDefer defer;
+    defer.wait = d_wait;
+    defer.patience = patience;
+    return pool_group_launch(d_len, d_active, d_order, N, W, B, min_group, d_window, d_window_size, d_batch_of,
+                             d_slot_of, d_members, d_mlen, d_mpad, d_mactive, d_bsize, d_bkind, d_blen,
+                             d_n_batches, d_counters, Alg3Gate{}, stream, false, defer);
+}
+
 extern "C" int specdec_pool_getbatch(const int32_t *d_len, const uint8_t *d_active,
                                      const int32_t *d_order, int32_t N, int32_t W, int32_t B,
                                      int32_t min_group, int32_t *d_window, int32_t *d_window_size,
@@ -675,7 +708,7 @@ int specdec::pool_group_launch(const int32_t *d_len, const uint8_t *d_active, co
                                int32_t *d_members, int32_t *d_mlen, int32_t *d_mpad, uint8_t *d_mactive,
                                int32_t *d_bsize, uint8_t *d_bkind, int32_t *d_blen, int32_t *d_n_batches,
                                int64_t *d_counters, const Alg3Gate &gate, specdec_stream_t stream,
-                               bool one_batch) {
+                               bool one_batch, const PoolDefer &defer) {
     if (N < 1 || W < 1 || W > kPoolMaxW || B < 1 || B > W) return SPECDEC_ERR_SHAPE;
     if (min_group < 1) return SPECDEC_ERR_ARG;
     if (!d_len || !d_active || !d_order || !d_window || !d_window_size || !d_batch_of ||
@@ -706,5 +739,5 @@ int specdec::pool_group_launch(const int32_t *d_len, const uint8_t *d_active, co
     return launch_k(pool_group_kernel, dim3(1), dim3(threads), smem,
                     reinterpret_cast<cudaStream_t>(stream), d_len, d_active, d_order, N, W, B,
                     min_group, d_window, d_window_size, d_batch_of, d_slot_of, d_members, d_mlen,
-                    d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches, d_counters, gate, exp);
+                    d_mpad, d_mactive, d_bsize, d_bkind, d_blen, d_n_batches, d_counters, gate, exp, defer);
 }

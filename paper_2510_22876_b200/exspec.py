@@ -29,7 +29,8 @@ from .eqspec import TORCH_DT
 class SequencePool:
     def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
                  max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True,
-                 dense_consumer=False, n_staging=1, consumer=None, verify_group=8, scatter_stream=False):
+                 dense_consumer=False, n_staging=1, consumer=None, verify_group=8, scatter_stream=False,
+                 patience=0):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         if B > W:
@@ -37,6 +38,11 @@ class SequencePool:
         self.N, self.cap, self.layers, self.H, self.D, self.k = N, cap, layers, H, D, k
         self.n_planes = 2 * layers
         self.W, self.B, self.min_group = W, B, min_group
+        # deferred fallback (R27): an epoch's leftovers wait up to `patience` epochs for a
+        # same-length partner (specdec_pool_group_deferred); 0 = the R11 plan
+        if patience < 0:
+            raise ValueError("patience must be >= 0")
+        self.patience = int(patience)
         self.max_new, self.eos_id, self.pad_id = max_new, eos_id, pad_id
         self.device = dev
         # the consumer of a batch's KV (specdec_pool_desc::dense_consumer): "zero-copy"
@@ -55,6 +61,7 @@ class SequencePool:
         self.gen = torch.zeros(N, dtype=i32, device=dev)
         self.active = torch.zeros(N, dtype=u8, device=dev)
         self.order = torch.arange(N, dtype=i32, device=dev)
+        self.wait = torch.zeros(N, dtype=i32, device=dev)      # R27: epochs sat out
         self.tokens = torch.full((N, self.cap_tok), pad_id, dtype=i64, device=dev)
         self.out_buf = torch.zeros((N, max_new), dtype=i64, device=dev)
         alloc = torch.zeros if kv_init else torch.empty
@@ -110,6 +117,7 @@ class SequencePool:
         tokens [N, cap_tok], admission order (default by id) and KV."""
         self.len.copy_(torch.as_tensor(np.asarray(prompts_lens), dtype=torch.int32))
         self.gen.zero_()
+        self.wait.zero_()
         self.active.fill_(1)
         if order is not None:
             self.order.copy_(torch.as_tensor(np.asarray(order), dtype=torch.int32))
@@ -136,10 +144,17 @@ class SequencePool:
     def plan(self, stream=None):
         """K4 over the window; returns the host copy of the plan header
         (n_batches, kinds, widths, sizes) -- the epoch's single device->host sync."""
-        _abi.specdec_pool_group(self.len, self.active, self.order, self.W, self.B, self.min_group,
-                                self.window, self.window_size, self.batch_of, self.slot_of,
-                                self.members, self.mlen, self.mpad, self.mactive, self.bsize,
-                                self.bkind, self.blen, self.n_batches, self.counters, stream=stream)
+        if self.patience > 0:
+            _abi.specdec_pool_group_deferred(self.len, self.active, self.order, self.W, self.B, self.min_group,
+                                             self.wait, self.patience, self.window, self.window_size,
+                                             self.batch_of, self.slot_of, self.members, self.mlen, self.mpad,
+                                             self.mactive, self.bsize, self.bkind, self.blen, self.n_batches,
+                                             self.counters, stream=stream)
+        else:
+            _abi.specdec_pool_group(self.len, self.active, self.order, self.W, self.B, self.min_group,
+                                    self.window, self.window_size, self.batch_of, self.slot_of,
+                                    self.members, self.mlen, self.mpad, self.mactive, self.bsize,
+                                    self.bkind, self.blen, self.n_batches, self.counters, stream=stream)
         W = self.W
         hdr = self._pinned
         # the copies are ordered after K4 on the stream it ran on, and that stream is the one
@@ -270,6 +285,7 @@ class SequencePool:
         d.ring_n = len(ring)
         d.ring_pos = ctypes.addressof(self._ring_pos)
         d.dense_consumer = {"zero-copy": 0, "dense": 1, "slot": 2}[self.consumer]
+        d.wait, d.patience = self.wait.data_ptr(), self.patience
         # the gathers take K2 work tickets (SPECDEC_DYNAMIC) from a zeroed 128-byte header
         self._gather_ws = torch.zeros(128, dtype=torch.uint8, device=self.device)
         d.gather_ws = self._gather_ws.data_ptr()

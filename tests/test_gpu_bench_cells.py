@@ -173,7 +173,8 @@ def _pool_cell(cuda, cli, seqs_checked=16):
     sp = SequencePool(n_loc, cap, sh.layers, sh.H, sh.D, k, W=Wn, B=Bp, min_group=args.min_group,
                       max_new=args.max_new, device=cuda, kv_init=False,
                       dense_consumer=args.pool_consumer == "dense",
-                      n_staging=args.pool_staging if args.pool_exec == "native" else 1)
+                      n_staging=args.pool_staging if args.pool_exec == "native" else 1,
+                      patience=args.pool_patience)
     local_lens = lens[mine]
     local_order = np.arange(n_loc)
     seed = args.seed
@@ -212,11 +213,17 @@ def _pool_cell(cuda, cli, seqs_checked=16):
                 break
             oracle_batch(plan["batches"][0], plan["blen"][0], (ring_pos + it) % bench.RING)
     else:
-        plan = OP.form_batches(o_len, o_act, local_order, Wn, Bp, args.min_group)
-        ran = sp.epoch_native()[0]
-        assert ran == len(plan["batches"])
-        for b, mem in enumerate(plan["batches"]):
-            oracle_batch(mem, plan["blen"][b], (ring_pos + b) % bench.RING)
+        # with deferred fallback (R27) the waits matter from the second epoch on: 4 epochs
+        o_wait = np.zeros(n_loc, np.int64)
+        for _ in range(4 if args.pool_patience > 0 else 1):
+            plan = OP.form_batches_deferred(o_len, o_act, local_order, Wn, Bp, args.min_group, o_wait,
+                                            args.pool_patience)
+            ran = sp.epoch_native()[0]
+            assert ran == len(plan["batches"])
+            for b, mem in enumerate(plan["batches"]):
+                oracle_batch(mem, plan["blen"][b], (ring_pos + b) % bench.RING)
+            ring_pos += ran
+        assert np.array_equal(sp.wait.cpu().numpy(), o_wait)
     torch.cuda.synchronize()
     tag = str(cli)
     assert np.array_equal(sp.len.cpu().numpy(), o_len), tag

@@ -141,3 +141,26 @@ def test_pool_getbatch_brute_force(cuda):
                     _check_getbatch(g, OP.form_batches(lens, [1] * Wn, order, Wn, B, mg), lens, B)
                     cnt += 1
     assert cnt > 10_000
+
+
+def test_pool_group_deferred_brute_force(cuda):
+    """The deferred-fallback plan (R27) on every window of W <= 6 sequences with lengths in
+    {1, 2, 3}, every B <= W, min_group in {1, 2, B}, patience 1 and 2, seeded waits in
+    {0, 1, 2}: plan, deferred members and updated waits == the oracle's."""
+    from tests.test_gpu_pool import _check_deferred, _plan_gpu_deferred
+    cnt = 0
+    for Wn in range(1, 7):
+        for lens in itertools.product((1, 2, 3), repeat=Wn):
+            lens = list(lens)
+            order = list(range(Wn))
+            rng = np.random.default_rng(sum(l * 3 ** i for i, l in enumerate(lens)) + 7 * Wn)
+            for B in range(1, Wn + 1):
+                for mg in sorted({1, 2, B}):
+                    for patience in (1, 2):
+                        wait = rng.integers(0, 3, Wn).astype(np.int64)
+                        g = _plan_gpu_deferred(cuda, lens, [1] * Wn, order, Wn, B, mg, wait, patience)
+                        o_wait = wait.copy()
+                        o = OP.form_batches_deferred(lens, [1] * Wn, order, Wn, B, mg, o_wait, patience)
+                        _check_deferred(g, o, lens, B, o_wait)
+                        cnt += 1
+    assert cnt > 10_000

@@ -36,6 +36,13 @@ POOL = (
     + [(f"P N1024 W{w}", ["--config", "pool", "--pool-W", str(w)]) for w in (8, 16, 32)]
     + [("P N1024 min_group 8", ["--config", "pool", "--min-group", "8"]),
        ("P N1024 alg3", ["--config", "pool", "--pool-mode", "alg3"]),
+       # the epoch plan: R11's full plan (patience 0) and deferred fallback (R27; default 2)
+       ("P N1024 patience 0", ["--config", "pool", "--pool-patience", "0"]),
+       ("P N1024 patience 1", ["--config", "pool", "--pool-patience", "1"]),
+       ("P N1024 patience 4", ["--config", "pool", "--pool-patience", "4"]),
+       ("P N1024 W32 patience 0", ["--config", "pool", "--pool-W", "32", "--pool-patience", "0"]),
+       ("P N1024 emulated x8 patience 0", ["--config", "pool", "--emulate-ranks", "8", "--pool-patience", "0"]),
+       ("P N1024 emulated x8 patience 1", ["--config", "pool", "--emulate-ranks", "8", "--pool-patience", "1"]),
        ("P N1024 dense consumer", ["--config", "pool", "--pool-consumer", "dense"]),
        ("P N1024 slot consumer", ["--config", "pool", "--pool-consumer", "slot"]),
        ("P N1024 serial executor", ["--config", "pool", "--pool-staging", "1"]),
