@@ -47,6 +47,28 @@ bool pdl_enabled() {
     return on != 0 && g_pdl_suppress == 0;
 }
 
+// SPECDEC_CARVEOUT (percent of the unified L1 / shared-memory array given to shared memory,
+// 0-100; unset or < 0: the driver's per-kernel default): every specdec kernel gets the same
+// preferred carveout, so an SM switching between them (K1 -> K3 -> K2 of a round, K2's
+// ~200 KB of shared memory) need not be reconfigured between kernels.
+void ensure_carveout(const void *fn) {
+    static int pct = -2;
+    static std::mutex mu;
+    static const void *done[128];
+    static int n_done = 0;
+    if (pct == -2) {
+        const char *e = getenv("SPECDEC_CARVEOUT");
+        pct = e ? atoi(e) : -1;
+    }
+    if (pct < 0) return;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < n_done; ++i)
+        if (done[i] == fn) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+    cudaGetLastError();
+    if (n_done < 128) done[n_done++] = fn;
+}
+
 }  // namespace specdec
 
 extern "C" int specdec_version(void) { return 121; }  // 1.21: specdec_batch_init

@@ -32,6 +32,7 @@ inline int check_launch() {
 bool pdl_enabled();  // SPECDEC_PDL (default on), unless suppressed on this thread
 void pdl_suppress(bool on);             // nestable: launches on this thread without PDL
 int annotate_error(int rc, const char *where);  // prefixes the last CUDA error message
+void ensure_carveout(const void *fn);   // SPECDEC_CARVEOUT: one shared-memory carveout for all kernels
 
 // Launch with the programmatic-stream-serialization attribute (PDL) when enabled; the
 // kernels call pdl_wait() before reading anything a predecessor may write.
@@ -48,6 +49,7 @@ int launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    ensure_carveout(reinterpret_cast<const void *>(kernel));
     cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
     return e == cudaSuccess ? SPECDEC_OK : record_cuda_error(e);
 }
