@@ -62,6 +62,7 @@ struct RealignParams {
     char *ws;         // boundary slots (in-place segmentation), or null
     int64_t ws_slots;
     int64_t seg_bytes;  // >= kSegBytes (the workspace is sized for kSegBytes)
+    int64_t seg_rows;   // max(1, seg_bytes / rb), computed on the host
     unsigned long long *moved;
     uint32_t *status;
 };
@@ -103,7 +104,7 @@ __device__ __forceinline__ bool row_geom(const RealignParams &p, int r, RowGeom 
 // Segments of one slab.  In place, a slab is segmented only when a slot can hold its
 // boundary rows (and a workspace exists); distinct buffers never have boundaries.
 __device__ __forceinline__ int64_t seg_rows(const RealignParams &p) {
-    return imax64(1, p.seg_bytes / p.rb);
+    return p.seg_rows;
 }
 __device__ __forceinline__ int64_t n_segments(const RealignParams &p, const RowGeom &g) {
     const int64_t sr = seg_rows(p);
@@ -215,13 +216,18 @@ __device__ void build_table(const RealignParams &p, UnitTable &t, bool report) {
 // unit index -> (plane, moving row, head, segment); the row is the fastest index, so the
 // units processed together (one grid-wide round, below) lie in one contiguous span of
 // planes -- measured 5-7 % faster than the row as the slowest index (tools/kbench.py).
+// 32-bit divisions: a unit index is < 2^32 (the host checks the bound), and 64-bit ones
+// cost the single issuing lane hundreds of cycles per unit -- time in which it issues no
+// copy (kbench: small out-of-place slabs ran at 0.64 of the copy peak).
 __device__ __forceinline__ void locate(const RealignParams &p, const UnitTable &t, int64_t u,
                                       int64_t &plane, int64_t &head, int &mi, int64_t &j) {
-    const int64_t U = t.units_per_ph;
-    plane = u / (p.H * U);
-    const int64_t rem = u % (p.H * U);
+    const uint32_t U = static_cast<uint32_t>(t.units_per_ph);
+    const uint32_t HU = static_cast<uint32_t>(p.H) * U;
+    const uint32_t u32 = static_cast<uint32_t>(u);
+    plane = u32 / HU;
+    const uint32_t rem = u32 - static_cast<uint32_t>(plane) * HU;
     head = rem / U;
-    const int32_t r2 = static_cast<int32_t>(rem % U);
+    const int32_t r2 = static_cast<int32_t>(rem - static_cast<uint32_t>(head) * U);
     int lo = 0, hi = t.n_mv - 1;  // last mi with pre[mi] <= r2
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -363,7 +369,7 @@ __device__ __forceinline__ void iter_unit(const RealignParams &p, const RealignS
     locate(p, sm.t, it.u, plane, head, mi, j);
     RowGeom g;
     unit_geom(p, sm.t, mi, g);
-    make_unit(p, g, plane, head, j, n_segments(p, g), it.un);
+    make_unit(p, g, plane, head, j, sm.t.pre[mi + 1] - sm.t.pre[mi], it.un);  // segments of row mi
     it.q = 0;
     it.nmain = ((it.un.main_hi - it.un.main_lo) * p.rb + CHUNK - 1) / CHUNK;
     it.bnd_left = it.un.b_rows > 0;
@@ -643,6 +649,7 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     if ((flags & SPECDEC_ZERO_PADS) && !inplace) return SPECDEC_ERR_ARG;
     if (count_bound < 0) return SPECDEC_ERR_ARG;
     const int64_t units = max_units_bound(n_planes, n_rows, H, rb, cap_src);
+    if (units >= (int64_t{1} << 32)) return SPECDEC_ERR_SHAPE;  // unit indices are 32-bit on the device
     const bool segmented = (flags & SPECDEC_SEGMENTED) && inplace;
     if ((flags & (SPECDEC_DYNAMIC | SPECDEC_SEGMENTED)) && !d_ws) return SPECDEC_ERR_ARG;
     if (d_ws && (!aligned16(d_ws) ||
@@ -681,6 +688,7 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
     }
     p.policy_mode = pol;
     p.seg_bytes = g_seg_bytes;
+    p.seg_rows = std::max<int64_t>(1, g_seg_bytes / rb);
     if (count_bound > 0 && count_bound * rb <= kSmallBytes) {
         p.ws = nullptr;  // small slabs are never segmented
         p.ws_slots = 0;
