@@ -12,7 +12,7 @@ import numpy as np
 
 from .align import (anchor_plan, build_batch, copy_rows, mask_pos_row, realign_kv, repad_tokens,
                     unpad)
-from .pool import admission_order, form_batches, form_batches_deferred
+from .pool import admission_order, form_batches, form_batches_deferred, mixed_members, pipeline_window_active
 from .toy_lm import ToyLM, greedy_fp32
 from .verify import batch_verify
 
@@ -133,10 +133,12 @@ def eqspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, ca
 
 def exspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, cap, W, B,
                   min_group=2, sort_by_length=True, noise=0.0, pad_id=0, sequential=False,
-                  patience=0):
+                  patience=0, pipeline=False):
     """Alg. 3 over a SequencePool.  Each epoch plans the whole window (K4 semantics);
     with sequential=True only batch 0 runs per iteration (Alg. 3's one-batch GetBatch);
-    patience > 0: the epoch plan defers leftovers (form_batches_deferred, reading R27).
+    patience > 0: the epoch plan defers leftovers (form_batches_deferred, reading R27);
+    pipeline: an epoch's mixed batches run beside the next epoch, whose plan excludes their
+    members (reading R28; results applied at once -- the batches have disjoint members).
     Returns (outputs, stats)."""
     N = len(prompts)
     lens = np.array([len(p) for p in prompts], np.int32)
@@ -152,11 +154,14 @@ def exspec_decode(target: ToyLM, drafter: ToyLM, prompts, k, max_new, eos_id, ca
             target.token_forward(t, c, c, pool_kv[s], ones)
     stats = dict(verify_calls=0, batches=0, same_length=0, realigned_members=0)
     wait = np.zeros(N, np.int64)
+    inflight = []
     while active.any():
+        act_plan = pipeline_window_active(active, inflight) if pipeline else active
         if patience > 0:
-            plan = form_batches_deferred(lens, active, order, W, B, min_group, wait, patience)
+            plan = form_batches_deferred(lens, act_plan, order, W, B, min_group, wait, patience)
         else:
-            plan = form_batches(lens, active, order, W, B, min_group)
+            plan = form_batches(lens, act_plan, order, W, B, min_group)
+        inflight = mixed_members(plan) if pipeline else []
         todo = plan["batches"][:1] if sequential else plan["batches"]
         kinds = plan["kind"][:1] if sequential else plan["kind"]
         for members, kind in zip(todo, kinds):

@@ -5,7 +5,8 @@ Test infrastructure only (see oracle/__init__.py).
 Readings: R11 full-partition plan with a min_group parameter; R12 window =
 first W active sequences in admission order; R13 grouping key = total token length;
 R14 grouping rate = same-length batches / all batches; R27 deferred fallback (an epoch's
-leftovers wait up to `patience` epochs for a same-length partner).
+leftovers wait up to `patience` epochs for a same-length partner); R28 pipelined fallback
+(an epoch's mixed batches run beside the next epoch, whose plan excludes their members).
 """
 from __future__ import annotations
 
@@ -114,6 +115,22 @@ def form_batches_deferred(lens, active, order, W, B, min_group, wait, patience):
                          len(window), len(count), len(deferred)], np.int64)
     return dict(window=window, batches=batches, kind=kind, blen=blen, counters=counters,
                 deferred=deferred)
+
+
+def pipeline_window_active(active, inflight):
+    """Reading R28 (pipelined fallback): the mixed-length (realigned) batches of epoch e run
+    beside epoch e+1, so their members sit out epoch e+1's plan -- for exactly one epoch --
+    and are planned again from epoch e+2 on.  Returns the `active` array epoch e+1 plans
+    with: active and not in epoch e's mixed batches (`inflight`: their ids)."""
+    eff = np.array(active, np.uint8, copy=True)
+    for s in inflight:
+        eff[s] = 0
+    return eff
+
+
+def mixed_members(plan):
+    """The members of a plan's mixed-length batches (kind 0): R28's in-flight set."""
+    return [s for b, kd in zip(plan["batches"], plan["kind"]) if not kd for s in b]
 
 
 def writeback(pool_len, pool_gen, pool_active, pool_tokens, out_buf, members, E_rows, finished):

@@ -214,3 +214,27 @@ def test_exspec_deferred_equals_autoregressive_greedy(patience, W, B):
     out, st = exspec_decode(T, T, prompts, 4, 14, 1, 64, W=W, B=B, min_group=2, noise=0.3,
                             patience=patience)
     assert out == ref
+
+
+@pytest.mark.parametrize("patience,W,B", [(0, 6, 2), (2, 6, 3), (1, 7, 2)])
+def test_exspec_pipelined_equals_autoregressive_greedy(patience, W, B):
+    """R28: running an epoch's mixed batches beside the next epoch (their members out of
+    that epoch's plan) changes when a sequence is verified, never what it emits."""
+    T = ToyLM(seed=7)
+    rng = np.random.default_rng(patience * 100 + W * 10 + B)
+    prompts = [list(map(int, rng.integers(2, 32, size=int(l)))) for l in rng.integers(1, 12, 8)]
+    ref = [T.greedy_generate(p, 14, 1, 64) for p in prompts]
+    out, st = exspec_decode(T, T, prompts, 4, 14, 1, 64, W=W, B=B, min_group=2, noise=0.3,
+                            patience=patience, pipeline=True)
+    assert out == ref
+
+
+def test_pipeline_window_excludes_exactly_the_previous_mixed_members():
+    """R28 by hand: epoch e's mixed batch [0, 2] (lengths 5, 4) keeps 0 and 2 out of epoch
+    e+1's window; the same-length batch [1, 3] does not."""
+    from oracle.pool import mixed_members, pipeline_window_active
+    plan = form_batches([5, 6, 4, 6], [1] * 4, [0, 1, 2, 3], 4, 2, 2)
+    assert plan["batches"] == [[1, 3], [0, 2]] and plan["kind"] == [1, 0]
+    assert mixed_members(plan) == [0, 2]
+    assert pipeline_window_active([1, 1, 1, 1], mixed_members(plan)).tolist() == [0, 1, 0, 1]
+    assert pipeline_window_active([1, 0, 1, 1], []).tolist() == [1, 0, 1, 1]
