@@ -79,6 +79,9 @@ def parse(argv=None):
                     help="pool epoch plan: leftovers wait up to P epochs for a same-length partner before "
                          "a fallback batch (reading R27, specdec_pool_group_deferred); 0 = R11's full plan "
                          "(N=1024: 3003 seq/s at P=0, 7428 at P=2)")
+    ap.add_argument("--pool-pipeline", type=int, default=0,
+                    help="pool epoch mode, native executor: a plan's mixed batches run on the copy stream beside "
+                         "the next plan, which leaves their members out (reading R28)")
     ap.add_argument("--pool-mode", default="epoch", choices=["epoch", "alg3"],
                     help="epoch: run every batch of the window plan; alg3: batch 0 then re-plan")
     ap.add_argument("--B", type=int, default=0, help="override batch size")
@@ -650,6 +653,8 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
     Wn = min(args.pool_W or N, 2048, N)
     o_len, gen, act = lens.astype(np.int64), np.zeros(N, np.int64), np.ones(N, np.uint8)
     wait = np.zeros(N, np.int64)          # R27 (epoch mode with --pool-patience)
+    pipe = bool(args.pool_pipeline) and args.pool_mode != "alg3"
+    inflight = []                         # R28 (--pool-pipeline): the last plan's mixed members
     truth = [W.gen_round_truth(args.seed, r, B, k, V, args.pattern, alpha=args.alpha) for r in range(RING)]
     t_plan = 0.0
     n_batches = n_same = same_members = fb_members = 0
@@ -658,11 +663,17 @@ def oracle_pool_sample(args, verify_samples=2, threads=1):
     slot = args.pool_consumer == "slot"
     while act.any():
         t0 = time.perf_counter()
+        act_plan = OP.pipeline_window_active(act, inflight) if pipe else act
         if args.pool_patience > 0 and args.pool_mode != "alg3":
-            plan = OP.form_batches_deferred(o_len, act, order, Wn, B, args.min_group, wait, args.pool_patience)
+            plan = OP.form_batches_deferred(o_len, act_plan, order, Wn, B, args.min_group, wait, args.pool_patience)
         else:
-            plan = OP.form_batches(o_len, act, order, Wn, B, args.min_group)
+            plan = OP.form_batches(o_len, act_plan, order, Wn, B, args.min_group)
         t_plan += time.perf_counter() - t0
+        if pipe:
+            if not plan["batches"]:       # every active member in flight: they finish, then re-plan
+                inflight = []
+                continue
+            inflight = OP.mixed_members(plan)
         nb = 1 if args.pool_mode == "alg3" else len(plan["batches"])
         for b in range(nb):
             mem = plan["batches"][b]
@@ -759,6 +770,7 @@ def run_pool(args, rank, world, device, emulate=False):
                       min_group=args.min_group, max_new=args.max_new, device=device, kv_init=False,
                       consumer=args.pool_consumer, verify_group=args.pool_verify_group,
                       scatter_stream=bool(args.pool_scatter_stream), patience=args.pool_patience,
+                      pipeline=bool(args.pool_pipeline) and args.pool_mode == "epoch" and args.pool_exec == "native",
                       n_staging=args.pool_staging if args.pool_exec == "native" else 1)
     local_lens = lens[mine]
     local_order = np.arange(n_loc)            # `mine` is already in admission order
@@ -1005,6 +1017,8 @@ def run_pool(args, rank, world, device, emulate=False):
                                f"sort on, {args.shard} shards, EOS off, mode {args.pool_mode}"
                                + (f" (deferred fallback, patience {args.pool_patience})"
                                   if args.pool_patience > 0 and args.pool_mode == "epoch" else "")
+                               + (" (pipelined fallback: mixed batches beside the next plan)"
+                                  if sp.pipeline else "")
                                + f", {args.pool_consumer} consumer, "
                                f"{args.pool_exec} launch loop"
                                + (f", fallback gathers overlapped ({sp.n_staging} staging buffers"

@@ -294,12 +294,21 @@ int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active, const int3
  * planned member, +1 for every deferred one, untouched outside the window; a member is
  * thus deferred at most `patience` epochs in a row.  d_counters[7] += deferred members.
  * patience == 0 is specdec_pool_group exactly (d_wait may then be NULL; if given, its
- * window entries are zeroed).  Errors: as specdec_pool_group; SPECDEC_ERR_ARG for
- * patience < 0, or patience > 0 with d_wait NULL.
+ * window entries are zeroed).
+ * Pipelined fallback (reading R28; both NULL = off): d_epoch [1] int32 counts the plans
+ * made (the call reads e = *d_epoch and stores e + 1); d_fb_epoch [N] int32 (caller-owned,
+ * initialised to a value below -1) is the plan that last put each sequence in a
+ * mixed-length batch.  A sequence with d_fb_epoch[s] == e - 1 is left out of the window:
+ * its mixed batch of the previous plan may still be running (the caller runs mixed
+ * batches beside the next plan); the members of this plan's mixed batches get
+ * d_fb_epoch[s] = e.  d_len / d_active of an excluded sequence are not used.
+ * Errors: as specdec_pool_group; SPECDEC_ERR_ARG for patience < 0, patience > 0 with
+ * d_wait NULL, or exactly one of d_fb_epoch / d_epoch NULL.
  */
 int specdec_pool_group_deferred(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order,
                                 int32_t N, int32_t W, int32_t B, int32_t min_group, int32_t *d_wait,
-                                int32_t patience, int32_t *d_window, int32_t *d_window_size,
+                                int32_t patience, int32_t *d_fb_epoch, int32_t *d_epoch,
+                                int32_t *d_window, int32_t *d_window_size,
                                 int32_t *d_batch_of, int32_t *d_slot_of, int32_t *d_members,
                                 int32_t *d_mlen, int32_t *d_mpad, uint8_t *d_mactive, int32_t *d_bsize,
                                 uint8_t *d_bkind, int32_t *d_blen, int32_t *d_n_batches,
@@ -522,6 +531,27 @@ typedef struct specdec_pool_desc {
      * unaffected: its GetBatch already falls back only when no group qualifies. */
     int32_t *wait;
     int32_t patience;
+    /* pipelined fallback (reading R28), pipeline = 1: each call makes ONE plan
+     * (specdec_pool_group_deferred with fb_epoch / plan_epoch), verifies its same-length
+     * batches on `stream` and runs its mixed-length batches -- gather, verify + write-back,
+     * scatter -- on copy_stream into staging_ring[i % n_staging], returning without waiting
+     * for them; the next plan leaves their members out, the one after waits for them
+     * (pipe_events).  The plan rows alternate between two halves: members / mlen / mpad /
+     * mactive must hold 2W batch rows.  Requires forward == NULL, max_batches <= 0,
+     * dense_consumer == 0, the packed plan header, n_staging >= 1 with staging_ring and
+     * copy_stream, accept_ring.  A call that plans nothing while mixed batches are in flight
+     * waits for them and plans again; a call returning 0 batches leaves the pool drained
+     * and `stream` after every chain.  Results equal the oracle's R28 drain. */
+    int32_t pipeline;
+    int32_t *fb_epoch;     /* device [N], initialised below -1 at admission */
+    int32_t *plan_epoch;   /* device [1], 0 at admission */
+    void *ws2;             /* specdec_verify workspace of the copy stream's verifies */
+    size_t ws2_bytes;
+    int64_t *bonus2;       /* device [B]: their bonus / emit / finished scratch */
+    int32_t *emit2;
+    uint8_t *finished2;
+    void *const *pipe_events; /* host array of 2 cudaEvent_t (timing disabled) */
+    int64_t *pipe_host;    /* host [2]: plans made, mixed batches of the last plan; 0 at admission */
 } specdec_pool_desc;
 
 int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward, void *ctx,

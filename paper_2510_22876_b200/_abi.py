@@ -47,8 +47,8 @@ _SIGS = {
                             ctypes.c_size_t, _P, _P, _P], _INT),
     "specdec_pool_group": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                             _P, _P, _P, _P, _P, _P], _INT),
-    "specdec_pool_group_deferred": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P,
-                                     _P, _P, _P, _P, _P, _P, _P, _P, _P], _INT),
+    "specdec_pool_group_deferred": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
+                                     _P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _INT),
     "specdec_pool_getbatch": ([_P, _P, _P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                                _P, _P, _P, _P, _P, _P], _INT),
     "specdec_pool_writeback": ([_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
@@ -95,6 +95,8 @@ class PoolDesc(ctypes.Structure):
         ("verify_group", _I32), ("host_launches", _P),
         ("scatter_stream", _P), ("scatter_events", _P),
         ("wait", _P), ("patience", _I32),
+        ("pipeline", _I32), ("fb_epoch", _P), ("plan_epoch", _P), ("ws2", _P), ("ws2_bytes", ctypes.c_size_t),
+        ("bonus2", _P), ("emit2", _P), ("finished2", _P), ("pipe_events", _P), ("pipe_host", _P),
     ]
 
 
@@ -379,11 +381,12 @@ def specdec_pool_group(length, active, order, W, B, min_group, window, window_si
 
 def specdec_pool_group_deferred(length, active, order, W, B, min_group, wait, patience, window,
                                 window_size, batch_of, slot_of, members, mlen, mpad, mactive, bsize,
-                                bkind, blen, n_batches, counters, *, stream=None):
-    """The epoch plan with deferred fallback (R27; include/specdec.h); `wait` is updated."""
+                                bkind, blen, n_batches, counters, *, fb_epoch=None, epoch=None, stream=None):
+    """The epoch plan with deferred fallback (R27) and, with fb_epoch / epoch, pipelined
+    fallback (R28) (include/specdec.h); `wait` (and fb_epoch / epoch) are updated."""
     _check(load().specdec_pool_group_deferred(
         _ptr(length), _ptr(active), _ptr(order), length.numel(), W, B, min_group, _ptr(wait), patience,
-        _ptr(window), _ptr(window_size), _ptr(batch_of), _ptr(slot_of), _ptr(members), _ptr(mlen),
+        _ptr(fb_epoch), _ptr(epoch), _ptr(window), _ptr(window_size), _ptr(batch_of), _ptr(slot_of), _ptr(members), _ptr(mlen),
         _ptr(mpad), _ptr(mactive), _ptr(bsize), _ptr(bkind), _ptr(blen), _ptr(n_batches),
         _ptr(counters), _stream(stream)), "specdec_pool_group_deferred")
 

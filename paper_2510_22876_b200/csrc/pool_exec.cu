@@ -26,6 +26,139 @@
 
 using namespace specdec;
 
+// ---- Pipelined fallback (reading R28; specdec_pool_desc.pipeline): one plan per call, its
+// same-length batches verified on `stream` (grouped), its mixed-length batches -- gather,
+// verify + write-back, scatter, in plan order -- on the copy stream, left running when the
+// call returns.  The next plan leaves their members out (K4's fb_epoch stamp), so it need
+// not wait for them; the plan after it waits (pipe_events[parity], recorded after the
+// chain) before their members rejoin.  Plans alternate between two halves of the plan
+// rows (members / mlen / mpad / mactive are [2W][B]), so a running chain's rows are never
+// overwritten by the next plan.  Plan e's rows and pipe_events slot: e % 2 (pipe_host[0]
+// = plans made, pipe_host[1] = mixed batches of the last plan).
+static int pool_epoch_pipelined(const specdec_pool_desc *d, int32_t *h_ran, int32_t *h_same,
+                                int32_t *h_members_same, int32_t *h_members_fallback, specdec_stream_t stream) {
+    const int32_t W = d->W, B = d->B;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(d->copy_stream);
+    auto pev = [&](int64_t e) { return reinterpret_cast<cudaEvent_t>(d->pipe_events[e & 1]); };
+    const int64_t hcd = d->H * d->cap * d->D;
+    const int64_t p_plane = hcd, p_row = d->n_planes * hcd, p_head = d->cap * d->D;
+    const int64_t s_plane = B * hcd, s_row = hcd, s_head = d->cap * d->D;
+    int32_t G = std::min<int32_t>(std::max<int32_t>(d->verify_group, 1), 16);
+    while (G > 1 && specdec_verify_workspace_size(static_cast<int64_t>(G) * B, d->k) > d->ws_bytes) --G;
+    const int kv1 = specdec_verify_kernels(1);
+    int64_t launches = 0;
+    cudaError_t e;
+    int rc;
+    for (;;) {
+        const int64_t ep = d->pipe_host[0];
+        const int64_t off = (ep & 1) * static_cast<int64_t>(W) * B;
+        int32_t *members = d->members + off, *mlen = d->mlen + off, *mpad = d->mpad + off;
+        uint8_t *mactive = d->mactive + off;
+        // the chain of plan ep - 2 used these rows and its members rejoin now
+        if (ep >= 2 && (e = cudaStreamWaitEvent(s, pev(ep), 0)) != cudaSuccess) return record_cuda_error(e);
+        rc = specdec_pool_group_deferred(d->len, d->active, d->order, d->N, W, B, d->min_group, d->wait,
+                                         d->patience, d->fb_epoch, d->plan_epoch, d->window, d->window_size,
+                                         d->batch_of, d->slot_of, members, mlen, mpad, mactive, d->bsize,
+                                         d->bkind, d->blen, d->n_batches, d->counters, stream);
+        if (rc) return rc;
+        ++launches;
+        int32_t *hh = d->host_header;
+        e = cudaMemcpyAsync(hh, d->n_batches, (1 + 3 * static_cast<size_t>(W)) * sizeof(int32_t),
+                            cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return record_cuda_error(e);
+        d->pipe_host[0] = ep + 1;
+        const int32_t nb = hh[0];
+        const uint8_t *kinds = reinterpret_cast<const uint8_t *>(hh + 1);
+        const int32_t *blens = hh + 1 + W, *sizes = hh + 1 + 2 * W;
+        if (nb == 0) {
+            const int64_t prev_mixed = d->pipe_host[1];
+            d->pipe_host[1] = 0;
+            // every active sequence may be in the last plan's mixed batches: let them finish
+            // (this call's plan stamped nobody, so the next one plans them), then plan again;
+            // with none in flight the pool is drained -- the call ends with the copy stream
+            if ((e = cudaEventRecord(pev(ep), cs)) != cudaSuccess || (e = cudaStreamWaitEvent(s, pev(ep), 0)) != cudaSuccess)
+                return record_cuda_error(e);
+            if (prev_mixed > 0) continue;
+            if (d->host_launches) *d->host_launches += launches;
+            if (h_ran) *h_ran = 0;
+            if (h_same) *h_same = 0;
+            if (h_members_same) *h_members_same = 0;
+            if (h_members_fallback) *h_members_fallback = 0;
+            return SPECDEC_OK;
+        }
+        const int32_t ring_base = *d->ring_pos;
+        auto rows = [&](int32_t b) -> int32_t { return sizes[b] > 0 && sizes[b] < B ? sizes[b] : B; };
+        int32_t same = 0, msame = 0, mfb = 0, n_mixed = 0;
+        // same-length batches: grouped verifies on `stream`, in plan order
+        const void *g_lg[16] = {};
+        const int64_t *g_dr[16] = {};
+        int32_t g_off[16] = {}, g_rows[16] = {};
+        int32_t ng = 0;
+        auto flush = [&]() -> int {
+            if (!ng) return SPECDEC_OK;
+            const int r = specdec_pool_verify_group(ng, g_lg, g_dr, g_off, g_rows, d->logit_dtype, d->k, d->V,
+                                                    d->logit_stride, members, mlen, mactive, d->eos_id, d->pad_id,
+                                                    d->accept, d->bonus, d->emit, d->finished, d->len, d->gen,
+                                                    d->active, d->tokens, d->cap_tok, d->out_buf, d->max_new,
+                                                    d->status, d->ws, d->ws_bytes, stream);
+            launches += kv1;
+            ng = 0;
+            return r;
+        };
+        for (int32_t b = 0; b < nb; ++b) {
+            const int32_t j = (ring_base + b) % d->ring_n;
+            if (kinds[b]) {
+                ++same;
+                msame += sizes[b];
+                g_lg[ng] = d->logits_ring[j];
+                g_dr[ng] = d->draft_ring[j];
+                g_off[ng] = static_cast<int32_t>(static_cast<int64_t>(b) * B);
+                g_rows[ng] = rows(b);
+                if (++ng == G && (rc = flush())) return rc;
+                continue;
+            }
+            // a mixed batch: its whole chain on the copy stream (stream order frees the
+            // staging buffer and the side verify's scratch for the next one)
+            mfb += sizes[b];
+            const int64_t o = static_cast<int64_t>(b) * B;
+            void *stg = d->staging_ring[n_mixed % d->n_staging];
+            ++n_mixed;
+            rc = specdec_realign_kv(d->kv, stg, d->kv_dtype, d->n_planes, rows(b), d->H, d->D, p_plane, p_row,
+                                    p_head, d->cap, s_plane, s_row, s_head, d->cap, nullptr, 0, mpad + o, 0,
+                                    mlen + o, -1, 0, members + o, nullptr, d->gather_ws ? SPECDEC_DYNAMIC : 0u,
+                                    d->gather_ws, d->gather_ws ? 128 : 0, d->moved, d->status,
+                                    reinterpret_cast<specdec_stream_t>(cs));
+            if (rc) return rc;
+            rc = specdec_pool_verify(d->logits_ring[j], d->logit_dtype, rows(b), d->k, d->V, d->logit_stride,
+                                     d->draft_ring[j], members + o, mlen + o, mactive + o, d->eos_id, d->pad_id,
+                                     d->accept_ring, d->bonus2, d->emit2, d->finished2, d->len, d->gen,
+                                     d->active, d->tokens, d->cap_tok, d->out_buf, d->max_new, d->status,
+                                     d->ws2, d->ws2_bytes, reinterpret_cast<specdec_stream_t>(cs));
+            if (rc) return rc;
+            rc = specdec_realign_kv(stg, d->kv, d->kv_dtype, d->n_planes, rows(b), d->H, d->D, s_plane, s_row,
+                                    s_head, d->cap, p_plane, p_row, p_head, d->cap, nullptr, blens[b] - 1,
+                                    mlen + o, -1, d->accept_ring, 1, static_cast<int32_t>(d->k + 1), nullptr,
+                                    members + o, 0, nullptr, 0, d->moved, d->status,
+                                    reinterpret_cast<specdec_stream_t>(cs));
+            if (rc) return rc;
+            launches += 2 + kv1;
+        }
+        if ((rc = flush())) return rc;
+        // the chain's completion, waited on by the plan after next (and at the drain's end)
+        if ((e = cudaEventRecord(pev(ep), cs)) != cudaSuccess) return record_cuda_error(e);
+        d->pipe_host[1] = n_mixed;
+        *d->ring_pos = ring_base + nb;
+        if (d->host_launches) *d->host_launches += launches;
+        if (h_ran) *h_ran = nb;
+        if (h_same) *h_same = same;
+        if (h_members_same) *h_members_same = msame;
+        if (h_members_fallback) *h_members_fallback = mfb;
+        return SPECDEC_OK;
+    }
+}
+
 extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn forward,
                                   void *ctx, int32_t max_batches, int32_t *h_ran,
                                   int32_t *h_same, int32_t *h_members_same,
@@ -40,13 +173,27 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
             if (!d->staging_ring[i] || !d->events[i] || !d->events[d->n_staging + i] ||
                 (d->scatter_stream && (!d->scatter_events || !d->scatter_events[i])))
                 return SPECDEC_ERR_ARG;
+    if (d->pipeline) {
+        // R28: ring inputs, the paper's consumer, a copy stream and its staging ring, the
+        // side verify's own workspace / scratch, the events and the host state
+        if (forward || max_batches > 0 || d->dense_consumer != 0 || d->n_staging < 1 || !d->staging_ring ||
+            !d->copy_stream || !d->fb_epoch || !d->plan_epoch || !d->ws2 || !d->bonus2 || !d->emit2 ||
+            !d->finished2 || !d->accept_ring || !d->pipe_events || !d->pipe_events[0] || !d->pipe_events[1] ||
+            !d->pipe_host)
+            return SPECDEC_ERR_ARG;
+        const int32_t W = d->W;  // the packed plan header (one D2H copy)
+        if (reinterpret_cast<const char *>(d->bkind) != reinterpret_cast<const char *>(d->n_batches + 1) ||
+            d->blen != d->n_batches + 1 + W || d->bsize != d->n_batches + 1 + 2 * W)
+            return SPECDEC_ERR_ARG;
+        return pool_epoch_pipelined(d, h_ran, h_same, h_members_same, h_members_fallback, stream);
+    }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int32_t W = d->W, B = d->B;
     // the epoch plan: R11's whole-window plan, or with d->patience > 0 the deferred-fallback
     // plan (R27: leftovers wait up to `patience` epochs for a same-length partner)
     int rc = d->patience > 0
         ? specdec_pool_group_deferred(d->len, d->active, d->order, d->N, W, B, d->min_group, d->wait,
-                                      d->patience, d->window, d->window_size, d->batch_of, d->slot_of,
+                                      d->patience, nullptr, nullptr, d->window, d->window_size, d->batch_of, d->slot_of,
                                       d->members, d->mlen, d->mpad, d->mactive, d->bsize, d->bkind, d->blen,
                                       d->n_batches, d->counters, stream)
         : specdec_pool_group(d->len, d->active, d->order, d->N, W, B, d->min_group, d->window,

@@ -29,6 +29,12 @@ struct Alg3Gate {
 struct PoolDefer {
     int32_t *wait = nullptr;
     int32_t patience = 0;
+    // Pipelined fallback (reading R28): epoch[0] counts the plans; fb_epoch[s] is the plan
+    // that last put s in a mixed-length batch.  A sequence with fb_epoch[s] == epoch - 1
+    // is left out of the window (its batch runs beside this plan); members of this plan's
+    // mixed batches get fb_epoch = epoch.  fb_epoch == nullptr: off.
+    int32_t *fb_epoch = nullptr;
+    int32_t *epoch = nullptr;
 };
 
 int pool_group_launch(const int32_t *d_len, const uint8_t *d_active, const int32_t *d_order, int32_t N,

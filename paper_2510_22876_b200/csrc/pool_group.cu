@@ -222,7 +222,7 @@ __device__ void block_bitonic_sort(uint32_t *key, int n) {
 // ---- RefillWindow: the first W active ids in admission order, into
 // sm.wid / sm.wlen; returns the window size.
 __device__ int refill_window(PoolSmem &sm, const int32_t *len, const uint8_t *active, const int32_t *order,
-                             int32_t N, int32_t W) {
+                             int32_t N, int32_t W, const int32_t *fb_epoch = nullptr, int32_t prev_epoch = 0) {
     const int tid = threadIdx.x, T = blockDim.x;
     int filled = 0;
     for (int base = 0; base < N && filled < W; base += T) {
@@ -230,7 +230,8 @@ __device__ int refill_window(PoolSmem &sm, const int32_t *len, const uint8_t *ac
         int s = -1, f = 0;
         if (t < N) {
             s = order[t];
-            f = active[s] ? 1 : 0;
+            // R28: a member of the previous plan's mixed batches is still in flight
+            f = active[s] && !(fb_epoch && fb_epoch[s] == prev_epoch) ? 1 : 0;
         }
         int tot;
         const int pos = filled + block_exclusive_scan(f, sm.warp, tot);
@@ -404,6 +405,7 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
     }
     __syncthreads();
     long long lsame = 0, lsame_m = 0, lfb_m = 0, lfb_tok = 0;
+    const int32_t ep = defer.fb_epoch ? *defer.epoch : 0;  // read before thread 0 advances it
     for (int w = tid; w < Wn; w += T) {
         const int flat = sm.rank[w], b = flat / B;
         if (flat < 0) continue;
@@ -413,6 +415,7 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
         } else {
             ++lfb_m;
             lfb_tok += sm.wlen[w];
+            if (defer.fb_epoch) defer.fb_epoch[sm.wid[w]] = ep;  // R28: in flight next plan
         }
     }
     for (int b = tid; b < nb_total; b += T) {
@@ -437,6 +440,10 @@ __device__ void plan_full(PoolSmem &sm, int Wn, int32_t B, int32_t min_group, in
         atomicAdd(reinterpret_cast<unsigned long long *>(counters + 6), static_cast<unsigned long long>(n_groups));
         if (n_deferred)
             atomicAdd(reinterpret_cast<unsigned long long *>(counters + 7), static_cast<unsigned long long>(n_deferred));
+    }
+    if (defer.fb_epoch) {
+        __syncthreads();  // every thread has read the epoch
+        if (tid == 0) *defer.epoch = ep + 1;
     }
     if (gate.members) {
         // Alg. 3 device loop: batch 0 as the row maps of this iteration's gather / verify /
@@ -485,7 +492,8 @@ __global__ void __launch_bounds__(kPoolThreads) pool_group_kernel(
         batch_of[s] = -1;
         slot_of[s] = -1;
     }
-    const int Wn = refill_window(sm, len, active, order, N, W);
+    const int Wn = refill_window(sm, len, active, order, N, W, defer.fb_epoch,
+                                 defer.fb_epoch ? *defer.epoch - 1 : 0);
     plan_full(sm, Wn, B, min_group, window, window_size, batch_of, slot_of, members, mlen, mpad, mactive, bsize,
               bkind, blen, n_batches, counters, gate, exp, defer);
 }
@@ -674,16 +682,19 @@ extern "C" int specdec_pool_group(const int32_t *d_len, const uint8_t *d_active,
 extern "C" int specdec_pool_group_deferred(const int32_t *d_len, const uint8_t *d_active,
                                            const int32_t *d_order, int32_t N, int32_t W, int32_t B,
                                            int32_t min_group, int32_t *d_wait, int32_t patience,
+                                           int32_t *d_fb_epoch, int32_t *d_epoch,
                                            int32_t *d_window, int32_t *d_window_size,
                                            int32_t *d_batch_of, int32_t *d_slot_of, int32_t *d_members,
                                            int32_t *d_mlen, int32_t *d_mpad, uint8_t *d_mactive,
                                            int32_t *d_bsize, uint8_t *d_bkind, int32_t *d_blen,
                                            int32_t *d_n_batches, int64_t *d_counters,
                                            specdec_stream_t stream) {
-    if (patience < 0 || (patience > 0 && !d_wait)) return SPECDEC_ERR_ARG;
+    if (patience < 0 || (patience > 0 && !d_wait) || (!d_fb_epoch != !d_epoch)) return SPECDEC_ERR_ARG;
     PoolDefer defer;
     defer.wait = d_wait;
     defer.patience = patience;
+    defer.fb_epoch = d_fb_epoch;
+    defer.epoch = d_epoch;
     return pool_group_launch(d_len, d_active, d_order, N, W, B, min_group, d_window, d_window_size, d_batch_of,
                              d_slot_of, d_members, d_mlen, d_mpad, d_mactive, d_bsize, d_bkind, d_blen,
                              d_n_batches, d_counters, Alg3Gate{}, stream, false, defer);

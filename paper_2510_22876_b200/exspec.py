@@ -30,7 +30,7 @@ class SequencePool:
     def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
                  max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True,
                  dense_consumer=False, n_staging=1, consumer=None, verify_group=8, scatter_stream=False,
-                 patience=0):
+                 patience=0, pipeline=False):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
         if B > W:
@@ -43,6 +43,11 @@ class SequencePool:
         if patience < 0:
             raise ValueError("patience must be >= 0")
         self.patience = int(patience)
+        # pipelined fallback (R28, native executor only): a plan's mixed batches run on the
+        # copy stream beside the next plan, which leaves their members out
+        self.pipeline = bool(pipeline)
+        if self.pipeline and self.consumer != "zero-copy":
+            raise ValueError("pipeline needs the zero-copy consumer")
         self.max_new, self.eos_id, self.pad_id = max_new, eos_id, pad_id
         self.device = dev
         # the consumer of a batch's KV (specdec_pool_desc::dense_consumer): "zero-copy"
@@ -62,6 +67,8 @@ class SequencePool:
         self.active = torch.zeros(N, dtype=u8, device=dev)
         self.order = torch.arange(N, dtype=i32, device=dev)
         self.wait = torch.zeros(N, dtype=i32, device=dev)      # R27: epochs sat out
+        self.fb_epoch = torch.full((N,), -2, dtype=i32, device=dev)   # R28: plan of the last mixed batch
+        self.plan_epoch = torch.zeros(1, dtype=i32, device=dev)       # R28: plans made
         self.tokens = torch.full((N, self.cap_tok), pad_id, dtype=i64, device=dev)
         self.out_buf = torch.zeros((N, max_new), dtype=i64, device=dev)
         alloc = torch.zeros if kv_init else torch.empty
@@ -78,10 +85,10 @@ class SequencePool:
         self.window_size = torch.zeros(1, dtype=i32, device=dev)
         self.batch_of = torch.zeros(N, dtype=i32, device=dev)
         self.slot_of = torch.zeros(N, dtype=i32, device=dev)
-        self.members = torch.zeros((W, B), dtype=i32, device=dev)
-        self.mlen = torch.zeros((W, B), dtype=i32, device=dev)
-        self.mpad = torch.zeros((W, B), dtype=i32, device=dev)
-        self.mactive = torch.zeros((W, B), dtype=u8, device=dev)
+        # plan rows: 2W batch rows, the pipelined executor alternates between the halves
+        # (R28); every other path uses the first W
+        self._rows_full = [torch.zeros((2 * W, B), dtype=dt, device=dev) for dt in (i32, i32, i32, u8)]
+        self.members, self.mlen, self.mpad, self.mactive = (t[:W] for t in self._rows_full)
         # the plan header arrays share one buffer laid out like the pinned host header
         # (n_batches | bkind in W int32 slots | blen | bsize): one D2H copy per epoch
         self._hdr_dev = torch.zeros(1 + 3 * W, dtype=i32, device=dev)
@@ -118,6 +125,10 @@ class SequencePool:
         self.len.copy_(torch.as_tensor(np.asarray(prompts_lens), dtype=torch.int32))
         self.gen.zero_()
         self.wait.zero_()
+        self.fb_epoch.fill_(-2)
+        self.plan_epoch.zero_()
+        if getattr(self, "_pipe_host", None) is not None:
+            self._pipe_host[0] = self._pipe_host[1] = 0
         self.active.fill_(1)
         if order is not None:
             self.order.copy_(torch.as_tensor(np.asarray(order), dtype=torch.int32))
@@ -292,7 +303,32 @@ class SequencePool:
         d.verify_group = self.verify_group
         self._launches = ctypes.c_int64(0)      # libspecdec kernels the executor launched
         d.host_launches = ctypes.addressof(self._launches)
-        if self.n_staging >= 2:
+        if self.pipeline:
+            self._pipe_copy = torch.cuda.Stream(self.device)
+            self._pipe_events = [torch.cuda.Event(enable_timing=False) for _ in range(2)]
+            for ev in self._pipe_events:
+                ev.record(torch.cuda.current_stream(self.device))
+            self._pipe_ev_ptrs = (ctypes.c_void_p * 2)(*[ev.cuda_event for ev in self._pipe_events])
+            self._pipe_host = (ctypes.c_int64 * 2)(0, 0)
+            # the chain runs on one stream: one staging buffer is enough (stream order)
+            self._pipe_stg = (ctypes.c_void_p * 1)(self.staging.data_ptr())
+            self._pipe_accept = torch.zeros(self.B, dtype=torch.int32, device=self.device)
+            ws2 = _abi.specdec_verify_workspace_size(self.B, self.k)
+            self._ws2 = torch.zeros((ws2 + 7) // 8, dtype=torch.int64, device=self.device)
+            self._bonus2 = torch.zeros(self.B, dtype=torch.int64, device=self.device)
+            self._emit2 = torch.zeros(self.B, dtype=torch.int32, device=self.device)
+            self._finished2 = torch.zeros(self.B, dtype=torch.uint8, device=self.device)
+            d.pipeline = 1
+            d.fb_epoch, d.plan_epoch = self.fb_epoch.data_ptr(), self.plan_epoch.data_ptr()
+            d.ws2, d.ws2_bytes = self._ws2.data_ptr(), self._ws2.numel() * 8
+            d.bonus2, d.emit2, d.finished2 = self._bonus2.data_ptr(), self._emit2.data_ptr(), self._finished2.data_ptr()
+            d.pipe_events = ctypes.cast(self._pipe_ev_ptrs, ctypes.c_void_p)
+            d.pipe_host = ctypes.addressof(self._pipe_host)
+            d.n_staging = 1
+            d.staging_ring = ctypes.cast(self._pipe_stg, ctypes.c_void_p)
+            d.copy_stream = self._pipe_copy.cuda_stream
+            d.accept_ring = self._pipe_accept.data_ptr()
+        elif self.n_staging >= 2:
             ns = self.n_staging
             self._copy_stream = torch.cuda.Stream(self.device)
             self._events = [torch.cuda.Event(enable_timing=False) for _ in range(2 * ns)]
@@ -322,6 +358,8 @@ class SequencePool:
     def epoch_native(self, max_batches=0, stream=None, forward=None):
         """One epoch (or, with max_batches=1, one Alg. 3 iteration) in the native executor.
         `forward`: optional _abi.FORWARD_FN called per batch for its (logits, draft).
+        pipeline (R28): one plan per call, its mixed batches left running on the copy
+        stream; a call returning 0 batches leaves the pool drained and every chain done.
         Returns (batches run, same-length batches run, members same, members fallback)."""
         r = _abi.specdec_pool_epoch(self._desc, max_batches, stream, forward)
         self.verify_calls += r[0]
