@@ -174,7 +174,8 @@ def _pool_cell(cuda, cli, seqs_checked=16):
                       max_new=args.max_new, device=cuda, kv_init=False,
                       dense_consumer=args.pool_consumer == "dense",
                       n_staging=args.pool_staging if args.pool_exec == "native" else 1,
-                      patience=args.pool_patience)
+                      patience=args.pool_patience,
+                      pipeline=bool(args.pool_pipeline) and args.pool_mode == "epoch")
     local_lens = lens[mine]
     local_order = np.arange(n_loc)
     seed = args.seed
@@ -213,11 +214,14 @@ def _pool_cell(cuda, cli, seqs_checked=16):
                 break
             oracle_batch(plan["batches"][0], plan["blen"][0], (ring_pos + it) % bench.RING)
     else:
-        # with deferred fallback (R27) the waits matter from the second epoch on: 4 epochs
+        # with deferred fallback (R27) the waits matter from the second epoch on: 4 epochs;
+        # pipelined fallback (R28): the last plan's mixed members sit the next plan out
         o_wait = np.zeros(n_loc, np.int64)
-        for _ in range(4 if args.pool_patience > 0 else 1):
-            plan = OP.form_batches_deferred(o_len, o_act, local_order, Wn, Bp, args.min_group, o_wait,
-                                            args.pool_patience)
+        inflight = []
+        for _ in range(4 if args.pool_patience > 0 or sp.pipeline else 1):
+            plan = OP.form_batches_deferred(o_len, OP.pipeline_window_active(o_act, inflight), local_order, Wn,
+                                            Bp, args.min_group, o_wait, args.pool_patience)
+            inflight = OP.mixed_members(plan) if sp.pipeline else []
             ran = sp.epoch_native()[0]
             assert ran == len(plan["batches"])
             for b, mem in enumerate(plan["batches"]):

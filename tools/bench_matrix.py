@@ -41,6 +41,7 @@ POOL = (
        ("P N1024 patience 1", ["--config", "pool", "--pool-patience", "1"]),
        ("P N1024 patience 4", ["--config", "pool", "--pool-patience", "4"]),
        ("P N1024 W32 patience 0", ["--config", "pool", "--pool-W", "32", "--pool-patience", "0"]),
+       ("P N1024 pipelined fallback", ["--config", "pool", "--pool-pipeline", "1"]),
        ("P N1024 emulated x8 patience 0", ["--config", "pool", "--emulate-ranks", "8", "--pool-patience", "0"]),
        ("P N1024 emulated x8 patience 1", ["--config", "pool", "--emulate-ranks", "8", "--pool-patience", "1"]),
        ("P N1024 dense consumer", ["--config", "pool", "--pool-consumer", "dense"]),
