@@ -46,8 +46,6 @@ class SequencePool:
         # pipelined fallback (R28, native executor only): a plan's mixed batches run on the
         # copy stream beside the next plan, which leaves their members out
         self.pipeline = bool(pipeline)
-        if self.pipeline and self.consumer != "zero-copy":
-            raise ValueError("pipeline needs the zero-copy consumer")
         self.max_new, self.eos_id, self.pad_id = max_new, eos_id, pad_id
         self.device = dev
         # the consumer of a batch's KV (specdec_pool_desc::dense_consumer): "zero-copy"
@@ -58,6 +56,8 @@ class SequencePool:
         if self.consumer not in ("zero-copy", "dense", "slot"):
             raise ValueError(f"consumer {self.consumer!r}")
         self.dense_consumer = self.consumer == "dense"
+        if self.pipeline and self.consumer != "zero-copy":
+            raise ValueError("pipeline needs the zero-copy consumer")
         # verify + write-back in one launch (specdec_pool_verify); False: the two calls
         self.fused = True
         self.cap_tok = cap_tok or cap
