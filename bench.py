@@ -63,7 +63,7 @@ def parse(argv=None):
                          "2: the KV moves in conditional graph nodes)")
     ap.add_argument("--pool-scatter-stream", type=int, default=1,
                     help="pool (native, overlapped): the scatters on a third stream beside the gathers")
-    ap.add_argument("--pool-verify-group", type=int, default=8,
+    ap.add_argument("--pool-verify-group", type=int, default=64,
                     help="pool (native executor): same-length batches verified per launch (1 = per batch)")
     ap.add_argument("--pool-staging", type=int, default=2,
                     help="pool, native executor: staging buffers; >= 2 overlaps the fallback "

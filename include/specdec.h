@@ -59,6 +59,8 @@ typedef struct CUstream_st *specdec_stream_t; /* == cudaStream_t */
 #define SPECDEC_SEGMENTED 8u    /* in place: cut slabs into segments (workspace slots) */
 #define SPECDEC_DYNAMIC_FORCE 16u /* with SPECDEC_DYNAMIC: tickets even for few units per CTA */
 
+#define SPECDEC_MAX_VERIFY_GROUP 64 /* specdec_pool_verify_group: batches per launch */
+
 /* ------------------------------------------------------------------------------ misc */
 int specdec_version(void);                /* ABI version (major*100 + minor) */
 const char *specdec_last_cuda_error(void); /* message for the last SPECDEC_ERR_CUDA (thread-local) */
@@ -378,7 +380,7 @@ int specdec_pool_verify(const void *d_logits, int dtype, int64_t B, int64_t k, i
                         int64_t *d_out_buf, int64_t max_new, uint32_t *d_status, void *d_ws,
                         size_t ws_bytes, specdec_stream_t stream);
 
-/* specdec_pool_verify_group -- specdec_pool_verify over n_batches (1..16) batches of one
+/* specdec_pool_verify_group -- specdec_pool_verify over n_batches (1..SPECDEC_MAX_VERIFY_GROUP) batches of one
  * epoch plan in ONE launch (reading R21: the batches of one plan have disjoint members and
  * are planned from one window state, so verifying them together changes no result; the
  * executor calls each batch's forward first).  Batch g: logits h_logits[g] [h_rows[g]][k+1]
@@ -509,7 +511,7 @@ typedef struct specdec_pool_desc {
     /* optional >= 128-byte zeroed workspace: the fallback gathers take SPECDEC_DYNAMIC
      * work tickets from it (they run one after another on one stream); NULL = static */
     void *gather_ws;
-    /* same-length batches verified per launch (specdec_pool_verify_group, <= 16); <= 1:
+    /* same-length batches verified per launch (specdec_pool_verify_group, <= SPECDEC_MAX_VERIFY_GROUP); <= 1:
      * one specdec_pool_verify per batch.  Runs of same-length batches in the processing
      * order are grouped; forward() is called for every batch of a group before the group's
      * verify, so the buffers it returns must stay valid until then.  Needs `ws` of

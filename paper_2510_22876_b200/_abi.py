@@ -125,6 +125,7 @@ class RoundDesc(ctypes.Structure):
 
 
 HOST_SLOTS = 4
+MAX_VERIFY_GROUP = 64   # SPECDEC_MAX_VERIFY_GROUP (include/specdec.h)
 _PS = _P * HOST_SLOTS
 
 

@@ -44,7 +44,7 @@ static int pool_epoch_pipelined(const specdec_pool_desc *d, int32_t *h_ran, int3
     const int64_t hcd = d->H * d->cap * d->D;
     const int64_t p_plane = hcd, p_row = d->n_planes * hcd, p_head = d->cap * d->D;
     const int64_t s_plane = B * hcd, s_row = hcd, s_head = d->cap * d->D;
-    int32_t G = std::min<int32_t>(std::max<int32_t>(d->verify_group, 1), 16);
+    int32_t G = std::min<int32_t>(std::max<int32_t>(d->verify_group, 1), SPECDEC_MAX_VERIFY_GROUP);
     while (G > 1 && specdec_verify_workspace_size(static_cast<int64_t>(G) * B, d->k) > d->ws_bytes) --G;
     const int kv1 = specdec_verify_kernels(1);
     int64_t launches = 0;
@@ -92,9 +92,9 @@ static int pool_epoch_pipelined(const specdec_pool_desc *d, int32_t *h_ran, int3
         auto rows = [&](int32_t b) -> int32_t { return sizes[b] > 0 && sizes[b] < B ? sizes[b] : B; };
         int32_t same = 0, msame = 0, mfb = 0, n_mixed = 0;
         // same-length batches: grouped verifies on `stream`, in plan order
-        const void *g_lg[16] = {};
-        const int64_t *g_dr[16] = {};
-        int32_t g_off[16] = {}, g_rows[16] = {};
+        const void *g_lg[SPECDEC_MAX_VERIFY_GROUP] = {};
+        const int64_t *g_dr[SPECDEC_MAX_VERIFY_GROUP] = {};
+        int32_t g_off[SPECDEC_MAX_VERIFY_GROUP] = {}, g_rows[SPECDEC_MAX_VERIFY_GROUP] = {};
         int32_t ng = 0;
         auto flush = [&]() -> int {
             if (!ng) return SPECDEC_OK;
@@ -235,7 +235,7 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     const bool overlap = NS > 0 && run > 1;
     // same-length batches per verify launch (specdec_pool_verify_group), if the workspace
     // holds the grouped rows
-    int32_t G = std::min<int32_t>(std::max<int32_t>(d->verify_group, 1), 16);
+    int32_t G = std::min<int32_t>(std::max<int32_t>(d->verify_group, 1), SPECDEC_MAX_VERIFY_GROUP);
     while (G > 1 && specdec_verify_workspace_size(static_cast<int64_t>(G) * B, d->k) > d->ws_bytes) --G;
     int64_t launches = 1;  // K4
     std::vector<int32_t> seq, fb_rank(run, -1);
@@ -312,9 +312,9 @@ extern "C" int specdec_pool_epoch(const specdec_pool_desc *d, specdec_forward_fn
     }
     const int kv1 = specdec_verify_kernels(1);
     // a group of same-length batches: each batch's inputs (forward or ring), one launch
-    const void *g_lg[16] = {};
-    const int64_t *g_dr[16] = {};
-    int32_t g_off[16] = {}, g_rows[16] = {};
+    const void *g_lg[SPECDEC_MAX_VERIFY_GROUP] = {};
+    const int64_t *g_dr[SPECDEC_MAX_VERIFY_GROUP] = {};
+    int32_t g_off[SPECDEC_MAX_VERIFY_GROUP] = {}, g_rows[SPECDEC_MAX_VERIFY_GROUP] = {};
     int32_t ng = 0;
     auto flush_group = [&]() -> int {
         if (!ng) return SPECDEC_OK;

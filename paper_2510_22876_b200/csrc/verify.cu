@@ -31,7 +31,7 @@ constexpr int kMaxK = 31;  // k + 1 <= 32: one lane per slot in the epilogue
 constexpr int kEpiCache = 1024;  // rows whose n' the epilogue keeps in shared memory
 // default completion modes (VerifyParams::split), measured: tools/k1bench.py
 constexpr int kSplitEqSpec = 1, kSplitPool = 2;
-constexpr int kMaxGroup = 16;  // specdec_pool_verify_group: batches per launch
+constexpr int kMaxGroup = SPECDEC_MAX_VERIFY_GROUP;  // specdec_pool_verify_group: batches per launch
 
 struct VerifyParams {
     const void *logits;
@@ -74,9 +74,12 @@ struct VerifyParams {
 };
 
 __device__ __forceinline__ int group_of(const VerifyParams &p, int64_t i) {
-    int g = 0;
-    while (g + 1 < p.ngroup && p.g_row0[g + 1] <= i) ++g;
-    return g;
+    int lo = 0, hi = p.ngroup - 1;  // the last g with g_row0[g] <= i
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (p.g_row0[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    return lo;
 }
 // the plan-array index (members / lengths / active) of flat batch row i
 __device__ __forceinline__ int64_t src_row(const VerifyParams &p, int64_t i) {

@@ -29,7 +29,7 @@ from .eqspec import TORCH_DT
 class SequencePool:
     def __init__(self, N, cap, layers, H, D, k, *, kv_dtype="bf16", W=32, B=8, min_group=2,
                  max_new=256, eos_id=-1, pad_id=0, cap_tok=None, device="cuda", kv_init=True,
-                 dense_consumer=False, n_staging=1, consumer=None, verify_group=8, scatter_stream=False,
+                 dense_consumer=False, n_staging=1, consumer=None, verify_group=64, scatter_stream=False,
                  patience=0, pipeline=False):
         dev = torch.device(device)
         i32, i64, u8 = torch.int32, torch.int64, torch.uint8
@@ -99,7 +99,7 @@ class SequencePool:
         self.counters = torch.zeros(8, dtype=i64, device=dev)
         # per-batch verify scratch; the native executor verifies up to `verify_group`
         # same-length batches per launch (specdec_pool_verify_group): rows for all of them
-        self.verify_group = max(1, min(int(verify_group), 16))
+        self.verify_group = max(1, min(int(verify_group), _abi.MAX_VERIFY_GROUP))
         GB = self.verify_group * B
         self.accept = torch.zeros(GB, dtype=i32, device=dev)
         self.bonus = torch.zeros(GB, dtype=i64, device=dev)

@@ -89,11 +89,12 @@ def test_host_validation_without_gpu(lib):
     # batch init: NULL lengths / B < 1
     assert L.specdec_batch_init(None, 4, nz, None, None, None, 0, None, None) == _abi.ERR_ARG
     assert L.specdec_batch_init(nz, 0, nz, None, None, None, 0, None, None) == _abi.ERR_SHAPE
-    # grouped pool verify: 0 or more than 16 batches, a batch with no rows
-    P = ctypes.c_void_p * 17
-    I = ctypes.c_int32 * 17
-    ptrs, offs, rows = P(*([16] * 17)), I(*([0] * 17)), I(*([1] * 17))
-    for n in (0, 17):
+    # grouped pool verify: 0 or more than SPECDEC_MAX_VERIFY_GROUP batches, a batch with no rows
+    G1 = _abi.MAX_VERIFY_GROUP + 1
+    P = ctypes.c_void_p * G1
+    I = ctypes.c_int32 * G1
+    ptrs, offs, rows = P(*([16] * G1)), I(*([0] * G1)), I(*([1] * G1))
+    for n in (0, G1):
         rc = L.specdec_pool_verify_group(n, ptrs, ptrs, offs, rows, 2, 5, 100, 104, *([nz] * 3), -1, 0,
                                          *([nz] * 7), None, 0, None, 16, None, nz, 1 << 20, None)
         assert rc == _abi.ERR_ARG, n
@@ -203,3 +204,10 @@ def test_host_round_binding_rejects_unpinned(lib):
     import torch
     with pytest.raises(_abi.SpecdecError):
         _abi.specdec_eqspec_round_host(_abi.RoundDesc(), _abi.HostIO(), 0, 0, torch.zeros(4), torch.zeros(4))
+
+
+def test_max_verify_group_matches_header():
+    """The binding's MAX_VERIFY_GROUP is the header's SPECDEC_MAX_VERIFY_GROUP."""
+    import re
+    h = open(os.path.join(ROOT, "include", "specdec.h")).read()
+    assert int(re.search(r"#define SPECDEC_MAX_VERIFY_GROUP (\d+)", h).group(1)) == _abi.MAX_VERIFY_GROUP
