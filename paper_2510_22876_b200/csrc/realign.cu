@@ -59,6 +59,7 @@ struct RealignParams {
     uint32_t flags;
     int inplace;
     int policy_mode;  // 0: L2 evict_first on the streamed bytes, 1: evict_normal
+    int exp;          // SPECDEC_K2_EXP timing probe (results invalid): 1 = prologue only, no copies
     char *ws;         // boundary slots (in-place segmentation), or null
     int64_t ws_slots;
     int64_t seg_bytes;  // >= kSegBytes (the workspace is sized for kSegBytes)
@@ -412,7 +413,7 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
     fence_proxy_async_smem();  // zero buffer (generic writes) visible to the bulk engine
     __syncwarp();
     if (lane != 0) return;
-    if (sm.t.n_mv == 0) { dyn_done(p, 0u); return; }
+    if (sm.t.n_mv == 0 || p.exp == 1) { dyn_done(p, 0u); return; }
 
     const uint64_t pol = p.policy_mode == 0 ? policy_evict_first() : policy_evict_normal();
     ChunkIter it;
@@ -687,6 +688,8 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
         g_seg_bytes = std::max<int64_t>(kSegBytes, sg ? atoll(sg) : kSegBytes);
     }
     p.policy_mode = pol;
+    static const int k2_exp = getenv("SPECDEC_K2_EXP") ? atoi(getenv("SPECDEC_K2_EXP")) : 0;
+    p.exp = k2_exp;
     p.seg_bytes = g_seg_bytes;
     p.seg_rows = std::max<int64_t>(1, g_seg_bytes / rb);
     if (count_bound > 0 && count_bound * rb <= kSmallBytes) {
