@@ -995,6 +995,15 @@ def run_pool(args, rank, world, device, emulate=False):
                 "note": "latency-bound launches of mean batch size "
                         f"{(int(cnt[2]) + int(cnt[3])) / max(1, int(cnt[0])):.2f}; event-timed one by one",
                 "peak_source": peak_src}
+    # the whole timed drain against the same peak: every algorithmic byte of the path -- the
+    # KV moved by the gathers and scatters plus the logits every verified row reads ((k+1)
+    # x V x 2 B) -- over the drain time.  With deferred fallback and 64-batch grouped
+    # verifies the two kernels are about even (ncu launch list: K1 49 %, K2 45 %), so this is
+    # the pool's own roofline; `roofline` keeps the K2 gather / scatter launches alone.
+    lg_all = (int(cnt[2]) + int(cnt[3])) * (k + 1) * V * 2
+    drain_gbps = (moved + lg_all) / (ms / 1e3) / 1e9 if ms else 0.0
+    roof["drain"] = {"bytes": moved + lg_all, "kv_bytes": moved, "logit_bytes": lg_all,
+                     "achieved": drain_gbps, "frac": drain_gbps / peak, "unit": "GB/s"}
     cb = pool_cpu_baseline(args) if (world == 1 and rank == 0) else None
     check = None
     if cb is not None:
