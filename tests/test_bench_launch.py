@@ -88,16 +88,19 @@ def test_default_line_has_the_contract_keys():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["epoch", "alg3"])
+@pytest.mark.parametrize("mode", ["epoch", "alg3", "pipelined"])
 def test_pool_line_drain_matches_the_oracle(mode):
-    """The pool line's timed drain (native executor; Alg. 3: the graph-replayed device loop)
-    against the oracle's own plan-driven drain of the same workload (the cpu_baseline leg):
-    batches, same-length batches and members, fallback members and KV bytes, exactly."""
+    """The pool line's timed drain (native executor with the default deferred fallback; Alg. 3:
+    the graph-replayed device loop; pipelined: R28) against the oracle's own plan-driven drain
+    of the same workload (the cpu_baseline leg): batches, same-length batches and members,
+    fallback members and KV bytes, exactly; the whole-drain byte roofline is reported."""
+    extra = ["--pool-pipeline", "1"] if mode == "pipelined" else ["--pool-mode", mode]
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "pool", "--pool-n", "192",
-                        "--max-new", "64", "--pool-mode", mode], capture_output=True, text=True, timeout=900,
-                       cwd=ROOT)
+                        "--max-new", "64"] + extra, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     d = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     chk = d["oracle_drain_check"]
     assert chk["match"], chk
     assert d["cpu_baseline"]["kind"] == "oracle" and d["gpu_launches"] > 0 and d["status"] == 0
+    dr = d["roofline"]["drain"]
+    assert dr["bytes"] == dr["kv_bytes"] + dr["logit_bytes"] and 0 < dr["frac"] < 1.2
