@@ -39,6 +39,7 @@ constexpr int64_t kSlotBytes = 4096;          // boundary slot: |shift| * row by
 static int g_ctas_per_sm = 0;                 // tuning override (SPECDEC_REALIGN_CTAS)
 static int64_t g_grid_cap = 0;                // tuning override (SPECDEC_REALIGN_GRID): max CTAs
 constexpr int kTicketLead = 3;                // SPECDEC_DYNAMIC: chunks of lead for the next ticket
+static int g_ticket_lead = kTicketLead;       // tuning override (SPECDEC_REALIGN_LEAD)
 constexpr int64_t kWsHeader = 128;            // workspace header: the dynamic-schedule counters
 static int64_t g_seg_bytes = kSegBytes;       // tuning override (SPECDEC_REALIGN_SEG, >= default)
 
@@ -60,6 +61,7 @@ struct RealignParams {
     int inplace;
     int policy_mode;  // 0: L2 evict_first on the streamed bytes, 1: evict_normal
     int exp;          // SPECDEC_K2_EXP timing probe (results invalid): 1 = prologue only, no copies
+    int ticket_lead;  // SPECDEC_DYNAMIC: chunk loads of the current unit left when the next ticket is taken
     char *ws;         // boundary slots (in-place segmentation), or null
     int64_t ws_slots;
     int64_t seg_bytes;  // >= kSegBytes (the workspace is sized for kSegBytes)
@@ -458,7 +460,7 @@ __device__ __forceinline__ void realign_body(const RealignParams &p, RealignSmem
             dst = un.d + off;
             ++it.q;
             last = it.q == it.nmain && !it.bnd_left;
-            if (p.sched && !have_next && (it.nmain - it.q) + (it.bnd_left ? 1 : 0) <= kTicketLead) {
+            if (p.sched && !have_next && (it.nmain - it.q) + (it.bnd_left ? 1 : 0) <= p.ticket_lead) {
                 next_ticket = atomicAdd(p.sched, 1u);
                 have_next = true;
             }
@@ -684,12 +686,15 @@ extern "C" int specdec_realign_kv(const void *d_kv_src, void *d_kv_dst, int dtyp
         g_ctas_per_sm = c ? atoi(c) : 0;
         const char *gc = getenv("SPECDEC_REALIGN_GRID");
         g_grid_cap = gc ? atoll(gc) : 0;
+        const char *tl = getenv("SPECDEC_REALIGN_LEAD");
+        g_ticket_lead = tl && atoi(tl) > 0 ? atoi(tl) : kTicketLead;
         const char *sg = getenv("SPECDEC_REALIGN_SEG");
         g_seg_bytes = std::max<int64_t>(kSegBytes, sg ? atoll(sg) : kSegBytes);
     }
     p.policy_mode = pol;
     static const int k2_exp = getenv("SPECDEC_K2_EXP") ? atoi(getenv("SPECDEC_K2_EXP")) : 0;
     p.exp = k2_exp;
+    p.ticket_lead = g_ticket_lead;
     p.seg_bytes = g_seg_bytes;
     p.seg_rows = std::max<int64_t>(1, g_seg_bytes / rb);
     if (count_bound > 0 && count_bound * rb <= kSmallBytes) {
